@@ -1,0 +1,253 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes loaders for the two CPU checkers.
+
+Only tests/, ``__graft_entry__.smoke()`` and ``bench.py`` (cpu_baseline leg and
+``--impl reference``) may import this module. The product package
+``paper_2208_11617_b200`` never imports it.
+
+* ``Restated``  — oracle/libsmx_oracle.so, the plain-C restatement (smx_oracle.c).
+* ``Reference`` — oracle/_ref/libsmx_ref.so, the unmodified reference headers
+  compiled in place (ref_harness.cpp); absent if it was never built.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+RESTATED_SO = os.path.join(HERE, "libsmx_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libsmx_ref.so")
+
+# map_kind ordinals (maps.hpp:19)
+BB, RB, LAMBDA, H2D, TRAP, PADDED, H3D = range(7)
+
+_u64p = np.ctypeslib.ndpointer(np.uint64, flags="C")
+_i64p = np.ctypeslib.ndpointer(np.int64, flags="C")
+_u32p = np.ctypeslib.ndpointer(np.uint32, flags="C")
+_u8p = np.ctypeslib.ndpointer(np.uint8, flags="C")
+
+
+def build() -> None:
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def tri_cells(side: int) -> int:
+    return side * (side + 1) // 2 if side >= 1 else 0
+
+
+def tet_cells(side: int) -> int:
+    return side * (side + 1) * (side + 2) // 6 if side >= 1 else 0
+
+
+def cells_of(m: int, side: int) -> int:
+    return tri_cells(side) if m == 2 else tet_cells(side)
+
+
+def ncpu() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+class Restated:
+    """The plain-C restatement (oracle/smx_oracle.c)."""
+
+    def __init__(self, path: str = RESTATED_SO):
+        if not os.path.exists(path):
+            build()
+        L = C.CDLL(path)
+        L.orc_grid.argtypes = [C.c_int, C.c_int, C.c_int64, _i64p]
+        L.orc_map_outcomes.argtypes = [C.c_int, C.c_int, C.c_int64, _i64p, C.c_uint64]
+        L.orc_map_h2d.argtypes = [C.c_int64, C.c_int64, _i64p]
+        L.orc_map_h3d.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64, _i64p]
+        L.orc_map_bb.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int, _i64p]
+        L.orc_sweep.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, _u64p]
+        L.orc_state_hash.argtypes = [C.c_int, C.c_int64, C.c_void_p, C.c_uint64]
+        L.orc_state_hash.restype = C.c_uint64
+        L.orc_make_life_state.argtypes = [C.c_int, C.c_int64, C.c_uint64, _u8p, C.c_uint64, C.c_int]
+        L.orc_ca3d_run.argtypes = [C.c_int64, C.c_int64, _u8p, C.c_uint64, C.c_int]
+        L.orc_ca3d_run_literal.argtypes = [C.c_int64, C.c_int64, _u8p, C.c_uint64]
+        L.orc_first_defect.argtypes = [C.c_int, C.c_int64, _u32p, C.c_uint64, _i64p, _u64p]
+        L.orc_tet_layer_prefix.argtypes = [C.c_int64, C.c_int64]
+        L.orc_tet_layer_prefix.restype = C.c_uint64
+        self.L = L
+
+    @staticmethod
+    def _ok(rc: int, what: str) -> None:
+        if rc != 0:
+            raise OracleError(f"{what}: status {rc}")
+
+    def grid(self, kind: int, m: int, n: int):
+        e = np.zeros(3, np.int64)
+        self._ok(self.L.orc_grid(kind, m, n, e), "grid")
+        return tuple(int(v) for v in e)
+
+    def map_outcomes(self, kind: int, m: int, n: int) -> np.ndarray:
+        ex, ey, ez = self.grid(kind, m, n)
+        out = np.zeros((ex * ey * ez, 6), np.int64)
+        self._ok(self.L.orc_map_outcomes(kind, m, n, out, out.shape[0]), "map_outcomes")
+        return out
+
+    def map_one(self, kind: int, m: int, n: int, x: int, y: int, z: int = 0):
+        o = np.zeros(6, np.int64)
+        if kind == H2D:
+            rc = self.L.orc_map_h2d(x, y, o)
+        elif kind == H3D:
+            rc = self.L.orc_map_h3d(x, y, z, n, o)
+        else:
+            rc = self.L.orc_map_bb(x, y, z, n, m, o)
+        self._ok(rc, "map_one")
+        return tuple(int(v) for v in o)
+
+    def sweep(self, kind: int, m: int, n: int, rho: int, coverage: bool = True,
+              cells: np.ndarray | None = None):
+        side = (n if kind == BB else n - 1) * rho
+        cov = np.zeros(cells_of(m, side), np.uint32) if coverage else None
+        cnt = np.zeros(4, np.uint64)
+        self._ok(self.L.orc_sweep(kind, m, n, rho,
+                                  cov.ctypes.data if cov is not None else None,
+                                  cells.ctypes.data if cells is not None else None, cnt), "sweep")
+        return cov, [int(v) for v in cnt]
+
+    def state_hash(self, m: int, side: int, arr: np.ndarray) -> int:
+        a = np.ascontiguousarray(arr)
+        return int(self.L.orc_state_hash(m, side, a.ctypes.data, a.nbytes))
+
+    def make_life_state(self, m: int, side: int, seed: int, threads: int | None = None) -> np.ndarray:
+        out = np.empty(cells_of(m, side), np.uint8)
+        self._ok(self.L.orc_make_life_state(m, side, seed, out, out.size, threads or ncpu()), "life")
+        return out
+
+    def ca3d_run(self, side: int, steps: int, cells: np.ndarray, threads: int | None = None) -> np.ndarray:
+        self._ok(self.L.orc_ca3d_run(side, steps, cells, cells.size, threads or ncpu()), "ca3d")
+        return cells
+
+    def ca3d_run_literal(self, side: int, steps: int, cells: np.ndarray) -> np.ndarray:
+        self._ok(self.L.orc_ca3d_run_literal(side, steps, cells, cells.size), "ca3d_literal")
+        return cells
+
+    def first_defect(self, m: int, side: int, cov: np.ndarray):
+        w = np.zeros(3, np.int64)
+        mult = np.zeros(1, np.uint64)
+        exact = self.L.orc_first_defect(m, side, cov, cov.size, w, mult)
+        return bool(exact), tuple(int(v) for v in w), int(mult[0])
+
+
+class Reference:
+    """The unmodified reference headers compiled in place (oracle/_ref)."""
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        L = C.CDLL(path)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_make_grid.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, _i64p,
+                                    _u64p, _i64p]
+        L.ref_map_outcomes.argtypes = [C.c_int, C.c_int, C.c_int64, _i64p, C.c_uint64]
+        L.ref_map_one.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, _i64p]
+        L.ref_launch_map.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                                     C.c_uint64, C.c_uint64, _u64p]
+        L.ref_launch_accum.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                       _u32p, C.c_uint64, _u64p, _u64p, C.POINTER(C.c_double)]
+        L.ref_make_life_state.argtypes = [C.c_int, C.c_int64, C.c_uint64, _u8p, C.c_uint64]
+        L.ref_kernel_ca_run.argtypes = [C.c_int, C.c_int64, C.c_int64, _u8p, C.c_uint64,
+                                        C.POINTER(C.c_double)]
+        L.ref_launch_ca.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                    _u8p, C.c_uint64, _u64p, _u64p, C.POINTER(C.c_double)]
+        L.ref_state_hash.argtypes = [C.c_int, C.c_int64, C.c_void_p, C.c_uint64]
+        L.ref_state_hash.restype = C.c_uint64
+        L.ref_verify_exact_cover.argtypes = [C.c_int, C.c_int64, _u32p, C.c_uint64,
+                                             C.POINTER(C.c_int), _i64p, _u64p]
+        self.L = L
+
+    def _ok(self, rc: int, what: str) -> None:
+        if rc != 0:
+            raise OracleError(f"{what}: status {rc}: {self.L.ref_last_error().decode()}")
+
+    def make_grid(self, kind: int, m: int, n: int, rho: int = 1, T: int = 1):
+        e = np.zeros(3, np.int64)
+        b = np.zeros(1, np.uint64)
+        ds = np.zeros(1, np.int64)
+        self._ok(self.L.ref_make_grid(kind, m, n, rho, T, e, b, ds), "make_grid")
+        return tuple(int(v) for v in e), int(b[0]), int(ds[0])
+
+    def map_outcomes(self, kind: int, m: int, n: int) -> np.ndarray:
+        (ex, ey, ez), blocks, _ = self.make_grid(kind, m, n)
+        out = np.zeros((blocks, 6), np.int64)
+        self._ok(self.L.ref_map_outcomes(kind, m, n, out, blocks), "map_outcomes")
+        return out
+
+    def map_one(self, kind: int, m: int, n: int, x: int, y: int, z: int = 0):
+        o = np.zeros(6, np.int64)
+        rc = self.L.ref_map_one(kind, m, n, x, y, z, o)
+        if rc == 1:
+            raise ValueError(self.L.ref_last_error().decode())
+        self._ok(rc, "map_one")
+        return tuple(int(v) for v in o)
+
+    def launch_map(self, kind: int, m: int, n: int, rho: int = 1, T: int = 1,
+                   coverage: bool = True, salt: int = 0):
+        _, _, ds = self.make_grid(kind, m, n, rho, T)
+        side = ds * rho
+        cov = np.zeros(cells_of(m, side), np.uint32) if coverage else None
+        cnt = np.zeros(6, np.uint64)
+        self._ok(self.L.ref_launch_map(kind, m, n, rho, T,
+                                       cov.ctypes.data if cov is not None else None,
+                                       cells_of(m, side), salt, cnt), "launch_map")
+        return cov, [int(v) for v in cnt]
+
+    def launch_accum(self, kind: int, m: int, n: int, rho: int, passes: int = 1,
+                     cells: np.ndarray | None = None, T: int = 1):
+        _, _, ds = self.make_grid(kind, m, n, rho, T)
+        side = ds * rho
+        if cells is None:
+            cells = np.zeros(cells_of(m, side), np.uint32)
+        cnt = np.zeros(6, np.uint64)
+        h = np.zeros(1, np.uint64)
+        secs = C.c_double(0.0)
+        self._ok(self.L.ref_launch_accum(kind, m, n, rho, T, passes, cells, cells.size, cnt, h,
+                                         C.byref(secs)), "launch_accum")
+        return cells, [int(v) for v in cnt], int(h[0]), secs.value
+
+    def make_life_state(self, m: int, side: int, seed: int) -> np.ndarray:
+        out = np.empty(cells_of(m, side), np.uint8)
+        self._ok(self.L.ref_make_life_state(m, side, seed, out, out.size), "make_life_state")
+        return out
+
+    def kernel_ca_run(self, m: int, side: int, steps: int, cells: np.ndarray):
+        secs = C.c_double(0.0)
+        self._ok(self.L.ref_kernel_ca_run(m, side, steps, cells, cells.size, C.byref(secs)),
+                 "kernel_ca_run")
+        return cells, secs.value
+
+    def launch_ca(self, kind: int, m: int, n: int, rho: int, steps: int, cells: np.ndarray,
+                  T: int = 1):
+        cnt = np.zeros(6, np.uint64)
+        h = np.zeros(1, np.uint64)
+        secs = C.c_double(0.0)
+        self._ok(self.L.ref_launch_ca(kind, m, n, rho, T, steps, cells, cells.size, cnt, h,
+                                      C.byref(secs)), "launch_ca")
+        return cells, [int(v) for v in cnt], int(h[0]), secs.value
+
+    def state_hash(self, m: int, side: int, arr: np.ndarray) -> int:
+        a = np.ascontiguousarray(arr)
+        return int(self.L.ref_state_hash(m, side, a.ctypes.data, a.nbytes))
+
+    def verify_exact_cover(self, m: int, side: int, cov: np.ndarray):
+        exact = C.c_int(0)
+        w = np.zeros(3, np.int64)
+        mult = np.zeros(1, np.uint64)
+        self._ok(self.L.ref_verify_exact_cover(m, side, cov, cov.size, C.byref(exact), w, mult),
+                 "verify_exact_cover")
+        return bool(exact.value), tuple(int(v) for v in w), int(mult[0])
+
+
+def reference_available() -> bool:
+    return os.path.exists(REF_SO)

@@ -1,0 +1,256 @@
+// TEST INFRASTRUCTURE ONLY — never linked into, loaded by, or called from the product.
+//
+// A thin extern "C" shim over the UNMODIFIED reference headers
+// (/root/reference/proj/include/simplexmap/*.hpp, included in place, never copied).
+// `oracle/Makefile` compiles this file with the reference's own Release flags
+// (CMakeLists.txt:9-12: -O3 -DNDEBUG -Wall -Wextra, C++20) into
+// oracle/_ref/libsmx_ref.so. Callers: tests/ (golden fixtures, parity), bench.py's
+// cpu_baseline leg and `bench.py --impl reference`.
+//
+// Every entry point returns 0 on success, 1 on std::invalid_argument, 2 on
+// std::overflow_error, 3 on any other exception; the message is kept in a
+// thread-local buffer read by ref_last_error().
+
+#include <simplexmap/report.hpp>
+#include <simplexmap/simulator.hpp>
+
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <string>
+
+using namespace simplexmap;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::overflow_error& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+map_kind kind_of(int k) {
+    switch (k) {
+        case 0: return map_kind::bb;
+        case 1: return map_kind::rb;
+        case 2: return map_kind::lambda2d;
+        case 3: return map_kind::h2d;
+        case 4: return map_kind::h2d_trapezoid;
+        case 5: return map_kind::h2d_padded;
+        case 6: return map_kind::h3d;
+    }
+    throw std::invalid_argument("ref harness: unknown map kind");
+}
+
+simplex_spec domain_of(const grid_spec& g) { return {g.dims, g.domain_side() * g.rho - 1}; }
+
+void put_counters(const sim_report& rep, uint64_t* c) {
+    if (!c) return;
+    c[0] = rep.blocks_launched;
+    c[1] = rep.blocks_void;
+    c[2] = rep.threads_launched;
+    c[3] = rep.threads_useful;
+    // space_overhead as an exact rational (num, den); the i128 values fit i64
+    // for every grid the tests use.
+    c[4] = uint64_t(int64_t(rep.space_overhead.num));
+    c[5] = uint64_t(int64_t(rep.space_overhead.den));
+}
+
+} // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// grid_spec via make_grid (report.hpp:48-66): extents[3], blocks, domain_side.
+int ref_make_grid(int kind, int m, int64_t n, int64_t rho, int64_t T, int64_t* ext3,
+                  uint64_t* blocks, int64_t* domain_side) {
+    return guarded([&] {
+        grid_spec g = make_grid(kind_of(kind), m, n, rho, T);
+        for (int i = 0; i < 3; ++i) ext3[i] = g.extents[std::size_t(i)];
+        *blocks = g.blocks();
+        *domain_side = g.domain_side();
+    });
+}
+
+// One map_outcome per block, natural z, y, x order (simulator.hpp:113-118):
+// 6 x int64 {is_void, x, y, z, level_b, index_q}.
+int ref_map_outcomes(int kind, int m, int64_t n, int64_t* out, uint64_t count) {
+    return guarded([&] {
+        grid_spec g = make_grid(kind_of(kind), m, n);
+        if (g.blocks() != count) throw std::invalid_argument("ref_map_outcomes: count mismatch");
+        uint64_t i = 0;
+        for (int64_t z = 0; z < g.extents[2]; ++z)
+            for (int64_t y = 0; y < g.extents[1]; ++y)
+                for (int64_t x = 0; x < g.extents[0]; ++x) {
+                    map_outcome o;
+                    block_coord w{x, y, z};
+                    if (g.kind == map_kind::h2d) o = map_h2d(w);
+                    else if (g.kind == map_kind::h3d) o = map_h3d(w, g.n);
+                    else if (g.kind == map_kind::bb) o = map_bb(w, g.n, g.dims);
+                    else throw std::invalid_argument("ref_map_outcomes: bb/h2d/h3d only");
+                    int64_t* r = out + 6 * i++;
+                    r[0] = o.is_void;
+                    r[1] = o.target.x;
+                    r[2] = o.target.y;
+                    r[3] = o.target.z;
+                    r[4] = o.level_b;
+                    r[5] = o.index_q;
+                }
+    });
+}
+
+// Single-block map probes (maps.hpp:107,200,302), for pinned points + error behaviour.
+int ref_map_one(int kind, int m, int64_t n, int64_t x, int64_t y, int64_t z, int64_t* out6) {
+    return guarded([&] {
+        block_coord w{x, y, z};
+        map_outcome o;
+        if (kind == 0) o = map_bb(w, n, m);
+        else if (kind == 3) o = map_h2d(w);
+        else if (kind == 6) o = map_h3d(w, n);
+        else throw std::invalid_argument("ref_map_one: bb/h2d/h3d only");
+        out6[0] = o.is_void;
+        out6[1] = o.target.x;
+        out6[2] = o.target.y;
+        out6[3] = o.target.z;
+        out6[4] = o.level_b;
+        out6[5] = o.index_q;
+    });
+}
+
+// launch_map (simulator.hpp:303-310). coverage may be null (record_coverage=false).
+// counters: 6 x u64 {blocks, void, threads, useful, overhead_num, overhead_den}.
+int ref_launch_map(int kind, int m, int64_t n, int64_t rho, int64_t T, uint32_t* coverage,
+                   uint64_t ncells, uint64_t salt, uint64_t* counters) {
+    return guarded([&] {
+        grid_spec g = make_grid(kind_of(kind), m, n, rho, T);
+        launch_opts o;
+        o.record_coverage = coverage != nullptr;
+        o.block_order_salt = salt;
+        sim_report rep = launch_map(g, domain_of(g), o);
+        if (coverage) {
+            if (rep.coverage.size() != ncells) throw std::invalid_argument("ncells mismatch");
+            std::memcpy(coverage, rep.coverage.data(), ncells * sizeof(uint32_t));
+        }
+        put_counters(rep, counters);
+    });
+}
+
+// launch_accum (simulator.hpp:313-327), `passes` times on the same state.
+int ref_launch_accum(int kind, int m, int64_t n, int64_t rho, int64_t T, int64_t passes,
+                     uint32_t* cells, uint64_t ncells, uint64_t* counters, uint64_t* hash,
+                     double* seconds) {
+    return guarded([&] {
+        grid_spec g = make_grid(kind_of(kind), m, n, rho, T);
+        simplex_spec dom = domain_of(g);
+        simplex_grid_state<u32> st(m, dom.n + 1);
+        if (st.cells.size() != ncells) throw std::invalid_argument("ncells mismatch");
+        std::memcpy(st.cells.data(), cells, ncells * sizeof(uint32_t));
+        launch_opts o;
+        o.record_coverage = false;
+        sim_report rep;
+        auto t0 = std::chrono::steady_clock::now();
+        for (int64_t p = 0; p < passes; ++p) rep = launch_accum(g, dom, st, o);
+        auto t1 = std::chrono::steady_clock::now();
+        if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+        std::memcpy(cells, st.cells.data(), ncells * sizeof(uint32_t));
+        put_counters(rep, counters);
+        if (hash) *hash = st.hash();
+    });
+}
+
+// make_life_state (simulator.hpp:390-398).
+int ref_make_life_state(int m, int64_t side, uint64_t seed, uint8_t* out, uint64_t ncells) {
+    return guarded([&] {
+        auto s = make_life_state(m, side, seed);
+        if (s.cells.size() != ncells) throw std::invalid_argument("ncells mismatch");
+        std::memcpy(out, s.cells.data(), ncells);
+    });
+}
+
+// kernel_ca_run (simulator.hpp:402-425), dead3d for m = 3, periodic2d for m = 2.
+int ref_kernel_ca_run(int m, int64_t side, int64_t steps, uint8_t* cells, uint64_t ncells,
+                      double* seconds) {
+    return guarded([&] {
+        simplex_grid_state<u8> s(m, side);
+        if (s.cells.size() != ncells) throw std::invalid_argument("ncells mismatch");
+        std::memcpy(s.cells.data(), cells, ncells);
+        auto t0 = std::chrono::steady_clock::now();
+        kernel_ca_run(s, steps, m == 3 ? ca_boundary::dead3d : ca_boundary::periodic2d);
+        auto t1 = std::chrono::steady_clock::now();
+        if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+        std::memcpy(cells, s.cells.data(), ncells);
+    });
+}
+
+// launch_ca (simulator.hpp:431-463) over a map-driven grid.
+int ref_launch_ca(int kind, int m, int64_t n, int64_t rho, int64_t T, int64_t steps,
+                  uint8_t* cells, uint64_t ncells, uint64_t* counters, uint64_t* hash,
+                  double* seconds) {
+    return guarded([&] {
+        grid_spec g = make_grid(kind_of(kind), m, n, rho, T);
+        simplex_spec dom = domain_of(g);
+        simplex_grid_state<u8> s(m, dom.n + 1);
+        if (s.cells.size() != ncells) throw std::invalid_argument("ncells mismatch");
+        std::memcpy(s.cells.data(), cells, ncells);
+        launch_opts o;
+        o.record_coverage = false;
+        o.steps = steps;
+        o.boundary = m == 3 ? ca_boundary::dead3d : ca_boundary::periodic2d;
+        auto t0 = std::chrono::steady_clock::now();
+        sim_report rep = launch_ca(g, dom, s, o);
+        auto t1 = std::chrono::steady_clock::now();
+        if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+        std::memcpy(cells, s.cells.data(), ncells);
+        put_counters(rep, counters);
+        if (hash) *hash = rep.state_hash;
+    });
+}
+
+// simplex_grid_state<T>::hash (simulator.hpp:68-73) over raw cell bytes.
+uint64_t ref_state_hash(int m, int64_t side, const void* bytes, uint64_t nbytes) {
+    u64 h = fnv1a_seed;
+    h = fnv1a_append_u64(h, u64(m));
+    h = fnv1a_append_u64(h, u64(side));
+    return fnv1a_append(h, bytes, nbytes);
+}
+
+// Cell counts (core.hpp:125-133).
+uint64_t ref_tri_cells(int64_t side) { return uint64_t(tri_cells(side)); }
+uint64_t ref_tet_cells(int64_t side) { return uint64_t(tet_cells(side)); }
+uint64_t ref_tet_linear_index(int64_t side, int64_t x, int64_t y, int64_t z) {
+    return tet_linear_index(side, x, y, z);
+}
+
+// verify_exact_cover (simulator.hpp:467-478) over a coverage array.
+int ref_verify_exact_cover(int m, int64_t cell_side, const uint32_t* coverage, uint64_t ncells,
+                           int* exact, int64_t* witness3, uint64_t* multiplicity) {
+    return guarded([&] {
+        sim_report rep;
+        rep.m = m;
+        rep.cell_side = cell_side;
+        rep.coverage.assign(coverage, coverage + ncells);
+        rep.coverage_recorded = true;
+        cover_verdict v = verify_exact_cover(rep, simplex_spec{m, cell_side - 1});
+        *exact = v.exact;
+        witness3[0] = v.witness.x;
+        witness3[1] = v.witness.y;
+        witness3[2] = v.witness.z;
+        *multiplicity = v.multiplicity;
+    });
+}
+
+} // extern "C"
