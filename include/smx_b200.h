@@ -1,0 +1,170 @@
+/*
+ * smx_b200.h — the C ABI of the B200-native H-map hot path.
+ *
+ * Plain C: no torch, no C++ types. Every entry point replaces one function of
+ * the reference's header-only C++ API (arXiv 2208.11617 reference `simplexmap`,
+ * /root/reference/proj/include/simplexmap/); the citation on each declaration
+ * names the reference interface (file:line) it stands in for. The C++ drop-in
+ * (include/simplexmap_b200.hpp) and the Python mirror
+ * (paper_2208_11617_b200/api.py) both call exactly these symbols.
+ *
+ * Conventions
+ *  - Return value: SMX_OK (0) or an error code; smx_last_error() returns the
+ *    thread-local message (the reference's exception text where one exists).
+ *    SMX_EINVAL <-> std::invalid_argument, SMX_ERANGE <-> std::overflow_error.
+ *  - `device_ptr` != 0: the buffer arguments are device pointers (cudaMalloc /
+ *    torch CUDA tensors) and the call only enqueues work on `stream`.
+ *    `device_ptr` == 0: host buffers; the call stages them through a cached
+ *    device pool, runs, copies results back and synchronises `stream`
+ *    (the reference's mutate-in-place semantics, simulator.hpp:313-326,431-463).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).
+ *  - Cell state is the reference's packed layout: 2-D row-major triangle
+ *    index y(y+1)/2 + x (core.hpp:136-138); 3-D layer prefix tet(S)-tet(S-z)
+ *    plus the triangle index (core.hpp:140-149). u32 cells for ACCUM, u8 for CA.
+ */
+#ifndef SMX_B200_H
+#define SMX_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMX_OK 0
+#define SMX_EINVAL 1 /* std::invalid_argument */
+#define SMX_ERANGE 2 /* std::overflow_error   */
+#define SMX_ECUDA 3  /* CUDA runtime error (message carries cudaGetErrorString) */
+#define SMX_ENOMEM 4
+
+/* map_kind (maps.hpp:19); only BB, H2D and H3D are on this hot path. */
+#define SMX_BB 0
+#define SMX_RB 1
+#define SMX_LAMBDA 2
+#define SMX_H2D 3
+#define SMX_TRAP 4
+#define SMX_PADDED 5
+#define SMX_H3D 6
+
+/* Execution schemes for the workload kernels.
+ * SMX_EXEC_BLOCK: one CUDA thread-block per map block, rho^m threads — the
+ *                 paper's launch model (the reference's detail::sweep one to one).
+ * SMX_EXEC_RUNS:  one CUDA thread-block per strip/patch of map blocks; the
+ *                 blocks are mapped lane-parallel, their tiles merged into
+ *                 contiguous x-runs and streamed with 128-bit accesses. */
+#define SMX_EXEC_AUTO (-1) /* RUNS where supported, else BLOCK */
+#define SMX_EXEC_BLOCK 0
+#define SMX_EXEC_RUNS 1
+
+/* grid_spec (maps.hpp:64-92) for the BB/H2D/H3D kinds. */
+typedef struct smx_grid {
+    int32_t kind;
+    int32_t dims;
+    int64_t n;   /* map parameter */
+    int64_t rho; /* block edge: rho^dims cells per block */
+    int64_t threshold;
+    int64_t extents[3];
+} smx_grid;
+
+/* sim_report counters (simulator.hpp:76-88). */
+typedef struct smx_counters {
+    uint64_t blocks_launched;
+    uint64_t blocks_void;
+    uint64_t threads_launched;
+    uint64_t threads_useful;
+} smx_counters;
+
+/* map_outcome (maps.hpp:40-47), 32 bytes. */
+typedef struct smx_outcome {
+    int32_t is_void;
+    int32_t x, y, z;
+    int32_t level_b;
+    int32_t index_q;
+    int32_t pad0, pad1;
+} smx_outcome;
+
+/* Thread-local message of the last failing call. */
+const char* smx_last_error(void);
+
+/* make_grid (report.hpp:48-66) -> grid_bb / grid_h2d / grid_h3d (maps.hpp:96-105,
+ * 188-198, 285-295). Same validity rules and messages. */
+int smx_make_grid(int32_t kind, int32_t m, int64_t n, int64_t rho, int64_t threshold,
+                  smx_grid* out);
+
+/* grid_spec::domain_side()*rho: the cell side S of a launch (simulator.hpp:257-264). */
+int64_t smx_cell_side(const smx_grid* g);
+
+/* tri_cells / tet_cells (core.hpp:130-133). */
+uint64_t smx_cell_count(int32_t m, int64_t side);
+
+/* map_bb / map_h2d / map_h3d for ONE block on the host (maps.hpp:107,200,302),
+ * same shared arithmetic the kernels inline (include/smx_maps.hpp), with the
+ * reference's range checks. out: the raw (strict-view) outcome. */
+int smx_map_one(int32_t kind, int32_t m, int64_t n, int64_t wx, int64_t wy, int64_t wz,
+                smx_outcome* out);
+
+/* map_h2d / map_h3d / map_bb over every block of the grid, natural z,y,x order
+ * (simulator.hpp:113-118) — the bit-exact coordinate check. */
+int smx_map_outcomes(const smx_grid* g, smx_outcome* out, uint64_t count, int device_ptr,
+                     void* stream);
+
+/* launch_map (simulator.hpp:303-310): coverage multiset (nullable) + counters
+ * (nullable). coverage must hold smx_cell_count(dims, S) u32 and is ACCUMULATED into. */
+int smx_launch_map(const smx_grid* g, uint32_t* coverage, uint64_t ncells, int device_ptr,
+                   smx_counters* counters, void* stream);
+
+/* The paper's MAP kernel for timing: map + thread expansion + membership +
+ * packed index per thread, reduced to a register checksum (no memory sink). */
+int smx_map_kernel(const smx_grid* g, void* stream);
+
+/* launch_accum (simulator.hpp:313-327), `passes` times: ++cells[idx] per useful
+ * thread. coverage (nullable) receives the first pass's visit counts. */
+int smx_accum(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passes, int32_t exec,
+              int device_ptr, uint32_t* coverage, smx_counters* counters, void* stream);
+
+/* make_life_state (simulator.hpp:390-398) for m = 3 (and m = 2): writes
+ * smx_cell_count(m, side) bytes. */
+int smx_life_init(int32_t m, int64_t side, uint64_t seed, uint8_t* cells, uint64_t ncells,
+                  int device_ptr, void* stream);
+
+/* One dead-boundary 3-D Life step through the map (the body of launch_ca's step
+ * loop, simulator.hpp:440-459, with alive_neighbors_3d_dead :242-253 and
+ * life_next :220-223). Device pointers only; cur and next must not alias. */
+int smx_ca_step(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint64_t ncells,
+                int32_t exec, void* stream);
+
+/* launch_ca (simulator.hpp:431-463) for m = 3: `steps` steps in place.
+ * scratch: optional device buffer of ncells bytes (device_ptr mode); NULL =
+ * library-managed. coverage/counters as for smx_accum (first step). */
+int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, int32_t exec,
+           int device_ptr, uint8_t* scratch, uint32_t* coverage, smx_counters* counters,
+           void* stream);
+
+/* simplex_grid_state::hash (simulator.hpp:68-73): FNV-1a-64 over u64 m,
+ * u64 side, then the raw cell bytes. Host bytes. */
+uint64_t smx_state_hash(int32_t m, int64_t side, const void* bytes, uint64_t nbytes);
+
+/* ---- multi-GPU shard support (H block-space partitioner) ----
+ * One Life step restricted to H-grid blocks with wz in [wz_lo, wz_hi) (a
+ * contiguous sub-box of whole sub-orthotope levels). Device pointers. */
+int smx_ca_step_range(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint64_t ncells,
+                      int64_t wz_lo, int64_t wz_hi, int32_t exec, void* stream);
+
+/* Gather / scatter whole tiles for the halo exchange. `tiles` is a DEVICE array
+ * of int32 tile coordinates (X, Y, Z) in the with-diagonal tile view; tile k
+ * occupies bytes [k*rho^3, (k+1)*rho^3) of the buffer in lz, ly, lx order;
+ * cells outside the tetrahedron pack as 0 and are skipped on unpack. */
+uint64_t smx_tile_bytes(const smx_grid* g, uint64_t ntiles);
+int smx_tiles_pack(const smx_grid* g, const uint8_t* cells, const int32_t* tiles, uint64_t ntiles,
+                   uint8_t* out, void* stream);
+int smx_tiles_unpack(const smx_grid* g, uint8_t* cells, const int32_t* tiles, uint64_t ntiles,
+                     const uint8_t* in, void* stream);
+
+/* cudaDeviceSynchronize on the current device. */
+int smx_device_sync(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SMX_B200_H */

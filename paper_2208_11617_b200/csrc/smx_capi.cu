@@ -1,0 +1,533 @@
+// The C ABI (include/smx_b200.h): argument validation with the reference's
+// contract messages, host<->device staging for host-buffer calls, the per-side
+// layer-prefix tables, and dispatch to the sm_100a kernels.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "smx_b200.h"
+#include "smx_common.cuh"
+#include "smx_launch.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+const char* kind_name(int k) {
+    switch (k) {
+        case SMX_BB: return "bb";
+        case SMX_RB: return "rb";
+        case SMX_LAMBDA: return "lambda";
+        case SMX_H2D: return "h2d";
+        case SMX_TRAP: return "trapezoid";
+        case SMX_PADDED: return "h2d-padded";
+        case SMX_H3D: return "h3d";
+    }
+    return "?";
+}
+
+// map_supports_m / valid_pairs_text (report.hpp:28-46)
+bool supports_m(int k, int m) {
+    if (k == SMX_BB) return m == 2 || m == 3;
+    if (k == SMX_H3D) return m == 3;
+    return m == 2;
+}
+std::string valid_pairs() {
+    return "bb (m=2,3), rb (m=2), lambda (m=2), h2d (m=2), trapezoid (m=2), h2d-padded (m=2), h3d (m=3)";
+}
+
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// Device-side resources, per device: layer-prefix tables keyed by side, a
+// grow-only staging pool for host-buffer calls, counters and the MAP sink.
+struct DeviceRes {
+    std::map<int64_t, unsigned long long*> prefix;
+    void* pool[3] = {nullptr, nullptr, nullptr};
+    size_t pool_bytes[3] = {0, 0, 0};
+    smx::DevCounters* counters = nullptr;
+    unsigned* sink = nullptr;
+};
+std::mutex g_mu;
+std::map<int, DeviceRes> g_res;
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(SMX_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define TRY(expr)                                          \
+    do {                                                   \
+        cudaError_t _e = (expr);                           \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+    } while (0)
+
+int device_res(DeviceRes** out) {
+    int dev = 0;
+    TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    *out = &g_res[dev];
+    return SMX_OK;
+}
+
+int get_prefix(int64_t side, const unsigned long long** out) {
+    DeviceRes* r;
+    if (int rc = device_res(&r)) return rc;
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = r->prefix.find(side);
+    if (it != r->prefix.end()) {
+        *out = it->second;
+        return SMX_OK;
+    }
+    std::vector<unsigned long long> h(size_t(side) + 2);
+    for (int64_t z = 0; z < side + 2; ++z) h[size_t(z)] = smx::tet_layer_prefix(side, z);
+    unsigned long long* d = nullptr;
+    TRY(cudaMalloc(&d, h.size() * sizeof(unsigned long long)));
+    TRY(cudaMemcpy(d, h.data(), h.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    r->prefix[side] = d;
+    *out = d;
+    return SMX_OK;
+}
+
+int pool_get(int slot, size_t bytes, void** out) {
+    DeviceRes* r;
+    if (int rc = device_res(&r)) return rc;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (r->pool_bytes[slot] < bytes) {
+        if (r->pool[slot]) TRY(cudaFree(r->pool[slot]));
+        r->pool[slot] = nullptr;
+        r->pool_bytes[slot] = 0;
+        TRY(cudaMalloc(&r->pool[slot], bytes));
+        r->pool_bytes[slot] = bytes;
+    }
+    *out = r->pool[slot];
+    return SMX_OK;
+}
+
+int counters_buf(smx::DevCounters** out) {
+    DeviceRes* r;
+    if (int rc = device_res(&r)) return rc;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!r->counters) TRY(cudaMalloc(&r->counters, sizeof(smx::DevCounters)));
+    if (!r->sink) TRY(cudaMalloc(&r->sink, 64));
+    *out = r->counters;
+    return SMX_OK;
+}
+
+int sink_buf(unsigned** out) {
+    smx::DevCounters* c;
+    if (int rc = counters_buf(&c)) return rc;
+    DeviceRes* r;
+    if (int rc = device_res(&r)) return rc;
+    *out = r->sink;
+    return SMX_OK;
+}
+
+int64_t cell_side_of(const smx_grid* g) {
+    const int64_t ds = g->kind == SMX_BB ? g->n : g->n - 1;
+    return ds * g->rho;
+}
+
+// Kernel-facing geometry; every coordinate must fit int32 and every CUDA grid
+// dimension the block scheme uses must fit the launch limits.
+int make_geom(const smx_grid* g, smx::Geom* out, bool need_prefix) {
+    if (!g) return fail(SMX_EINVAL, "null grid");
+    if (g->kind != SMX_BB && g->kind != SMX_H2D && g->kind != SMX_H3D)
+        return fail(SMX_EINVAL, std::string("map ") + kind_name(g->kind) +
+                                    " is outside the B200 hot path (bb, h2d, h3d)");
+    if (g->rho < 1) return fail(SMX_EINVAL, "launch: rho must be >= 1");
+    const int64_t side = cell_side_of(g);
+    if (side >= (int64_t(1) << 30) || g->extents[0] > 0x7fffffff || g->extents[1] > 65535 ||
+        g->extents[2] > 65535 || g->rho > 1024)
+        return fail(SMX_ERANGE, "grid exceeds the device launch limits (extents.y,z <= 65535, side < 2^30)");
+    smx::Geom k{};
+    k.kind = g->kind;
+    k.dims = g->dims;
+    k.n = int(g->n);
+    k.rho = int(g->rho);
+    k.ex = int(g->extents[0]);
+    k.ey = int(g->extents[1]);
+    k.ez = int(g->extents[2]);
+    k.strict = g->kind != SMX_BB;
+    k.side = int(side);
+    k.prefix = nullptr;
+    if (need_prefix && g->dims == 3) {
+        if (int rc = get_prefix(side, &k.prefix)) return rc;
+    }
+    *out = k;
+    return SMX_OK;
+}
+
+uint64_t cells_of(int m, int64_t side) { return m == 2 ? smx::tri_cells(side) : smx::tet_cells(side); }
+
+int check_cells(const smx_grid* g, uint64_t ncells) {
+    if (ncells != cells_of(g->dims, cell_side_of(g)))
+        return fail(SMX_EINVAL, "launch: state does not match the domain");
+    return SMX_OK;
+}
+
+int fill_counters(const smx_grid* g, const smx::Geom& k, smx_counters* c, cudaStream_t s,
+                  uint32_t* dev_cov) {
+    smx::DevCounters* dc = nullptr;
+    if (c) {
+        if (int rc = counters_buf(&dc)) return rc;
+        TRY(cudaMemsetAsync(dc, 0, sizeof(smx::DevCounters), s));
+    }
+    smx::launch_map_block(k, dev_cov, dc, nullptr, s);
+    TRY(cudaGetLastError());
+    if (c) {
+        smx::DevCounters h;
+        TRY(cudaMemcpyAsync(&h, dc, sizeof h, cudaMemcpyDeviceToHost, s));
+        TRY(cudaStreamSynchronize(s));
+        uint64_t v = 0, u = 0;
+        for (int i = 0; i < smx::NSLOT; ++i) {
+            v += h.blocks_void[i];
+            u += h.threads_useful[i];
+        }
+        const uint64_t blocks = uint64_t(g->extents[0]) * uint64_t(g->extents[1]) * uint64_t(g->extents[2]);
+        uint64_t tpb = uint64_t(g->rho) * uint64_t(g->rho);
+        if (g->dims == 3) tpb *= uint64_t(g->rho);
+        c->blocks_launched = blocks;
+        c->blocks_void = v;
+        c->threads_launched = blocks * tpb;
+        c->threads_useful = u;
+    }
+    return SMX_OK;
+}
+
+int resolve_exec(int exec, const smx_grid* g) {
+    if (exec == SMX_EXEC_BLOCK || exec == SMX_EXEC_RUNS) return exec;
+    return -1;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* smx_last_error(void) { return g_err.c_str(); }
+
+int smx_make_grid(int32_t kind, int32_t m, int64_t n, int64_t rho, int64_t threshold, smx_grid* out) {
+    if (!out) return fail(SMX_EINVAL, "null output");
+    if (kind < SMX_BB || kind > SMX_H3D) return fail(SMX_EINVAL, "unknown map kind");
+    if (!supports_m(kind, m))
+        return fail(SMX_EINVAL, std::string("map ") + kind_name(kind) + " does not support m=" +
+                                    std::to_string(m) + "; valid: " + valid_pairs());
+    if (rho < 1) return fail(SMX_EINVAL, "rho must be >= 1");
+    smx_grid g{};
+    g.kind = kind;
+    g.dims = m;
+    g.n = n;
+    g.rho = rho;
+    g.threshold = threshold;
+    switch (kind) {
+        case SMX_BB:
+            if (n < 1) return fail(SMX_EINVAL, "grid_bb: n must be >= 1");
+            g.extents[0] = n;
+            g.extents[1] = n;
+            g.extents[2] = m == 3 ? n : 1;
+            break;
+        case SMX_H2D:
+            if (n < 2 || !is_pow2(n))
+                return fail(SMX_EINVAL,
+                            "grid_h2d: n must be a power of two >= 2; use decompose_trapezoids or "
+                            "grid_h2d_padded for general n");
+            g.extents[0] = n / 2;
+            g.extents[1] = n - 1;
+            g.extents[2] = 1;
+            break;
+        case SMX_H3D:
+            if (n < 4 || !is_pow2(n))
+                return fail(SMX_EINVAL,
+                            "grid_h3d: n must be a power of two >= 4 (general-n 3D decomposition is "
+                            "unsupported)");
+            g.extents[0] = n / 2;
+            g.extents[1] = n / 2;
+            g.extents[2] = (3 * (n - 1) + 3) / 4;
+            break;
+        default:
+            return fail(SMX_EINVAL, std::string("map ") + kind_name(kind) +
+                                        " is outside the B200 hot path (bb, h2d, h3d)");
+    }
+    *out = g;
+    return SMX_OK;
+}
+
+int64_t smx_cell_side(const smx_grid* g) { return g ? cell_side_of(g) : -1; }
+
+uint64_t smx_cell_count(int32_t m, int64_t side) {
+    if ((m != 2 && m != 3) || side < 1) return 0;
+    return cells_of(m, side);
+}
+
+int smx_map_one(int32_t kind, int32_t m, int64_t n, int64_t wx, int64_t wy, int64_t wz, smx_outcome* out) {
+    if (!out) return fail(SMX_EINVAL, "null output");
+    smx::outcome<int64_t> o;
+    if (kind == SMX_BB) {
+        if (m != 2 && m != 3) return fail(SMX_EINVAL, "map_bb: m must be 2 or 3");
+        const bool in = wx >= 0 && wx < n && wy >= 0 && wy < n && (m == 2 ? wz == 0 : (wz >= 0 && wz < n));
+        if (!in) return fail(SMX_EINVAL, "map_bb: omega outside the n^m grid");
+        o = smx::map_bb<int64_t>(wx, wy, wz, n, m);
+    } else if (kind == SMX_H2D) {
+        if (wx < 0 || wy < 0) return fail(SMX_EINVAL, "map_h2d: omega components must be >= 0");
+        if (wx >= (int64_t(1) << 31) || wy >= (int64_t(1) << 31))
+            return fail(SMX_ERANGE, "map_h2d: omega beyond the 2^31 block range of this build");
+        o = smx::map_h2d<int64_t>(wx, wy);
+    } else if (kind == SMX_H3D) {
+        if (n < 4 || !is_pow2(n)) return fail(SMX_EINVAL, "map_h3d: n must be a power of two >= 4");
+        if (wx < 0 || wx >= n / 2 || wy < 0 || wy >= n / 2 || wz < 0 || wz >= (3 * (n - 1) + 3) / 4)
+            return fail(SMX_EINVAL, "map_h3d: omega outside the grid");
+        o = smx::map_h3d<int64_t>(wx, wy, wz, n);
+    } else {
+        return fail(SMX_EINVAL, std::string("map ") + kind_name(kind) + " is outside the B200 hot path (bb, h2d, h3d)");
+    }
+    *out = smx_outcome{int32_t(o.is_void), int32_t(o.x), int32_t(o.y), int32_t(o.z),
+                       int32_t(o.level_b), int32_t(o.index_q), 0, 0};
+    return SMX_OK;
+}
+
+int smx_map_outcomes(const smx_grid* g, smx_outcome* out, uint64_t count, int device_ptr, void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, false)) return rc;
+    const uint64_t blocks = uint64_t(g->extents[0]) * uint64_t(g->extents[1]) * uint64_t(g->extents[2]);
+    if (count != blocks) return fail(SMX_EINVAL, "map_outcomes: count != grid blocks");
+    cudaStream_t s = (cudaStream_t)stream;
+    smx_outcome* d = out;
+    if (!device_ptr) {
+        void* p;
+        if (int rc = pool_get(0, blocks * sizeof(smx_outcome), &p)) return rc;
+        d = (smx_outcome*)p;
+    }
+    smx::launch_outcomes(k, d, blocks, s);
+    TRY(cudaGetLastError());
+    if (!device_ptr) {
+        TRY(cudaMemcpyAsync(out, d, blocks * sizeof(smx_outcome), cudaMemcpyDeviceToHost, s));
+        TRY(cudaStreamSynchronize(s));
+    }
+    return SMX_OK;
+}
+
+int smx_launch_map(const smx_grid* g, uint32_t* coverage, uint64_t ncells, int device_ptr,
+                   smx_counters* counters, void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t* dcov = coverage;
+    if (coverage) {
+        if (int rc = check_cells(g, ncells)) return rc;
+        if (!device_ptr) {
+            void* p;
+            if (int rc = pool_get(0, ncells * 4, &p)) return rc;
+            dcov = (uint32_t*)p;
+            TRY(cudaMemcpyAsync(dcov, coverage, ncells * 4, cudaMemcpyHostToDevice, s));
+        }
+    }
+    if (int rc = fill_counters(g, k, counters, s, dcov)) return rc;
+    if (coverage && !device_ptr) {
+        TRY(cudaMemcpyAsync(coverage, dcov, ncells * 4, cudaMemcpyDeviceToHost, s));
+        TRY(cudaStreamSynchronize(s));
+    }
+    return SMX_OK;
+}
+
+int smx_map_kernel(const smx_grid* g, void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    unsigned* sink;
+    if (int rc = sink_buf(&sink)) return rc;
+    smx::launch_map_block(k, nullptr, nullptr, sink, (cudaStream_t)stream);
+    TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
+int smx_accum(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passes, int32_t exec,
+              int device_ptr, uint32_t* coverage, smx_counters* counters, void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    if (g->dims != 2) return fail(SMX_EINVAL, "accum: the B200 ACCUM path is the 2-simplex kernel");
+    if (int rc = check_cells(g, ncells)) return rc;
+    if (passes < 0) return fail(SMX_EINVAL, "accum: passes must be >= 0");
+    if (exec < 0) exec = SMX_EXEC_RUNS;
+    if (resolve_exec(exec, g) < 0) return fail(SMX_EINVAL, "accum: unknown exec scheme");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t* d = cells;
+    uint32_t* dcov = coverage;
+    if (!device_ptr) {
+        void* p;
+        if (int rc = pool_get(1, ncells * 4, &p)) return rc;
+        d = (uint32_t*)p;
+        TRY(cudaMemcpyAsync(d, cells, ncells * 4, cudaMemcpyHostToDevice, s));
+        if (coverage) {
+            if (int rc = pool_get(0, ncells * 4, &p)) return rc;
+            dcov = (uint32_t*)p;
+            TRY(cudaMemcpyAsync(dcov, coverage, ncells * 4, cudaMemcpyHostToDevice, s));
+        }
+    }
+    if (coverage || counters)
+        if (int rc = fill_counters(g, k, counters, s, dcov)) return rc;
+    for (int64_t p = 0; p < passes; ++p) smx::launch_accum(k, d, exec, s);
+    TRY(cudaGetLastError());
+    if (!device_ptr) {
+        TRY(cudaMemcpyAsync(cells, d, ncells * 4, cudaMemcpyDeviceToHost, s));
+        if (coverage) TRY(cudaMemcpyAsync(coverage, dcov, ncells * 4, cudaMemcpyDeviceToHost, s));
+        TRY(cudaStreamSynchronize(s));
+    }
+    return SMX_OK;
+}
+
+int smx_life_init(int32_t m, int64_t side, uint64_t seed, uint8_t* cells, uint64_t ncells, int device_ptr,
+                  void* stream) {
+    if (m != 2 && m != 3) return fail(SMX_EINVAL, "simplex_grid_state: m must be 2 or 3");
+    if (side < 1) return fail(SMX_EINVAL, "simplex_grid_state: side must be >= 1");
+    if (ncells != cells_of(m, side)) return fail(SMX_EINVAL, "life_init: ncells does not match the side");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* d = cells;
+    if (!device_ptr) {
+        void* p;
+        if (int rc = pool_get(1, ncells, &p)) return rc;
+        d = (uint8_t*)p;
+    }
+    smx::launch_life_init(seed, d, ncells, s);
+    TRY(cudaGetLastError());
+    if (!device_ptr) {
+        TRY(cudaMemcpyAsync(cells, d, ncells, cudaMemcpyDeviceToHost, s));
+        TRY(cudaStreamSynchronize(s));
+    }
+    return SMX_OK;
+}
+
+static int ca_validate(const smx_grid* g, uint64_t ncells, int32_t* exec) {
+    if (g->dims != 3)
+        return fail(SMX_EINVAL, "launch_ca: the B200 CA path is the dead-boundary 3-simplex kernel");
+    if (int rc = check_cells(g, ncells)) return rc;
+    if (*exec < 0) *exec = smx::ca_runs_supported(int(g->rho)) ? SMX_EXEC_RUNS : SMX_EXEC_BLOCK;
+    if (*exec != SMX_EXEC_BLOCK && *exec != SMX_EXEC_RUNS) return fail(SMX_EINVAL, "ca: unknown exec scheme");
+    if (*exec == SMX_EXEC_RUNS && !smx::ca_runs_supported(int(g->rho)))
+        return fail(SMX_EINVAL, "ca: the x-run scheme supports rho in {4, 8}; use SMX_EXEC_BLOCK");
+    return SMX_OK;
+}
+
+int smx_ca_step(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint64_t ncells, int32_t exec,
+                void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    if (int rc = ca_validate(g, ncells, &exec)) return rc;
+    if (cur == next) return fail(SMX_EINVAL, "ca_step: cur and next must not alias");
+    smx::launch_ca(k, 0, k.ez, cur, next, exec, (cudaStream_t)stream);
+    TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
+int smx_ca_step_range(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint64_t ncells, int64_t wz_lo,
+                      int64_t wz_hi, int32_t exec, void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    if (int rc = ca_validate(g, ncells, &exec)) return rc;
+    if (wz_lo < 0 || wz_hi > g->extents[2] || wz_lo > wz_hi)
+        return fail(SMX_EINVAL, "ca_step_range: wz range outside the grid");
+    smx::launch_ca(k, int(wz_lo), int(wz_hi), cur, next, exec, (cudaStream_t)stream);
+    TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
+int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, int32_t exec, int device_ptr,
+           uint8_t* scratch, uint32_t* coverage, smx_counters* counters, void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    if (int rc = ca_validate(g, ncells, &exec)) return rc;
+    if (steps < 0) return fail(SMX_EINVAL, "launch_ca: steps must be >= 0");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* a = cells;
+    uint8_t* b = scratch;
+    uint32_t* dcov = coverage;
+    void* p;
+    if (!device_ptr) {
+        if (int rc = pool_get(1, ncells, &p)) return rc;
+        a = (uint8_t*)p;
+        TRY(cudaMemcpyAsync(a, cells, ncells, cudaMemcpyHostToDevice, s));
+        if (coverage) {
+            if (int rc = pool_get(0, ncells * 4, &p)) return rc;
+            dcov = (uint32_t*)p;
+            TRY(cudaMemcpyAsync(dcov, coverage, ncells * 4, cudaMemcpyHostToDevice, s));
+        }
+    }
+    if (!b) {
+        if (int rc = pool_get(2, ncells, &p)) return rc;
+        b = (uint8_t*)p;
+    }
+    if ((coverage || counters) && steps > 0)
+        if (int rc = fill_counters(g, k, counters, s, dcov)) return rc;
+    uint8_t* cur = a;
+    uint8_t* nxt = b;
+    for (int64_t st = 0; st < steps; ++st) {
+        smx::launch_ca(k, 0, k.ez, cur, nxt, exec, s);
+        std::swap(cur, nxt);
+    }
+    TRY(cudaGetLastError());
+    if (device_ptr) {
+        if (cur != cells) TRY(cudaMemcpyAsync(cells, cur, ncells, cudaMemcpyDeviceToDevice, s));
+    } else {
+        TRY(cudaMemcpyAsync(cells, cur, ncells, cudaMemcpyDeviceToHost, s));
+        if (coverage) TRY(cudaMemcpyAsync(coverage, dcov, ncells * 4, cudaMemcpyDeviceToHost, s));
+        TRY(cudaStreamSynchronize(s));
+    }
+    return SMX_OK;
+}
+
+uint64_t smx_state_hash(int32_t m, int64_t side, const void* bytes, uint64_t nbytes) {
+    uint64_t h = 0xcbf29ce484222325ull;
+    auto mix_u64 = [&h](uint64_t v) {
+        for (int i = 0; i < 8; ++i) {
+            h ^= (v >> (8 * i)) & 0xffu;
+            h *= 0x100000001b3ull;
+        }
+    };
+    mix_u64(uint64_t(m));
+    mix_u64(uint64_t(side));
+    const unsigned char* p = (const unsigned char*)bytes;
+    for (uint64_t i = 0; i < nbytes; ++i) {
+        h ^= p[i];
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+
+uint64_t smx_tile_bytes(const smx_grid* g, uint64_t ntiles) {
+    uint64_t r3 = uint64_t(g->rho) * uint64_t(g->rho) * uint64_t(g->rho);
+    return r3 * ntiles;
+}
+
+int smx_tiles_pack(const smx_grid* g, const uint8_t* cells, const int32_t* tiles, uint64_t ntiles, uint8_t* out,
+                   void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    if (g->dims != 3) return fail(SMX_EINVAL, "tiles_pack: 3-simplex only");
+    smx::launch_tiles_pack(k, cells, tiles, ntiles, out, (cudaStream_t)stream);
+    TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
+int smx_tiles_unpack(const smx_grid* g, uint8_t* cells, const int32_t* tiles, uint64_t ntiles, const uint8_t* in,
+                     void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    if (g->dims != 3) return fail(SMX_EINVAL, "tiles_unpack: 3-simplex only");
+    smx::launch_tiles_unpack(k, cells, tiles, ntiles, in, (cudaStream_t)stream);
+    TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
+int smx_device_sync(void) {
+    TRY(cudaDeviceSynchronize());
+    return SMX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,437 @@
+// sm_100a kernels for the H-map hot path: block-outcome dump, the paper's MAP
+// kernel, ACCUM (block and x-run schemes), Life init, 3-D Life (block scheme)
+// and the tile pack/unpack used by the multi-GPU halo exchange.
+//
+// Reference semantics: detail::sweep (simulator.hpp:177-218) — map -> Void ->
+// strict y-1 -> rho^m cells -> membership -> packed index -> body.
+#include "smx_common.cuh"
+#include "smx_launch.hpp"
+
+namespace smx {
+
+#define FULL_MASK 0xffffffffu
+
+// ---------------------------------------------------------------------------
+// Block outcome dump: one thread per block, raw map_outcome (no strict shift),
+// natural z, y, x order (simulator.hpp:113-118).
+template <int KIND>
+__global__ void k_outcomes(Geom g, smx_outcome* out, unsigned long long count) {
+    const unsigned long long exy = (unsigned long long)g.ex * (unsigned long long)g.ey;
+    for (unsigned long long b = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; b < count;
+         b += (unsigned long long)gridDim.x * blockDim.x) {
+        const int wz = int(b / exy);
+        const unsigned long long r = b - (unsigned long long)wz * exy;
+        const int wy = int(r / (unsigned long long)g.ex);
+        const int wx = int(r - (unsigned long long)wy * g.ex);
+        outcome<int> o;
+        if (KIND == SMX_H2D) o = map_h2d<int>(wx, wy);
+        else if (KIND == SMX_H3D) o = map_h3d<int>(wx, wy, wz, g.n);
+        else o = map_bb<int>(wx, wy, wz, g.n, g.dims);
+        int4* dst = reinterpret_cast<int4*>(out + b);
+        dst[0] = make_int4(o.is_void, o.x, o.y, o.z);
+        dst[1] = make_int4(o.level_b, o.index_q, 0, 0);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Block scheme helpers. CTA = one map block; blockDim = (min(rho,1024),
+// min(rho, 1024/bx), ...) and threads loop over the remaining local extent.
+// The map is evaluated once per warp (lane 0) and broadcast with shuffles.
+struct BlockTarget {
+    int is_void, x, y, z;
+};
+
+template <int KIND>
+__device__ __forceinline__ BlockTarget warp_map(const Geom& g, int wx, int wy, int wz) {
+    const unsigned m = __activemask();
+    const int lane = (threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z)) & 31;
+    outcome<int> o{0, 0, 0, 0, 1, 0};
+    const int leader = __ffs(m) - 1;
+    if (lane == leader) o = map_block<KIND>(g, wx, wy, wz);
+    BlockTarget t;
+    t.is_void = __shfl_sync(m, o.is_void, leader);
+    t.x = __shfl_sync(m, o.x, leader);
+    t.y = __shfl_sync(m, o.y, leader);
+    t.z = __shfl_sync(m, o.z, leader);
+    return t;
+}
+
+__device__ __forceinline__ int flat_tid() {
+    return threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+}
+
+// MODE bit 0: coverage atomics; bit 1: counters; MODE 0: checksum sink only
+// (the paper's MAP kernel for timing).
+template <int KIND, int MODE>
+__global__ void k_map_block(Geom g, int wz0, uint32_t* __restrict__ cov, DevCounters* cnt,
+                            unsigned* sink) {
+    const int wx = blockIdx.x, wy = blockIdx.y, wz = blockIdx.z + wz0;
+    const BlockTarget t = warp_map<KIND>(g, wx, wy, wz);
+    const int slot = (wx + 7 * wy + 13 * wz) & (NSLOT - 1);
+    if (t.is_void) {
+        if ((MODE & 2) && flat_tid() == 0) atomicAdd(&cnt->blocks_void[slot], 1ull);
+        return;
+    }
+    const int rho = g.rho, S = g.side;
+    const int zext = g.dims == 3 ? rho : 1;
+    unsigned acc = 0;
+    unsigned useful = 0;
+    for (int lz = threadIdx.z; lz < zext; lz += blockDim.z)
+        for (int ly = threadIdx.y; ly < rho; ly += blockDim.y)
+            for (int lx = threadIdx.x; lx < rho; lx += blockDim.x) {
+                const int cx = t.x * rho + lx, cy = t.y * rho + ly, cz = t.z * rho + lz;
+                const bool member = g.dims == 3 ? tet_contains<int>(S, cx, cy, cz)
+                                                : tri_contains<int>(S, cx, cy);
+                if (!member) continue;
+                unsigned long long idx = tri_idx(cx, cy);
+                if (g.dims == 3) idx += g.prefix[cz];
+                ++useful;
+                acc ^= unsigned(idx) * 0x9E3779B1u;
+                if (MODE & 1) atomicAdd(&cov[idx], 1u);
+            }
+    if (MODE & 2) {
+        const unsigned m = __activemask();
+        unsigned s = __reduce_add_sync(m, useful);
+        if ((flat_tid() & 31) == __ffs(m) - 1) atomicAdd(&cnt->threads_useful[slot], (unsigned long long)s);
+    }
+    if (MODE == 0 && acc == 0x5bd1e995u) sink[0] = acc;  // keeps the map live, never true in practice
+}
+
+// ---------------------------------------------------------------------------
+// ACCUM, block scheme (the paper's launch model): ++cells[idx] per useful thread.
+template <int KIND>
+__global__ void k_accum_block(Geom g, uint32_t* __restrict__ cells) {
+    const int wx = blockIdx.x, wy = blockIdx.y;
+    const BlockTarget t = warp_map<KIND>(g, wx, wy, 0);
+    if (t.is_void) return;
+    const int rho = g.rho, S = g.side;
+    for (int ly = threadIdx.y; ly < rho; ly += blockDim.y)
+        for (int lx = threadIdx.x; lx < rho; lx += blockDim.x) {
+            const int cx = t.x * rho + lx, cy = t.y * rho + ly;
+            if (!tri_contains<int>(S, cx, cy)) continue;
+            cells[tri_idx(cx, cy)] += 1u;
+        }
+}
+
+// ---------------------------------------------------------------------------
+// ACCUM, x-run scheme. CTA (256 threads) = KX consecutive map blocks of one
+// grid row. Warp 0 maps them lane-parallel; tiles whose predecessor lane maps to
+// the x-adjacent tile join one run (H2D: every q-run of length b; BB: the row
+// segment left of the diagonal). Each run is then streamed row by row with
+// 128-bit loads/stores over its 16-byte-aligned interior and scalar head/tail.
+constexpr int ACC_THREADS = 256;
+
+__device__ __forceinline__ void accum_rows2(uint32_t* __restrict__ cells, unsigned long long e0a,
+                                            unsigned long long e1a, unsigned long long e0b,
+                                            unsigned long long e1b, int lane) {
+    // Row A and row B, each [e0, e1). Interior vectors of both rows are loaded
+    // before any store so every lane keeps up to 2*NV 16-byte loads in flight.
+    constexpr int NV = 4;
+    unsigned long long a0[2], a1[2], e0[2] = {e0a, e0b}, e1[2] = {e1a, e1b};
+    uint4 v[2][NV];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        a0[r] = (e0[r] + 3) & ~3ull;
+        a1[r] = e1[r] & ~3ull;
+        if (a0[r] > a1[r]) a0[r] = a1[r] = e1[r];  // short row: all scalar
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const unsigned long long p = a0[r] + 4ull * (lane + 32 * k);
+            if (p < a1[r]) v[r][k] = *reinterpret_cast<const uint4*>(cells + p);
+        }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const unsigned long long p = a0[r] + 4ull * (lane + 32 * k);
+            if (p < a1[r]) {
+                uint4 t = v[r][k];
+                t.x += 1u; t.y += 1u; t.z += 1u; t.w += 1u;
+                *reinterpret_cast<uint4*>(cells + p) = t;
+            }
+        }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        // long rows beyond the unrolled window
+        for (unsigned long long p = a0[r] + 4ull * (lane + 32 * NV); p < a1[r]; p += 128ull) {
+            uint4 t = *reinterpret_cast<const uint4*>(cells + p);
+            t.x += 1u; t.y += 1u; t.z += 1u; t.w += 1u;
+            *reinterpret_cast<uint4*>(cells + p) = t;
+        }
+        // scalar head [e0, a0) and tail [a1, e1): at most 3 + 3 cells, or a short row
+        const unsigned long long nh = a0[r] - e0[r];
+        for (unsigned long long i = lane; i < nh; i += 32) cells[e0[r] + i] += 1u;
+        const unsigned long long nt = e1[r] - a1[r];
+        for (unsigned long long i = lane; i < nt; i += 32) cells[a1[r] + i] += 1u;
+    }
+}
+
+template <int KIND, int KX>
+__global__ void __launch_bounds__(ACC_THREADS) k_accum_runs(Geom g, uint32_t* __restrict__ cells) {
+    static_assert(KX <= 32, "one warp maps the strip");
+    __shared__ int s_run[KX][3];
+    __shared__ int s_nruns;
+    const int x0 = blockIdx.x * KX, wy = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        const int wx = x0 + lane;
+        int valid = lane < KX && wx < g.ex;
+        outcome<int> o{1, 0, 0, 0, 1, 0};
+        if (valid) {
+            o = map_block<KIND>(g, wx, wy, 0);
+            valid = !o.is_void;
+        }
+        const int px = __shfl_up_sync(FULL_MASK, o.x, 1);
+        const int py = __shfl_up_sync(FULL_MASK, o.y, 1);
+        const int pv = __shfl_up_sync(FULL_MASK, valid, 1);
+        const bool head = valid && !(lane > 0 && pv && px == o.x - 1 && py == o.y);
+        const unsigned heads = __ballot_sync(FULL_MASK, head);
+        const unsigned vmask = __ballot_sync(FULL_MASK, valid);
+        if (head) {
+            const int r = __popc(heads & ((1u << lane) - 1u));
+            const unsigned above = lane == 31 ? 0u : ~((2u << lane) - 1u);
+            const unsigned stop = (heads | ~vmask) & above;
+            const int end = stop ? __ffs(stop) - 1 : 32;
+            s_run[r][0] = o.x;
+            s_run[r][1] = o.y;
+            s_run[r][2] = end - lane;
+        }
+        if (lane == 0) s_nruns = __popc(heads);
+    }
+    __syncthreads();
+    const int nruns = s_nruns;
+    const int rho = g.rho, S = g.side;
+    const int rows = nruns * rho;
+    constexpr int NW = ACC_THREADS / 32;
+    for (int row = warp; row < rows; row += 2 * NW) {
+        unsigned long long e[2][2] = {{0, 0}, {0, 0}};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int rr = row + h * NW;
+            if (rr >= rows) continue;
+            const int r = rr / rho, ly = rr - r * rho;
+            const int cy = s_run[r][1] * rho + ly;
+            const int xlo = s_run[r][0] * rho;
+            int xhi = (s_run[r][0] + s_run[r][2]) * rho;
+            if (xhi > cy + 1) xhi = cy + 1;  // tri_contains: x <= y
+            if (cy > S - 1 || xlo >= xhi) continue;
+            const unsigned long long base = tri_idx(0, cy);
+            e[h][0] = base + xlo;
+            e[h][1] = base + xhi;
+        }
+        accum_rows2(cells, e[0][0], e[0][1], e[1][0], e[1][1], lane);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// make_life_state (simulator.hpp:390-398): alive iff
+// splitmix64(fnv1a_append_u64(seed, i)) >> 62 == 0 (bits.hpp:84-109).
+__device__ __forceinline__ unsigned char life_bit(unsigned long long seed, unsigned long long i) {
+    unsigned long long h = seed;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        h ^= (i >> (8 * k)) & 0xffull;
+        h *= 0x100000001b3ull;
+    }
+    unsigned long long z = h + 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    return (z >> 62) == 0 ? 1 : 0;
+}
+
+__global__ void k_life_init(unsigned long long seed, uint8_t* __restrict__ cells, unsigned long long n) {
+    const unsigned long long nvec = n / 16;
+    for (unsigned long long v = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; v < nvec;
+         v += (unsigned long long)gridDim.x * blockDim.x) {
+        uint32_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc |= uint32_t(life_bit(seed, v * 16 + 4 * j + b)) << (8 * b);
+            w[j] = acc;
+        }
+        reinterpret_cast<uint4*>(cells)[v] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 16) {
+        const unsigned long long i = nvec * 16 + threadIdx.x;
+        if (i < n) cells[i] = life_bit(seed, i);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// 3-D Life, block scheme: one CTA per map block, one thread per cell; the 26
+// neighbours are read through the packed index with the tetrahedron membership
+// filter (alive_neighbors_3d_dead, simulator.hpp:242-253), life_next :220-223.
+__device__ __forceinline__ int life_rule(int alive, int nb) {
+    return alive ? (nb == 2 || nb == 3) : (nb == 3);
+}
+
+template <int KIND>
+__global__ void k_ca_block(Geom g, int wz0, const uint8_t* __restrict__ cur, uint8_t* __restrict__ next) {
+    const int wx = blockIdx.x, wy = blockIdx.y, wz = blockIdx.z + wz0;
+    const BlockTarget t = warp_map<KIND>(g, wx, wy, wz);
+    if (t.is_void) return;
+    const int rho = g.rho, S = g.side;
+    const unsigned long long* __restrict__ P = g.prefix;
+    for (int lz = threadIdx.z; lz < rho; lz += blockDim.z)
+        for (int ly = threadIdx.y; ly < rho; ly += blockDim.y)
+            for (int lx = threadIdx.x; lx < rho; lx += blockDim.x) {
+                const int cx = t.x * rho + lx, cy = t.y * rho + ly, cz = t.z * rho + lz;
+                if (!tet_contains<int>(S, cx, cy, cz)) continue;
+                int count = 0;
+#pragma unroll
+                for (int dz = -1; dz <= 1; ++dz) {
+                    const int zz = cz + dz;
+                    if (zz < 0 || zz > S - 1) continue;
+                    const unsigned long long pz = __ldg(P + zz);
+#pragma unroll
+                    for (int dy = -1; dy <= 1; ++dy) {
+                        const int yy = cy + dy;
+                        if (yy < 0 || yy + zz > S - 1) continue;
+                        const uint8_t* row = cur + pz + tri_idx(0, yy);
+#pragma unroll
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            const int xx = cx + dx;
+                            if (xx >= 0 && xx <= yy) count += __ldg(row + xx);
+                        }
+                    }
+                }
+                const unsigned long long idx = P[cz] + tri_idx(cx, cy);
+                const int me = cur[idx];
+                next[idx] = (uint8_t)life_rule(me, count - me);
+            }
+}
+
+// ---------------------------------------------------------------------------
+// Halo tile pack/unpack (multi-GPU exchange): tile k occupies rho^3 bytes of
+// the buffer in lz, ly, lx order; cells outside the tetrahedron pack as 0 and
+// are skipped on unpack.
+__global__ void k_tiles_pack(Geom g, const uint8_t* __restrict__ cells, const int* __restrict__ tiles,
+                             uint8_t* __restrict__ out) {
+    const int k = blockIdx.x;
+    const int X = tiles[3 * k], Y = tiles[3 * k + 1], Z = tiles[3 * k + 2];
+    const int rho = g.rho, S = g.side, r3 = rho * rho * rho;
+    for (int t = threadIdx.x; t < r3; t += blockDim.x) {
+        const int lx = t % rho, ly = (t / rho) % rho, lz = t / (rho * rho);
+        const int cx = X * rho + lx, cy = Y * rho + ly, cz = Z * rho + lz;
+        uint8_t v = 0;
+        if (tet_contains<int>(S, cx, cy, cz)) v = cells[g.prefix[cz] + tri_idx(cx, cy)];
+        out[(unsigned long long)k * r3 + t] = v;
+    }
+}
+
+__global__ void k_tiles_unpack(Geom g, uint8_t* __restrict__ cells, const int* __restrict__ tiles,
+                               const uint8_t* __restrict__ in) {
+    const int k = blockIdx.x;
+    const int X = tiles[3 * k], Y = tiles[3 * k + 1], Z = tiles[3 * k + 2];
+    const int rho = g.rho, S = g.side, r3 = rho * rho * rho;
+    for (int t = threadIdx.x; t < r3; t += blockDim.x) {
+        const int lx = t % rho, ly = (t / rho) % rho, lz = t / (rho * rho);
+        const int cx = X * rho + lx, cy = Y * rho + ly, cz = Z * rho + lz;
+        if (tet_contains<int>(S, cx, cy, cz))
+            cells[g.prefix[cz] + tri_idx(cx, cy)] = in[(unsigned long long)k * r3 + t];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Launchers.
+static dim3 block_shape(const Geom& g) {
+    const int bx = g.rho < 1024 ? g.rho : 1024;
+    int by = 1024 / bx;
+    if (by > g.rho) by = g.rho;
+    int bz = 1;
+    if (g.dims == 3) {
+        bz = 1024 / (bx * by);
+        if (bz > g.rho) bz = g.rho;
+        if (bz < 1) bz = 1;
+    }
+    return dim3(bx, by, bz);
+}
+
+#define SMX_DISPATCH_KIND(kind, F, ...)                       \
+    do {                                                      \
+        if ((kind) == SMX_H2D) F<SMX_H2D>(__VA_ARGS__);       \
+        else if ((kind) == SMX_H3D) F<SMX_H3D>(__VA_ARGS__);  \
+        else F<SMX_BB>(__VA_ARGS__);                          \
+    } while (0)
+
+template <int KIND>
+static void launch_outcomes_k(const Geom& g, smx_outcome* out, unsigned long long count, cudaStream_t s) {
+    const int threads = 256;
+    unsigned long long blocks = (count + threads - 1) / threads;
+    if (blocks > 148ull * 64) blocks = 148ull * 64;
+    if (blocks == 0) blocks = 1;
+    k_outcomes<KIND><<<(unsigned)blocks, threads, 0, s>>>(g, out, count);
+}
+void launch_outcomes(const Geom& g, smx_outcome* out, unsigned long long count, cudaStream_t s) {
+    SMX_DISPATCH_KIND(g.kind, launch_outcomes_k, g, out, count, s);
+}
+
+template <int KIND>
+static void launch_map_block_k(const Geom& g, int wz0, int wz1, uint32_t* cov, DevCounters* cnt,
+                               unsigned* sink, cudaStream_t s) {
+    const dim3 grid(g.ex, g.ey, wz1 - wz0), blk = block_shape(g);
+    const int mode = (cov ? 1 : 0) | (cnt ? 2 : 0);
+    switch (mode) {
+        case 0: k_map_block<KIND, 0><<<grid, blk, 0, s>>>(g, wz0, cov, cnt, sink); break;
+        case 1: k_map_block<KIND, 1><<<grid, blk, 0, s>>>(g, wz0, cov, cnt, sink); break;
+        case 2: k_map_block<KIND, 2><<<grid, blk, 0, s>>>(g, wz0, cov, cnt, sink); break;
+        default: k_map_block<KIND, 3><<<grid, blk, 0, s>>>(g, wz0, cov, cnt, sink); break;
+    }
+}
+void launch_map_block(const Geom& g, uint32_t* cov, DevCounters* cnt, unsigned* sink, cudaStream_t s) {
+    SMX_DISPATCH_KIND(g.kind, launch_map_block_k, g, 0, g.ez, cov, cnt, sink, s);
+}
+
+template <int KIND>
+static void launch_accum_k(const Geom& g, uint32_t* cells, int exec, cudaStream_t s) {
+    if (exec == SMX_EXEC_BLOCK) {
+        k_accum_block<KIND><<<dim3(g.ex, g.ey, 1), block_shape(g), 0, s>>>(g, cells);
+    } else {
+        constexpr int KX = 16;
+        k_accum_runs<KIND, KX><<<dim3((g.ex + KX - 1) / KX, g.ey, 1), ACC_THREADS, 0, s>>>(g, cells);
+    }
+}
+void launch_accum(const Geom& g, uint32_t* cells, int exec, cudaStream_t s) {
+    SMX_DISPATCH_KIND(g.kind, launch_accum_k, g, cells, exec, s);
+}
+
+void launch_life_init(unsigned long long seed, uint8_t* cells, unsigned long long n, cudaStream_t s) {
+    const int threads = 256;
+    unsigned long long blocks = (n / 16 + threads - 1) / threads;
+    if (blocks > 148ull * 32) blocks = 148ull * 32;
+    if (blocks == 0) blocks = 1;
+    k_life_init<<<(unsigned)blocks, threads, 0, s>>>(seed, cells, n);
+}
+
+template <int KIND>
+static void launch_ca_k(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t* next, int exec,
+                        cudaStream_t s) {
+    if (wz1 <= wz0) return;
+    if (exec == SMX_EXEC_RUNS) {
+        launch_ca_runs(g, KIND, wz0, wz1, cur, next, s);
+        return;
+    }
+    k_ca_block<KIND><<<dim3(g.ex, g.ey, wz1 - wz0), block_shape(g), 0, s>>>(g, wz0, cur, next);
+}
+void launch_ca(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s) {
+    SMX_DISPATCH_KIND(g.kind, launch_ca_k, g, wz0, wz1, cur, next, exec, s);
+}
+
+void launch_tiles_pack(const Geom& g, const uint8_t* cells, const int* tiles, unsigned long long ntiles,
+                       uint8_t* out, cudaStream_t s) {
+    if (ntiles == 0) return;
+    k_tiles_pack<<<(unsigned)ntiles, 256, 0, s>>>(g, cells, tiles, out);
+}
+void launch_tiles_unpack(const Geom& g, uint8_t* cells, const int* tiles, unsigned long long ntiles,
+                         const uint8_t* in, cudaStream_t s) {
+    if (ntiles == 0) return;
+    k_tiles_unpack<<<(unsigned)ntiles, 256, 0, s>>>(g, cells, tiles, in);
+}
+
+}  // namespace smx

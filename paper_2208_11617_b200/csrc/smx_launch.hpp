@@ -1,0 +1,23 @@
+// Internal launcher declarations shared by the kernel files and the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "smx_common.cuh"
+
+namespace smx {
+
+void launch_outcomes(const Geom& g, smx_outcome* out, unsigned long long count, cudaStream_t s);
+void launch_map_block(const Geom& g, uint32_t* cov, DevCounters* cnt, unsigned* sink, cudaStream_t s);
+void launch_accum(const Geom& g, uint32_t* cells, int exec, cudaStream_t s);
+void launch_life_init(unsigned long long seed, uint8_t* cells, unsigned long long n, cudaStream_t s);
+void launch_ca(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s);
+bool ca_runs_supported(int rho);
+void launch_ca_runs(const Geom& g, int kind, int wz0, int wz1, const uint8_t* cur, uint8_t* next,
+                    cudaStream_t s);
+void launch_tiles_pack(const Geom& g, const uint8_t* cells, const int* tiles, unsigned long long ntiles,
+                       uint8_t* out, cudaStream_t s);
+void launch_tiles_unpack(const Geom& g, uint8_t* cells, const int* tiles, unsigned long long ntiles,
+                         const uint8_t* in, cudaStream_t s);
+
+}  // namespace smx
