@@ -1,0 +1,544 @@
+// 3-D Life, x-run scheme (SMX_EXEC_RUNS), sm_100a: bit-shadow engine.
+//
+// Three kernels, the packed u8 state (reference layout) at both ends:
+//
+// k_pack_bits    u8 state -> "bit shadow": one bit per cell in a PITCHED layout,
+//                every packed row (y, z) padded to WP 32-bit words at word row
+//                LR(z) + y, LR(z) = z*S - z(z-1)/2 (rows of the layer back to
+//                back). A warp walks 32 rows, 8 lanes per row, streaming each row's bytes as
+//                32-byte aligned chunks (2 x 16B loads per lane), packing them
+//                (IMAD gather + PRMT) and realigning at the bit level.
+// k_ca_bits      bit shadow -> next bit shadow. Work assignment is the map: a CTA
+//                owns a P x P patch of map blocks at one wz; its threads map the
+//                blocks lane-parallel and chain x-adjacent tiles (predecessor at
+//                patch neighbour (wx-1, wy) for unfolded H tiles / wall plane / BB
+//                rows, (wx, wy-1) for the hinge fold, maps.hpp:334-336) into
+//                chunks of <= 96 cells. A warp takes a chunk: one 2-D TMA tensor
+//                box per halo layer (rho+2 rows x 12 words) lands the bit rows in
+//                shared memory (double-buffered across chunks, mbarrier
+//                completion), lanes form the horizontal 3-sums as bit-planes, and
+//                lane (ly, w) marches along z with carry-save adders: 32 cells per
+//                LOP3. Output is whole 32-bit words: a word shared by two chunks
+//                gets identical values from both (every cell of a computed word is
+//                computed from the same input), so the writes are idempotent.
+// k_unpack_bits  bit shadow -> u8 state: 16-byte vector stores over each row's
+//                aligned interior, one byte store per lane for its two ends.
+//
+// A single step (smx_ca_step) is pack -> ca -> unpack; a multi-step run
+// (smx_ca) packs once and then runs ca -> unpack per step, so every step still
+// materialises the full u8 state in the reference layout.
+//
+// Semantics: alive_neighbors_3d_dead + life_next (simulator.hpp:220-253) for
+// every cell of every tile the map emits; each tile is processed by exactly one
+// chunk. Bits for x > y of a row (not cells) are never trusted: every reader
+// masks them.
+#include <cuda.h>
+
+#include "smx_common.cuh"
+#include "smx_launch.hpp"
+
+namespace smx {
+
+namespace {
+
+constexpr int OWN = 96;   // max owned cells per chunk row
+// words per TMA box row: the box must start on a 16-byte (4-word) boundary, so
+// it starts at floor4(w0 - 1) and 12 words always cover words w0-1 .. w0+4.
+constexpr int BOXW = 12;
+constexpr int NWARP = 4;  // warps per CTA
+constexpr int NTHR = NWARP * 32;
+
+template <int RHO>
+struct Cfg {
+    static constexpr int LMAX = OWN / RHO;              // tiles per chunk
+    static constexpr int P = LMAX;                      // patch edge (blocks)
+    static constexpr int NB = P * P;                    // blocks per CTA
+    static constexpr int HL = RHO + 2;                  // halo layers == halo rows per layer
+    static constexpr int LPC = RHO * 4;                 // compute lanes per chunk
+    static constexpr int CPI = 32 / LPC;                // chunks per warp item
+    static constexpr int BOXB = HL * BOXW * 4;          // bytes per TMA box
+    static constexpr int SLOT = (BOXB + 127) & ~127;    // 128B-aligned slot per box
+    static constexpr int BUF = CPI * HL * SLOT;         // one buffer: all boxes of an item
+    static constexpr int HROWS = CPI * HL * HL;         // halo rows per item
+    static constexpr int WARP_BYTES = (2 * BUF + HROWS * 32 + 64 + 127) & ~127;  // TMA dst: 128B aligned
+    static constexpr int SMEM = NWARP * WARP_BYTES + NB * 16 + NB * 16 + 128;
+};
+
+struct Chunk {
+    int x0, y0, z0, w;  // cell box origin and owned width (cells)
+};
+
+__device__ __forceinline__ int layer_row(int z, int S) { return z * S - (z * (z - 1)) / 2; }
+
+// ---- PTX helpers ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// 32 bytes (each 0 or 1) -> 32 bits, bit i = byte i. t = w0 | w1 << 4 puts
+// bytes i and i+4 into one byte; * 0x01020408 gathers bit 0 of byte i to bit
+// 24+i and bit 4 to bit 28+i with no carries (all partial products below bit 24
+// land on distinct bits).
+__device__ __forceinline__ uint32_t pack32(uint4 a, uint4 b) {
+    const uint32_t M = 0x01020408u;
+    const uint32_t p0 = (a.y * 16u + a.x) * M;
+    const uint32_t p1 = (a.w * 16u + a.z) * M;
+    const uint32_t p2 = (b.y * 16u + b.x) * M;
+    const uint32_t p3 = (b.w * 16u + b.z) * M;
+    return __byte_perm(__byte_perm(p0, p1, 0x0073), __byte_perm(p2, p3, 0x0073), 0x5410);
+}
+
+// 4 bits -> 4 bytes (0/1): n * (1 + 2^7 + 2^14 + 2^21) puts bit i at 9i.
+__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
+__device__ __forceinline__ uint4 spread16(uint32_t b) {
+    return make_uint4(spread4(b & 0xf), spread4((b >> 4) & 0xf), spread4((b >> 8) & 0xf), spread4((b >> 12) & 0xf));
+}
+
+// bits [lo, hi] (inclusive) of a 32-bit word; 0 when hi < lo
+__device__ __forceinline__ uint32_t range_mask(int lo, int hi) {
+    lo = lo < 0 ? 0 : lo;
+    hi = hi > 31 ? 31 : hi;
+    if (hi < lo) return 0u;
+    return (0xffffffffu >> (31 - hi)) & (0xffffffffu << lo);
+}
+
+struct Planes4 {
+    uint32_t b0, b1, b2, b3;
+};
+
+// sum of three 2-bit numbers (<= 9) as 4 bit-planes
+__device__ __forceinline__ Planes4 add3x2(uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1, uint32_t c0,
+                                          uint32_t c1) {
+    const uint32_t s0 = a0 ^ b0 ^ c0;
+    const uint32_t k1 = (a0 & b0) | (a0 & c0) | (b0 & c0);
+    const uint32_t t = a1 ^ b1 ^ c1;
+    const uint32_t u = (a1 & b1) | (a1 & c1) | (b1 & c1);
+    const uint32_t c = t & k1;
+    return Planes4{s0, t ^ k1, u ^ c, u & c};
+}
+
+// B3/S23 from three 4-plane partial sums (the 27-sum includes the cell):
+// next = (S == 3) | (alive & S == 4).
+__device__ __forceinline__ uint32_t life_planes(const Planes4& a, const Planes4& b, const Planes4& c,
+                                                uint32_t alive) {
+    const uint32_t s0 = a.b0 ^ b.b0 ^ c.b0, k1 = (a.b0 & b.b0) | (a.b0 & c.b0) | (b.b0 & c.b0);
+    const uint32_t s1 = a.b1 ^ b.b1 ^ c.b1, k2 = (a.b1 & b.b1) | (a.b1 & c.b1) | (b.b1 & c.b1);
+    const uint32_t s2 = a.b2 ^ b.b2 ^ c.b2, k3 = (a.b2 & b.b2) | (a.b2 & c.b2) | (b.b2 & c.b2);
+    const uint32_t s3 = a.b3 ^ b.b3 ^ c.b3, k4 = (a.b3 & b.b3) | (a.b3 & c.b3) | (b.b3 & c.b3);
+    const uint32_t r1 = s1 ^ k1, c2 = s1 & k1;
+    const uint32_t r2 = s2 ^ k2 ^ c2, c3 = (s2 & k2) | (s2 & c2) | (k2 & c2);
+    const uint32_t r3 = s3 ^ k3 ^ c3, c4 = (s3 & k3) | (s3 & c3) | (k3 & c3);
+    const uint32_t r4 = k4 ^ c4;
+    const uint32_t eq3 = s0 & r1 & ~r2;
+    const uint32_t eq4 = ~s0 & ~r1 & r2;
+    return (eq3 | (eq4 & alive)) & ~(r3 | r4);
+}
+
+// 32 bytes at 32B-aligned byte offset A of a u8 array of n bytes -> 32 bits
+__device__ __forceinline__ uint32_t load_chunk_bits(const uint8_t* __restrict__ p, long long A,
+                                                    unsigned long long n) {
+    if ((unsigned long long)(A + 32) <= n) {
+        const uint4* q = reinterpret_cast<const uint4*>(p + A);
+        return pack32(__ldg(q), __ldg(q + 1));
+    }
+    uint32_t v = 0;
+    for (int i = 0; i < 32; ++i)
+        if ((unsigned long long)(A + i) < n) v |= uint32_t(p[A + i] & 1) << i;
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// Row walk shared by pack/unpack. A warp owns 32 consecutive pitched rows and
+// works on 4 of them at a time, one 8-lane group per row (group g takes rows
+// r0+g, r0+g+4, ...): per-row bookkeeping is shared by the 8 lanes of a group
+// and each lane moves 32 bytes per pass.
+constexpr int ROWS_PER_WARP = 32;
+
+struct RowCursor {
+    int z, y;
+    long long rowbase;  // packed index of cell (0, y, z)
+};
+
+__device__ __forceinline__ RowCursor row_at(int row, int S, const unsigned long long* __restrict__ PZ) {
+    int lo = 0, hi = S - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (layer_row(mid, S) <= row) lo = mid;
+        else hi = mid - 1;
+    }
+    const int y = row - layer_row(lo, S);
+    return RowCursor{lo, y, (long long)(PZ[lo] + tri_idx(0, y))};
+}
+
+__device__ __forceinline__ void row_next(RowCursor& c, int S, const unsigned long long* __restrict__ PZ) {
+    if (c.y + 1 + c.z <= S - 1) {
+        c.rowbase += c.y + 1;
+        ++c.y;
+    } else {
+        ++c.z;
+        c.y = 0;
+        c.rowbase = (long long)PZ[c.z];
+    }
+}
+
+// u8 packed state -> pitched bit shadow (bits beyond x = y are zero).
+__global__ void __launch_bounds__(256) k_pack_bits(const uint8_t* __restrict__ cur, uint32_t* __restrict__ bits,
+                                                   int S, int WP, int nrows, const unsigned long long* __restrict__ PZ,
+                                                   unsigned long long ncells) {
+    const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
+    const unsigned gmask = 0xffu << (8 * grp);
+    const int row0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * ROWS_PER_WARP;
+    int r = row0 + grp;
+    if (r >= nrows) return;
+    RowCursor c = row_at(r, S, PZ);
+    for (;;) {
+        const int n = c.y + 1, nw = (n + 31) >> 5;
+        const long long A0 = c.rowbase & ~31ll;
+        const int d = int(c.rowbase - A0);
+        uint32_t* out = bits + (long long)r * WP;
+        // lane gl packs chunk k; word k needs chunks k and k+1, so a pass emits
+        // 7 words (lanes 0..6) and the next pass starts 7 chunks on
+#pragma unroll 2
+        for (int base = 0; base < nw; base += 7) {
+            const int k = base + gl;
+            const long long ck = A0 + 32ll * k;
+            const uint32_t B = (ck < c.rowbase + n) ? load_chunk_bits(cur, ck, ncells) : 0u;
+            const uint32_t Bn = __shfl_down_sync(gmask, B, 1, 8);
+            if (gl < 7 && k < nw) {
+                uint32_t wv = d ? __funnelshift_r(B, Bn, d) : B;
+                const int valid = n - 32 * k;
+                if (valid < 32) wv &= (1u << valid) - 1u;
+                out[k] = wv;
+            }
+        }
+        r += 4;
+        if (r >= nrows || r >= row0 + ROWS_PER_WARP) break;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) row_next(c, S, PZ);
+    }
+}
+
+// pitched bit shadow -> u8 packed state. Interior 16-byte windows of a row
+// are vector stores; the <= 15 + 15 bytes at the row's two ends (shared with the
+// neighbouring rows' windows) are byte stores.
+__global__ void __launch_bounds__(256) k_unpack_bits(const uint32_t* __restrict__ bits, uint8_t* __restrict__ out,
+                                                     int S, int WP, int nrows,
+                                                     const unsigned long long* __restrict__ PZ) {
+    const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
+    const int row0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * ROWS_PER_WARP;
+    int r = row0 + grp;
+    if (r >= nrows) return;
+    RowCursor c = row_at(r, S, PZ);
+    for (;;) {
+        const int n = c.y + 1;
+        const uint32_t* src = bits + (long long)r * WP;
+        const long long e0 = c.rowbase, e1 = c.rowbase + n;
+        long long a_lo = (e0 + 15) & ~15ll, a_hi = e1 & ~15ll;
+        if (a_lo > a_hi) a_lo = a_hi = e1;  // no full window: every byte is an edge byte
+        const int nwin = int((a_hi - a_lo) >> 4);
+        // group pass: 16 consecutive windows (256 B); lane gl writes windows
+        // base+gl and base+8+gl so each store instruction covers 128 B per row
+#pragma unroll 2
+        for (int base = 0; base < nwin; base += 16) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int k = base + 8 * h + gl;
+                if (k < nwin) {
+                    const long long A = a_lo + 16ll * k;
+                    const int x = int(A - e0), j = x >> 5, o = x & 31;
+                    const uint32_t w1 = __ldg(src + j);
+                    const uint32_t w2 = o > 16 ? __ldg(src + j + 1) : 0u;
+                    *reinterpret_cast<uint4*>(out + A) = spread16(__funnelshift_r(w1, w2, o) & 0xffffu);
+                }
+            }
+        }
+        const int nhead = int(a_lo - e0), ntail = int(e1 - a_hi);
+        for (int t = gl; t < nhead + ntail; t += 8) {
+            const long long pos = t < nhead ? e0 + t : a_hi + (t - nhead);
+            const int x = int(pos - e0);
+            out[pos] = (uint8_t)((__ldg(src + (x >> 5)) >> (x & 31)) & 1u);
+        }
+        r += 4;
+        if (r >= nrows || r >= row0 + ROWS_PER_WARP) break;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) row_next(c, S, PZ);
+    }
+}
+
+// TMA issue for one warp item (lane 0): one box per valid halo layer per chunk.
+template <int RHO>
+__device__ __forceinline__ void issue_item(const CUtensorMap* tm, const Chunk* s_chunk, int nchunks, int item,
+                                           uint8_t* buf, uint32_t mbar, int S) {
+    using C = Cfg<RHO>;
+    uint32_t bytes = 0;
+    for (int c = 0; c < C::CPI; ++c) {
+        const int ci = item * C::CPI + c;
+        if (ci >= nchunks) break;
+        const Chunk ch = s_chunk[ci];
+        for (int zi = 0; zi < C::HL; ++zi) {
+            const int zz = ch.z0 - 1 + zi;
+            if (zz >= 0 && zz <= S - 1) bytes += C::BOXB;
+        }
+    }
+    mbar_expect_tx(mbar, bytes);
+    for (int c = 0; c < C::CPI; ++c) {
+        const int ci = item * C::CPI + c;
+        if (ci >= nchunks) break;
+        const Chunk ch = s_chunk[ci];
+        const int w0 = ch.x0 >> 5;
+        for (int zi = 0; zi < C::HL; ++zi) {
+            const int zz = ch.z0 - 1 + zi;
+            if (zz < 0 || zz > S - 1) continue;
+            const int c0 = (w0 - 1) - ((w0 - 1) & 3);
+            tma_load_2d(smem_u32(buf + (c * C::HL + zi) * C::SLOT), tm, c0, layer_row(zz, S) + ch.y0 - 1, mbar);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+template <int KIND, int RHO>
+__global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_constant__ CUtensorMap tmap,
+                                                  uint32_t* __restrict__ nbits, int WP, int P) {
+    using C = Cfg<RHO>;
+    const int NBP = P * P;  // blocks in this launch's patch (P <= C::P)
+    constexpr int HL = C::HL;
+    extern __shared__ __align__(128) uint8_t smem[];
+    int4* s_tile = reinterpret_cast<int4*>(smem + NWARP * C::WARP_BYTES);
+    Chunk* s_chunk = reinterpret_cast<Chunk*>(smem + NWARP * C::WARP_BYTES + C::NB * 16);
+    int* s_nchunks = reinterpret_cast<int*>(smem + NWARP * C::WARP_BYTES + 2 * C::NB * 16);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wz = blockIdx.z + wz0;
+    const int S = g.side;
+    const unsigned long long* __restrict__ PZ = g.prefix;
+
+    uint8_t* wbase = smem + warp * C::WARP_BYTES;
+    uint32_t* sH = reinterpret_cast<uint32_t*>(wbase + 2 * C::BUF);  // [HROWS][8]: h0 w0..3, h1 w0..3
+    const uint32_t mbar0 = smem_u32(wbase + 2 * C::BUF + C::HROWS * 32);
+
+    // ---- 1. map the patch ----
+    if (tid == 0) *s_nchunks = 0;
+    if (lane == 0) {
+        mbar_init(mbar0, 1);
+        mbar_init(mbar0 + 8, 1);
+    }
+    for (int t = tid; t < NBP; t += NTHR) {
+        const int wx = blockIdx.x * P + (t % P), wy = blockIdx.y * P + (t / P);
+        int4 v = make_int4(0, 0, 0, 0);
+        if (wx < g.ex && wy < g.ey) {
+            const outcome<int> o = map_block<KIND>(g, wx, wy, wz);
+            if (!o.is_void) v = make_int4(o.x, o.y, o.z, 1);
+        }
+        s_tile[t] = v;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncthreads();
+    // ---- 2. chains of x-adjacent tiles -> chunks ----
+    for (int t = tid; t < NBP; t += NTHR) {
+        const int4 me = s_tile[t];
+        if (!me.w) continue;
+        const int px = t % P, py = t / P;
+        auto is_tile = [&](int i, int x) {
+            const int4 o = s_tile[i];
+            return o.w && o.x == x && o.y == me.y && o.z == me.z;
+        };
+        if ((px > 0 && is_tile(t - 1, me.x - 1)) || (py > 0 && is_tile(t - P, me.x - 1))) continue;
+        int u = t, len = 1, x0 = me.x;
+        for (;;) {
+            const int ux = u % P, uy = u / P;
+            const int xn = s_tile[u].x + 1;
+            int nxt = -1;
+            if (ux + 1 < P && is_tile(u + 1, xn)) nxt = u + 1;
+            else if (uy + 1 < P && is_tile(u + P, xn)) nxt = u + P;
+            if (nxt < 0 || len == C::LMAX) {
+                const int c = atomicAdd(s_nchunks, 1);
+                s_chunk[c] = Chunk{x0 * RHO, me.y * RHO, me.z * RHO, len * RHO};
+                if (nxt < 0) break;
+                x0 = s_tile[nxt].x;
+                len = 0;
+            }
+            u = nxt;
+            ++len;
+        }
+    }
+    __syncthreads();
+    const int nchunks = *s_nchunks;
+    const int nitems = (nchunks + C::CPI - 1) / C::CPI;
+
+    uint32_t phases = 0u;  // bit b: parity of buffer b
+    int item = warp, b = 0;
+    const CUtensorMap* tm = &tmap;
+    if (item < nitems && lane == 0) {
+        fence_proxy_async();
+        issue_item<RHO>(tm, s_chunk, nchunks, item, wbase, mbar0, S);
+    }
+    for (; item < nitems; item += NWARP, b ^= 1) {
+        const int nxt = item + NWARP;
+        if (nxt < nitems && lane == 0) {
+            fence_proxy_async();
+            issue_item<RHO>(tm, s_chunk, nchunks, nxt, wbase + (b ^ 1) * C::BUF, mbar0 + 8 * (b ^ 1), S);
+        }
+        while (!mbar_try_wait(mbar0 + 8 * b, (phases >> b) & 1u)) {
+        }
+        phases ^= 1u << b;
+        const uint8_t* buf = wbase + b * C::BUF;
+
+        // ---- 3. horizontal 3-sums (bit-planes), lane per halo row ----
+        for (int r = lane; r < C::HROWS; r += 32) {
+            const int c = r / (HL * HL), rr = r % (HL * HL);
+            const int zi = rr / HL, yi = rr % HL;
+            const int ci = item * C::CPI + c;
+            uint4 h0 = make_uint4(0, 0, 0, 0), h1 = h0;
+            if (ci < nchunks) {
+                const Chunk ch = s_chunk[ci];
+                const int zz = ch.z0 - 1 + zi, yy = ch.y0 - 1 + yi;
+                if (zz >= 0 && yy >= 0 && yy + zz <= S - 1) {
+                    const int off = ((ch.x0 >> 5) - 1) & 3;  // box word of w0 - 1
+                    const uint32_t* src =
+                        reinterpret_cast<const uint32_t*>(buf + (c * HL + zi) * C::SLOT + yi * BOXW * 4) + off;
+                    uint32_t T[6];
+#pragma unroll
+                    for (int j = 0; j < 6; ++j) T[j] = src[j];
+                    const int xb = ((ch.x0 >> 5) - 1) * 32;  // x of T[0] bit 0
+                    if (xb + 191 > yy) {
+#pragma unroll
+                        for (int j = 0; j < 6; ++j) T[j] &= range_mask(-(xb + 32 * j), yy - (xb + 32 * j));
+                    }
+                    uint32_t a[4], bb[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t cc = T[j + 1];
+                        const uint32_t l = __funnelshift_l(T[j], cc, 1);
+                        const uint32_t rg = __funnelshift_r(cc, T[j + 2], 1);
+                        a[j] = l ^ cc ^ rg;
+                        bb[j] = (l & cc) | (l & rg) | (cc & rg);
+                    }
+                    h0 = make_uint4(a[0], a[1], a[2], a[3]);
+                    h1 = make_uint4(bb[0], bb[1], bb[2], bb[3]);
+                }
+            }
+            reinterpret_cast<uint4*>(sH + 8 * r)[0] = h0;
+            reinterpret_cast<uint4*>(sH + 8 * r)[1] = h1;
+        }
+        __syncwarp();
+
+        // ---- 4. march along z: vertical sums, rule, stores ----
+        {
+            const int cl = lane / C::LPC, l = lane % C::LPC;
+            const int ly = l >> 2, w = l & 3;
+            const int ci = item * C::CPI + cl;
+            const bool cvalid = ci < nchunks;
+            const Chunk ch = cvalid ? s_chunk[ci] : Chunk{0, 0, 0, 0};
+            const uint32_t* H = sH + 8 * (cl * HL * HL);
+            const uint8_t* cbuf = buf + cl * HL * C::SLOT;
+            auto vsum = [&](int zi) {
+                const int r0 = zi * HL + ly;
+                return add3x2(H[8 * r0 + w], H[8 * r0 + 4 + w], H[8 * (r0 + 1) + w], H[8 * (r0 + 1) + 4 + w],
+                              H[8 * (r0 + 2) + w], H[8 * (r0 + 2) + 4 + w]);
+            };
+            Planes4 va = vsum(0), vb = vsum(1);
+            const int y = ch.y0 + ly;
+            const int w0 = ch.x0 >> 5;
+            const int xw = 32 * (w0 + w);  // x of this lane's word
+            const int lastw = (ch.x0 + ch.w - 1) >> 5;
+#pragma unroll 2
+            for (int lz = 0; lz < RHO; ++lz) {
+                const Planes4 vc = vsum(lz + 2);
+                const uint32_t alive = reinterpret_cast<const uint32_t*>(cbuf + (lz + 1) * C::SLOT +
+                                                                         (ly + 1) * BOXW * 4)[((w0 - 1) & 3) + 1 + w];
+                const uint32_t O = life_planes(va, vb, vc, alive);
+                va = vb;
+                vb = vc;
+                const int z = ch.z0 + lz;
+                if (!cvalid || y + z > S - 1 || ch.x0 > y || w0 + w > lastw || xw > y) continue;
+                nbits[(long long)(layer_row(z, S) + y) * WP + w0 + w] = O;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+template <int KIND, int RHO>
+void launch_t(const Geom& g, int wz0, int wz1, const CUtensorMap& tmap, uint32_t* nbits, int WP, cudaStream_t s) {
+    using C = Cfg<RHO>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_ca_bits<KIND, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        attr_set = true;
+    }
+    // patch edge: the largest that still gives >= 4 CTAs per SM (small grids
+    // trade chunk length for parallelism)
+    int P = C::P;
+    auto ctas = [&](int p) { return (long long)((g.ex + p - 1) / p) * ((g.ey + p - 1) / p) * (wz1 - wz0); };
+    while (P > 4 && ctas(P) < 4 * 148) P = P / 2 > 4 ? P / 2 : 4;
+    const dim3 grid((g.ex + P - 1) / P, (g.ey + P - 1) / P, wz1 - wz0);
+    k_ca_bits<KIND, RHO><<<grid, NTHR, C::SMEM, s>>>(g, wz0, tmap, nbits, WP, P);
+}
+
+template <int KIND>
+void launch_kind(const Geom& g, int wz0, int wz1, const CUtensorMap& tmap, uint32_t* nbits, int WP, cudaStream_t s) {
+    if (g.rho == 4) launch_t<KIND, 4>(g, wz0, wz1, tmap, nbits, WP, s);
+    else launch_t<KIND, 8>(g, wz0, wz1, tmap, nbits, WP, s);
+}
+
+}  // namespace
+
+bool ca_runs_supported(int rho) { return rho == 4 || rho == 8; }
+
+// words per pitched row: >= 8, multiple of 4 (16-byte row stride for TMA)
+int bits_pitch_words(int side) {
+    const int w = ((side + 31) / 32 + 3) & ~3;
+    return w < 8 ? 8 : w;
+}
+
+unsigned long long bits_rows(int side) { return (unsigned long long)side * (side + 1) / 2; }
+
+int tma_box_rows(int rho) { return rho + 2; }
+
+int tma_box_words() { return BOXW; }
+
+void launch_pack_bits(const Geom& g, const uint8_t* cur, uint32_t* bits, cudaStream_t s) {
+    const int S = g.side, WP = bits_pitch_words(S);
+    const int nrows = int(bits_rows(S));
+    const int warps = (nrows + ROWS_PER_WARP - 1) / ROWS_PER_WARP;
+    k_pack_bits<<<(warps + 7) / 8, 256, 0, s>>>(cur, bits, S, WP, nrows, g.prefix, tet_cells(S));
+}
+
+void launch_unpack_bits(const Geom& g, const uint32_t* bits, uint8_t* out, cudaStream_t s) {
+    const int S = g.side, WP = bits_pitch_words(S);
+    const int nrows = int(bits_rows(S));
+    const int warps = (nrows + ROWS_PER_WARP - 1) / ROWS_PER_WARP;
+    k_unpack_bits<<<(warps + 7) / 8, 256, 0, s>>>(bits, out, S, WP, nrows, g.prefix);
+}
+
+void launch_ca_bits(const Geom& g, int kind, int wz0, int wz1, const void* tmap_ptr, uint32_t* nbits, cudaStream_t s) {
+    const CUtensorMap& tmap = *reinterpret_cast<const CUtensorMap*>(tmap_ptr);
+    const int WP = bits_pitch_words(g.side);
+    if (wz1 <= wz0) return;
+    if (kind == SMX_H3D) launch_kind<SMX_H3D>(g, wz0, wz1, tmap, nbits, WP, s);
+    else launch_kind<SMX_BB>(g, wz0, wz1, tmap, nbits, WP, s);
+}
+
+}  // namespace smx

@@ -1,6 +1,8 @@
 // The C ABI (include/smx_b200.h): argument validation with the reference's
 // contract messages, host<->device staging for host-buffer calls, the per-side
 // layer-prefix tables, and dispatch to the sm_100a kernels.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -54,8 +56,9 @@ bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 // grow-only staging pool for host-buffer calls, counters and the MAP sink.
 struct DeviceRes {
     std::map<int64_t, unsigned long long*> prefix;
-    void* pool[3] = {nullptr, nullptr, nullptr};
-    size_t pool_bytes[3] = {0, 0, 0};
+    void* pool[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // 0 cov, 1/2 u8, 3/4 bit shadows
+    size_t pool_bytes[5] = {0, 0, 0, 0, 0};
+    std::map<std::pair<const void*, std::pair<int64_t, int64_t>>, CUtensorMap> tmaps;
     smx::DevCounters* counters = nullptr;
     unsigned* sink = nullptr;
 };
@@ -106,7 +109,7 @@ int pool_get(int slot, size_t bytes, void** out) {
         if (r->pool[slot]) TRY(cudaFree(r->pool[slot]));
         r->pool[slot] = nullptr;
         r->pool_bytes[slot] = 0;
-        TRY(cudaMalloc(&r->pool[slot], bytes));
+        TRY(cudaMalloc(&r->pool[slot], bytes + 256));  // 16B-granule reads past the end stay inside
         r->pool_bytes[slot] = bytes;
     }
     *out = r->pool[slot];
@@ -207,6 +210,67 @@ int fill_counters(const smx_grid* g, const smx::Geom& k, smx_counters* c, cudaSt
 int resolve_exec(int exec, const smx_grid* g) {
     if (exec == SMX_EXEC_BLOCK || exec == SMX_EXEC_RUNS) return exec;
     return -1;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2-D tiled tensor map over a pitched bit shadow: dim0 = WP words, dim1 = rows;
+// box = tma_box_words() x (rho + 2) rows; out-of-range coordinates read as zero.
+int bits_tmap(const uint32_t* bits, int64_t side, int64_t rho, const CUtensorMap** out) {
+    DeviceRes* r;
+    if (int rc = device_res(&r)) return rc;
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto key = std::make_pair((const void*)bits, std::make_pair(side, rho));
+    auto it = r->tmaps.find(key);
+    if (it != r->tmaps.end()) {
+        *out = &it->second;
+        return SMX_OK;
+    }
+    auto fn = encode_fn();
+    if (!fn) return fail(SMX_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    const int WP = smx::bits_pitch_words(int(side));
+    cuuint64_t dims[2] = {cuuint64_t(WP), cuuint64_t(smx::bits_rows(int(side)))};
+    cuuint64_t strides[1] = {cuuint64_t(WP) * 4};
+    cuuint32_t box[2] = {cuuint32_t(smx::tma_box_words()), cuuint32_t(smx::tma_box_rows(int(rho)))};
+    cuuint32_t estr[2] = {1u, 1u};
+    CUtensorMap m;
+    CUresult cr = fn(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(bits), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(SMX_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(cr)));
+    auto res = r->tmaps.emplace(key, m);
+    *out = &res.first->second;
+    return SMX_OK;
+}
+
+size_t bits_bytes(int64_t side) {
+    return size_t(smx::bits_rows(int(side))) * size_t(smx::bits_pitch_words(int(side))) * 4;
+}
+
+// One x-run step u8 -> u8: pack cur into pooled bit shadow A, k_ca_bits A -> B,
+// unpack B into next.
+int ca_runs_step(const smx_grid* g, const smx::Geom& k, int64_t wz0, int64_t wz1, const uint8_t* cur, uint8_t* next,
+                 cudaStream_t s) {
+    void *pa, *pb;
+    if (int rc = pool_get(3, bits_bytes(k.side), &pa)) return rc;
+    if (int rc = pool_get(4, bits_bytes(k.side), &pb)) return rc;
+    const CUtensorMap* tm;
+    if (int rc = bits_tmap((const uint32_t*)pa, k.side, k.rho, &tm)) return rc;
+    smx::launch_pack_bits(k, cur, (uint32_t*)pa, s);
+    smx::launch_ca_bits(k, g->kind, int(wz0), int(wz1), tm, (uint32_t*)pb, s);
+    smx::launch_unpack_bits(k, (const uint32_t*)pb, next, s);
+    TRY(cudaGetLastError());
+    return SMX_OK;
 }
 
 }  // namespace
@@ -421,6 +485,7 @@ int smx_ca_step(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint64_t n
     if (int rc = make_geom(g, &k, true)) return rc;
     if (int rc = ca_validate(g, ncells, &exec)) return rc;
     if (cur == next) return fail(SMX_EINVAL, "ca_step: cur and next must not alias");
+    if (exec == SMX_EXEC_RUNS) return ca_runs_step(g, k, 0, k.ez, cur, next, (cudaStream_t)stream);
     smx::launch_ca(k, 0, k.ez, cur, next, exec, (cudaStream_t)stream);
     TRY(cudaGetLastError());
     return SMX_OK;
@@ -433,6 +498,7 @@ int smx_ca_step_range(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint
     if (int rc = ca_validate(g, ncells, &exec)) return rc;
     if (wz_lo < 0 || wz_hi > g->extents[2] || wz_lo > wz_hi)
         return fail(SMX_EINVAL, "ca_step_range: wz range outside the grid");
+    if (exec == SMX_EXEC_RUNS) return ca_runs_step(g, k, wz_lo, wz_hi, cur, next, (cudaStream_t)stream);
     smx::launch_ca(k, int(wz_lo), int(wz_hi), cur, next, exec, (cudaStream_t)stream);
     TRY(cudaGetLastError());
     return SMX_OK;
@@ -467,9 +533,31 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
         if (int rc = fill_counters(g, k, counters, s, dcov)) return rc;
     uint8_t* cur = a;
     uint8_t* nxt = b;
-    for (int64_t st = 0; st < steps; ++st) {
-        smx::launch_ca(k, 0, k.ez, cur, nxt, exec, s);
-        std::swap(cur, nxt);
+    if (exec == SMX_EXEC_RUNS && steps > 0) {
+        // bit-shadow engine: pack once, then ca + unpack per step (every step writes the u8 state)
+        void *pa, *pb;
+        if (int rc = pool_get(3, bits_bytes(k.side), &pa)) return rc;
+        if (int rc = pool_get(4, bits_bytes(k.side), &pb)) return rc;
+        const CUtensorMap *ta, *tb;
+        if (int rc = bits_tmap((const uint32_t*)pa, k.side, k.rho, &ta)) return rc;
+        if (int rc = bits_tmap((const uint32_t*)pb, k.side, k.rho, &tb)) return rc;
+        smx::launch_pack_bits(k, cur, (uint32_t*)pa, s);
+        uint32_t* bc = (uint32_t*)pa;
+        uint32_t* bn = (uint32_t*)pb;
+        const CUtensorMap* tc = ta;
+        const CUtensorMap* tn = tb;
+        for (int64_t st = 0; st < steps; ++st) {
+            smx::launch_ca_bits(k, g->kind, 0, k.ez, tc, bn, s);
+            smx::launch_unpack_bits(k, bn, nxt, s);
+            std::swap(cur, nxt);
+            std::swap(bc, bn);
+            std::swap(tc, tn);
+        }
+    } else {
+        for (int64_t st = 0; st < steps; ++st) {
+            smx::launch_ca(k, 0, k.ez, cur, nxt, exec, s);
+            std::swap(cur, nxt);
+        }
     }
     TRY(cudaGetLastError());
     if (device_ptr) {

@@ -413,12 +413,9 @@ template <int KIND>
 static void launch_ca_k(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t* next, int exec,
                         cudaStream_t s) {
     if (wz1 <= wz0) return;
-    if (exec == SMX_EXEC_RUNS) {
-        launch_ca_runs(g, KIND, wz0, wz1, cur, next, s);
-        return;
-    }
     k_ca_block<KIND><<<dim3(g.ex, g.ey, wz1 - wz0), block_shape(g), 0, s>>>(g, wz0, cur, next);
 }
+// block scheme only; the x-run scheme is driven by the C ABI (pack + k_ca_bits)
 void launch_ca(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s) {
     SMX_DISPATCH_KIND(g.kind, launch_ca_k, g, wz0, wz1, cur, next, exec, s);
 }

@@ -13,8 +13,15 @@ void launch_accum(const Geom& g, uint32_t* cells, int exec, cudaStream_t s);
 void launch_life_init(unsigned long long seed, uint8_t* cells, unsigned long long n, cudaStream_t s);
 void launch_ca(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s);
 bool ca_runs_supported(int rho);
-void launch_ca_runs(const Geom& g, int kind, int wz0, int wz1, const uint8_t* cur, uint8_t* next,
-                    cudaStream_t s);
+// bit-shadow engine (smx_ca_bits.cu)
+int bits_pitch_words(int side);
+unsigned long long bits_rows(int side);
+int tma_box_rows(int rho);
+int tma_box_words();
+void launch_pack_bits(const Geom& g, const uint8_t* cur, uint32_t* bits, cudaStream_t s);
+void launch_unpack_bits(const Geom& g, const uint32_t* bits, uint8_t* out, cudaStream_t s);
+// tmap: CUtensorMap over the input bit shadow; writes the next bit shadow
+void launch_ca_bits(const Geom& g, int kind, int wz0, int wz1, const void* tmap, uint32_t* nbits, cudaStream_t s);
 void launch_tiles_pack(const Geom& g, const uint8_t* cells, const int* tiles, unsigned long long ntiles,
                        uint8_t* out, cudaStream_t s);
 void launch_tiles_unpack(const Geom& g, uint8_t* cells, const int* tiles, unsigned long long ntiles,
