@@ -4,8 +4,8 @@
 //
 // k_pack_bits    u8 state -> "bit shadow": one bit per cell in a PITCHED layout,
 //                every packed row (y, z) padded to WP 32-bit words at word row
-//                LR(z) + y, LR(z) = z*S - z(z-1)/2 (rows of the layer back to
-//                back). A warp walks 32 rows, 8 lanes per row, streaming each row's bytes as
+//                z*S + y (a full S x S square per layer stack, so (w, y, z) is
+//                an affine 3-D tensor for TMA; rows y > S-1-z are never used). A warp walks 32 rows, 8 lanes per row, streaming each row's bytes as
 //                32-byte aligned chunks (2 x 16B loads per lane), packing them
 //                (IMAD gather + PRMT) and realigning at the bit level.
 // k_ca_bits      bit shadow -> next bit shadow. Work assignment is the map: a CTA
@@ -13,8 +13,8 @@
 //                blocks lane-parallel and chain x-adjacent tiles (predecessor at
 //                patch neighbour (wx-1, wy) for unfolded H tiles / wall plane / BB
 //                rows, (wx, wy-1) for the hinge fold, maps.hpp:334-336) into
-//                chunks of <= 96 cells. A warp takes a chunk: one 2-D TMA tensor
-//                box per halo layer (rho+2 rows x 12 words) lands the bit rows in
+//                chunks of <= 96 cells. A warp takes a chunk: one 3-D TMA tensor
+//                box (12 words x rho+2 rows x rho+2 layers) lands its halo in
 //                shared memory (double-buffered across chunks, mbarrier
 //                completion), lanes form the horizontal 3-sums as bit-planes, and
 //                lane (ly, w) marches along z with carry-save adders: 32 cells per
@@ -52,16 +52,17 @@ template <int RHO>
 struct Cfg {
     static constexpr int LMAX = OWN / RHO;              // tiles per chunk
     static constexpr int P = LMAX;                      // patch edge (blocks)
-    static constexpr int NB = P * P;                    // blocks per CTA
+    static constexpr int NZ = 4;                        // max wz layers per CTA
+    static constexpr int NB = P * P * NZ;               // max blocks per CTA
     static constexpr int HL = RHO + 2;                  // halo layers == halo rows per layer
     static constexpr int LPC = RHO * 4;                 // compute lanes per chunk
     static constexpr int CPI = 32 / LPC;                // chunks per warp item
-    static constexpr int BOXB = HL * BOXW * 4;          // bytes per TMA box
+    static constexpr int BOXB = HL * HL * BOXW * 4;     // bytes per TMA box (one per chunk)
     static constexpr int SLOT = (BOXB + 127) & ~127;    // 128B-aligned slot per box
-    static constexpr int BUF = CPI * HL * SLOT;         // one buffer: all boxes of an item
+    static constexpr int BUF = CPI * SLOT;              // one buffer: the boxes of an item
     static constexpr int HROWS = CPI * HL * HL;         // halo rows per item
     static constexpr int WARP_BYTES = (2 * BUF + HROWS * 32 + 64 + 127) & ~127;  // TMA dst: 128B aligned
-    static constexpr int SMEM = NWARP * WARP_BYTES + NB * 16 + NB * 16 + 128;
+    static int smem(int nb) { return NWARP * WARP_BYTES + nb * 32 + 128; }
 };
 
 struct Chunk {
@@ -89,10 +90,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint32_t mbar) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar)
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(mbar)
         : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
@@ -170,8 +173,8 @@ __device__ __forceinline__ uint32_t load_chunk_bits(const uint8_t* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
-// Row walk shared by pack/unpack. A warp owns 32 consecutive pitched rows and
-// works on 4 of them at a time, one 8-lane group per row (group g takes rows
+// Row walk shared by pack/unpack. A warp owns rpw (<= 32, a multiple of 4)
+// consecutive rows and works on 4 of them at a time, one 8-lane group per row (group g takes rows
 // r0+g, r0+g+4, ...): per-row bookkeeping is shared by the 8 lanes of a group
 // and each lane moves 32 bytes per pass.
 constexpr int ROWS_PER_WARP = 32;
@@ -206,10 +209,10 @@ __device__ __forceinline__ void row_next(RowCursor& c, int S, const unsigned lon
 // u8 packed state -> pitched bit shadow (bits beyond x = y are zero).
 __global__ void __launch_bounds__(256) k_pack_bits(const uint8_t* __restrict__ cur, uint32_t* __restrict__ bits,
                                                    int S, int WP, int nrows, const unsigned long long* __restrict__ PZ,
-                                                   unsigned long long ncells) {
+                                                   unsigned long long ncells, int rpw) {
     const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
     const unsigned gmask = 0xffu << (8 * grp);
-    const int row0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * ROWS_PER_WARP;
+    const int row0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * rpw;
     int r = row0 + grp;
     if (r >= nrows) return;
     RowCursor c = row_at(r, S, PZ);
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(256) k_pack_bits(const uint8_t* __restrict__ c
         const int n = c.y + 1, nw = (n + 31) >> 5;
         const long long A0 = c.rowbase & ~31ll;
         const int d = int(c.rowbase - A0);
-        uint32_t* out = bits + (long long)r * WP;
+        uint32_t* out = bits + ((long long)c.z * S + c.y) * WP;
         // lane gl packs chunk k; word k needs chunks k and k+1, so a pass emits
         // 7 words (lanes 0..6) and the next pass starts 7 chunks on
 #pragma unroll 2
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(256) k_pack_bits(const uint8_t* __restrict__ c
             }
         }
         r += 4;
-        if (r >= nrows || r >= row0 + ROWS_PER_WARP) break;
+        if (r >= nrows || r >= row0 + rpw) break;
 #pragma unroll
         for (int t = 0; t < 4; ++t) row_next(c, S, PZ);
     }
@@ -245,15 +248,15 @@ __global__ void __launch_bounds__(256) k_pack_bits(const uint8_t* __restrict__ c
 // neighbouring rows' windows) are byte stores.
 __global__ void __launch_bounds__(256) k_unpack_bits(const uint32_t* __restrict__ bits, uint8_t* __restrict__ out,
                                                      int S, int WP, int nrows,
-                                                     const unsigned long long* __restrict__ PZ) {
+                                                     const unsigned long long* __restrict__ PZ, int rpw) {
     const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
-    const int row0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * ROWS_PER_WARP;
+    const int row0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * rpw;
     int r = row0 + grp;
     if (r >= nrows) return;
     RowCursor c = row_at(r, S, PZ);
     for (;;) {
         const int n = c.y + 1;
-        const uint32_t* src = bits + (long long)r * WP;
+        const uint32_t* src = bits + ((long long)c.z * S + c.y) * WP;
         const long long e0 = c.rowbase, e1 = c.rowbase + n;
         long long a_lo = (e0 + 15) & ~15ll, a_hi = e1 & ~15ll;
         if (a_lo > a_hi) a_lo = a_hi = e1;  // no full window: every byte is an edge byte
@@ -281,56 +284,43 @@ __global__ void __launch_bounds__(256) k_unpack_bits(const uint32_t* __restrict_
             out[pos] = (uint8_t)((__ldg(src + (x >> 5)) >> (x & 31)) & 1u);
         }
         r += 4;
-        if (r >= nrows || r >= row0 + ROWS_PER_WARP) break;
+        if (r >= nrows || r >= row0 + rpw) break;
 #pragma unroll
         for (int t = 0; t < 4; ++t) row_next(c, S, PZ);
     }
 }
 
-// TMA issue for one warp item (lane 0): one box per valid halo layer per chunk.
+// TMA issue for one warp item (lane 0): one 3-D box (12 words x rho+2 rows x
+// rho+2 layers) per chunk; out-of-range coordinates land as zeros.
 template <int RHO>
 __device__ __forceinline__ void issue_item(const CUtensorMap* tm, const Chunk* s_chunk, int nchunks, int item,
-                                           uint8_t* buf, uint32_t mbar, int S) {
+                                           uint8_t* buf, uint32_t mbar) {
     using C = Cfg<RHO>;
-    uint32_t bytes = 0;
-    for (int c = 0; c < C::CPI; ++c) {
-        const int ci = item * C::CPI + c;
-        if (ci >= nchunks) break;
-        const Chunk ch = s_chunk[ci];
-        for (int zi = 0; zi < C::HL; ++zi) {
-            const int zz = ch.z0 - 1 + zi;
-            if (zz >= 0 && zz <= S - 1) bytes += C::BOXB;
-        }
-    }
-    mbar_expect_tx(mbar, bytes);
-    for (int c = 0; c < C::CPI; ++c) {
-        const int ci = item * C::CPI + c;
-        if (ci >= nchunks) break;
-        const Chunk ch = s_chunk[ci];
+    const int nc = min(C::CPI, nchunks - item * C::CPI);
+    mbar_expect_tx(mbar, uint32_t(nc * C::BOXB));
+    for (int c = 0; c < nc; ++c) {
+        const Chunk ch = s_chunk[item * C::CPI + c];
         const int w0 = ch.x0 >> 5;
-        for (int zi = 0; zi < C::HL; ++zi) {
-            const int zz = ch.z0 - 1 + zi;
-            if (zz < 0 || zz > S - 1) continue;
-            const int c0 = (w0 - 1) - ((w0 - 1) & 3);
-            tma_load_2d(smem_u32(buf + (c * C::HL + zi) * C::SLOT), tm, c0, layer_row(zz, S) + ch.y0 - 1, mbar);
-        }
+        const int c0 = (w0 - 1) - ((w0 - 1) & 3);
+        tma_load_3d(smem_u32(buf + c * C::SLOT), tm, c0, ch.y0 - 1, ch.z0 - 1, mbar);
     }
 }
 
 // ---------------------------------------------------------------------------
 template <int KIND, int RHO>
 __global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_constant__ CUtensorMap tmap,
-                                                  uint32_t* __restrict__ nbits, int WP, int P) {
+                                                  uint32_t* __restrict__ nbits, int WP, int P, int NZ, int wz1) {
     using C = Cfg<RHO>;
-    const int NBP = P * P;  // blocks in this launch's patch (P <= C::P)
+    const int PP = P * P;
+    const int NBP = PP * NZ;  // blocks of this CTA: a P x P patch at NZ consecutive wz
     constexpr int HL = C::HL;
     extern __shared__ __align__(128) uint8_t smem[];
     int4* s_tile = reinterpret_cast<int4*>(smem + NWARP * C::WARP_BYTES);
-    Chunk* s_chunk = reinterpret_cast<Chunk*>(smem + NWARP * C::WARP_BYTES + C::NB * 16);
-    int* s_nchunks = reinterpret_cast<int*>(smem + NWARP * C::WARP_BYTES + 2 * C::NB * 16);
+    Chunk* s_chunk = reinterpret_cast<Chunk*>(smem + NWARP * C::WARP_BYTES + NBP * 16);
+    int* s_nchunks = reinterpret_cast<int*>(smem + NWARP * C::WARP_BYTES + 2 * NBP * 16);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wz = blockIdx.z + wz0;
+    const int wzb = wz0 + blockIdx.z * NZ;
     const int S = g.side;
     const unsigned long long* __restrict__ PZ = g.prefix;
 
@@ -345,11 +335,12 @@ __global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_
         mbar_init(mbar0 + 8, 1);
     }
     for (int t = tid; t < NBP; t += NTHR) {
-        const int wx = blockIdx.x * P + (t % P), wy = blockIdx.y * P + (t / P);
+        const int tl = t % PP, wz = wzb + t / PP;
+        const int wx = blockIdx.x * P + (tl % P), wy = blockIdx.y * P + (tl / P);
         int4 v = make_int4(0, 0, 0, 0);
-        if (wx < g.ex && wy < g.ey) {
+        if (wx < g.ex && wy < g.ey && wz < wz1) {
             const outcome<int> o = map_block<KIND>(g, wx, wy, wz);
-            if (!o.is_void) v = make_int4(o.x, o.y, o.z, 1);
+            if (!o.is_void) v = make_int4(o.x, o.y, o.z, 1 | ((tl % P) << 8) | ((tl / P) << 16));
         }
         s_tile[t] = v;
     }
@@ -359,7 +350,7 @@ __global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_
     for (int t = tid; t < NBP; t += NTHR) {
         const int4 me = s_tile[t];
         if (!me.w) continue;
-        const int px = t % P, py = t / P;
+        const int px = (me.w >> 8) & 0xff, py = me.w >> 16;
         auto is_tile = [&](int i, int x) {
             const int4 o = s_tile[i];
             return o.w && o.x == x && o.y == me.y && o.z == me.z;
@@ -367,7 +358,7 @@ __global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_
         if ((px > 0 && is_tile(t - 1, me.x - 1)) || (py > 0 && is_tile(t - P, me.x - 1))) continue;
         int u = t, len = 1, x0 = me.x;
         for (;;) {
-            const int ux = u % P, uy = u / P;
+            const int uw = s_tile[u].w, ux = (uw >> 8) & 0xff, uy = uw >> 16;
             const int xn = s_tile[u].x + 1;
             int nxt = -1;
             if (ux + 1 < P && is_tile(u + 1, xn)) nxt = u + 1;
@@ -392,13 +383,13 @@ __global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_
     const CUtensorMap* tm = &tmap;
     if (item < nitems && lane == 0) {
         fence_proxy_async();
-        issue_item<RHO>(tm, s_chunk, nchunks, item, wbase, mbar0, S);
+        issue_item<RHO>(tm, s_chunk, nchunks, item, wbase, mbar0);
     }
     for (; item < nitems; item += NWARP, b ^= 1) {
         const int nxt = item + NWARP;
         if (nxt < nitems && lane == 0) {
             fence_proxy_async();
-            issue_item<RHO>(tm, s_chunk, nchunks, nxt, wbase + (b ^ 1) * C::BUF, mbar0 + 8 * (b ^ 1), S);
+            issue_item<RHO>(tm, s_chunk, nchunks, nxt, wbase + (b ^ 1) * C::BUF, mbar0 + 8 * (b ^ 1));
         }
         while (!mbar_try_wait(mbar0 + 8 * b, (phases >> b) & 1u)) {
         }
@@ -417,7 +408,7 @@ __global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_
                 if (zz >= 0 && yy >= 0 && yy + zz <= S - 1) {
                     const int off = ((ch.x0 >> 5) - 1) & 3;  // box word of w0 - 1
                     const uint32_t* src =
-                        reinterpret_cast<const uint32_t*>(buf + (c * HL + zi) * C::SLOT + yi * BOXW * 4) + off;
+                        reinterpret_cast<const uint32_t*>(buf + c * C::SLOT + (zi * HL + yi) * BOXW * 4) + off;
                     uint32_t T[6];
 #pragma unroll
                     for (int j = 0; j < 6; ++j) T[j] = src[j];
@@ -452,7 +443,7 @@ __global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_
             const bool cvalid = ci < nchunks;
             const Chunk ch = cvalid ? s_chunk[ci] : Chunk{0, 0, 0, 0};
             const uint32_t* H = sH + 8 * (cl * HL * HL);
-            const uint8_t* cbuf = buf + cl * HL * C::SLOT;
+            const uint8_t* cbuf = buf + cl * C::SLOT;
             auto vsum = [&](int zi) {
                 const int r0 = zi * HL + ly;
                 return add3x2(H[8 * r0 + w], H[8 * r0 + 4 + w], H[8 * (r0 + 1) + w], H[8 * (r0 + 1) + 4 + w],
@@ -466,14 +457,14 @@ __global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_
 #pragma unroll 2
             for (int lz = 0; lz < RHO; ++lz) {
                 const Planes4 vc = vsum(lz + 2);
-                const uint32_t alive = reinterpret_cast<const uint32_t*>(cbuf + (lz + 1) * C::SLOT +
-                                                                         (ly + 1) * BOXW * 4)[((w0 - 1) & 3) + 1 + w];
+                const uint32_t alive = reinterpret_cast<const uint32_t*>(
+                    cbuf + ((lz + 1) * HL + ly + 1) * BOXW * 4)[((w0 - 1) & 3) + 1 + w];
                 const uint32_t O = life_planes(va, vb, vc, alive);
                 va = vb;
                 vb = vc;
                 const int z = ch.z0 + lz;
                 if (!cvalid || y + z > S - 1 || ch.x0 > y || w0 + w > lastw || xw > y) continue;
-                nbits[(long long)(layer_row(z, S) + y) * WP + w0 + w] = O;
+                nbits[((long long)z * S + y) * WP + w0 + w] = O;
             }
         }
         __syncwarp();
@@ -485,16 +476,21 @@ void launch_t(const Geom& g, int wz0, int wz1, const CUtensorMap& tmap, uint32_t
     using C = Cfg<RHO>;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_ca_bits<KIND, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(k_ca_bits<KIND, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(C::NB));
         attr_set = true;
     }
     // patch edge: the largest that still gives >= 4 CTAs per SM (small grids
     // trade chunk length for parallelism)
-    int P = C::P;
-    auto ctas = [&](int p) { return (long long)((g.ex + p - 1) / p) * ((g.ey + p - 1) / p) * (wz1 - wz0); };
-    while (P > 4 && ctas(P) < 4 * 148) P = P / 2 > 4 ? P / 2 : 4;
-    const dim3 grid((g.ex + P - 1) / P, (g.ey + P - 1) / P, wz1 - wz0);
-    k_ca_bits<KIND, RHO><<<grid, NTHR, C::SMEM, s>>>(g, wz0, tmap, nbits, WP, P);
+    // and up to NZ wz layers per CTA (more chunks per warp keep the TMA
+    // double buffer busy) while the grid still gives >= 4 CTAs per SM
+    int P = C::P, NZ = C::NZ;
+    auto ctas = [&](int p, int nz) {
+        return (long long)((g.ex + p - 1) / p) * ((g.ey + p - 1) / p) * ((wz1 - wz0 + nz - 1) / nz);
+    };
+    while (NZ > 1 && ctas(P, NZ) < 4 * 148) NZ /= 2;
+    while (P > 4 && ctas(P, NZ) < 4 * 148) P = P / 2 > 4 ? P / 2 : 4;
+    const dim3 grid((g.ex + P - 1) / P, (g.ey + P - 1) / P, (wz1 - wz0 + NZ - 1) / NZ);
+    k_ca_bits<KIND, RHO><<<grid, NTHR, C::smem(P * P * NZ), s>>>(g, wz0, tmap, nbits, WP, P, NZ, wz1);
 }
 
 template <int KIND>
@@ -513,7 +509,17 @@ int bits_pitch_words(int side) {
     return w < 8 ? 8 : w;
 }
 
-unsigned long long bits_rows(int side) { return (unsigned long long)side * (side + 1) / 2; }
+// the shadow is a full S x S square of pitched rows per layer stack: row
+// (y, z) at z * S + y, so a chunk's halo is ONE 3-D tensor box
+unsigned long long bits_rows(int side) { return (unsigned long long)side * side; }
+static int tri_rows(int side) { return int((long long)side * (side + 1) / 2); }
+// rows per warp for pack/unpack: 32 on big states, fewer (>= 4) until the grid
+// has ~32 warps per SM
+static int rows_per_warp(int nrows) {
+    int r = ROWS_PER_WARP;
+    while (r > 4 && (nrows + r - 1) / r < 148 * 32) r /= 2;
+    return r;
+}
 
 int tma_box_rows(int rho) { return rho + 2; }
 
@@ -521,16 +527,18 @@ int tma_box_words() { return BOXW; }
 
 void launch_pack_bits(const Geom& g, const uint8_t* cur, uint32_t* bits, cudaStream_t s) {
     const int S = g.side, WP = bits_pitch_words(S);
-    const int nrows = int(bits_rows(S));
-    const int warps = (nrows + ROWS_PER_WARP - 1) / ROWS_PER_WARP;
-    k_pack_bits<<<(warps + 7) / 8, 256, 0, s>>>(cur, bits, S, WP, nrows, g.prefix, tet_cells(S));
+    const int nrows = tri_rows(S);
+    const int rpw = rows_per_warp(nrows);
+    const int warps = (nrows + rpw - 1) / rpw;
+    k_pack_bits<<<(warps + 7) / 8, 256, 0, s>>>(cur, bits, S, WP, nrows, g.prefix, tet_cells(S), rpw);
 }
 
 void launch_unpack_bits(const Geom& g, const uint32_t* bits, uint8_t* out, cudaStream_t s) {
     const int S = g.side, WP = bits_pitch_words(S);
-    const int nrows = int(bits_rows(S));
-    const int warps = (nrows + ROWS_PER_WARP - 1) / ROWS_PER_WARP;
-    k_unpack_bits<<<(warps + 7) / 8, 256, 0, s>>>(bits, out, S, WP, nrows, g.prefix);
+    const int nrows = tri_rows(S);
+    const int rpw = rows_per_warp(nrows);
+    const int warps = (nrows + rpw - 1) / rpw;
+    k_unpack_bits<<<(warps + 7) / 8, 256, 0, s>>>(bits, out, S, WP, nrows, g.prefix, rpw);
 }
 
 void launch_ca_bits(const Geom& g, int kind, int wz0, int wz1, const void* tmap_ptr, uint32_t* nbits, cudaStream_t s) {

@@ -224,8 +224,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// 2-D tiled tensor map over a pitched bit shadow: dim0 = WP words, dim1 = rows;
-// box = tma_box_words() x (rho + 2) rows; out-of-range coordinates read as zero.
+// 3-D tiled tensor map over a pitched bit shadow: (WP words, S rows, S layers);
+// box = tma_box_words() x (rho + 2) x (rho + 2); out-of-range coordinates read as zero.
 int bits_tmap(const uint32_t* bits, int64_t side, int64_t rho, const CUtensorMap** out) {
     DeviceRes* r;
     if (int rc = device_res(&r)) return rc;
@@ -239,12 +239,13 @@ int bits_tmap(const uint32_t* bits, int64_t side, int64_t rho, const CUtensorMap
     auto fn = encode_fn();
     if (!fn) return fail(SMX_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
     const int WP = smx::bits_pitch_words(int(side));
-    cuuint64_t dims[2] = {cuuint64_t(WP), cuuint64_t(smx::bits_rows(int(side)))};
-    cuuint64_t strides[1] = {cuuint64_t(WP) * 4};
-    cuuint32_t box[2] = {cuuint32_t(smx::tma_box_words()), cuuint32_t(smx::tma_box_rows(int(rho)))};
-    cuuint32_t estr[2] = {1u, 1u};
+    const cuuint32_t HB = cuuint32_t(smx::tma_box_rows(int(rho)));
+    cuuint64_t dims[3] = {cuuint64_t(WP), cuuint64_t(side), cuuint64_t(side)};
+    cuuint64_t strides[2] = {cuuint64_t(WP) * 4, cuuint64_t(WP) * 4 * cuuint64_t(side)};
+    cuuint32_t box[3] = {cuuint32_t(smx::tma_box_words()), HB, HB};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
     CUtensorMap m;
-    CUresult cr = fn(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(bits), dims, strides, box, estr,
+    CUresult cr = fn(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(bits), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return fail(SMX_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(cr)));

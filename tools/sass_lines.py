@@ -63,7 +63,7 @@ def main():
         stall[key] += float(r[ist] or 0)
         tot += v
     st = sum(stall.values()) or 1
-    for k, v in inst.most_common(40):
+    for k, v in inst.most_common(int(os.environ.get("TOPN", "40"))):
         print(f"{100 * v / tot:6.2f}% inst  {100 * stall[k] / st:6.2f}% stall  {k}")
 
 
