@@ -1,0 +1,272 @@
+"""Multi-GPU sharding of the H3D block space for the 3-D Life CA.
+
+The H grid is split along wz into contiguous ranges of whole layers — the major
+half-cube layers (wz < n/2) and the stacked power-of-two slab levels above them —
+balanced by useful (non-Void) block count. Every rank keeps a full replica of the
+packed u8 state, steps only the blocks of its wz range (smx_ca_step_range), and
+then exchanges, over torch.distributed (NCCL on GPUs), whole tiles of its fresh
+output that a peer's tiles touch through the 26-neighbourhood. The halo plan is
+static (the map is): built once from the grid's map outcomes.
+
+ACCUM and the MAP kernel need no exchange (blocks are independent): a rank simply
+runs its wz/wy range; only the u64 counters would be summed.
+
+The exchange is the only collective on the data path: one grouped
+send/recv (all-to-all-v over NVSwitch) of rho^3-byte tiles per step.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+
+
+def tet_cells(side: int) -> int:
+    return side * (side + 1) * (side + 2) // 6 if side >= 1 else 0
+
+
+def tet_index(side: int, x, y, z):
+    """core.hpp:140-149 vectorised (int64 numpy arrays)."""
+    full = tet_cells(side)
+    s = side - z
+    rest = np.where(z >= side, 0, s * (s + 1) * (s + 2) // 6)
+    prefix = np.where(z == 0, 0, full - rest)
+    return prefix + y * (y + 1) // 2 + x
+
+
+def tet_contains(side: int, x, y, z):
+    return (x >= 0) & (x <= y) & (z >= 0) & (y <= side - 1 - z)
+
+
+@dataclasses.dataclass
+class HaloPlan:
+    world: int
+    wz_ranges: list[tuple[int, int]]       # rank -> [lo, hi) of the H grid's wz
+    send: list[dict[int, np.ndarray]]      # rank -> {peer: (k, 3) int32 tiles, sorted}
+    owned_tiles: list[np.ndarray]          # rank -> (k, 3) int32 tiles it computes
+    domain_blocks: int                     # D: with-diagonal block-domain side
+
+    def recv(self, rank: int) -> dict[int, np.ndarray]:
+        return {q: self.send[q][rank] for q in range(self.world) if rank in self.send[q]}
+
+    def halo_tiles(self, rank: int) -> int:
+        return int(sum(v.shape[0] for v in self.send[rank].values()))
+
+
+def tiles_from_outcomes(outcomes: np.ndarray, strict: bool):
+    """Non-void block outcomes -> with-diagonal tile coords (simulator.hpp:202)."""
+    o = np.asarray(outcomes)
+    keep = o[:, 0] == 0
+    t = o[keep][:, 1:4].astype(np.int64).copy()
+    if strict:
+        t[:, 1] -= 1
+    return keep, t
+
+
+def partition_wz(useful_per_wz: np.ndarray, world: int) -> list[tuple[int, int]]:
+    """Contiguous wz ranges with ~equal useful-block counts (whole layers)."""
+    ez = useful_per_wz.size
+    total = float(useful_per_wz.sum())
+    cum = np.concatenate([[0.0], np.cumsum(useful_per_wz, dtype=np.float64)])
+    cuts = [0]
+    for r in range(1, world):
+        target = total * r / world
+        k = int(np.searchsorted(cum, target, side="left"))
+        k = max(cuts[-1], min(k, ez))
+        cuts.append(k)
+    cuts.append(ez)
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+_OFFSETS = np.array([(dx, dy, dz) for dz in (-1, 0, 1) for dy in (-1, 0, 1) for dx in (-1, 0, 1)
+                     if (dx, dy, dz) != (0, 0, 0)], np.int64)
+
+
+def build_plan(extents: tuple[int, int, int], outcomes: np.ndarray, strict: bool, domain_blocks: int,
+               world: int) -> HaloPlan:
+    """outcomes: one row per block in natural z, y, x order, columns
+    {is_void, x, y, z, ...} (api.map_outcomes / oracle outcomes)."""
+    ex, ey, ez = extents
+    o = np.asarray(outcomes)
+    wz = np.arange(o.shape[0], dtype=np.int64) // (ex * ey)
+    keep, tiles = tiles_from_outcomes(o, strict)
+    wz = wz[keep]
+    useful = np.bincount(wz, minlength=ez)
+    ranges = partition_wz(useful, world)
+    owner_of_block = np.zeros(tiles.shape[0], np.int32)
+    for r, (lo, hi) in enumerate(ranges):
+        owner_of_block[(wz >= lo) & (wz < hi)] = r
+    D = domain_blocks
+    owner = np.full(tet_cells(D), -1, np.int32)
+    idx = tet_index(D, tiles[:, 0], tiles[:, 1], tiles[:, 2])
+    owner[idx] = owner_of_block
+    send: list[dict[int, np.ndarray]] = [dict() for _ in range(world)]
+    pairs = []
+    for off in _OFFSETS:
+        nb = tiles + off
+        ok = tet_contains(D, nb[:, 0], nb[:, 1], nb[:, 2])
+        nb_owner = np.full(tiles.shape[0], -1, np.int32)
+        nb_owner[ok] = owner[tet_index(D, nb[ok, 0], nb[ok, 1], nb[ok, 2])]
+        m = ok & (nb_owner != owner_of_block) & (nb_owner >= 0)
+        if m.any():
+            pairs.append(np.stack([owner_of_block[m], nb_owner[m], np.nonzero(m)[0]], axis=1))
+    if pairs:
+        P = np.unique(np.concatenate(pairs), axis=0)
+        for q in range(world):
+            for r in range(world):
+                sel = P[(P[:, 0] == q) & (P[:, 1] == r), 2]
+                if sel.size:
+                    t = tiles[np.unique(sel)]
+                    order = np.lexsort((t[:, 0], t[:, 1], t[:, 2]))
+                    send[q][r] = np.ascontiguousarray(t[order].astype(np.int32))
+    owned = [np.ascontiguousarray(tiles[owner_of_block == r].astype(np.int32)) for r in range(world)]
+    return HaloPlan(world, ranges, send, owned, D)
+
+
+class ShardedLife:
+    """One rank of a sharded 3-D Life run. `ops` provides the compute:
+        ops.step_range(cur, nxt, wz_lo, wz_hi)
+        ops.pack(cells, tiles, out)      tiles (k,3) int32 -> out (k*rho^3,) u8
+        ops.unpack(cells, tiles, buf)
+        ops.empty(nbytes) -> u8 buffer, ops.tiles(np_array) -> tile tensor
+    so the same orchestration runs on CUDA tensors over NCCL (the product) and on
+    CPU tensors over gloo (tests)."""
+
+    def __init__(self, plan: HaloPlan, rank: int, rho: int, ops, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.plan, self.rank, self.rho, self.ops, self.group = plan, rank, rho, ops, group
+        self.lo, self.hi = plan.wz_ranges[rank]
+        r3 = rho ** 3
+        self.send_t = {q: ops.tiles(t) for q, t in plan.send[rank].items()}
+        self.recv_t = {q: ops.tiles(t) for q, t in plan.recv(rank).items()}
+        self.send_b = {q: ops.empty(t.shape[0] * r3) for q, t in plan.send[rank].items()}
+        self.recv_b = {q: ops.empty(t.shape[0] * r3) for q, t in plan.recv(rank).items()}
+
+    def exchange(self, buf) -> None:
+        d = self.dist
+        for q, t in self.send_t.items():
+            self.ops.pack(buf, t, self.send_b[q])
+        ops = [d.P2POp(d.isend, self.send_b[q], q, self.group) for q in self.send_b]
+        ops += [d.P2POp(d.irecv, self.recv_b[q], q, self.group) for q in self.recv_b]
+        if ops:
+            for req in d.batch_isend_irecv(ops):
+                req.wait()
+        for q, t in self.recv_t.items():
+            self.ops.unpack(buf, t, self.recv_b[q])
+
+    def step(self, cur, nxt) -> None:
+        self.ops.step_range(cur, nxt, self.lo, self.hi)
+        self.exchange(nxt)
+
+    def run(self, cur, nxt, steps: int):
+        for _ in range(steps):
+            self.step(cur, nxt)
+            cur, nxt = nxt, cur
+        return cur
+
+    def gather_owned(self, cells, dst=0):
+        """Every rank's owned tiles onto `dst` (for hashing / parity)."""
+        d = self.dist
+        r3 = self.rho ** 3
+        owned = self.plan.owned_tiles
+        if self.rank == dst:
+            for q in range(self.plan.world):
+                if q == dst:
+                    continue
+                buf = self.ops.empty(owned[q].shape[0] * r3)
+                d.recv(buf, q, self.group)
+                self.ops.unpack(cells, self.ops.tiles(owned[q]), buf)
+        else:
+            t = self.ops.tiles(owned[self.rank])
+            buf = self.ops.empty(owned[self.rank].shape[0] * r3)
+            self.ops.pack(cells, t, buf)
+            d.send(buf, dst, self.group)
+
+
+class CudaOps:
+    """The product ops: sm_100a kernels through the C ABI on CUDA tensors."""
+
+    def __init__(self, grid, exec_=None):
+        from . import api
+
+        self.api, self.g = api, grid
+        self.exec = api.EXEC_AUTO if exec_ is None else exec_
+
+    def step_range(self, cur, nxt, lo, hi):
+        self.api.ca_step_range_device(self.g, cur, nxt, lo, hi, self.exec)
+
+    def pack(self, cells, tiles, out):
+        self.api.tiles_pack_device(self.g, cells, tiles, out)
+
+    def unpack(self, cells, tiles, buf):
+        self.api.tiles_unpack_device(self.g, cells, tiles, buf)
+
+    def empty(self, n):
+        import torch
+        return torch.empty(max(n, 1), dtype=torch.uint8, device="cuda")
+
+    def tiles(self, t):
+        import torch
+        return torch.from_numpy(np.ascontiguousarray(t, dtype=np.int32).reshape(-1, 3)).cuda()
+
+
+def bench_sharded(args, api):
+    """bench.py --gpus N under torchrun: the C2 CA step sharded over N GPUs."""
+    import json  # noqa: F401
+    import os
+    import statistics
+
+    import torch
+    import torch.distributed as dist
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from bench import SEED, WORKLOADS, Flusher, load_peaks, timed_steps  # noqa: E402
+
+    desc, kind, n, rho = WORKLOADS[args.workload]
+    g = api.make_grid(api.map_kind[kind], 3, n, rho)
+    side = g.cell_side()
+    cells = api.tet_cells(side)
+    out = api.map_outcomes(g)
+    plan = build_plan(g.extents, out, True, g.domain_side(), world)
+    ops = CudaOps(g)
+    sh = ShardedLife(plan, rank, rho, ops)
+    a = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
+    b = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
+    api.life_init_device(3, side, SEED, a)
+    bufs = [a, b]
+    flush = Flusher()
+
+    def step(i):
+        sh.step(bufs[i % 2], bufs[(i + 1) % 2])
+
+    dist.barrier()
+    timed_steps(step, args.warmup, flush)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = timed_steps(step, args.steps, flush)
+    tot = torch.tensor([sum(ms)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms_step = float(tot.item()) / args.steps
+    peak, peak_src = load_peaks()
+    line = None
+    if rank == 0:
+        line = {
+            "metric": "Gcells/s (3-simplex CA step, H map) — BASELINE metric: Gcells/s and H-vs-BB speedup; "
+                      "HBM GB/s vs peak; J/cell",
+            "value": round(cells / (ms_step * 1e-3) / 1e9, 3), "unit": "Gcells/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 6),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (make_life_state seed 42)", "impl": "ours",
+            "config": {"workload": desc, "map": kind, "n_b": n, "rho": rho, "side": side, "cells": cells,
+                       "parallelism": f"H wz-range shards x{world}, tile halo over NCCL",
+                       "wz_ranges": plan.wz_ranges, "halo_tiles_per_rank": [plan.halo_tiles(r) for r in
+                                                                            range(world)]},
+            "gpu_launches": args.steps * 3,
+        }
+    dist.destroy_process_group()
+    return line

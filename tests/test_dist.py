@@ -1,0 +1,134 @@
+"""Multi-rank path on CPU (gloo, world sizes 2 and 3): the H3D wz partition, the
+static tile halo plan and the exchange orchestration of paper_2208_11617_b200.dist,
+with the CPU oracle standing in for the per-rank step (test infrastructure only).
+
+Non-owned cells are poisoned after every local step, so the result is correct
+only if every tile a rank reads arrives through the halo plan."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle.oracle import BB, H3D, Restated, tet_cells
+from paper_2208_11617_b200 import dist as D
+
+
+def tile_cells(side, rho, tiles):
+    """(k, rho^3) packed indices (or -1) of every tile's cells, lz, ly, lx order."""
+    l = np.arange(rho)
+    lz, ly, lx = np.meshgrid(l, l, l, indexing="ij")
+    t = np.asarray(tiles, np.int64).reshape(-1, 3)
+    cx = t[:, 0, None] * rho + lx.ravel()[None]
+    cy = t[:, 1, None] * rho + ly.ravel()[None]
+    cz = t[:, 2, None] * rho + lz.ravel()[None]
+    ok = D.tet_contains(side, cx, cy, cz)
+    idx = np.where(ok, D.tet_index(side, np.where(ok, cx, 0), np.where(ok, cy, 0), np.where(ok, cz, 0)), -1)
+    return idx
+
+
+class OracleOps:
+    """CPU stand-in for CudaOps: oracle full step, keep own tiles, poison the rest."""
+
+    def __init__(self, orc, side, rho, own_idx, seed):
+        self.orc, self.side, self.rho = orc, side, rho
+        self.own = np.zeros(tet_cells(side), bool)
+        self.own[own_idx[own_idx >= 0]] = True
+        self.rng = np.random.default_rng(seed)
+
+    def step_range(self, cur, nxt, lo, hi):
+        c = cur.numpy().copy()
+        self.orc.ca3d_run(self.side, 1, c, threads=1)
+        n = nxt.numpy()
+        n[:] = self.rng.integers(0, 2, n.size, dtype=np.uint8)
+        n[self.own] = c[self.own]
+
+    def pack(self, cells, tiles, out):
+        idx = tile_cells(self.side, self.rho, tiles.numpy())
+        v = np.where(idx >= 0, cells.numpy()[np.maximum(idx, 0)], 0).astype(np.uint8)
+        out.numpy()[:] = v.ravel()
+
+    def unpack(self, cells, tiles, buf):
+        idx = tile_cells(self.side, self.rho, tiles.numpy()).ravel()
+        b = buf.numpy()
+        m = idx >= 0
+        cells.numpy()[idx[m]] = b[m]
+
+    def empty(self, n):
+        return torch.zeros(max(n, 1), dtype=torch.uint8)
+
+    def tiles(self, t):
+        return torch.from_numpy(np.ascontiguousarray(t, dtype=np.int32).reshape(-1, 3))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, kind, n, rho, steps, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Restated()
+    m = 3
+    outcomes = orc.map_outcomes(kind, m, n)
+    ext = orc.grid(kind, m, n)
+    strict = kind == H3D
+    dom_blocks = n - 1 if strict else n
+    side = dom_blocks * rho
+    plan = D.build_plan(ext, outcomes, strict, dom_blocks, world)
+    own_idx = tile_cells(side, rho, plan.owned_tiles[rank])
+    ops = OracleOps(orc, side, rho, own_idx, seed=rank + 7)
+    sh = D.ShardedLife(plan, rank, rho, ops)
+    cur = torch.from_numpy(orc.make_life_state(3, side, 42, threads=1))
+    nxt = torch.zeros_like(cur)
+    res = sh.run(cur, nxt, steps)
+    sh.gather_owned(res, 0)
+    if rank == 0:
+        want = orc.make_life_state(3, side, 42, threads=1)
+        orc.ca3d_run(side, steps, want, threads=1)
+        q.put((bool((res.numpy() == want).all()), plan.wz_ranges, [plan.halo_tiles(r) for r in range(world)]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,kind,n,rho,steps", [(2, H3D, 16, 2, 4), (3, H3D, 16, 2, 3), (2, BB, 15, 2, 3),
+                                                    (2, H3D, 32, 1, 3)])
+def test_sharded_life_matches_oracle(world, kind, n, rho, steps):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, n, rho, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    ok, ranges, halos = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert ok, (ranges, halos)
+    assert len(ranges) == world and ranges[0][0] == 0
+    assert all(h > 0 for h in halos)
+
+
+def test_partition_balanced_whole_levels():
+    orc = Restated()
+    for n, world in [(64, 8), (128, 8), (32, 2)]:
+        out = orc.map_outcomes(H3D, 3, n)
+        ext = orc.grid(H3D, 3, n)
+        plan = D.build_plan(ext, out, True, n - 1, world)
+        counts = [t.shape[0] for t in plan.owned_tiles]
+        assert sum(counts) == tet_cells(n - 1)
+        assert max(counts) / (sum(counts) / world) < 1.15
+        # contiguous, covering wz ranges
+        assert plan.wz_ranges[0][0] == 0 and plan.wz_ranges[-1][1] == ext[2]
+        assert all(a[1] == b[0] for a, b in zip(plan.wz_ranges, plan.wz_ranges[1:]))
+        # halo symmetric bookkeeping: what q sends r is what r receives from q
+        for r in range(world):
+            for q, t in plan.recv(r).items():
+                assert (plan.send[q][r] == t).all()

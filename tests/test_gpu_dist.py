@@ -1,0 +1,83 @@
+"""The sharded 3-D Life path on ONE GPU: two ranks on cuda:0 run the real
+sm_100a step-range and tile pack/unpack kernels; their halo travels over gloo
+through host staging (NCCL rejects two ranks on one device). The orchestration
+is paper_2208_11617_b200.dist.ShardedLife, unchanged."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, kind, n, rho, ex, steps, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle.oracle import Restated
+    from paper_2208_11617_b200 import api
+    from paper_2208_11617_b200 import dist as D
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    class StagedOps(D.CudaOps):
+        def empty(self, n_):
+            return torch.zeros(max(n_, 1), dtype=torch.uint8)  # host buffers for gloo
+
+        def pack(self, cells, tiles, out):
+            tmp = torch.empty(out.numel(), dtype=torch.uint8, device="cuda")
+            super().pack(cells, tiles, tmp)
+            out.copy_(tmp.cpu())
+
+        def unpack(self, cells, tiles, buf):
+            super().unpack(cells, tiles, buf.cuda())
+
+    g = api.make_grid(api.map_kind[kind], 3, n, rho)
+    side = g.cell_side()
+    cells = api.tet_cells(side)
+    plan = D.build_plan(g.extents, api.map_outcomes(g), kind == "h3d", g.domain_side(), world)
+    sh = D.ShardedLife(plan, rank, rho, StagedOps(g, ex))
+    a = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
+    b = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
+    api.life_init_device(3, side, 42, a)
+    b.fill_(1)  # garbage outside owned + halo tiles must never matter
+    res = sh.run(a, b, steps)
+    torch.cuda.synchronize()
+    sh.gather_owned(res, 0)
+    if rank == 0:
+        orc = Restated()
+        want = orc.make_life_state(3, side, 42)
+        orc.ca3d_run(side, steps, want)
+        q.put(bool((res.cpu().numpy() == want).all()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,n,rho,ex", [("h3d", 32, 4, 1), ("h3d", 32, 8, 1), ("bb", 31, 4, 1),
+                                           ("h3d", 16, 4, 0)])
+def test_sharded_step_on_one_gpu(cuda, kind, n, rho, ex):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 2
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, n, rho, ex, 4, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert ok
