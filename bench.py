@@ -159,24 +159,72 @@ class Flusher:
 
 
 def ca_case(api, kind, n, rho, steps, warmup, flush, exec_=None):
-    """Time `steps` CA steps on grid (kind, n, rho); returns dict."""
+    """Time `steps` CA steps (u8 state -> u8 state) on grid (kind, n, rho).
+    x-run scheme: the three stages smx_ca_step chains (pack -> bit-sliced step ->
+    unpack) are timed individually with events on the launching stream; the
+    step time is pack-start to unpack-end. Block scheme: one kernel."""
     import torch
     g = api.make_grid(api.map_kind[kind], 3, n, rho)
     side = g.cell_side()
     cells = api.tet_cells(side)
-    a = torch.empty(cells, dtype=torch.uint8, device="cuda")
-    b = torch.empty_like(a)
+    a = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
+    b = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
     api.life_init_device(3, side, SEED, a)
-    ex = api.EXEC_AUTO if exec_ is None else exec_
+    ex = api.EXEC_RUNS if exec_ is None else exec_
     bufs = [a, b]
+    res = {"grid": f"{kind}({n}) rho={rho}", "side": side, "cells": cells, "g": g, "bufs": bufs}
+    if ex == api.EXEC_BLOCK:
+        def step(i):
+            api.ca_step_device(g, bufs[i % 2], bufs[(i + 1) % 2], ex)
 
-    def step(i):
-        api.ca_step_device(g, bufs[i % 2], bufs[(i + 1) % 2], ex)
+        timed_steps(step, warmup, flush)
+        res["ms"] = timed_steps(step, steps, flush)
+        res["step"] = step
+        return res
+    sa, sb = api.bits_buffer(g), api.bits_buffer(g)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
 
-    timed_steps(step, warmup, flush)
-    ms = timed_steps(step, steps, flush)
-    return {"grid": f"{kind}({n}) rho={rho}", "side": side, "cells": cells, "ms": ms, "g": g,
-            "bufs": bufs, "step": step}
+    def step(i, e=None):
+        cur, nxt = bufs[i % 2], bufs[(i + 1) % 2]
+        if e: e[0].record()
+        api.bits_pack_device(g, cur, sa)
+        if e: e[1].record()
+        api.bits_step_device(g, sa, sb)
+        if e: e[2].record()
+        api.bits_unpack_device(g, sb, nxt)
+        if e: e[3].record()
+
+    for i in range(warmup):
+        flush()
+        step(i)
+    for i in range(steps):
+        flush()
+        step(i, ev[i])
+    torch.cuda.synchronize()
+    res["stage_ms"] = {name: statistics.mean(e[k].elapsed_time(e[k + 1]) for e in ev)
+                       for k, name in enumerate(("pack", "step", "unpack"))}
+
+    # the step itself: ONE smx_ca_step call (the library launches the three
+    # kernels back to back; per-stage events above would add host gaps)
+    def abi_step(i):
+        api.ca_step_device(g, bufs[i % 2], bufs[(i + 1) % 2], api.EXEC_RUNS)
+
+    timed_steps(abi_step, warmup, flush)
+    res["ms"] = timed_steps(abi_step, steps, flush)
+    res["step"] = abi_step
+
+    # multi-step engine (smx_ca): the bit shadow carries over, so a step is
+    # step + unpack (the u8 state is still written every step)
+    def estep(i):
+        src, dst = (sa, sb) if i % 2 == 0 else (sb, sa)
+        api.bits_step_device(g, src, dst)
+        api.bits_unpack_device(g, dst, bufs[(i + 1) % 2])
+
+    api.bits_pack_device(g, a, sa)
+    timed_steps(estep, 2, flush)
+    api.bits_pack_device(g, a, sa)
+    res["engine_ms"] = timed_steps(estep, steps, flush)
+    return res
 
 
 def accum_case(api, kind, n, rho, steps, warmup, flush, exec_):
@@ -217,6 +265,18 @@ def energy_per_cell(sampler, step, cells, seconds=0.5):
     return (e1 - e0) * 1e-3 / (cells * i) if e1 is not None else None
 
 
+def ncu_step_traffic():
+    """DRAM bytes per C2 step (sum over the step's kernels) from the committed
+    ncu summary (profiles/ncu_summary.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        return json.load(open(p)).get("c2_step", {}).get("dram_bytes_per_step")
+    except Exception:
+        return None
+
+
 def run_ours(args):
     import torch
     from paper_2208_11617_b200 import api
@@ -235,14 +295,15 @@ def run_ours(args):
     with sampler:
         h = ca_case(api, kind, n, rho, args.steps, args.warmup, flush)
     bb = ca_case(api, "bb", n - 1, rho, args.steps, args.warmup, flush)
+    hb = ca_case(api, kind, n, rho, args.steps, args.warmup, flush, api.EXEC_BLOCK)
+    bbb = ca_case(api, "bb", n - 1, rho, args.steps, args.warmup, flush, api.EXEC_BLOCK)
     cells = h["cells"]
-    ms_h = statistics.mean(h["ms"])
-    ms_bb = statistics.mean(bb["ms"])
+    ms_h, ms_bb = statistics.mean(h["ms"]), statistics.mean(bb["ms"])
     value = gcells(cells, ms_h)
     achieved = 2.0 * cells / (ms_h * 1e-3) / 1e9
-    traffic = ncu_traffic("ca_runs_c2")
 
-    # e2e: reference-facing C ABI call with host (pinned) buffers, H2D+step+D2H
+    # e2e: the reference-facing C ABI (smx_ca, launch_ca's semantics) with host
+    # pinned buffers: H2D + one step + D2H inside the timed region
     host = torch.empty(cells, dtype=torch.uint8, pin_memory=True)
     api.life_init_device(3, h["side"], SEED, h["bufs"][0])
     host.copy_(h["bufs"][0].cpu())
@@ -259,14 +320,11 @@ def run_ours(args):
     timed_steps(e2e_step, args.warmup)
     e2e_ms = statistics.mean(timed_steps(e2e_step, args.steps))
 
-    # energy per cell, H vs BB (NVML total energy over ~0.5 s of back-to-back steps)
     j_h = energy_per_cell(sampler, h["step"], cells)
     j_bb = energy_per_cell(sampler, bb["step"], cells)
-
-    # CPU baseline: the reference's launch_ca on the same grid, 1 step, 1 core
     cpu = cpu_baseline_c2(kind, n, rho, h["side"])
-
     configs = {} if args.no_configs else extra_configs(api, flush, sampler, peak, args)
+    st = h["stage_ms"]
     line = {
         "metric": "Gcells/s (3-simplex CA step, H map) — BASELINE metric: Gcells/s and H-vs-BB speedup; "
                   "HBM GB/s vs peak; J/cell",
@@ -283,20 +341,29 @@ def run_ours(args):
         "data": "synthetic (make_life_state seed 42, ~25% alive)",
         "impl": "ours",
         "config": {"workload": desc, "map": "h3d", "n_b": n, "rho": rho, "side": h["side"], "cells": cells,
-                   "exec": "runs", "l2": "flushed before every timed step (256 MiB write)",
-                   "parallelism": "single GPU"},
+                   "exec": "x-run (pack -> bit-sliced step -> unpack)",
+                   "l2": "flushed before every timed step (256 MiB write)", "parallelism": "single GPU"},
         "h_vs_bb": round(ms_bb / ms_h, 3),
         "bb": {"grid": bb["grid"], "gcells_s": round(gcells(cells, ms_bb), 3), "ms_per_step": round(ms_bb, 6)},
+        "block_scheme": {"h_gcells_s": round(gcells(cells, statistics.mean(hb["ms"])), 3),
+                         "bb_gcells_s": round(gcells(cells, statistics.mean(bbb["ms"])), 3),
+                         "h_vs_bb": round(statistics.mean(bbb["ms"]) / statistics.mean(hb["ms"]), 3),
+                         "note": "the paper's launch model: one CTA per map block, rho^3 threads"},
+        "engine": {"gcells_s": round(gcells(cells, statistics.mean(h["engine_ms"])), 3),
+                   "ms_per_step": round(statistics.mean(h["engine_ms"]), 6),
+                   "note": "multi-step launch_ca: bit shadow carried across steps (step + unpack per step)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "basis": "2 B per useful cell per step (u8 read + write), CUDA events per launch",
+                     "frac": round(achieved / peak, 4), "traffic": ncu_step_traffic(),
+                     "kernel": "one u8->u8 CA step = k_pack_bits + k_ca_bits + k_unpack_bits",
+                     "basis": "2 B per useful cell per step (u8 read + u8 write); per-launch CUDA events",
+                     "stage_ms": {k: round(v, 6) for k, v in st.items()},
                      "peak_source": peak_src},
         "e2e": {"value": round(gcells(cells, e2e_ms), 3), "unit": "Gcells/s", "h2d_bytes_per_step": cells,
                 "d2h_bytes_per_step": cells, "ms_per_step": round(e2e_ms, 4),
-                "path": "smx_ca(host buffer) C ABI"},
+                "path": "smx_ca(host buffer, steps=1) through the C ABI"},
         "energy": {"j_per_cell_h": j_h, "j_per_cell_bb": j_bb},
         "cpu_baseline": cpu,
-        "gpu_launches": args.steps,
+        "gpu_launches": 3 * args.steps,
         "clocks": sampler.summary(),
         "configs": configs,
     }
@@ -320,27 +387,29 @@ def cpu_baseline_c2(kind, n, rho, side):
 
 
 def extra_configs(api, flush, sampler, peak, args):
+    """The other BASELINE configs at 1 GPU (H and BB, both execution schemes)."""
     import torch
     out = {}
     K, W = max(5, min(args.steps, 10)), 3
 
-    def accum_pair(name, n, rho):
+    def accum_pair(n, rho):
         r = {}
         for ex_name, ex in (("runs", api.EXEC_RUNS), ("block", api.EXEC_BLOCK)):
             h = accum_case(api, "h2d", n, rho, K, W, flush, ex)
             hms = statistics.mean(h["ms"])
+            if ex_name == "runs":
+                r["j_per_cell_h"] = energy_per_cell(sampler, h["step"], h["cells"], 0.3)
             del h["tensor"]
             torch.cuda.empty_cache()
             b = accum_case(api, "bb", n - 1, rho, K, W, flush, ex)
             bms = statistics.mean(b["ms"])
+            if ex_name == "runs":
+                r["j_per_cell_bb"] = energy_per_cell(sampler, b["step"], b["cells"], 0.3)
             gbs = 8.0 * h["cells"] / (hms * 1e-3) / 1e9
             r[ex_name] = {"h_gcells_s": round(gcells(h["cells"], hms), 2),
                           "bb_gcells_s": round(gcells(b["cells"], bms), 2),
                           "h_vs_bb": round(bms / hms, 3), "h_gb_s": round(gbs, 1),
                           "h_roofline_frac": round(gbs / peak, 4), "parity_ok": h["ok"] and b["ok"]}
-            if ex_name == "runs":
-                r["j_per_cell_h"] = energy_per_cell(sampler, h["step"], h["cells"], 0.3)
-                r["j_per_cell_bb"] = energy_per_cell(sampler, b["step"], b["cells"], 0.3)
             del b["tensor"]
             torch.cuda.empty_cache()
         r["cells"] = api.tri_cells((n - 1) * rho)
@@ -354,35 +423,44 @@ def extra_configs(api, flush, sampler, peak, args):
         for name, g in (("h", gh), ("bb", gb)):
             ms = timed_steps(lambda i: api.map_kernel_device(g), K + W)[W:]
             res[name + "_ms"] = round(statistics.mean(ms), 4)
+            res[name + "_gblocks_s"] = round(g.blocks() / (statistics.mean(ms) * 1e-3) / 1e9, 2)
         res["h_vs_bb"] = round(res["bb_ms"] / res["h_ms"], 3)
-        res["grid"] = f"MAP kernel h(n={n}) vs bb({n - 1}), rho=1, m={m}"
+        res["grid"] = f"MAP kernel h(n={n}) vs bb({n - 1}), rho=1, m={m} (same cell domain)"
         return res
 
-    def ca_pair(name, n, rho):
+    def ca_pair(n, rho):
         r = {}
         for ex_name, ex in (("runs", api.EXEC_RUNS), ("block", api.EXEC_BLOCK)):
             h = ca_case(api, "h3d", n, rho, K, W, flush, ex)
-            b = ca_case(api, "bb", n - 1, rho, K, W, flush, ex)
-            hms, bms = statistics.mean(h["ms"]), statistics.mean(b["ms"])
-            gbs = 2.0 * h["cells"] / (hms * 1e-3) / 1e9
-            r[ex_name] = {"h_gcells_s": round(gcells(h["cells"], hms), 2),
-                          "bb_gcells_s": round(gcells(b["cells"], bms), 2),
-                          "h_vs_bb": round(bms / hms, 3), "h_gb_s": round(gbs, 1),
-                          "h_roofline_frac": round(gbs / peak, 4)}
             if ex_name == "runs":
                 r["j_per_cell_h"] = energy_per_cell(sampler, h["step"], h["cells"], 0.3)
+            hms = statistics.mean(h["ms"])
+            extra = {}
+            if ex_name == "runs":
+                extra = {"stage_ms": {k: round(v, 4) for k, v in h["stage_ms"].items()},
+                         "engine_gcells_s": round(gcells(h["cells"], statistics.mean(h["engine_ms"])), 2)}
+            del h
+            torch.cuda.empty_cache()
+            b = ca_case(api, "bb", n - 1, rho, K, W, flush, ex)
+            if ex_name == "runs":
                 r["j_per_cell_bb"] = energy_per_cell(sampler, b["step"], b["cells"], 0.3)
-            del h, b
+            bms = statistics.mean(b["ms"])
+            cells = b["cells"]
+            gbs = 2.0 * cells / (hms * 1e-3) / 1e9
+            r[ex_name] = {"h_gcells_s": round(gcells(cells, hms), 2), "bb_gcells_s": round(gcells(cells, bms), 2),
+                          "h_vs_bb": round(bms / hms, 3), "h_gb_s": round(gbs, 1),
+                          "h_roofline_frac": round(gbs / peak, 4), **extra}
+            del b
             torch.cuda.empty_cache()
         r["cells"] = api.tet_cells((n - 1) * rho)
         r["grid"] = f"h3d({n}) vs bb({n - 1}), rho={rho}"
         return r
 
-    out["C1_accum_n1024"] = accum_pair("c1", 1024, 16)
+    out["C1_accum_n1024"] = accum_pair(1024, 16)
     out["C1_map_kernel_2d"] = map_pair(2, 1024)
-    out["C3_accum_n65536"] = accum_pair("c3", 4096, 16)
-    out["C4_ca_n1024_1gpu"] = ca_pair("c4", 128, 8)
-    out["C5_ca_n2048_1gpu"] = ca_pair("c5", 256, 8)
+    out["C3_accum_n65536"] = accum_pair(4096, 16)
+    out["C4_ca_n1024_1gpu"] = ca_pair(128, 8)
+    out["C5_ca_n2048_1gpu"] = ca_pair(256, 8)
     out["map_kernel_3d"] = map_pair(3, 256)
     return out
 

@@ -140,6 +140,19 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
            int device_ptr, uint8_t* scratch, uint32_t* coverage, smx_counters* counters,
            void* stream);
 
+/* ---- the x-run CA engine's stages (what smx_ca_step / smx_ca chain) ----
+ * A bit shadow holds one bit per cell in pitched rows (row (y, z) at word row
+ * z*S + y, smx_bits_words() 32-bit words per row). Device pointers only.
+ *   smx_bits_pack:   u8 packed state -> bit shadow
+ *   smx_bits_step:   one Life step, bit shadow -> bit shadow, blocks with wz in
+ *                    [wz_lo, wz_hi) of the map grid (the map drives the work)
+ *   smx_bits_unpack: bit shadow -> u8 packed state */
+uint64_t smx_bits_bytes(const smx_grid* g);
+int smx_bits_pack(const smx_grid* g, const uint8_t* cells, uint64_t ncells, uint32_t* bits, void* stream);
+int smx_bits_step(const smx_grid* g, const uint32_t* bits_in, uint32_t* bits_out, int64_t wz_lo, int64_t wz_hi,
+                  void* stream);
+int smx_bits_unpack(const smx_grid* g, const uint32_t* bits, uint8_t* cells, uint64_t ncells, void* stream);
+
 /* simplex_grid_state::hash (simulator.hpp:68-73): FNV-1a-64 over u64 m,
  * u64 side, then the raw cell bytes. Host bytes. */
 uint64_t smx_state_hash(int32_t m, int64_t side, const void* bytes, uint64_t nbytes);

@@ -466,6 +466,28 @@ def tiles_unpack_device(g: grid_spec, cells, tiles, buf) -> None:
     check(lib().smx_tiles_unpack(C.byref(g.raw), _ptr(cells), _ptr(tiles), tiles.shape[0], _ptr(buf), _stream()))
 
 
+def bits_buffer(g: grid_spec):
+    """A device bit shadow for the x-run engine stages (with TMA-read slack)."""
+    import torch
+    n = int(lib().smx_bits_bytes(C.byref(g.raw)))
+    if n == 0:
+        raise InvalidArgument("bits_buffer: 3-simplex grids only")
+    return torch.zeros((n + 511) // 4, dtype=torch.int32, device="cuda")
+
+
+def bits_pack_device(g: grid_spec, cells, bits) -> None:
+    check(lib().smx_bits_pack(C.byref(g.raw), _ptr(cells), cells.numel(), _ptr(bits), _stream()))
+
+
+def bits_step_device(g: grid_spec, bits_in, bits_out, wz_lo: int = 0, wz_hi: int | None = None) -> None:
+    hi = g.extents[2] if wz_hi is None else wz_hi
+    check(lib().smx_bits_step(C.byref(g.raw), _ptr(bits_in), _ptr(bits_out), wz_lo, hi, _stream()))
+
+
+def bits_unpack_device(g: grid_spec, bits, cells) -> None:
+    check(lib().smx_bits_unpack(C.byref(g.raw), _ptr(bits), _ptr(cells), cells.numel(), _stream()))
+
+
 def state_hash(m: int, side: int, arr: np.ndarray) -> int:
     a = np.ascontiguousarray(arr)
     return int(lib().smx_state_hash(m, side, a.ctypes.data, a.nbytes))

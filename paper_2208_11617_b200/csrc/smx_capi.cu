@@ -571,6 +571,47 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
     return SMX_OK;
 }
 
+uint64_t smx_bits_bytes(const smx_grid* g) {
+    if (!g || g->dims != 3) return 0;
+    return bits_bytes(cell_side_of(g));
+}
+
+int smx_bits_pack(const smx_grid* g, const uint8_t* cells, uint64_t ncells, uint32_t* bits, void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    int32_t ex = SMX_EXEC_RUNS;
+    if (int rc = ca_validate(g, ncells, &ex)) return rc;
+    smx::launch_pack_bits(k, cells, bits, (cudaStream_t)stream);
+    TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
+int smx_bits_step(const smx_grid* g, const uint32_t* bits_in, uint32_t* bits_out, int64_t wz_lo, int64_t wz_hi,
+                  void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    int32_t ex = SMX_EXEC_RUNS;
+    if (int rc = ca_validate(g, smx::tet_cells(k.side), &ex)) return rc;
+    if (wz_lo < 0 || wz_hi > g->extents[2] || wz_lo > wz_hi)
+        return fail(SMX_EINVAL, "bits_step: wz range outside the grid");
+    if (bits_in == bits_out) return fail(SMX_EINVAL, "bits_step: input and output must not alias");
+    const CUtensorMap* tm;
+    if (int rc = bits_tmap(bits_in, k.side, k.rho, &tm)) return rc;
+    smx::launch_ca_bits(k, g->kind, int(wz_lo), int(wz_hi), tm, bits_out, (cudaStream_t)stream);
+    TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
+int smx_bits_unpack(const smx_grid* g, const uint32_t* bits, uint8_t* cells, uint64_t ncells, void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    int32_t ex = SMX_EXEC_RUNS;
+    if (int rc = ca_validate(g, ncells, &ex)) return rc;
+    smx::launch_unpack_bits(k, bits, cells, (cudaStream_t)stream);
+    TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
 uint64_t smx_state_hash(int32_t m, int64_t side, const void* bytes, uint64_t nbytes) {
     uint64_t h = 0xcbf29ce484222325ull;
     auto mix_u64 = [&h](uint64_t v) {
