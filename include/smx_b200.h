@@ -51,10 +51,16 @@ extern "C" {
  *                 paper's launch model (the reference's detail::sweep one to one).
  * SMX_EXEC_RUNS:  one CUDA thread-block per strip/patch of map blocks; the
  *                 blocks are mapped lane-parallel, their tiles merged into
- *                 contiguous x-runs and streamed with 128-bit accesses. */
+ *                 contiguous x-runs and streamed with 128-bit accesses. For the
+ *                 CA this is ONE fused u8 -> u8 kernel per step.
+ * SMX_EXEC_BITS:  CA only — the bit-shadow engine: the u8 state is packed to
+ *                 one bit per cell once, every step runs bits -> bits through
+ *                 the map, and the u8 state is unpacked once after the last
+ *                 step (smx_ca); smx_ca_step is pack -> step -> unpack. */
 #define SMX_EXEC_AUTO (-1) /* RUNS where supported, else BLOCK */
 #define SMX_EXEC_BLOCK 0
 #define SMX_EXEC_RUNS 1
+#define SMX_EXEC_BITS 2
 
 /* grid_spec (maps.hpp:64-92) for the BB/H2D/H3D kinds. */
 typedef struct smx_grid {

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libsmx_b200.so")
 
 SMX_OK, SMX_EINVAL, SMX_ERANGE, SMX_ECUDA, SMX_ENOMEM = 0, 1, 2, 3, 4
-EXEC_AUTO, EXEC_BLOCK, EXEC_RUNS = -1, 0, 1
+EXEC_AUTO, EXEC_BLOCK, EXEC_RUNS, EXEC_BITS = -1, 0, 1, 2
 
 
 class smx_grid(C.Structure):

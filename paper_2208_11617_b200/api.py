@@ -36,7 +36,7 @@ from fractions import Fraction
 import numpy as np
 
 from . import _lib
-from ._lib import EXEC_AUTO, EXEC_BLOCK, EXEC_RUNS, InvalidArgument, Overflow, check, lib
+from ._lib import EXEC_AUTO, EXEC_BITS, EXEC_BLOCK, EXEC_RUNS, InvalidArgument, Overflow, check, lib
 
 
 class map_kind(enum.IntEnum):

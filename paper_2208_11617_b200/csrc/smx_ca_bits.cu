@@ -34,12 +34,14 @@
 // masks them.
 #include <cuda.h>
 
-#include "smx_common.cuh"
+#include "smx_ca_common.cuh"
 #include "smx_launch.hpp"
 
 namespace smx {
 
 namespace {
+
+using namespace ca;
 
 constexpr int OWN = 96;   // max owned cells per chunk row
 // words per TMA box row: the box must start on a 16-byte (4-word) boundary, so
@@ -63,10 +65,6 @@ struct Cfg {
     static constexpr int HROWS = CPI * HL * HL;         // halo rows per item
     static constexpr int WARP_BYTES = (2 * BUF + HROWS * 32 + 64 + 127) & ~127;  // TMA dst: 128B aligned
     static int smem(int nb) { return NWARP * WARP_BYTES + nb * 32 + 128; }
-};
-
-struct Chunk {
-    int x0, y0, z0, w;  // cell box origin and owned width (cells)
 };
 
 __device__ __forceinline__ int layer_row(int z, int S) { return z * S - (z * (z - 1)) / 2; }
@@ -99,65 +97,6 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
         : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-
-// 32 bytes (each 0 or 1) -> 32 bits, bit i = byte i. t = w0 | w1 << 4 puts
-// bytes i and i+4 into one byte; * 0x01020408 gathers bit 0 of byte i to bit
-// 24+i and bit 4 to bit 28+i with no carries (all partial products below bit 24
-// land on distinct bits).
-__device__ __forceinline__ uint32_t pack32(uint4 a, uint4 b) {
-    const uint32_t M = 0x01020408u;
-    const uint32_t p0 = (a.y * 16u + a.x) * M;
-    const uint32_t p1 = (a.w * 16u + a.z) * M;
-    const uint32_t p2 = (b.y * 16u + b.x) * M;
-    const uint32_t p3 = (b.w * 16u + b.z) * M;
-    return __byte_perm(__byte_perm(p0, p1, 0x0073), __byte_perm(p2, p3, 0x0073), 0x5410);
-}
-
-// 4 bits -> 4 bytes (0/1): n * (1 + 2^7 + 2^14 + 2^21) puts bit i at 9i.
-__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
-__device__ __forceinline__ uint4 spread16(uint32_t b) {
-    return make_uint4(spread4(b & 0xf), spread4((b >> 4) & 0xf), spread4((b >> 8) & 0xf), spread4((b >> 12) & 0xf));
-}
-
-// bits [lo, hi] (inclusive) of a 32-bit word; 0 when hi < lo
-__device__ __forceinline__ uint32_t range_mask(int lo, int hi) {
-    lo = lo < 0 ? 0 : lo;
-    hi = hi > 31 ? 31 : hi;
-    if (hi < lo) return 0u;
-    return (0xffffffffu >> (31 - hi)) & (0xffffffffu << lo);
-}
-
-struct Planes4 {
-    uint32_t b0, b1, b2, b3;
-};
-
-// sum of three 2-bit numbers (<= 9) as 4 bit-planes
-__device__ __forceinline__ Planes4 add3x2(uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1, uint32_t c0,
-                                          uint32_t c1) {
-    const uint32_t s0 = a0 ^ b0 ^ c0;
-    const uint32_t k1 = (a0 & b0) | (a0 & c0) | (b0 & c0);
-    const uint32_t t = a1 ^ b1 ^ c1;
-    const uint32_t u = (a1 & b1) | (a1 & c1) | (b1 & c1);
-    const uint32_t c = t & k1;
-    return Planes4{s0, t ^ k1, u ^ c, u & c};
-}
-
-// B3/S23 from three 4-plane partial sums (the 27-sum includes the cell):
-// next = (S == 3) | (alive & S == 4).
-__device__ __forceinline__ uint32_t life_planes(const Planes4& a, const Planes4& b, const Planes4& c,
-                                                uint32_t alive) {
-    const uint32_t s0 = a.b0 ^ b.b0 ^ c.b0, k1 = (a.b0 & b.b0) | (a.b0 & c.b0) | (b.b0 & c.b0);
-    const uint32_t s1 = a.b1 ^ b.b1 ^ c.b1, k2 = (a.b1 & b.b1) | (a.b1 & c.b1) | (b.b1 & c.b1);
-    const uint32_t s2 = a.b2 ^ b.b2 ^ c.b2, k3 = (a.b2 & b.b2) | (a.b2 & c.b2) | (b.b2 & c.b2);
-    const uint32_t s3 = a.b3 ^ b.b3 ^ c.b3, k4 = (a.b3 & b.b3) | (a.b3 & c.b3) | (b.b3 & c.b3);
-    const uint32_t r1 = s1 ^ k1, c2 = s1 & k1;
-    const uint32_t r2 = s2 ^ k2 ^ c2, c3 = (s2 & k2) | (s2 & c2) | (k2 & c2);
-    const uint32_t r3 = s3 ^ k3 ^ c3, c4 = (s3 & k3) | (s3 & c3) | (k3 & c3);
-    const uint32_t r4 = k4 ^ c4;
-    const uint32_t eq3 = s0 & r1 & ~r2;
-    const uint32_t eq4 = ~s0 & ~r1 & r2;
-    return (eq3 | (eq4 & alive)) & ~(r3 | r4);
-}
 
 // 32 bytes at 32B-aligned byte offset A of a u8 array of n bytes -> 32 bits
 __device__ __forceinline__ uint32_t load_chunk_bits(const uint8_t* __restrict__ p, long long A,
@@ -328,54 +267,13 @@ __global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_
     uint32_t* sH = reinterpret_cast<uint32_t*>(wbase + 2 * C::BUF);  // [HROWS][8]: h0 w0..3, h1 w0..3
     const uint32_t mbar0 = smem_u32(wbase + 2 * C::BUF + C::HROWS * 32);
 
-    // ---- 1. map the patch ----
-    if (tid == 0) *s_nchunks = 0;
+    // ---- 1-2. map the patch, chain x-adjacent tiles into chunks ----
     if (lane == 0) {
         mbar_init(mbar0, 1);
         mbar_init(mbar0 + 8, 1);
     }
-    for (int t = tid; t < NBP; t += NTHR) {
-        const int tl = t % PP, wz = wzb + t / PP;
-        const int wx = blockIdx.x * P + (tl % P), wy = blockIdx.y * P + (tl / P);
-        int4 v = make_int4(0, 0, 0, 0);
-        if (wx < g.ex && wy < g.ey && wz < wz1) {
-            const outcome<int> o = map_block<KIND>(g, wx, wy, wz);
-            if (!o.is_void) v = make_int4(o.x, o.y, o.z, 1 | ((tl % P) << 8) | ((tl / P) << 16));
-        }
-        s_tile[t] = v;
-    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    __syncthreads();
-    // ---- 2. chains of x-adjacent tiles -> chunks ----
-    for (int t = tid; t < NBP; t += NTHR) {
-        const int4 me = s_tile[t];
-        if (!me.w) continue;
-        const int px = (me.w >> 8) & 0xff, py = me.w >> 16;
-        auto is_tile = [&](int i, int x) {
-            const int4 o = s_tile[i];
-            return o.w && o.x == x && o.y == me.y && o.z == me.z;
-        };
-        if ((px > 0 && is_tile(t - 1, me.x - 1)) || (py > 0 && is_tile(t - P, me.x - 1))) continue;
-        int u = t, len = 1, x0 = me.x;
-        for (;;) {
-            const int uw = s_tile[u].w, ux = (uw >> 8) & 0xff, uy = uw >> 16;
-            const int xn = s_tile[u].x + 1;
-            int nxt = -1;
-            if (ux + 1 < P && is_tile(u + 1, xn)) nxt = u + 1;
-            else if (uy + 1 < P && is_tile(u + P, xn)) nxt = u + P;
-            if (nxt < 0 || len == C::LMAX) {
-                const int c = atomicAdd(s_nchunks, 1);
-                s_chunk[c] = Chunk{x0 * RHO, me.y * RHO, me.z * RHO, len * RHO};
-                if (nxt < 0) break;
-                x0 = s_tile[nxt].x;
-                len = 0;
-            }
-            u = nxt;
-            ++len;
-        }
-    }
-    __syncthreads();
-    const int nchunks = *s_nchunks;
+    const int nchunks = build_chunks<KIND>(g, wzb, wz1, P, NZ, C::LMAX, s_tile, s_chunk, s_nchunks);
     const int nitems = (nchunks + C::CPI - 1) / C::CPI;
 
     uint32_t phases = 0u;  // bit b: parity of buffer b

@@ -469,14 +469,22 @@ int smx_life_init(int32_t m, int64_t side, uint64_t seed, uint8_t* cells, uint64
     return SMX_OK;
 }
 
+// the x-run CA kernels move 16-byte vectors relative to the buffer base
+static int check_align16(const void* a, const void* b) {
+    if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15u)
+        return fail(SMX_EINVAL, "ca: device state buffers must be 16-byte aligned");
+    return SMX_OK;
+}
+
 static int ca_validate(const smx_grid* g, uint64_t ncells, int32_t* exec) {
     if (g->dims != 3)
         return fail(SMX_EINVAL, "launch_ca: the B200 CA path is the dead-boundary 3-simplex kernel");
     if (int rc = check_cells(g, ncells)) return rc;
     if (*exec < 0) *exec = smx::ca_runs_supported(int(g->rho)) ? SMX_EXEC_RUNS : SMX_EXEC_BLOCK;
-    if (*exec != SMX_EXEC_BLOCK && *exec != SMX_EXEC_RUNS) return fail(SMX_EINVAL, "ca: unknown exec scheme");
-    if (*exec == SMX_EXEC_RUNS && !smx::ca_runs_supported(int(g->rho)))
-        return fail(SMX_EINVAL, "ca: the x-run scheme supports rho in {4, 8}; use SMX_EXEC_BLOCK");
+    if (*exec != SMX_EXEC_BLOCK && *exec != SMX_EXEC_RUNS && *exec != SMX_EXEC_BITS)
+        return fail(SMX_EINVAL, "ca: unknown exec scheme");
+    if (*exec != SMX_EXEC_BLOCK && !smx::ca_runs_supported(int(g->rho)))
+        return fail(SMX_EINVAL, "ca: the x-run schemes support rho in {4, 8}; use SMX_EXEC_BLOCK");
     return SMX_OK;
 }
 
@@ -486,8 +494,10 @@ int smx_ca_step(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint64_t n
     if (int rc = make_geom(g, &k, true)) return rc;
     if (int rc = ca_validate(g, ncells, &exec)) return rc;
     if (cur == next) return fail(SMX_EINVAL, "ca_step: cur and next must not alias");
-    if (exec == SMX_EXEC_RUNS) return ca_runs_step(g, k, 0, k.ez, cur, next, (cudaStream_t)stream);
-    smx::launch_ca(k, 0, k.ez, cur, next, exec, (cudaStream_t)stream);
+    if (int rc = check_align16(cur, next)) return rc;
+    if (exec == SMX_EXEC_BITS) return ca_runs_step(g, k, 0, k.ez, cur, next, (cudaStream_t)stream);
+    if (exec == SMX_EXEC_RUNS) smx::launch_ca_fused(k, 0, int(k.ez), cur, next, (cudaStream_t)stream);
+    else smx::launch_ca(k, 0, k.ez, cur, next, exec, (cudaStream_t)stream);
     TRY(cudaGetLastError());
     return SMX_OK;
 }
@@ -499,8 +509,11 @@ int smx_ca_step_range(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint
     if (int rc = ca_validate(g, ncells, &exec)) return rc;
     if (wz_lo < 0 || wz_hi > g->extents[2] || wz_lo > wz_hi)
         return fail(SMX_EINVAL, "ca_step_range: wz range outside the grid");
-    if (exec == SMX_EXEC_RUNS) return ca_runs_step(g, k, wz_lo, wz_hi, cur, next, (cudaStream_t)stream);
-    smx::launch_ca(k, int(wz_lo), int(wz_hi), cur, next, exec, (cudaStream_t)stream);
+    if (cur == next) return fail(SMX_EINVAL, "ca_step_range: cur and next must not alias");
+    if (int rc = check_align16(cur, next)) return rc;
+    if (exec == SMX_EXEC_BITS) return ca_runs_step(g, k, wz_lo, wz_hi, cur, next, (cudaStream_t)stream);
+    if (exec == SMX_EXEC_RUNS) smx::launch_ca_fused(k, int(wz_lo), int(wz_hi), cur, next, (cudaStream_t)stream);
+    else smx::launch_ca(k, int(wz_lo), int(wz_hi), cur, next, exec, (cudaStream_t)stream);
     TRY(cudaGetLastError());
     return SMX_OK;
 }
@@ -534,8 +547,10 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
         if (int rc = fill_counters(g, k, counters, s, dcov)) return rc;
     uint8_t* cur = a;
     uint8_t* nxt = b;
-    if (exec == SMX_EXEC_RUNS && steps > 0) {
-        // bit-shadow engine: pack once, then ca + unpack per step (every step writes the u8 state)
+    if (device_ptr)
+        if (int rc = check_align16(a, b)) return rc;
+    if (exec == SMX_EXEC_BITS && steps > 0) {
+        // bit-shadow engine: pack once, steps x (bits -> bits), unpack once
         void *pa, *pb;
         if (int rc = pool_get(3, bits_bytes(k.side), &pa)) return rc;
         if (int rc = pool_get(4, bits_bytes(k.side), &pb)) return rc;
@@ -549,14 +564,15 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
         const CUtensorMap* tn = tb;
         for (int64_t st = 0; st < steps; ++st) {
             smx::launch_ca_bits(k, g->kind, 0, k.ez, tc, bn, s);
-            smx::launch_unpack_bits(k, bn, nxt, s);
-            std::swap(cur, nxt);
             std::swap(bc, bn);
             std::swap(tc, tn);
         }
+        smx::launch_unpack_bits(k, bc, nxt, s);
+        std::swap(cur, nxt);
     } else {
         for (int64_t st = 0; st < steps; ++st) {
-            smx::launch_ca(k, 0, k.ez, cur, nxt, exec, s);
+            if (exec == SMX_EXEC_RUNS) smx::launch_ca_fused(k, 0, k.ez, cur, nxt, s);
+            else smx::launch_ca(k, 0, k.ez, cur, nxt, exec, s);
             std::swap(cur, nxt);
         }
     }

@@ -24,10 +24,14 @@ def test_life_init_vs_reference(cuda):
         assert int(st.cells.sum(dtype=np.int64)) == row["alive"]
 
 
-@pytest.mark.parametrize("ex", [api.EXEC_BLOCK, api.EXEC_RUNS])
+XRUN = (api.EXEC_RUNS, api.EXEC_BITS)  # fused u8 step, bit-shadow engine
+ALL_EX = (api.EXEC_BLOCK,) + XRUN
+
+
+@pytest.mark.parametrize("ex", ALL_EX)
 def test_launch_ca_rows_vs_reference(cuda, ex):
     for row in golden("ca.json")["launch_ca"]:
-        if ex == api.EXEC_RUNS and row["rho"] not in (4, 8):
+        if ex in XRUN and row["rho"] not in (4, 8):
             continue
         g = api.make_grid(row["kind"], 3, row["n"], row["rho"])
         st = run_gpu(g, row["side"], row["seed"], row["steps"], ex)
@@ -52,7 +56,7 @@ def test_runs_scheme_vs_oracle_many_steps(cuda, orc, kind, rho):
         steps = 5
         want = orc.make_life_state(3, side, 7)
         orc.ca3d_run(side, steps, want)
-        for ex in (api.EXEC_BLOCK, api.EXEC_RUNS):
+        for ex in ALL_EX:
             got = run_gpu(g, side, 7, steps, ex)
             assert (got.cells == want).all(), (kind, n, rho, ex)
 
@@ -78,7 +82,7 @@ def test_dense_random_states(cuda, orc):
             init = (rng.random(api.tet_cells(side)) < p).astype(np.uint8)
             want = init.copy()
             orc.ca3d_run(side, 1, want)
-            for ex in (api.EXEC_BLOCK, api.EXEC_RUNS):
+            for ex in ALL_EX:
                 cur = torch.from_numpy(init).cuda()
                 nxt = torch.empty_like(cur)
                 api.ca_step_device(g, cur, nxt, ex)

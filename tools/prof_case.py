@@ -18,7 +18,7 @@ from paper_2208_11617_b200 import api  # noqa: E402
 
 def main():
     what, kind, n, rho = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4])
-    ex = {"runs": api.EXEC_RUNS, "block": api.EXEC_BLOCK}[sys.argv[5] if len(sys.argv) > 5 else "runs"]
+    ex = {"runs": api.EXEC_RUNS, "block": api.EXEC_BLOCK, "bits": api.EXEC_BITS}[sys.argv[5] if len(sys.argv) > 5 else "runs"]
     iters = int(sys.argv[6]) if len(sys.argv) > 6 else 5
     m = 2 if what == "accum" or (what == "map" and kind == "h2d") else 3
     if what == "map" and kind == "bb" and len(sys.argv) > 7:
