@@ -57,7 +57,7 @@ extern "C" {
  *                 one bit per cell once, every step runs bits -> bits through
  *                 the map, and the u8 state is unpacked once after the last
  *                 step (smx_ca); smx_ca_step is pack -> step -> unpack. */
-#define SMX_EXEC_AUTO (-1) /* RUNS where supported, else BLOCK */
+#define SMX_EXEC_AUTO (-1) /* CA: BITS (one small step: RUNS) where rho is 4 or 8, else BLOCK; ACCUM: RUNS */
 #define SMX_EXEC_BLOCK 0
 #define SMX_EXEC_RUNS 1
 #define SMX_EXEC_BITS 2

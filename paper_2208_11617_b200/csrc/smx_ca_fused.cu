@@ -41,29 +41,39 @@ constexpr int F_NTHR = F_NWARP * 32;
 template <int RHO>
 struct FCfg {
     static constexpr int LMAX = RHO == 8 ? 12 : 16;      // tiles per chunk (patch edge): w <= 96 / 64
-    // computed words per row: the owned cells plus up to 31 cells of the
-    // next chunk (sector ownership, see the store phase)
-    static constexpr int NW = (LMAX * RHO + 31 + 31) / 32;  // 4 / 3
+    // computed words per row: frame bit i is cell x0 - 1 + i; the words cover
+    // the owned cells plus up to 31 cells of the next chunk (sector ownership,
+    // see the store phase): [x0 - 1, x0 + w + 31) within NW words
+    static constexpr int NW = (LMAX * RHO + 32 + 31) / 32;  // 4 / 3
+    // halo row copy: NCH 16-byte chunks from floor16 of the row's cell x0 - 1
+    // (start residue d <= 15) hold the needed cells up to x0 + w + 32
+    static constexpr int NCH = (LMAX * RHO + 34 + 15 + 15) / 16;  // 10 / 8
+    static constexpr int PKW = NCH / 2;                  // packed 32-bit words per row
+    static_assert(PKW >= NW + 1 && NCH % 2 == 0, "row copy must cover the halo words");
+    static constexpr int RSTR = (NCH + 1) * 16;          // odd chunk stride: conflict-free lane-per-row reads
     static constexpr int HL = RHO + 2;                   // halo rows == halo layers
     static constexpr int HL2 = HL * HL;
     static constexpr int SLOT = RHO * NW;                // march lanes per chunk slot
-    static constexpr int CPI = 32 / SLOT;                // chunks per warp item (1 / 4)
+    static constexpr int CPI = 32 / SLOT;                // chunks per warp item (1 / 2)
     static constexpr int HROWS = CPI * HL2;              // halo rows per item
+    static constexpr int NPASS = (HROWS + 3) / 4;        // copy passes: 4 rows x 8 lanes
     static constexpr int OROWS = CPI * RHO * RHO;        // output rows per item
     static constexpr int HW = 3 * NW;                    // smem words per halo row: (h0, h1, raw) x NW
     static constexpr int OSTR = 33;                      // smem words per output layer (32 lanes + pad)
-    static constexpr int WARP_WORDS = HROWS * HW + RHO * OSTR + 1;
-    static int smem(int nb) { return F_NWARP * WARP_WORDS * 4 + nb * 32 + 16; }
+    // per-warp smem: raw rows | h-sums | outputs | row descriptors
+    static constexpr int H_OFF = HROWS * RSTR;
+    static constexpr int O_OFF = H_OFF + HROWS * HW * 4;
+    static constexpr int D_OFF = (O_OFF + (RHO * OSTR + 1) * 4 + 15) & ~15;
+    static constexpr int WARP_BYTES = (D_OFF + HROWS * 16 + 127) & ~127;
+    static int smem(int nb) { return F_NWARP * WARP_BYTES + nb * 32 + 16; }
 };
 
-// bits of the 32 bytes at 32B-aligned offset A of a u8 array of n bytes, for
-// the (at most one per row) piece that runs past the end of the array. Kept out
-// of line so the hot path is a plain branch, not a predicated byte loop.
-__device__ __noinline__ uint32_t tail_bits(const uint8_t* __restrict__ p, long long A, unsigned long long n) {
-    uint32_t v = 0;
-    for (int i = 0; i < 32; ++i)
-        if ((unsigned long long)(A + i) < n) v |= uint32_t(p[A + i] & 1) << i;
-    return v;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// 16-byte async copy global -> shared; bytes beyond `valid` are zero-filled
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid) : "memory");
 }
 
 // 2^K cells (K = 0..4) of output row o starting at cell offset off, stored at
@@ -82,79 +92,92 @@ __device__ __forceinline__ void store_cells(uint8_t* __restrict__ out, long long
 template <int KIND, int RHO>
 __global__ void __launch_bounds__(F_NTHR) k_ca_fused(Geom g, int wz0, int wz1, int P, int NZ, int exact,
                                                      const uint8_t* __restrict__ cur, uint8_t* __restrict__ next,
-                                                     unsigned long long ncells) {
+                                                     long long ncells) {
     using C = FCfg<RHO>;
     constexpr int HL = C::HL, HL2 = C::HL2, NW = C::NW, HW = C::HW;
-    extern __shared__ __align__(16) uint32_t fsm[];
+    extern __shared__ __align__(128) uint8_t fsm[];
     const int NBP = P * P * NZ;
-    int4* s_tile = reinterpret_cast<int4*>(fsm + ((F_NWARP * C::WARP_WORDS + 3) & ~3));  // 16-byte aligned
+    int4* s_tile = reinterpret_cast<int4*>(fsm + F_NWARP * C::WARP_BYTES);
     Chunk* s_chunk = reinterpret_cast<Chunk*>(s_tile + NBP);
     int* s_nchunks = reinterpret_cast<int*>(s_chunk + NBP);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int grp = lane >> 3, gl = lane & 7;
     const int S = g.side;
     const unsigned long long* __restrict__ PZ = g.prefix;
-    uint32_t* sH = fsm + warp * C::WARP_WORDS;  // [HROWS][HW]
-    uint32_t* sO = sH + C::HROWS * HW;           // [RHO][OSTR] (+1 pad word)
+    uint8_t* sR = fsm + warp * C::WARP_BYTES;                     // [HROWS][RSTR] raw u8 rows
+    uint32_t* sH = reinterpret_cast<uint32_t*>(sR + C::H_OFF);     // [HROWS][HW]
+    uint32_t* sO = reinterpret_cast<uint32_t*>(sR + C::O_OFF);     // [RHO][OSTR] (+1 pad word)
+    int4* sD = reinterpret_cast<int4*>(sR + C::D_OFF);             // [HROWS] row descriptors
 
     const int nchunks = build_chunks<KIND>(g, wz0 + blockIdx.z * NZ, wz1, P, NZ, C::LMAX, s_tile, s_chunk, s_nchunks);
     const int nitems = (nchunks + C::CPI - 1) / C::CPI;
 
     for (int item = warp; item < nitems; item += F_NWARP) {
-        // ---- load: a lane per halo row -> frame bits -> horizontal 3-sums ----
-        // Frame bit i of a row is cell x = x0 - 32 + i: frame words 1..NW are
-        // the computed cells [x0, x0 + 32 NW), words 0 and NW+1 the x halo.
-        // Only cells [x0 - 1, x0 + w + 32] are needed (the rest stay zero).
+        // ---- row descriptors (a lane per halo row) ----
+        // Frame bit i of a row is cell x = x0 - 1 + i. The row's bytes are
+        // copied from c0 = floor16(packed index of x0 - 1), frame bit 0 at
+        // byte d = F - c0. Cells outside the row (x < 0, x > y) are masked dead.
         for (int r = lane; r < C::HROWS; r += 32) {
             const int cl = r / HL2, rr = r - cl * HL2;
             const int ci = item * C::CPI + cl;
-            uint32_t* hrow = sH + r * HW;
             bool ok = ci < nchunks;
-            Chunk ch = ok ? s_chunk[ci] : Chunk{0, 0, 0, 0};
+            const Chunk ch = ok ? s_chunk[ci] : Chunk{0, 0, 0, 0};
             const int yy = ch.y0 - 1 + rr % HL, zz = ch.z0 - 1 + rr / HL;
             ok = ok && zz >= 0 && yy >= 0 && yy + zz <= S - 1 && ch.x0 - 1 <= yy;
-            const int lo = max(ch.x0 - 1, 0) - (ch.x0 - 32), hi = min(ch.x0 + ch.w + 32, yy) - (ch.x0 - 32);
-            long long F = 0;
-            if (ok) F = (long long)(__ldg(PZ + zz) + tri_idx(0, yy)) + ch.x0 - 32;
-            const long long Fa = F & ~31ll;
-            const int d = int(F - Fa);
-            const int klo = (lo + d) >> 5, khi = (hi + d) >> 5;  // pieces holding needed bytes
-            uint4 va[NW + 2], vb[NW + 2];
-            bool tail[NW + 2];
+            const int lo = ch.x0 == 0 ? 1 : 0, hi = min(ch.x0 + ch.w + 32, yy) - (ch.x0 - 1);
+            const long long F = ok ? (long long)(__ldg(PZ + zz) + tri_idx(0, yy)) + ch.x0 - 1 : 0;
+            const long long c0 = F & ~15ll;  // >= -16
+            sD[r] = make_int4(int(c0 & 0xffffffffll), int(c0 >> 32), ok ? (lo | (int(F - c0) << 4) | (hi << 16)) : -1, 0);
+        }
+        __syncwarp();
+
+        // ---- copy: 8 lanes x 16 bytes per row, 4 rows per pass (coalesced) ----
+#pragma unroll 4
+        for (int pass = 0; pass < C::NPASS; ++pass) {
+            const int r = pass * 4 + grp;
+            if (r >= C::HROWS) break;
+            const int4 dsc = sD[r];
+            if (dsc.z < 0) continue;
+            const long long c0 = ((long long)dsc.y << 32) | (unsigned)dsc.x;
+            const uint32_t dst = smem_u32(sR + r * C::RSTR);
 #pragma unroll
-            for (int k = 0; k < NW + 2; ++k) {
-                va[k] = make_uint4(0, 0, 0, 0);
-                vb[k] = va[k];
-                tail[k] = false;
-                if (ok && k >= klo && k <= khi) {
-                    const long long A = Fa + 32ll * k;
-                    if ((unsigned long long)(A + 32) <= ncells) {
-                        const uint4* q = reinterpret_cast<const uint4*>(cur + A);
-                        va[k] = __ldg(q);
-                        vb[k] = __ldg(q + 1);
-                    } else {
-                        tail[k] = true;
-                    }
-                }
+            for (int k = gl; k < C::NCH; k += 8) {
+                const long long o = c0 + 16 * k;
+                const long long v = o < 0 ? 0 : min(ncells - o, 16ll);
+                cp_async16(dst + 16 * k, v > 0 ? cur + o : cur, int(v > 0 ? v : 0));
             }
-            uint32_t p[NW + 3];
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncwarp();
+
+        // ---- bits + horizontal 3-sums: a lane per halo row ----
+        for (int r = lane; r < C::HROWS; r += 32) {
+            const int lh = sD[r].z;
+            uint32_t* hrow = sH + r * HW;
+            uint32_t f[NW + 1];
+            if (lh < 0) {
 #pragma unroll
-            for (int k = 0; k < NW + 2; ++k) {
-                p[k] = pack32(va[k], vb[k]);
-                if (tail[k]) p[k] = tail_bits(cur, Fa + 32ll * k, ncells);
+                for (int j = 0; j <= NW; ++j) f[j] = 0u;
+            } else {
+                const int lo = lh & 1, d = (lh >> 4) & 15, hi = lh >> 16;
+                const uint4* q = reinterpret_cast<const uint4*>(sR + r * C::RSTR);
+                uint32_t pk[C::PKW + 1];  // row bytes as bits, 32 per word
+#pragma unroll
+                for (int k = 0; k < C::PKW; ++k) pk[k] = pack32(q[2 * k], q[2 * k + 1]);
+                pk[C::PKW] = 0u;
+#pragma unroll
+                for (int j = 0; j <= NW; ++j)
+                    f[j] = __funnelshift_r(pk[j], pk[j + 1], d) & range_mask(lo - 32 * j, hi - 32 * j);
             }
-            p[NW + 2] = 0u;
-            uint32_t f[NW + 2];
 #pragma unroll
-            for (int j = 0; j < NW + 2; ++j)
-                f[j] = ok ? __funnelshift_r(p[j], p[j + 1], d) & range_mask(lo - 32 * j, hi - 32 * j) : 0u;
-#pragma unroll
-            for (int i = 1; i <= NW; ++i) {
-                const uint32_t l = __funnelshift_l(f[i - 1], f[i], 1);   // cell x-1
-                const uint32_t rg = __funnelshift_r(f[i], f[i + 1], 1);  // cell x+1
-                hrow[3 * (i - 1)] = l ^ f[i] ^ rg;
-                hrow[3 * (i - 1) + 1] = (l & f[i]) | (l & rg) | (f[i] & rg);
-                hrow[3 * (i - 1) + 2] = f[i];
+            for (int i = 0; i < NW; ++i) {
+                const uint32_t l = __funnelshift_l(i > 0 ? f[i - 1] : 0u, f[i], 1);  // cell x-1
+                const uint32_t rg = __funnelshift_r(f[i], f[i + 1], 1);            // cell x+1
+                hrow[3 * i] = l ^ f[i] ^ rg;
+                hrow[3 * i + 1] = (l & f[i]) | (l & rg) | (f[i] & rg);
+                hrow[3 * i + 2] = f[i];
             }
         }
         __syncwarp();
@@ -207,7 +230,7 @@ __global__ void __launch_bounds__(F_NTHR) k_ca_fused(Geom g, int wz0, int wz1, i
                 if (E0 >= E1) continue;
             }
             const int n = int(E1 - E0);
-            const int off0 = int(E0 - R) - ch.x0;  // cell offset of E0 in the computed words
+            const int off0 = int(E0 - R) - ch.x0 + 1;  // frame offset of E0 (frame bit 0 = cell x0 - 1)
             const uint32_t* o = sO + lz * C::OSTR + cl * C::SLOT + ly * NW;
             auto put = [&](auto kk, long long pos) {
                 constexpr int K = decltype(kk)::value;
@@ -253,7 +276,7 @@ void launch_fused_t(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t
         attr_set = true;
     }
     // patch edge and layers per CTA: as large as possible while the grid still
-    // has >= 4 CTAs per SM (small grids trade chunk length for parallelism)
+    // has >= 2 CTAs per SM (small grids trade chunk length for parallelism)
     int P = C::LMAX, NZ = NZMAX;
     auto ctas = [&](int p, int nz) {
         return (long long)((g.ex + p - 1) / p) * ((g.ey + p - 1) / p) * ((wz1 - wz0 + nz - 1) / nz);
@@ -263,7 +286,7 @@ void launch_fused_t(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t
     const dim3 grid((g.ex + P - 1) / P, (g.ey + P - 1) / P, (wz1 - wz0 + NZ - 1) / NZ);
     const int exact = (wz0 > 0 || wz1 < g.ez) ? 1 : 0;
     k_ca_fused<KIND, RHO><<<grid, F_NTHR, C::smem(P * P * NZ), s>>>(g, wz0, wz1, P, NZ, exact, cur, next,
-                                                                    tet_cells(g.side));
+                                                                    (long long)tet_cells(g.side));
 }
 
 template <int KIND>

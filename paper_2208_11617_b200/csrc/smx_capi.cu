@@ -254,6 +254,12 @@ int bits_tmap(const uint32_t* bits, int64_t side, int64_t rho, const CUtensorMap
     return SMX_OK;
 }
 
+int ca_fused_step(const smx::Geom& k, int64_t wz0, int64_t wz1, const uint8_t* cur, uint8_t* next, cudaStream_t s) {
+    smx::launch_ca_fused(k, int(wz0), int(wz1), cur, next, s);
+    TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
 size_t bits_bytes(int64_t side) {
     return size_t(smx::bits_rows(int(side))) * size_t(smx::bits_pitch_words(int(side))) * 4;
 }
@@ -476,11 +482,17 @@ static int check_align16(const void* a, const void* b) {
     return SMX_OK;
 }
 
+// EXEC_AUTO for ONE step: the fused u8 -> u8 kernel up to this many cells
+// (L2-resident states, where one launch beats pack + step + unpack), the
+// bit-shadow path above it. Multi-step launch_ca always uses the bit shadow
+// (pack once, unpack once). Measured on B200: profiles/r1/ca_exec_sweep.txt.
+constexpr uint64_t kFusedMaxCells = 48ull << 20;
+
 static int ca_validate(const smx_grid* g, uint64_t ncells, int32_t* exec) {
     if (g->dims != 3)
         return fail(SMX_EINVAL, "launch_ca: the B200 CA path is the dead-boundary 3-simplex kernel");
     if (int rc = check_cells(g, ncells)) return rc;
-    if (*exec < 0) *exec = smx::ca_runs_supported(int(g->rho)) ? SMX_EXEC_RUNS : SMX_EXEC_BLOCK;
+    if (*exec < 0) *exec = smx::ca_runs_supported(int(g->rho)) ? SMX_EXEC_BITS : SMX_EXEC_BLOCK;
     if (*exec != SMX_EXEC_BLOCK && *exec != SMX_EXEC_RUNS && *exec != SMX_EXEC_BITS)
         return fail(SMX_EINVAL, "ca: unknown exec scheme");
     if (*exec != SMX_EXEC_BLOCK && !smx::ca_runs_supported(int(g->rho)))
@@ -490,14 +502,16 @@ static int ca_validate(const smx_grid* g, uint64_t ncells, int32_t* exec) {
 
 int smx_ca_step(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint64_t ncells, int32_t exec,
                 void* stream) {
+    const bool auto_exec = exec < 0;
     smx::Geom k;
     if (int rc = make_geom(g, &k, true)) return rc;
     if (int rc = ca_validate(g, ncells, &exec)) return rc;
     if (cur == next) return fail(SMX_EINVAL, "ca_step: cur and next must not alias");
     if (int rc = check_align16(cur, next)) return rc;
+    if (auto_exec && exec == SMX_EXEC_BITS && ncells <= kFusedMaxCells) exec = SMX_EXEC_RUNS;
     if (exec == SMX_EXEC_BITS) return ca_runs_step(g, k, 0, k.ez, cur, next, (cudaStream_t)stream);
-    if (exec == SMX_EXEC_RUNS) smx::launch_ca_fused(k, 0, int(k.ez), cur, next, (cudaStream_t)stream);
-    else smx::launch_ca(k, 0, k.ez, cur, next, exec, (cudaStream_t)stream);
+    if (exec == SMX_EXEC_RUNS) return ca_fused_step(k, 0, k.ez, cur, next, (cudaStream_t)stream);
+    smx::launch_ca(k, 0, k.ez, cur, next, exec, (cudaStream_t)stream);
     TRY(cudaGetLastError());
     return SMX_OK;
 }
@@ -512,8 +526,8 @@ int smx_ca_step_range(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint
     if (cur == next) return fail(SMX_EINVAL, "ca_step_range: cur and next must not alias");
     if (int rc = check_align16(cur, next)) return rc;
     if (exec == SMX_EXEC_BITS) return ca_runs_step(g, k, wz_lo, wz_hi, cur, next, (cudaStream_t)stream);
-    if (exec == SMX_EXEC_RUNS) smx::launch_ca_fused(k, int(wz_lo), int(wz_hi), cur, next, (cudaStream_t)stream);
-    else smx::launch_ca(k, int(wz_lo), int(wz_hi), cur, next, exec, (cudaStream_t)stream);
+    if (exec == SMX_EXEC_RUNS) return ca_fused_step(k, wz_lo, wz_hi, cur, next, (cudaStream_t)stream);
+    smx::launch_ca(k, int(wz_lo), int(wz_hi), cur, next, exec, (cudaStream_t)stream);
     TRY(cudaGetLastError());
     return SMX_OK;
 }
@@ -571,8 +585,11 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
         std::swap(cur, nxt);
     } else {
         for (int64_t st = 0; st < steps; ++st) {
-            if (exec == SMX_EXEC_RUNS) smx::launch_ca_fused(k, 0, k.ez, cur, nxt, s);
-            else smx::launch_ca(k, 0, k.ez, cur, nxt, exec, s);
+            if (exec == SMX_EXEC_RUNS) {
+                if (int rc = ca_fused_step(k, 0, k.ez, cur, nxt, s)) return rc;
+            } else {
+                smx::launch_ca(k, 0, k.ez, cur, nxt, exec, s);
+            }
             std::swap(cur, nxt);
         }
     }
