@@ -1,19 +1,28 @@
 """Benchmark driver (one JSON line on rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-configs]
 
-Workload (BASELINE.json configs[1], "C2"): one dead-boundary 3-D Life step over
-the voxelised tetrahedron of side 252 through the H3D block-space map
-(grid_h3d(64), rho = 4: 2,699,004 u8 cells, seed 42). A bench "step" is one
-CA step; `value` is Gcells/s (useful cells x steps / device time), inputs
-resident in HBM, L2 flushed (256 MiB write) before every timed step because the
-2.7 MB state would otherwise sit in the 126 MB L2. `e2e` is the same step through
-the reference-facing C ABI with host (pinned) buffers: H2D + step + D2H per step.
+Workload (BASELINE.json configs[1], "C2"): dead-boundary 3-D Life
+over the voxelised tetrahedron of side 252 through the H3D block-space map
+(grid_h3d(64), rho = 4: 2,699,004 u8 cells, make_life_state seed 42), 100 CA
+steps. A bench "step" is ONE launch_ca call of those 100 CA steps (smx_ca,
+device buffers, EXEC_AUTO = the bit-shadow engine: pack once, 100 map-driven
+bit-sliced steps, unpack once); `value` is Gcell-steps/s = cells x 100 / device
+time. The L2 is flushed (256 MiB write) before every bench step; within a call
+the 2.7 MB state is L2-resident, as it is for the reference workload.
+`e2e` is the same call through the reference-facing C ABI with host (pinned)
+buffers: H2D + 100 steps + D2H per bench step.
 
-Also reported, per BASELINE config (C1, C3, C4, C5 at 1 GPU): H and BB Gcells/s,
-H-vs-BB speedup, HBM roofline fraction, J/cell from NVML, and the paper's MAP
-kernel block rate. Multi-GPU (torchrun, N > 1): the CA is sharded over whole H
-levels (paper_2208_11617_b200/dist.py) with a tile halo exchange; `value` is the
+`roofline` is for the dominant kernel, k_ca_bits (one bit-sliced step over the
+whole map grid), timed per launch with CUDA events on the launching stream,
+on SURVEY §8(d)'s basis of 2 B per useful cell per step.
+
+Also reported (`configs`), per BASELINE config at 1 GPU: H and BB Gcells/s,
+H-vs-BB speedup, HBM roofline fraction, J/cell from NVML — ACCUM C1/C3 (x-run
+and the paper's block launch model), the MAP kernel (2-D and 3-D), the CA at
+C4 (100 steps) and C5 (20 steps, rho sweep) plus single u8->u8 steps.
+Multi-GPU (torchrun, N > 1): the CA sharded over whole H levels
+(paper_2208_11617_b200/dist.py) with a tile halo exchange; `value` is the
 whole-domain throughput (strong scaling).
 
 `--impl reference` times the reference's own CPU implementation
@@ -34,9 +43,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 SEED = 42
+METRIC = ("Gcell-steps/s (3-simplex CA, H map) — BASELINE metric: Gcells/s and H-vs-BB speedup; "
+          "HBM GB/s vs peak; J/cell")
 WORKLOADS = {
-    # name: (description, kind, n, rho) for the H grid; BB uses (n-1) for h kinds
-    "c2": ("3-simplex n=256 CA step (C2): H3D(64) rho=4, side 252", "h3d", 64, 4),
+    # name: (description, kind, n, rho, CA steps per launch_ca call) for the H grid; BB uses n-1
+    "c2": ("3-simplex n=256 CA (C2): launch_ca over H3D(64) rho=4, side 252, 100 steps per call",
+           "h3d", 64, 4, 100),
 }
 
 
@@ -55,14 +67,14 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel_key: str):
-    """dram bytes per launch for the dominant kernel from the committed ncu summary."""
+def ncu_kernel_traffic(key: str):
+    """dram read + write bytes per launch of a kernel from the committed ncu
+    summary (profiles/ncu_summary.json), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     try:
-        d = json.load(open(p))
-        v = d.get(kernel_key, {}).get("dram_bytes_per_launch")
+        v = json.load(open(p)).get(key, {}).get("dram_bytes_per_launch")
         return float(v) if v is not None else None
     except Exception:
         return None
@@ -158,11 +170,7 @@ class Flusher:
         self.buf.fill_(1)
 
 
-def ca_case(api, kind, n, rho, steps, warmup, flush, exec_=None):
-    """Time `steps` CA steps (u8 state -> u8 state) on grid (kind, n, rho).
-    x-run scheme: the three stages smx_ca_step chains (pack -> bit-sliced step ->
-    unpack) are timed individually with events on the launching stream; the
-    step time is pack-start to unpack-end. Block scheme: one kernel."""
+def make_state(api, kind, n, rho):
     import torch
     g = api.make_grid(api.map_kind[kind], 3, n, rho)
     side = g.cell_side()
@@ -170,61 +178,50 @@ def ca_case(api, kind, n, rho, steps, warmup, flush, exec_=None):
     a = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
     b = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
     api.life_init_device(3, side, SEED, a)
-    ex = api.EXEC_RUNS if exec_ is None else exec_
-    bufs = [a, b]
-    res = {"grid": f"{kind}({n}) rho={rho}", "side": side, "cells": cells, "g": g, "bufs": bufs}
-    if ex == api.EXEC_BLOCK:
-        def step(i):
-            api.ca_step_device(g, bufs[i % 2], bufs[(i + 1) % 2], ex)
+    return g, side, cells, a, b
 
-        timed_steps(step, warmup, flush)
-        res["ms"] = timed_steps(step, steps, flush)
-        res["step"] = step
-        return res
+
+def engine_case(api, kind, n, rho, ca_steps, iters, warmup, flush):
+    """`iters` launch_ca calls of `ca_steps` CA steps each (device buffers, AUTO
+    = bit-shadow engine), L2 flushed before each call. ms per call."""
+    g, side, cells, a, b = make_state(api, kind, n, rho)
+
+    def call(i):
+        api.ca_device(g, a, ca_steps, api.EXEC_AUTO, b)
+
+    timed_steps(call, warmup, flush)
+    ms = timed_steps(call, iters, flush)
+    return {"grid": f"{kind}({n}) rho={rho}", "side": side, "cells": cells, "g": g, "ms": ms, "call": call,
+            "bufs": (a, b)}
+
+
+def engine_kernel_ms(api, g, a, ca_steps, iters):
+    """Average duration of the engine stage (smx_bits_run: the plan kernel plus
+    ONE persistent k_ca_bits_run launch of `ca_steps` steps), events on the
+    launching stream around each call; returns ms per call."""
+    import torch
     sa, sb = api.bits_buffer(g), api.bits_buffer(g)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
-
-    def step(i, e=None):
-        cur, nxt = bufs[i % 2], bufs[(i + 1) % 2]
-        if e: e[0].record()
-        api.bits_pack_device(g, cur, sa)
-        if e: e[1].record()
-        api.bits_step_device(g, sa, sb)
-        if e: e[2].record()
-        api.bits_unpack_device(g, sb, nxt)
-        if e: e[3].record()
-
-    for i in range(warmup):
-        flush()
-        step(i)
-    for i in range(steps):
-        flush()
-        step(i, ev[i])
+    api.bits_pack_device(g, a, sa)
+    api.bits_run_device(g, sa, sb, ca_steps)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    for e0, e1 in ev:
+        e0.record()
+        api.bits_run_device(g, sa, sb, ca_steps)
+        e1.record()
     torch.cuda.synchronize()
-    res["stage_ms"] = {name: statistics.mean(e[k].elapsed_time(e[k + 1]) for e in ev)
-                       for k, name in enumerate(("pack", "step", "unpack"))}
+    return statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev)
 
-    # the step itself: ONE smx_ca_step call (the library launches the three
-    # kernels back to back; per-stage events above would add host gaps)
-    def abi_step(i):
-        api.ca_step_device(g, bufs[i % 2], bufs[(i + 1) % 2], api.EXEC_RUNS)
 
-    timed_steps(abi_step, warmup, flush)
-    res["ms"] = timed_steps(abi_step, steps, flush)
-    res["step"] = abi_step
+def step_case(api, kind, n, rho, iters, warmup, flush, exec_):
+    """Single u8 -> u8 CA steps (smx_ca_step), L2 flushed before each. ms per step."""
+    g, side, cells, a, b = make_state(api, kind, n, rho)
+    bufs = [a, b]
 
-    # multi-step engine (smx_ca): the bit shadow carries over, so a step is
-    # step + unpack (the u8 state is still written every step)
-    def estep(i):
-        src, dst = (sa, sb) if i % 2 == 0 else (sb, sa)
-        api.bits_step_device(g, src, dst)
-        api.bits_unpack_device(g, dst, bufs[(i + 1) % 2])
+    def step(i):
+        api.ca_step_device(g, bufs[i % 2], bufs[(i + 1) % 2], exec_)
 
-    api.bits_pack_device(g, a, sa)
-    timed_steps(estep, 2, flush)
-    api.bits_pack_device(g, a, sa)
-    res["engine_ms"] = timed_steps(estep, steps, flush)
-    return res
+    timed_steps(step, warmup, flush)
+    return {"grid": f"{kind}({n}) rho={rho}", "cells": cells, "ms": timed_steps(step, iters, flush), "step": step}
 
 
 def accum_case(api, kind, n, rho, steps, warmup, flush, exec_):
@@ -265,18 +262,6 @@ def energy_per_cell(sampler, step, cells, seconds=0.5):
     return (e1 - e0) * 1e-3 / (cells * i) if e1 is not None else None
 
 
-def ncu_step_traffic():
-    """DRAM bytes per C2 step (sum over the step's kernels) from the committed
-    ncu summary (profiles/ncu_summary.json), or None."""
-    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if not os.path.exists(p):
-        return None
-    try:
-        return json.load(open(p)).get("c2_step", {}).get("dram_bytes_per_step")
-    except Exception:
-        return None
-
-
 def run_ours(args):
     import torch
     from paper_2208_11617_b200 import api
@@ -290,22 +275,35 @@ def run_ours(args):
 
     peak, peak_src = load_peaks()
     flush = Flusher()
-    desc, kind, n, rho = WORKLOADS[args.workload]
+    desc, kind, n, rho, nsteps = WORKLOADS["c2"]
     sampler = ClockSampler(local)
     with sampler:
-        h = ca_case(api, kind, n, rho, args.steps, args.warmup, flush)
-    bb = ca_case(api, "bb", n - 1, rho, args.steps, args.warmup, flush)
-    hb = ca_case(api, kind, n, rho, args.steps, args.warmup, flush, api.EXEC_BLOCK)
-    bbb = ca_case(api, "bb", n - 1, rho, args.steps, args.warmup, flush, api.EXEC_BLOCK)
-    cells = h["cells"]
+        h = engine_case(api, kind, n, rho, nsteps, args.steps, args.warmup, flush)
+    bb = engine_case(api, "bb", n - 1, rho, nsteps, args.steps, args.warmup, flush)
+    cells, side = h["cells"], h["side"]
     ms_h, ms_bb = statistics.mean(h["ms"]), statistics.mean(bb["ms"])
-    value = gcells(cells, ms_h)
-    achieved = 2.0 * cells / (ms_h * 1e-3) / 1e9
+    value = gcells(cells * nsteps, ms_h)
 
-    # e2e: the reference-facing C ABI (smx_ca, launch_ca's semantics) with host
-    # pinned buffers: H2D + one step + D2H inside the timed region
+    # roofline: the dominant kernel (k_ca_bits_run: all 100 steps in one
+    # persistent launch, timed with its plan kernel)
+    kms = engine_kernel_ms(api, h["g"], h["bufs"][0], nsteps, 10)
+    achieved = 2.0 * cells * nsteps / (kms * 1e-3) / 1e9
+    traffic = ncu_kernel_traffic("c2_ca_bits_run")
+
+    # single u8 -> u8 steps: AUTO (fused kernel at this size), the 3-kernel bit
+    # path, and the paper's one-CTA-per-block launch model; H and BB
+    single = {}
+    for name, ex in (("auto", api.EXEC_AUTO), ("bits", api.EXEC_BITS), ("block", api.EXEC_BLOCK)):
+        sh = step_case(api, kind, n, rho, args.steps, args.warmup, flush, ex)
+        sb = step_case(api, "bb", n - 1, rho, args.steps, args.warmup, flush, ex)
+        mh, mb = statistics.mean(sh["ms"]), statistics.mean(sb["ms"])
+        single[name] = {"h_gcells_s": round(gcells(cells, mh), 2), "bb_gcells_s": round(gcells(cells, mb), 2),
+                        "h_vs_bb": round(mb / mh, 3), "h_ms": round(mh, 5)}
+
+    # e2e: the reference-facing C ABI (smx_ca = launch_ca) with pinned host
+    # buffers: H2D + 100 steps + D2H inside the timed region
     host = torch.empty(cells, dtype=torch.uint8, pin_memory=True)
-    api.life_init_device(3, h["side"], SEED, h["bufs"][0])
+    api.life_init_device(3, side, SEED, h["bufs"][0])
     host.copy_(h["bufs"][0].cpu())
     hnp = host.numpy()
     import ctypes as C
@@ -313,57 +311,55 @@ def run_ours(args):
     L = _lib.lib()
     stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
-    def e2e_step(i):
-        _lib.check(L.smx_ca(C.byref(h["g"].raw), hnp.ctypes.data, cells, 1, api.EXEC_AUTO, 0, None, None, None,
-                            stream))
+    def e2e_call(i):
+        _lib.check(L.smx_ca(C.byref(h["g"].raw), hnp.ctypes.data, cells, nsteps, api.EXEC_AUTO, 0, None, None,
+                            None, stream))
 
-    timed_steps(e2e_step, args.warmup)
-    e2e_ms = statistics.mean(timed_steps(e2e_step, args.steps))
+    timed_steps(e2e_call, args.warmup, flush)
+    e2e_ms = statistics.mean(timed_steps(e2e_call, args.steps, flush))
 
-    j_h = energy_per_cell(sampler, h["step"], cells)
-    j_bb = energy_per_cell(sampler, bb["step"], cells)
-    cpu = cpu_baseline_c2(kind, n, rho, h["side"])
+    j_h = energy_per_cell(sampler, h["call"], cells * nsteps)
+    j_bb = energy_per_cell(sampler, bb["call"], cells * nsteps)
+    cpu = cpu_baseline_c2(kind, n, rho, side)
     configs = {} if args.no_configs else extra_configs(api, flush, sampler, peak, args)
-    st = h["stage_ms"]
     line = {
-        "metric": "Gcells/s (3-simplex CA step, H map) — BASELINE metric: Gcells/s and H-vs-BB speedup; "
-                  "HBM GB/s vs peak; J/cell",
+        "metric": METRIC,
         "value": round(value, 3),
-        "unit": "Gcells/s",
+        "unit": "Gcell-steps/s",
         "n_gpus": 1,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": round(ms_h, 6),
+        "ms_per_step": round(ms_h, 5),
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "u8",
         "data": "synthetic (make_life_state seed 42, ~25% alive)",
         "impl": "ours",
-        "config": {"workload": desc, "map": "h3d", "n_b": n, "rho": rho, "side": h["side"], "cells": cells,
-                   "exec": "x-run (pack -> bit-sliced step -> unpack)",
-                   "l2": "flushed before every timed step (256 MiB write)", "parallelism": "single GPU"},
+        "config": {"workload": desc, "map": "h3d", "n_b": n, "rho": rho, "side": side, "cells": cells,
+                   "ca_steps_per_call": nsteps,
+                   "exec": "bit-shadow engine: pack; map once (chunk list); ONE persistent launch of 100 "
+                           "bit-sliced steps (TMA halo boxes, grid barrier per step); unpack",
+                   "l2": "flushed before every bench step (256 MiB write); state L2-resident within a call",
+                   "parallelism": "single GPU"},
         "h_vs_bb": round(ms_bb / ms_h, 3),
-        "bb": {"grid": bb["grid"], "gcells_s": round(gcells(cells, ms_bb), 3), "ms_per_step": round(ms_bb, 6)},
-        "block_scheme": {"h_gcells_s": round(gcells(cells, statistics.mean(hb["ms"])), 3),
-                         "bb_gcells_s": round(gcells(cells, statistics.mean(bbb["ms"])), 3),
-                         "h_vs_bb": round(statistics.mean(bbb["ms"]) / statistics.mean(hb["ms"]), 3),
-                         "note": "the paper's launch model: one CTA per map block, rho^3 threads"},
-        "engine": {"gcells_s": round(gcells(cells, statistics.mean(h["engine_ms"])), 3),
-                   "ms_per_step": round(statistics.mean(h["engine_ms"]), 6),
-                   "note": "multi-step launch_ca: bit shadow carried across steps (step + unpack per step)"},
+        "bb": {"grid": bb["grid"], "gcell_steps_s": round(gcells(cells * nsteps, ms_bb), 3),
+               "ms_per_call": round(ms_bb, 5)},
+        "single_step": single,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": ncu_step_traffic(),
-                     "kernel": "one u8->u8 CA step = k_pack_bits + k_ca_bits + k_unpack_bits",
-                     "basis": "2 B per useful cell per step (u8 read + u8 write); per-launch CUDA events",
-                     "stage_ms": {k: round(v, 6) for k, v in st.items()},
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": "k_ca_bits_run<4> (+ its k_ca_plan): 100 map-driven bit-sliced steps per launch",
+                     "kernel_ms": round(kms, 6), "launches_per_call": 1,
+                     "basis": "2 B per useful cell per step (u8 read + u8 write, SURVEY 8(d)) x 100 steps; "
+                              "CUDA events around the launch; C2's 2.7 MB state is L2-resident, so HBM is "
+                              "not the binding roof here (see configs.C5 for the HBM-bound size)",
                      "peak_source": peak_src},
-        "e2e": {"value": round(gcells(cells, e2e_ms), 3), "unit": "Gcells/s", "h2d_bytes_per_step": cells,
-                "d2h_bytes_per_step": cells, "ms_per_step": round(e2e_ms, 4),
-                "path": "smx_ca(host buffer, steps=1) through the C ABI"},
-        "energy": {"j_per_cell_h": j_h, "j_per_cell_bb": j_bb},
+        "e2e": {"value": round(gcells(cells * nsteps, e2e_ms), 3), "unit": "Gcell-steps/s",
+                "h2d_bytes_per_step": cells, "d2h_bytes_per_step": cells, "ms_per_step": round(e2e_ms, 4),
+                "path": "smx_ca(host buffer, steps=100, EXEC_AUTO) through the C ABI"},
+        "energy": {"j_per_cell_step_h": j_h, "j_per_cell_step_bb": j_bb},
         "cpu_baseline": cpu,
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": 4 * args.steps,  # pack, plan, persistent run, unpack (+1 memset) per call
         "clocks": sampler.summary(),
         "configs": configs,
     }
@@ -379,11 +375,12 @@ def cpu_baseline_c2(kind, n, rho, side):
         s = R.make_life_state(3, side, SEED)
         _, _, _, secs = R.launch_ca(H3D, 3, n, rho, 1, s)
         cells = s.size
-        return {"value": round(cells / secs / 1e9, 6), "unit": "Gcells/s", "cores": 1, "kind": "reference",
-                "sample": f"reference launch_ca over grid_h3d({n}) rho={rho} (side {side}), 1 step, "
-                          f"{secs:.2f} s, g++ -O3 -DNDEBUG (CMake Release flags)"}
+        return {"value": round(cells / secs / 1e9, 6), "unit": "Gcell-steps/s", "cores": 1, "kind": "reference",
+                "sample": f"reference launch_ca over grid_h3d({n}) rho={rho} (side {side}): 1 of the 100 CA "
+                          f"steps, {secs:.2f} s on one host core, g++ -O3 -DNDEBUG (CMake Release flags)"}
     except Exception as e:  # pragma: no cover
-        return {"value": None, "unit": "Gcells/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+        return {"value": None, "unit": "Gcell-steps/s", "cores": 1, "kind": "reference",
+                "sample": f"unavailable: {e}"}
 
 
 def extra_configs(api, flush, sampler, peak, args):
@@ -428,39 +425,62 @@ def extra_configs(api, flush, sampler, peak, args):
         res["grid"] = f"MAP kernel h(n={n}) vs bb({n - 1}), rho=1, m={m} (same cell domain)"
         return res
 
-    def ca_pair(n, rho):
-        r = {}
-        for ex_name, ex in (("runs", api.EXEC_RUNS), ("block", api.EXEC_BLOCK)):
-            h = ca_case(api, "h3d", n, rho, K, W, flush, ex)
-            if ex_name == "runs":
-                r["j_per_cell_h"] = energy_per_cell(sampler, h["step"], h["cells"], 0.3)
-            hms = statistics.mean(h["ms"])
-            extra = {}
-            if ex_name == "runs":
-                extra = {"stage_ms": {k: round(v, 4) for k, v in h["stage_ms"].items()},
-                         "engine_gcells_s": round(gcells(h["cells"], statistics.mean(h["engine_ms"])), 2)}
-            del h
+    def ca_pair(n, rho, ca_steps):
+        """CA at 1 GPU: launch_ca engine calls of `ca_steps` steps (H and BB),
+        the dominant kernel's roofline, and single u8 -> u8 steps."""
+        r = {"grid": f"h3d({n}) vs bb({n - 1}), rho={rho}", "ca_steps_per_call": ca_steps}
+        h = engine_case(api, "h3d", n, rho, ca_steps, 3, 1, flush)
+        cells = h["cells"]
+        r["cells"] = cells
+        r["side"] = h["side"]
+        hms = statistics.mean(h["ms"])
+        kms = engine_kernel_ms(api, h["g"], h["bufs"][0], ca_steps, 3) / ca_steps
+        r["j_per_cell_step_h"] = energy_per_cell(sampler, h["call"], cells * ca_steps, 0.3)
+        del h
+        torch.cuda.empty_cache()
+        b = engine_case(api, "bb", n - 1, rho, ca_steps, 3, 1, flush)
+        bms = statistics.mean(b["ms"])
+        r["j_per_cell_step_bb"] = energy_per_cell(sampler, b["call"], cells * ca_steps, 0.3)
+        del b
+        torch.cuda.empty_cache()
+        gbs = 2.0 * cells * ca_steps / (hms * 1e-3) / 1e9
+        kgbs = 2.0 * cells / (kms * 1e-3) / 1e9
+        r["engine"] = {"h_gcell_steps_s": round(gcells(cells * ca_steps, hms), 2),
+                       "bb_gcell_steps_s": round(gcells(cells * ca_steps, bms), 2),
+                       "h_vs_bb": round(bms / hms, 3), "h_ms_per_call": round(hms, 4),
+                       "h_u8_basis_gb_s": round(gbs, 1), "h_roofline_frac": round(gbs / peak, 4),
+                       "run_kernel_ms_per_step": round(kms, 5), "run_kernel_roofline_frac": round(kgbs / peak, 4),
+                       "note": "pack + plan + ONE persistent launch of ca_steps steps + unpack per call; "
+                               "2 B/cell/step u8 basis"}
+        for name, ex in (("single_auto", api.EXEC_AUTO), ("single_fused", api.EXEC_RUNS),
+                         ("single_block", api.EXEC_BLOCK)):
+            K1 = 3 if name == "single_block" else K
+            sh = step_case(api, "h3d", n, rho, K1, 1, flush, ex)
+            mh = statistics.mean(sh["ms"])
+            del sh
             torch.cuda.empty_cache()
-            b = ca_case(api, "bb", n - 1, rho, K, W, flush, ex)
-            if ex_name == "runs":
-                r["j_per_cell_bb"] = energy_per_cell(sampler, b["step"], b["cells"], 0.3)
-            bms = statistics.mean(b["ms"])
-            cells = b["cells"]
-            gbs = 2.0 * cells / (hms * 1e-3) / 1e9
-            r[ex_name] = {"h_gcells_s": round(gcells(cells, hms), 2), "bb_gcells_s": round(gcells(cells, bms), 2),
-                          "h_vs_bb": round(bms / hms, 3), "h_gb_s": round(gbs, 1),
-                          "h_roofline_frac": round(gbs / peak, 4), **extra}
-            del b
+            sb = step_case(api, "bb", n - 1, rho, K1, 1, flush, ex)
+            mb = statistics.mean(sb["ms"])
+            del sb
             torch.cuda.empty_cache()
-        r["cells"] = api.tet_cells((n - 1) * rho)
-        r["grid"] = f"h3d({n}) vs bb({n - 1}), rho={rho}"
+            g1 = 2.0 * cells / (mh * 1e-3) / 1e9
+            r[name] = {"h_gcells_s": round(gcells(cells, mh), 2), "bb_gcells_s": round(gcells(cells, mb), 2),
+                       "h_vs_bb": round(mb / mh, 3), "h_ms": round(mh, 4), "h_roofline_frac": round(g1 / peak, 4)}
         return r
 
     out["C1_accum_n1024"] = accum_pair(1024, 16)
     out["C1_map_kernel_2d"] = map_pair(2, 1024)
     out["C3_accum_n65536"] = accum_pair(4096, 16)
-    out["C4_ca_n1024_1gpu"] = ca_pair(128, 8)
-    out["C5_ca_n2048_1gpu"] = ca_pair(256, 8)
+    out["C4_ca_n1024_1gpu"] = ca_pair(128, 8, 100)
+    out["C5_ca_n2048_1gpu"] = ca_pair(256, 8, 20)
+    # rho sweep at the same n = 2048 cell scale (SURVEY 8(d): trade map
+    # amortisation against the BB/H block ratio); r/beta are fixed at (2, 2)
+    # by the executable map (SURVEY 0.4)
+    c5r4 = engine_case(api, "h3d", 512, 4, 20, 3, 1, flush)
+    out["C5_rho4_engine"] = {"grid": "h3d(512) rho=4", "side": c5r4["side"], "cells": c5r4["cells"],
+                             "h_gcell_steps_s": round(gcells(c5r4["cells"] * 20, statistics.mean(c5r4["ms"])), 2)}
+    del c5r4
+    torch.cuda.empty_cache()
     out["map_kernel_3d"] = map_pair(3, 256)
     return out
 
@@ -468,14 +488,16 @@ def extra_configs(api, flush, sampler, peak, args):
 def run_reference(args):
     """The reference's own CPU implementation (oracle/_ref) on the C2 workload:
     one launch_ca step per replica, one replica per host core (the reference is
-    single-threaded within a launch, report.hpp:125-156)."""
+    single-threaded within a launch, report.hpp:125-156). Bounded sample: the
+    reference needs ~1 s per C2 step, so a bench step times 1 of the 100 CA
+    steps per replica; the value is Gcell-steps/s, the same metric as ours."""
     rank = env_int("RANK", 0)
     if rank != 0:
         return None
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle.oracle import H3D, Reference, ncpu, reference_available
-    desc, kind, n, rho = WORKLOADS[args.workload]
+    desc, kind, n, rho, nsteps = WORKLOADS["c2"]
     side = (n - 1) * rho
     if not reference_available():
         return {"impl": "reference", "unavailable": "oracle/_ref (reference headers compiled) not built"}
@@ -502,17 +524,17 @@ def run_reference(args):
     cells = init.size
     value = cores * cells / (ms * 1e-3) / 1e9
     return {
-        "metric": "Gcells/s (3-simplex CA step, H map) — BASELINE metric: Gcells/s and H-vs-BB speedup; "
-                  "HBM GB/s vs peak; J/cell",
-        "value": round(value, 6), "unit": "Gcells/s", "n_gpus": 0, "steps": K, "warmup": W,
+        "metric": METRIC,
+        "value": round(value, 6), "unit": "Gcell-steps/s", "n_gpus": 0, "steps": K, "warmup": W,
         "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "u8", "data": "synthetic (make_life_state seed 42)", "impl": "reference",
         "config": {"workload": desc, "map": "h3d", "n_b": n, "rho": rho, "side": side, "cells": cells,
                    "parallelism": f"{cores} independent replicas, one per host core"},
-        "cpu_baseline": {"value": round(value, 6), "unit": "Gcells/s", "cores": cores, "kind": "reference",
-                         "sample": f"reference launch_ca(grid_h3d({n}), rho={rho}) 1 step x {cores} replicas "
-                                   f"per bench step; K capped at 3 for a few-minute run"},
-        "e2e": {"value": round(value, 6), "unit": "Gcells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": round(value, 6), "unit": "Gcell-steps/s", "cores": cores, "kind": "reference",
+                         "sample": f"reference launch_ca(grid_h3d({n}), rho={rho}): 1 CA step x {cores} replicas "
+                                   f"per bench step (of the workload's {nsteps}); K capped at 3"},
+        "e2e": {"value": round(value, 6), "unit": "Gcell-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
     }
 
 
@@ -522,7 +544,6 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config table")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup

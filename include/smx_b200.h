@@ -158,6 +158,12 @@ int smx_bits_pack(const smx_grid* g, const uint8_t* cells, uint64_t ncells, uint
 int smx_bits_step(const smx_grid* g, const uint32_t* bits_in, uint32_t* bits_out, int64_t wz_lo, int64_t wz_hi,
                   void* stream);
 int smx_bits_unpack(const smx_grid* g, const uint32_t* bits, uint8_t* cells, uint64_t ncells, void* stream);
+/* The multi-step engine stage smx_ca runs between pack and unpack: the map is
+ * applied once (a chunk list of the grid's x-adjacent tile chains), then ONE
+ * persistent cooperative launch runs `steps` bit-sliced Life steps bits_a ->
+ * bits_b -> bits_a ... (grid barrier between steps). The result is in bits_a
+ * for even `steps`, bits_b for odd. Device pointers (smx_bits_bytes each). */
+int smx_bits_run(const smx_grid* g, uint32_t* bits_a, uint32_t* bits_b, int64_t steps, void* stream);
 
 /* simplex_grid_state::hash (simulator.hpp:68-73): FNV-1a-64 over u64 m,
  * u64 side, then the raw cell bytes. Host bytes. */

@@ -77,6 +77,7 @@ _SIGS = {
     "smx_bits_pack": ([_G, _VP, C.c_uint64, _VP, _VP], C.c_int),
     "smx_bits_step": ([_G, _VP, _VP, C.c_int64, C.c_int64, _VP], C.c_int),
     "smx_bits_unpack": ([_G, _VP, _VP, C.c_uint64, _VP], C.c_int),
+    "smx_bits_run": ([_G, _VP, _VP, C.c_int64, _VP], C.c_int),
 }
 
 _lib = None

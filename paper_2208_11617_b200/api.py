@@ -484,6 +484,12 @@ def bits_step_device(g: grid_spec, bits_in, bits_out, wz_lo: int = 0, wz_hi: int
     check(lib().smx_bits_step(C.byref(g.raw), _ptr(bits_in), _ptr(bits_out), wz_lo, hi, _stream()))
 
 
+def bits_run_device(g: grid_spec, bits_a, bits_b, steps: int) -> None:
+    """The engine stage: map once + one persistent launch of `steps` steps
+    (result in bits_a for even steps, bits_b for odd)."""
+    check(lib().smx_bits_run(C.byref(g.raw), _ptr(bits_a), _ptr(bits_b), steps, _stream()))
+
+
 def bits_unpack_device(g: grid_spec, bits, cells) -> None:
     check(lib().smx_bits_unpack(C.byref(g.raw), _ptr(bits), _ptr(cells), cells.numel(), _stream()))
 

@@ -39,6 +39,8 @@
 
 namespace smx {
 
+int bits_pitch_words(int side);
+
 namespace {
 
 using namespace ca;
@@ -246,45 +248,28 @@ __device__ __forceinline__ void issue_item(const CUtensorMap* tm, const Chunk* s
 }
 
 // ---------------------------------------------------------------------------
-template <int KIND, int RHO>
-__global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_constant__ CUtensorMap tmap,
-                                                  uint32_t* __restrict__ nbits, int WP, int P, int NZ, int wz1) {
+// One warp's share of a step: items item0, item0 + istride, ... of a chunk list
+// (CPI chunks per item). Per item ONE 3-D TMA box per chunk lands the halo in
+// shared memory (double-buffered across items, mbarrier completion), lanes
+// form the horizontal 3-sums as bit-planes, then lane (ly, w) marches z and
+// writes whole 32-bit words of the next bit shadow. `phases` carries the two
+// mbarriers' parities across calls (the persistent kernel reuses them).
+template <int RHO>
+__device__ __forceinline__ void run_items(const Chunk* __restrict__ s_chunk, int nchunks, int item0, int istride,
+                                          const CUtensorMap* tm, uint32_t* __restrict__ nbits, int S, int WP,
+                                          uint8_t* wbase, uint32_t mbar0, uint32_t& phases) {
     using C = Cfg<RHO>;
-    const int PP = P * P;
-    const int NBP = PP * NZ;  // blocks of this CTA: a P x P patch at NZ consecutive wz
     constexpr int HL = C::HL;
-    extern __shared__ __align__(128) uint8_t smem[];
-    int4* s_tile = reinterpret_cast<int4*>(smem + NWARP * C::WARP_BYTES);
-    Chunk* s_chunk = reinterpret_cast<Chunk*>(smem + NWARP * C::WARP_BYTES + NBP * 16);
-    int* s_nchunks = reinterpret_cast<int*>(smem + NWARP * C::WARP_BYTES + 2 * NBP * 16);
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wzb = wz0 + blockIdx.z * NZ;
-    const int S = g.side;
-    const unsigned long long* __restrict__ PZ = g.prefix;
-
-    uint8_t* wbase = smem + warp * C::WARP_BYTES;
+    const int lane = threadIdx.x & 31;
     uint32_t* sH = reinterpret_cast<uint32_t*>(wbase + 2 * C::BUF);  // [HROWS][8]: h0 w0..3, h1 w0..3
-    const uint32_t mbar0 = smem_u32(wbase + 2 * C::BUF + C::HROWS * 32);
-
-    // ---- 1-2. map the patch, chain x-adjacent tiles into chunks ----
-    if (lane == 0) {
-        mbar_init(mbar0, 1);
-        mbar_init(mbar0 + 8, 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    const int nchunks = build_chunks<KIND>(g, wzb, wz1, P, NZ, C::LMAX, s_tile, s_chunk, s_nchunks);
     const int nitems = (nchunks + C::CPI - 1) / C::CPI;
-
-    uint32_t phases = 0u;  // bit b: parity of buffer b
-    int item = warp, b = 0;
-    const CUtensorMap* tm = &tmap;
+    int item = item0, b = 0;
     if (item < nitems && lane == 0) {
         fence_proxy_async();
         issue_item<RHO>(tm, s_chunk, nchunks, item, wbase, mbar0);
     }
-    for (; item < nitems; item += NWARP, b ^= 1) {
-        const int nxt = item + NWARP;
+    for (; item < nitems; item += istride, b ^= 1) {
+        const int nxt = item + istride;
         if (nxt < nitems && lane == 0) {
             fence_proxy_async();
             issue_item<RHO>(tm, s_chunk, nchunks, nxt, wbase + (b ^ 1) * C::BUF, mbar0 + 8 * (b ^ 1));
@@ -369,6 +354,107 @@ __global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_
     }
 }
 
+// ---------------------------------------------------------------------------
+// Per-launch scheme: the CTA maps its P x P x NZ patch, builds its chunks in
+// shared memory and runs them (one launch per step; smx_bits_step).
+template <int KIND, int RHO>
+__global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_constant__ CUtensorMap tmap,
+                                                  uint32_t* __restrict__ nbits, int WP, int P, int NZ, int wz1) {
+    using C = Cfg<RHO>;
+    const int NBP = P * P * NZ;  // blocks of this CTA: a P x P patch at NZ consecutive wz
+    extern __shared__ __align__(128) uint8_t smem[];
+    int4* s_tile = reinterpret_cast<int4*>(smem + NWARP * C::WARP_BYTES);
+    Chunk* s_chunk = reinterpret_cast<Chunk*>(smem + NWARP * C::WARP_BYTES + NBP * 16);
+    int* s_nchunks = reinterpret_cast<int*>(smem + NWARP * C::WARP_BYTES + 2 * NBP * 16);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t* wbase = smem + warp * C::WARP_BYTES;
+    const uint32_t mbar0 = smem_u32(wbase + 2 * C::BUF + C::HROWS * 32);
+    if (lane == 0) {
+        mbar_init(mbar0, 1);
+        mbar_init(mbar0 + 8, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    const int nchunks = build_chunks<KIND>(g, wz0 + blockIdx.z * NZ, wz1, P, NZ, C::LMAX, s_tile, s_chunk, s_nchunks);
+    uint32_t phases = 0u;
+    run_items<RHO>(s_chunk, nchunks, warp, NWARP, &tmap, nbits, g.side, WP, wbase, mbar0, phases);
+}
+
+// ---------------------------------------------------------------------------
+// Multi-step engine (smx_ca, EXEC_BITS). The map is applied ONCE per launch_ca
+// call: k_ca_plan maps every patch of the grid and appends its chunks to one
+// global list; k_ca_bits_run is a persistent cooperative kernel that runs all
+// the steps over that list (every warp takes items round-robin, so consecutive
+// items — spatial neighbours — run concurrently) with a grid barrier between
+// steps. No per-step launch or re-mapping; the chain-building cost is paid once.
+template <int KIND, int RHO>
+__global__ void __launch_bounds__(NTHR) k_ca_plan(Geom g, int wz0, int wz1, int P, int NZ, Chunk* __restrict__ out,
+                                                  unsigned* __restrict__ count) {
+    using C = Cfg<RHO>;
+    const int NBP = P * P * NZ;
+    extern __shared__ __align__(128) uint8_t smem[];
+    int4* s_tile = reinterpret_cast<int4*>(smem);
+    Chunk* s_chunk = reinterpret_cast<Chunk*>(smem + NBP * 16);
+    int* s_nchunks = reinterpret_cast<int*>(smem + 2 * NBP * 16);
+    __shared__ unsigned s_base;
+    const int n = build_chunks<KIND>(g, wz0 + blockIdx.z * NZ, wz1, P, NZ, C::LMAX, s_tile, s_chunk, s_nchunks);
+    if (threadIdx.x == 0) s_base = atomicAdd(count, unsigned(n));
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[s_base + i] = s_chunk[i];
+}
+
+// all CTAs co-resident (cooperative launch); bar[0] = arrivals, bar[1] = generation
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+    // generic-proxy writes of this step must be visible to the next step's TMA reads
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g0 = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g0) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+
+constexpr int RUN_NWARP = 16;  // persistent kernel: one 16-warp CTA per SM (fewer barrier arrivals)
+
+template <int RHO>
+__global__ void __launch_bounds__(RUN_NWARP * 32) k_ca_bits_run(const __grid_constant__ CUtensorMap tmA,
+                                                      const __grid_constant__ CUtensorMap tmB, uint32_t* bitsA,
+                                                      uint32_t* bitsB, const Chunk* __restrict__ chunks,
+                                                      const unsigned* __restrict__ count, int steps, int S, int WP,
+                                                      unsigned* bar) {
+    using C = Cfg<RHO>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t* wbase = smem + warp * C::WARP_BYTES;
+    const uint32_t mbar0 = smem_u32(wbase + 2 * C::BUF + C::HROWS * 32);
+    if (lane == 0) {
+        mbar_init(mbar0, 1);
+        mbar_init(mbar0 + 8, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncthreads();
+    const int nchunks = int(*count);
+    const int gwarp = blockIdx.x * RUN_NWARP + warp, nwarps = gridDim.x * RUN_NWARP;
+    uint32_t phases = 0u;
+    for (int st = 0; st < steps; ++st) {
+        const bool even = (st & 1) == 0;
+        run_items<RHO>(chunks, nchunks, gwarp, nwarps, even ? &tmA : &tmB, even ? bitsB : bitsA, S, WP, wbase,
+                       mbar0, phases);
+        if (st + 1 < steps) grid_barrier(bar, gridDim.x);
+    }
+}
+
 template <int KIND, int RHO>
 void launch_t(const Geom& g, int wz0, int wz1, const CUtensorMap& tmap, uint32_t* nbits, int WP, cudaStream_t s) {
     using C = Cfg<RHO>;
@@ -389,6 +475,36 @@ void launch_t(const Geom& g, int wz0, int wz1, const CUtensorMap& tmap, uint32_t
     while (P > 4 && ctas(P, NZ) < 4 * 148) P = P / 2 > 4 ? P / 2 : 4;
     const dim3 grid((g.ex + P - 1) / P, (g.ey + P - 1) / P, (wz1 - wz0 + NZ - 1) / NZ);
     k_ca_bits<KIND, RHO><<<grid, NTHR, C::smem(P * P * NZ), s>>>(g, wz0, tmap, nbits, WP, P, NZ, wz1);
+}
+
+template <int KIND, int RHO>
+void launch_plan_t(const Geom& g, void* chunks, unsigned* count, cudaStream_t s) {
+    using C = Cfg<RHO>;
+    const int P = C::LMAX, NZ = 1;  // longest chains; the plan kernel is cheap
+    const dim3 grid((g.ex + P - 1) / P, (g.ey + P - 1) / P, g.ez);
+    k_ca_plan<KIND, RHO><<<grid, NTHR, 2 * P * P * NZ * 16 + 16, s>>>(g, 0, g.ez, P, NZ,
+                                                                      reinterpret_cast<Chunk*>(chunks), count);
+}
+
+template <int RHO>
+cudaError_t launch_run_t(const Geom& g, const CUtensorMap& tA, const CUtensorMap& tB, uint32_t* A, uint32_t* B,
+                         const void* chunks, const unsigned* count, int steps, unsigned* bar, cudaStream_t s) {
+    using C = Cfg<RHO>;
+    const int smem = RUN_NWARP * C::WARP_BYTES;
+    static int grid = [&] {
+        cudaFuncSetAttribute(k_ca_bits_run<RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int per_sm = 0, dev = 0, nsm = 148;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ca_bits_run<RHO>, RUN_NWARP * 32, smem);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        return (per_sm > 0 ? per_sm : 1) * nsm;
+    }();
+    const Chunk* ch = reinterpret_cast<const Chunk*>(chunks);
+    int S = g.side, WP = bits_pitch_words(g.side);
+    void* args[] = {const_cast<CUtensorMap*>(&tA), const_cast<CUtensorMap*>(&tB), &A, &B, &ch,
+                    const_cast<unsigned**>(&count), &steps, &S, &WP, &bar};
+    return cudaLaunchCooperativeKernel((const void*)k_ca_bits_run<RHO>, dim3(grid), dim3(RUN_NWARP * 32), args, smem,
+                                       s);
 }
 
 template <int KIND>
@@ -437,6 +553,26 @@ void launch_unpack_bits(const Geom& g, const uint32_t* bits, uint8_t* out, cudaS
     const int rpw = rows_per_warp(nrows);
     const int warps = (nrows + rpw - 1) / rpw;
     k_unpack_bits<<<(warps + 7) / 8, 256, 0, s>>>(bits, out, S, WP, nrows, g.prefix, rpw);
+}
+
+unsigned long long ca_plan_capacity(const Geom& g) { return (unsigned long long)g.ex * g.ey * g.ez; }
+
+void launch_ca_plan(const Geom& g, int kind, void* chunks, unsigned* count, cudaStream_t s) {
+    if (kind == SMX_H3D) {
+        if (g.rho == 4) launch_plan_t<SMX_H3D, 4>(g, chunks, count, s);
+        else launch_plan_t<SMX_H3D, 8>(g, chunks, count, s);
+    } else {
+        if (g.rho == 4) launch_plan_t<SMX_BB, 4>(g, chunks, count, s);
+        else launch_plan_t<SMX_BB, 8>(g, chunks, count, s);
+    }
+}
+
+cudaError_t launch_ca_bits_run(const Geom& g, const void* tmA, const void* tmB, uint32_t* A, uint32_t* B,
+                               const void* chunks, const unsigned* count, int steps, unsigned* bar, cudaStream_t s) {
+    const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(tmA);
+    const CUtensorMap& tb = *reinterpret_cast<const CUtensorMap*>(tmB);
+    if (g.rho == 4) return launch_run_t<4>(g, ta, tb, A, B, chunks, count, steps, bar, s);
+    return launch_run_t<8>(g, ta, tb, A, B, chunks, count, steps, bar, s);
 }
 
 void launch_ca_bits(const Geom& g, int kind, int wz0, int wz1, const void* tmap_ptr, uint32_t* nbits, cudaStream_t s) {

@@ -56,8 +56,9 @@ bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 // grow-only staging pool for host-buffer calls, counters and the MAP sink.
 struct DeviceRes {
     std::map<int64_t, unsigned long long*> prefix;
-    void* pool[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // 0 cov, 1/2 u8, 3/4 bit shadows
-    size_t pool_bytes[5] = {0, 0, 0, 0, 0};
+    // 0 cov, 1/2 u8, 3/4 bit shadows, 5 CA chunk list, 6 engine control words
+    void* pool[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    size_t pool_bytes[7] = {0, 0, 0, 0, 0, 0, 0};
     std::map<std::pair<const void*, std::pair<int64_t, int64_t>>, CUtensorMap> tmaps;
     smx::DevCounters* counters = nullptr;
     unsigned* sink = nullptr;
@@ -257,6 +258,22 @@ int bits_tmap(const uint32_t* bits, int64_t side, int64_t rho, const CUtensorMap
 int ca_fused_step(const smx::Geom& k, int64_t wz0, int64_t wz1, const uint8_t* cur, uint8_t* next, cudaStream_t s) {
     smx::launch_ca_fused(k, int(wz0), int(wz1), cur, next, s);
     TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
+// plan (map once -> chunk list) + persistent multi-step run, A -> B -> A ...
+int bits_engine(const smx_grid* g, const smx::Geom& k, uint32_t* A, uint32_t* B, const CUtensorMap* ta,
+                const CUtensorMap* tb, int64_t steps, cudaStream_t s) {
+    if (steps <= 0) return SMX_OK;
+    if (steps > INT32_MAX) return fail(SMX_ERANGE, "launch_ca: steps must fit int32");
+    void *pch, *pctl;
+    if (int rc = pool_get(5, size_t(smx::ca_plan_capacity(k)) * 16, &pch)) return rc;
+    if (int rc = pool_get(6, 64, &pctl)) return rc;
+    unsigned* count = (unsigned*)pctl;
+    unsigned* bar = count + 4;
+    TRY(cudaMemsetAsync(pctl, 0, 64, s));
+    smx::launch_ca_plan(k, g->kind, pch, count, s);
+    TRY(smx::launch_ca_bits_run(k, ta, tb, A, B, pch, count, int(steps), bar, s));
     return SMX_OK;
 }
 
@@ -571,18 +588,11 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
         const CUtensorMap *ta, *tb;
         if (int rc = bits_tmap((const uint32_t*)pa, k.side, k.rho, &ta)) return rc;
         if (int rc = bits_tmap((const uint32_t*)pb, k.side, k.rho, &tb)) return rc;
+        // the map applied once (chunk list), then ONE persistent launch for all
+        // steps, A -> B -> A ..., and the final shadow unpacked in place
         smx::launch_pack_bits(k, cur, (uint32_t*)pa, s);
-        uint32_t* bc = (uint32_t*)pa;
-        uint32_t* bn = (uint32_t*)pb;
-        const CUtensorMap* tc = ta;
-        const CUtensorMap* tn = tb;
-        for (int64_t st = 0; st < steps; ++st) {
-            smx::launch_ca_bits(k, g->kind, 0, k.ez, tc, bn, s);
-            std::swap(bc, bn);
-            std::swap(tc, tn);
-        }
-        smx::launch_unpack_bits(k, bc, nxt, s);
-        std::swap(cur, nxt);
+        if (int rc = bits_engine(g, k, (uint32_t*)pa, (uint32_t*)pb, ta, tb, steps, s)) return rc;
+        smx::launch_unpack_bits(k, (steps & 1) ? (const uint32_t*)pb : (const uint32_t*)pa, cur, s);
     } else {
         for (int64_t st = 0; st < steps; ++st) {
             if (exec == SMX_EXEC_RUNS) {
@@ -643,6 +653,19 @@ int smx_bits_unpack(const smx_grid* g, const uint32_t* bits, uint8_t* cells, uin
     smx::launch_unpack_bits(k, bits, cells, (cudaStream_t)stream);
     TRY(cudaGetLastError());
     return SMX_OK;
+}
+
+int smx_bits_run(const smx_grid* g, uint32_t* bits_a, uint32_t* bits_b, int64_t steps, void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    int32_t ex = SMX_EXEC_BITS;
+    if (int rc = ca_validate(g, smx::tet_cells(k.side), &ex)) return rc;
+    if (steps < 0) return fail(SMX_EINVAL, "bits_run: steps must be >= 0");
+    if (bits_a == bits_b) return fail(SMX_EINVAL, "bits_run: the two shadows must not alias");
+    const CUtensorMap *ta, *tb;
+    if (int rc = bits_tmap(bits_a, k.side, k.rho, &ta)) return rc;
+    if (int rc = bits_tmap(bits_b, k.side, k.rho, &tb)) return rc;
+    return bits_engine(g, k, bits_a, bits_b, ta, tb, steps, (cudaStream_t)stream);
 }
 
 uint64_t smx_state_hash(int32_t m, int64_t side, const void* bytes, uint64_t nbytes) {

@@ -114,36 +114,36 @@ __global__ void k_accum_block(Geom g, uint32_t* __restrict__ cells) {
 }
 
 // ---------------------------------------------------------------------------
-// ACCUM, x-run scheme. CTA (256 threads) = KX consecutive map blocks of one
+// ACCUM, x-run scheme. CTA (256 threads) = KX (32) consecutive map blocks of one
 // grid row. Warp 0 maps them lane-parallel; tiles whose predecessor lane maps to
 // the x-adjacent tile join one run (H2D: every q-run of length b; BB: the row
 // segment left of the diagonal). Each run is then streamed row by row with
 // 128-bit loads/stores over its 16-byte-aligned interior and scalar head/tail.
 constexpr int ACC_THREADS = 256;
 
-__device__ __forceinline__ void accum_rows2(uint32_t* __restrict__ cells, unsigned long long e0a,
-                                            unsigned long long e1a, unsigned long long e0b,
-                                            unsigned long long e1b, int lane) {
-    // Row A and row B, each [e0, e1). Interior vectors of both rows are loaded
-    // before any store so every lane keeps up to 2*NV 16-byte loads in flight.
-    constexpr int NV = 4;
-    unsigned long long a0[2], a1[2], e0[2] = {e0a, e0b}, e1[2] = {e1a, e1b};
-    uint4 v[2][NV];
+// RR rows per warp batch, each [e0, e1): the interior 16-byte vectors of all RR
+// rows are loaded before any store, so a lane keeps up to RR * NV 16-byte loads
+// in flight (the in-place read-modify-write is HBM-latency bound otherwise).
+template <int RR, int NV>
+__device__ __forceinline__ void accum_rows(uint32_t* __restrict__ cells, const unsigned long long (&e)[RR][2],
+                                           int lane) {
+    unsigned long long a0[RR], a1[RR];
+    uint4 v[RR][NV];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        a0[r] = (e0[r] + 3) & ~3ull;
-        a1[r] = e1[r] & ~3ull;
-        if (a0[r] > a1[r]) a0[r] = a1[r] = e1[r];  // short row: all scalar
+    for (int r = 0; r < RR; ++r) {
+        a0[r] = (e[r][0] + 3) & ~3ull;
+        a1[r] = e[r][1] & ~3ull;
+        if (a0[r] > a1[r]) a0[r] = a1[r] = e[r][1];  // short row: all scalar
     }
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+    for (int r = 0; r < RR; ++r)
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             const unsigned long long p = a0[r] + 4ull * (lane + 32 * k);
             if (p < a1[r]) v[r][k] = *reinterpret_cast<const uint4*>(cells + p);
         }
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+    for (int r = 0; r < RR; ++r)
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             const unsigned long long p = a0[r] + 4ull * (lane + 32 * k);
@@ -154,7 +154,7 @@ __device__ __forceinline__ void accum_rows2(uint32_t* __restrict__ cells, unsign
             }
         }
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < RR; ++r) {
         // long rows beyond the unrolled window
         for (unsigned long long p = a0[r] + 4ull * (lane + 32 * NV); p < a1[r]; p += 128ull) {
             uint4 t = *reinterpret_cast<const uint4*>(cells + p);
@@ -162,14 +162,14 @@ __device__ __forceinline__ void accum_rows2(uint32_t* __restrict__ cells, unsign
             *reinterpret_cast<uint4*>(cells + p) = t;
         }
         // scalar head [e0, a0) and tail [a1, e1): at most 3 + 3 cells, or a short row
-        const unsigned long long nh = a0[r] - e0[r];
-        for (unsigned long long i = lane; i < nh; i += 32) cells[e0[r] + i] += 1u;
-        const unsigned long long nt = e1[r] - a1[r];
+        const unsigned long long nh = a0[r] - e[r][0];
+        for (unsigned long long i = lane; i < nh; i += 32) cells[e[r][0] + i] += 1u;
+        const unsigned long long nt = e[r][1] - a1[r];
         for (unsigned long long i = lane; i < nt; i += 32) cells[a1[r] + i] += 1u;
     }
 }
 
-template <int KIND, int KX>
+template <int KIND, int KX, int RR, int NV>
 __global__ void __launch_bounds__(ACC_THREADS) k_accum_runs(Geom g, uint32_t* __restrict__ cells) {
     static_assert(KX <= 32, "one warp maps the strip");
     __shared__ int s_run[KX][3];
@@ -206,10 +206,11 @@ __global__ void __launch_bounds__(ACC_THREADS) k_accum_runs(Geom g, uint32_t* __
     const int rho = g.rho, S = g.side;
     const int rows = nruns * rho;
     constexpr int NW = ACC_THREADS / 32;
-    for (int row = warp; row < rows; row += 2 * NW) {
-        unsigned long long e[2][2] = {{0, 0}, {0, 0}};
+    for (int row = warp; row < rows; row += RR * NW) {
+        unsigned long long e[RR][2];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < RR; ++h) {
+            e[h][0] = e[h][1] = 0;
             const int rr = row + h * NW;
             if (rr >= rows) continue;
             const int r = rr / rho, ly = rr - r * rho;
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(ACC_THREADS) k_accum_runs(Geom g, uint32_t* __
             e[h][0] = base + xlo;
             e[h][1] = base + xhi;
         }
-        accum_rows2(cells, e[0][0], e[0][1], e[1][0], e[1][1], lane);
+        accum_rows<RR, NV>(cells, e, lane);
     }
 }
 
@@ -388,14 +389,20 @@ void launch_map_block(const Geom& g, uint32_t* cov, DevCounters* cnt, unsigned* 
     SMX_DISPATCH_KIND(g.kind, launch_map_block_k, g, 0, g.ez, cov, cnt, sink, s);
 }
 
+template <int KIND, int KX, int RR, int NV>
+static void launch_runs_t(const Geom& g, uint32_t* cells, cudaStream_t s) {
+    k_accum_runs<KIND, KX, RR, NV><<<dim3((g.ex + KX - 1) / KX, g.ey, 1), ACC_THREADS, 0, s>>>(g, cells);
+}
+
 template <int KIND>
 static void launch_accum_k(const Geom& g, uint32_t* cells, int exec, cudaStream_t s) {
     if (exec == SMX_EXEC_BLOCK) {
         k_accum_block<KIND><<<dim3(g.ex, g.ey, 1), block_shape(g), 0, s>>>(g, cells);
-    } else {
-        constexpr int KX = 16;
-        k_accum_runs<KIND, KX><<<dim3((g.ex + KX - 1) / KX, g.ey, 1), ACC_THREADS, 0, s>>>(g, cells);
+        return;
     }
+    // 32 blocks per CTA strip, 2 rows x 4 vectors in flight per lane: C3 at
+    // 0.80 of the measured HBM peak (profiles/r1/accum_sweep.txt)
+    launch_runs_t<KIND, 32, 2, 4>(g, cells, s);
 }
 void launch_accum(const Geom& g, uint32_t* cells, int exec, cudaStream_t s) {
     SMX_DISPATCH_KIND(g.kind, launch_accum_k, g, cells, exec, s);

@@ -24,6 +24,14 @@ void launch_pack_bits(const Geom& g, const uint8_t* cur, uint32_t* bits, cudaStr
 void launch_unpack_bits(const Geom& g, const uint32_t* bits, uint8_t* out, cudaStream_t s);
 // tmap: CUtensorMap over the input bit shadow; writes the next bit shadow
 void launch_ca_bits(const Geom& g, int kind, int wz0, int wz1, const void* tmap, uint32_t* nbits, cudaStream_t s);
+// multi-step engine: the map applied once (chunk list, 16 B per chunk, at most
+// ca_plan_capacity entries; *count must be zero), then ONE persistent
+// cooperative launch runs `steps` bit-sliced steps A -> B -> A ...
+// (bar: two zeroed u32 for the grid barrier)
+unsigned long long ca_plan_capacity(const Geom& g);
+void launch_ca_plan(const Geom& g, int kind, void* chunks, unsigned* count, cudaStream_t s);
+cudaError_t launch_ca_bits_run(const Geom& g, const void* tmA, const void* tmB, uint32_t* A, uint32_t* B,
+                               const void* chunks, const unsigned* count, int steps, unsigned* bar, cudaStream_t s);
 void launch_tiles_pack(const Geom& g, const uint8_t* cells, const int* tiles, unsigned long long ntiles,
                        uint8_t* out, cudaStream_t s);
 void launch_tiles_unpack(const Geom& g, uint8_t* cells, const int* tiles, unsigned long long ntiles,
