@@ -535,6 +535,7 @@ int smx_ca_step(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint64_t n
 
 int smx_ca_step_range(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint64_t ncells, int64_t wz_lo,
                       int64_t wz_hi, int32_t exec, void* stream) {
+    const bool auto_exec = exec < 0;
     smx::Geom k;
     if (int rc = make_geom(g, &k, true)) return rc;
     if (int rc = ca_validate(g, ncells, &exec)) return rc;
@@ -542,6 +543,7 @@ int smx_ca_step_range(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint
         return fail(SMX_EINVAL, "ca_step_range: wz range outside the grid");
     if (cur == next) return fail(SMX_EINVAL, "ca_step_range: cur and next must not alias");
     if (int rc = check_align16(cur, next)) return rc;
+    if (auto_exec && exec == SMX_EXEC_BITS && ncells <= kFusedMaxCells) exec = SMX_EXEC_RUNS;
     if (exec == SMX_EXEC_BITS) return ca_runs_step(g, k, wz_lo, wz_hi, cur, next, (cudaStream_t)stream);
     if (exec == SMX_EXEC_RUNS) return ca_fused_step(k, wz_lo, wz_hi, cur, next, (cudaStream_t)stream);
     smx::launch_ca(k, int(wz_lo), int(wz_hi), cur, next, exec, (cudaStream_t)stream);
