@@ -125,15 +125,18 @@ struct RowCursor {
     long long rowbase;  // packed index of cell (0, y, z)
 };
 
+// packed row r -> (z, y): layer z holds S - z rows, so rows before layer z are
+// layer_row(z) = z (2S + 1 - z) / 2; z = floor of the smaller root of
+// z^2 - (2S+1) z + 2r = 0, corrected by one either way (no dependent loads)
 __device__ __forceinline__ RowCursor row_at(int row, int S, const unsigned long long* __restrict__ PZ) {
-    int lo = 0, hi = S - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (layer_row(mid, S) <= row) lo = mid;
-        else hi = mid - 1;
-    }
-    const int y = row - layer_row(lo, S);
-    return RowCursor{lo, y, (long long)(PZ[lo] + tri_idx(0, y))};
+    const double b = 2.0 * S + 1.0;
+    int z = int((b - sqrt(b * b - 8.0 * row)) * 0.5);
+    if (z < 0) z = 0;
+    if (z > S - 1) z = S - 1;
+    while (z > 0 && layer_row(z, S) > row) --z;
+    while (z < S - 1 && layer_row(z + 1, S) <= row) ++z;
+    const int y = row - layer_row(z, S);
+    return RowCursor{z, y, (long long)(PZ[z] + tri_idx(0, y))};
 }
 
 __device__ __forceinline__ void row_next(RowCursor& c, int S, const unsigned long long* __restrict__ PZ) {
