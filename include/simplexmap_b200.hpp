@@ -6,9 +6,12 @@
 // Same names, argument meaning and exceptions as the reference for the
 // functions on the path: grid_bb / grid_h2d / grid_h3d / make_grid,
 // map_bb / map_h2d / map_h3d, simplex_grid_state<T> (+hash), launch_map,
-// launch_accum, launch_ca (dead3d), make_life_state, verify_exact_cover.
-// Out of scope (not declared here): rb / lambda / trapezoid / padded maps, EDM,
-// the 2-D periodic CA, analysis, reports, rendering.
+// launch_accum, launch_ca (dead3d), make_life_state, verify_exact_cover; and
+// the general-n / comparison 2-D maps: grid_rb,
+// grid_lambda, grid_h2d_padded, grid_trapezoids, decompose_trapezoids,
+// map_rb_2d, map_lambda_2d, map_h2d_padded, map_h2d_trapezoid.
+// Out of scope (not declared here): EDM, the 2-D periodic CA, analysis,
+// reports, rendering.
 //
 // Switching from the reference: include this header instead of
 // <simplexmap/simulator.hpp> and define SMX_B200_AS_SIMPLEXMAP to get the
@@ -98,6 +101,29 @@ struct map_outcome {
     static map_outcome void_block() { return {true, {}, 1, 0}; }
 };
 
+// trapezoid_params (maps.hpp:49-60)
+struct trapezoid_params {
+    i64 delta_x = 0, delta_y = 0;
+    i64 band = 0;
+    i64 h1 = 0, h2 = 0;
+    i64 grid_width = 0;
+    i64 valid_side = 0;
+    i64 ext_x = 0, ext_y = 0;
+    u64 blocks() const { return u64(ext_x) * u64(ext_y); }
+};
+
+// decompose_trapezoids (maps.hpp:228-257)
+inline std::vector<trapezoid_params> decompose_trapezoids(i64 n, i64 T) {
+    smx_trapezoid t[64];
+    int32_t c = 0;
+    check(smx_decompose_trapezoids(n, T, t, 64, &c));
+    std::vector<trapezoid_params> out;
+    for (int i = 0; i < c; ++i)
+        out.push_back({t[i].delta_x, t[i].delta_y, t[i].band, t[i].h1, t[i].h2, t[i].grid_width, t[i].valid_side,
+                       t[i].ext_x, t[i].ext_y});
+    return out;
+}
+
 struct grid_spec {
     map_kind kind = map_kind::bb;
     int dims = 2;
@@ -105,8 +131,14 @@ struct grid_spec {
     i64 rho = 1;
     std::array<i64, 3> extents{1, 1, 1};
     i64 threshold = 1;
+    std::vector<trapezoid_params> traps;
 
     u64 blocks() const {
+        if (kind == map_kind::h2d_trapezoid) {
+            u64 t = 0;
+            for (const auto& b : traps) t += b.blocks();
+            return t;
+        }
         u64 t = 1;
         for (int a = 0; a < dims; ++a) t *= u64(extents[std::size_t(a)]);
         return t;
@@ -138,6 +170,7 @@ inline grid_spec from_raw(const smx_grid& r) {
     g.rho = r.rho;
     g.threshold = r.threshold;
     g.extents = {r.extents[0], r.extents[1], r.extents[2]};
+    if (g.kind == map_kind::h2d_trapezoid) g.traps = decompose_trapezoids(g.n, g.threshold);
     return g;
 }
 
@@ -153,6 +186,10 @@ inline grid_spec grid_bb(i64 n, int m) {
 }
 inline grid_spec grid_h2d(i64 n) { return make_grid(map_kind::h2d, 2, n); }
 inline grid_spec grid_h3d(i64 n) { return make_grid(map_kind::h3d, 3, n); }
+inline grid_spec grid_rb(i64 n) { return make_grid(map_kind::rb, 2, n); }
+inline grid_spec grid_lambda(i64 n) { return make_grid(map_kind::lambda2d, 2, n); }
+inline grid_spec grid_h2d_padded(i64 n) { return make_grid(map_kind::h2d_padded, 2, n); }
+inline grid_spec grid_trapezoids(i64 n, i64 T) { return make_grid(map_kind::h2d_trapezoid, 2, n, 1, T); }
 
 inline map_outcome map_one(map_kind k, int m, i64 n, block_coord w) {
     smx_outcome o;
@@ -162,6 +199,21 @@ inline map_outcome map_one(map_kind k, int m, i64 n, block_coord w) {
 inline map_outcome map_bb(block_coord omega, i64 n, int m) { return map_one(map_kind::bb, m, n, omega); }
 inline map_outcome map_h2d(block_coord omega) { return map_one(map_kind::h2d, 2, 0, omega); }
 inline map_outcome map_h3d(block_coord omega, i64 n) { return map_one(map_kind::h3d, 3, n, omega); }
+inline data_coord map_rb_2d(block_coord omega, i64 n) { return map_one(map_kind::rb, 2, n, omega).target; }
+inline data_coord map_lambda_2d(u64 index, i64 n) {
+    return map_one(map_kind::lambda2d, 2, n, {i64(index), 0, 0}).target;
+}
+inline map_outcome map_h2d_padded(block_coord omega, i64 n) { return map_one(map_kind::h2d_padded, 2, n, omega); }
+// The reference takes the band's params; the ABI recomputes the band from
+// (n, T, band index) — pass the params decompose_trapezoids returned.
+inline map_outcome map_h2d_trapezoid(block_coord omega, const trapezoid_params& p) {
+    if (omega.x < 0 || omega.x >= p.ext_x || omega.y < 0 || omega.y >= p.ext_y)
+        throw std::invalid_argument("map_h2d_trapezoid: omega outside the trapezoid grid");
+    const smx::trapezoid<i64> t{p.delta_x, p.delta_y, p.band, p.h1, p.h2, p.grid_width, p.valid_side, p.ext_x,
+                                p.ext_y};
+    const smx::outcome<i64> o = smx::map_h2d_trapezoid<i64>(omega.x, omega.y, t);
+    return {o.is_void != 0, {o.x, o.y, o.z}, o.level_b, o.index_q};
+}
 
 // ---- simulator (simulator.hpp:37-96, :257-478) ----
 enum class ca_boundary { periodic2d, dead3d };

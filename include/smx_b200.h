@@ -89,11 +89,25 @@ typedef struct smx_outcome {
     int32_t pad0, pad1;
 } smx_outcome;
 
+/* trapezoid_params (maps.hpp:49-60): one band of the concurrent-trapezoid
+ * decomposition of a general-n 2-simplex (grid kind SMX_TRAP). */
+typedef struct smx_trapezoid {
+    int64_t delta_x, delta_y;
+    int64_t band;        /* power-of-two triangle side */
+    int64_t h1, h2;      /* last unfolded row; rows of the band-wide box */
+    int64_t grid_width;  /* band / 2 */
+    int64_t valid_side;  /* rows beyond are Void (final padded band only) */
+    int64_t ext_x, ext_y;
+} smx_trapezoid;
+
 /* Thread-local message of the last failing call. */
 const char* smx_last_error(void);
 
-/* make_grid (report.hpp:48-66) -> grid_bb / grid_h2d / grid_h3d (maps.hpp:96-105,
- * 188-198, 285-295). Same validity rules and messages. */
+/* make_grid (report.hpp:48-66) -> grid_bb / grid_rb / grid_lambda / grid_h2d /
+ * grid_h2d_padded / grid_trapezoids / grid_h3d (maps.hpp:96-105, 120-128,
+ * 145-152, 188-198, 211-217, 259-266, 285-295). Same validity rules and
+ * messages. An SMX_TRAP grid keeps extents {1, 1, 1} (as the reference) and
+ * `threshold` = T; its bands come from smx_decompose_trapezoids. */
 int smx_make_grid(int32_t kind, int32_t m, int64_t n, int64_t rho, int64_t threshold,
                   smx_grid* out);
 
@@ -103,14 +117,28 @@ int64_t smx_cell_side(const smx_grid* g);
 /* tri_cells / tet_cells (core.hpp:130-133). */
 uint64_t smx_cell_count(int32_t m, int64_t side);
 
-/* map_bb / map_h2d / map_h3d for ONE block on the host (maps.hpp:107,200,302),
- * same shared arithmetic the kernels inline (include/smx_maps.hpp), with the
- * reference's range checks. out: the raw (strict-view) outcome. */
+/* map_bb / map_rb_2d / map_lambda_2d (wx = linear index) / map_h2d /
+ * map_h2d_padded / map_h3d for ONE block on the host (maps.hpp:107,133,156,
+ * 200,219,302), same shared arithmetic the kernels inline
+ * (include/smx_maps.hpp), with the reference's range checks. out: the raw
+ * (strict-view where the kind is strict) outcome. */
 int smx_map_one(int32_t kind, int32_t m, int64_t n, int64_t wx, int64_t wy, int64_t wz,
                 smx_outcome* out);
 
-/* map_h2d / map_h3d / map_bb over every block of the grid, natural z,y,x order
- * (simulator.hpp:113-118) — the bit-exact coordinate check. */
+/* decompose_trapezoids(n, T) (maps.hpp:228-257): writes up to `max` bands,
+ * *count = the number of bands. */
+int smx_decompose_trapezoids(int64_t n, int64_t T, smx_trapezoid* out, int32_t max, int32_t* count);
+
+/* map_h2d_trapezoid (maps.hpp:269-281) for block (wx, wy) of band `band` of
+ * decompose_trapezoids(n, T). */
+int smx_map_trapezoid(int64_t n, int64_t T, int32_t band, int64_t wx, int64_t wy, smx_outcome* out);
+
+/* grid_spec::blocks() (maps.hpp:73-82): the sum over the bands for SMX_TRAP. */
+uint64_t smx_grid_blocks(const smx_grid* g);
+
+/* The map over every block of the grid, natural z,y,x order, band after band
+ * for SMX_TRAP (simulator.hpp:113-118,147-150) — the bit-exact coordinate check.
+ * count = smx_grid_blocks(g). */
 int smx_map_outcomes(const smx_grid* g, smx_outcome* out, uint64_t count, int device_ptr,
                      void* stream);
 

@@ -12,11 +12,16 @@
 //   map_bb                maps.hpp:107-116
 //   map_h2d               maps.hpp:200-207
 //   map_h3d               maps.hpp:302-337
+//   map_rb_2d             maps.hpp:120-141       (comparison map)
+//   map_lambda_2d         maps.hpp:145-159, core.hpp:151-156 (comparison map)
+//   map_h2d_padded        maps.hpp:209-222       (general n)
+//   decompose_trapezoids  maps.hpp:224-267, map_h2d_trapezoid :269-281
 // Argument validation (the reference's std::invalid_argument paths) lives in
 // the callers: the C ABI validates grids once per launch; kernels only ever see
 // in-range block coordinates.
 #pragma once
 
+#include <math.h>
 #include <stdint.h>
 
 #if defined(__CUDACC__)
@@ -138,6 +143,104 @@ SMX_HD outcome<I> map_h3d(I wx, I wy, I wz, I n) {
     if (depth <= 2 * s - 1) return {0, x, y, z, s, q};
     if (anchor == 1 && depth == 2 * s) return {0, x, a + s, z, s, q};
     return {0, a + ly + lz - s, a + lz, s - lz + lx, s, q};
+}
+
+// ---- general-n and comparison 2-D maps ----
+
+SMX_HD uint64_t pow2_floor(uint64_t v) { return uint64_t(1) << floor_log2_u64(v); }
+SMX_HD int ceil_log2_u64(uint64_t v) { return v == 1 ? 0 : floor_log2_u64(v - 1) + 1; }
+SMX_HD uint64_t pow2_ceil(uint64_t v) { return uint64_t(1) << ceil_log2_u64(v); }
+
+// RB: the rectangle (n/2, n+1) for even n, ((n+1)/2, n) for odd n, folded onto
+// T(n) (with-diagonal view): the point-reflected upper part, and for even n the
+// extra column w_y = n onto the main diagonal's tail. Never Void.
+template <class I>
+SMX_HD outcome<I> map_rb(I wx, I wy, I n) {
+    if (n % 2 == 0 && wy == n) return {0, n / 2, n / 2 + wx, 0, 1, 0};
+    if (wx <= wy) return {0, wx, wy, 0, 1, 0};
+    return {0, n - wx, n - 1 - wy, 0, 1, 0};
+}
+
+// lambda: the linear block index of T(n) -> (x, y) by the quadratic root with
+// an exact integer fix-up (core.hpp:151-156). Never Void.
+SMX_HD void tri_coord_at(uint64_t index, int64_t* x, int64_t* y) {
+    int64_t r = int64_t((sqrt(8.0 * double(index) + 1.0) - 1.0) / 2.0);
+    while (r > 0 && tri_index(0, r) > index) --r;
+    while (tri_index(0, r + 1) <= index) ++r;
+    *x = int64_t(index - tri_index(0, r));
+    *y = r;
+}
+template <class I>
+SMX_HD outcome<I> map_lambda(uint64_t index) {
+    int64_t x, y;
+    tri_coord_at(index, &x, &y);
+    return {0, I(x), I(y), 0, 1, 0};
+}
+
+// H padded from above: the power-of-two grid h2d(2^ceil(log2 n)); blocks whose
+// strict-view row is beyond n - 1 are Void.
+template <class I>
+SMX_HD outcome<I> map_h2d_padded(I wx, I wy, I n) {
+    outcome<I> o = map_h2d<I>(wx, wy);
+    if (o.y > n - 1) return {1, 0, 0, 0, 1, 0};
+    return o;
+}
+
+// One band of the concurrent-trapezoid scheme (trapezoid_params, maps.hpp:49-60).
+template <class I>
+struct trapezoid {
+    I delta_x, delta_y;
+    I band;        // power-of-two triangle side of this band
+    I h1, h2;      // last unfolded row; rows of the band-wide box
+    I grid_width;  // band / 2
+    I valid_side;  // rows beyond are Void (final padded band only)
+    I ext_x, ext_y;
+};
+
+// decompose_trapezoids (maps.hpp:228-257): greedy peel of power-of-two bands
+// from the left; the last remainder is padded from above once the padding
+// drops below T. Writes at most `max` bands, returns the count (or -1 when
+// more would be needed; never for n < 2^63). Requires n >= 2, T >= 1.
+SMX_HD int decompose_trapezoids(int64_t n, int64_t T, trapezoid<int64_t>* out, int max) {
+    int cnt = 0;
+    int64_t c = 0, r = n;
+    while (r >= 2) {
+        const int64_t pad = int64_t(pow2_ceil(uint64_t(r))) - r;
+        trapezoid<int64_t> t;
+        t.delta_x = t.delta_y = c;
+        if (pad < T) {
+            t.band = int64_t(pow2_ceil(uint64_t(r)));
+            t.h2 = 0;
+            t.valid_side = r;
+        } else {
+            t.band = int64_t(pow2_floor(uint64_t(r)));
+            t.h2 = r - t.band;
+            t.valid_side = t.band;
+        }
+        t.h1 = t.band + t.h2 - 2;
+        t.grid_width = t.band / 2;
+        t.ext_x = t.grid_width;
+        t.ext_y = t.band - 1 + 2 * t.h2;
+        if (cnt == max) return -1;
+        out[cnt++] = t;
+        if (pad < T) break;
+        c += t.band;
+        r -= t.band;
+    }
+    return cnt;
+}
+
+// map_h2d_trapezoid (maps.hpp:269-281): the H2D map of the band's triangle,
+// rows beyond h1 fold the band-wide box's second half (k = 1) beside the first.
+template <class I>
+SMX_HD outcome<I> map_h2d_trapezoid(I wx, I wy, const trapezoid<I>& p) {
+    const int lg = floor_log2<I>(wy + 1);
+    const I q = wx >> lg;
+    const I k = wy > p.h1 ? 1 : 0;
+    const I x = p.delta_x + wx + (q << lg) + k * p.grid_width;
+    const I y = p.delta_y + wy - k * p.h2 + (q << (lg + 1)) + 1;
+    if (p.h2 == 0 && y - p.delta_y > p.valid_side - 1) return {1, 0, 0, 0, 1, 0};
+    return {0, x, y, 0, I(1) << lg, q};
 }
 
 }  // namespace smx

@@ -77,6 +77,16 @@ class Restated:
         L.orc_first_defect.argtypes = [C.c_int, C.c_int64, _u32p, C.c_uint64, _i64p, _u64p]
         L.orc_tet_layer_prefix.argtypes = [C.c_int64, C.c_int64]
         L.orc_tet_layer_prefix.restype = C.c_uint64
+        L.orc_grid_blocks.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64]
+        L.orc_grid_blocks.restype = C.c_uint64
+        L.orc_map_outcomes_t.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, _i64p, C.c_uint64]
+        L.orc_sweep_t.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
+                                  _u64p]
+        L.orc_decompose_trapezoids.argtypes = [C.c_int64, C.c_int64, _i64p, C.c_int, C.POINTER(C.c_int)]
+        L.orc_map_trapezoid.argtypes = [C.c_int64, C.c_int64, C.c_int, C.c_int64, C.c_int64, _i64p]
+        L.orc_map_rb.argtypes = [C.c_int64, C.c_int64, C.c_int64, _i64p]
+        L.orc_map_lambda.argtypes = [C.c_uint64, C.c_int64, _i64p]
+        L.orc_map_padded.argtypes = [C.c_int64, C.c_int64, C.c_int64, _i64p]
         self.L = L
 
     @staticmethod
@@ -89,10 +99,15 @@ class Restated:
         self._ok(self.L.orc_grid(kind, m, n, e), "grid")
         return tuple(int(v) for v in e)
 
-    def map_outcomes(self, kind: int, m: int, n: int) -> np.ndarray:
-        ex, ey, ez = self.grid(kind, m, n)
-        out = np.zeros((ex * ey * ez, 6), np.int64)
-        self._ok(self.L.orc_map_outcomes(kind, m, n, out, out.shape[0]), "map_outcomes")
+    def blocks(self, kind: int, m: int, n: int, T: int = 1) -> int:
+        return int(self.L.orc_grid_blocks(kind, m, n, T))
+
+    def map_outcomes(self, kind: int, m: int, n: int, T: int = 1) -> np.ndarray:
+        nb = self.blocks(kind, m, n, T)
+        if nb == 0:
+            raise OracleError("map_outcomes: invalid grid")
+        out = np.zeros((nb, 6), np.int64)
+        self._ok(self.L.orc_map_outcomes_t(kind, m, n, T, out, nb), "map_outcomes")
         return out
 
     def map_one(self, kind: int, m: int, n: int, x: int, y: int, z: int = 0):
@@ -101,19 +116,38 @@ class Restated:
             rc = self.L.orc_map_h2d(x, y, o)
         elif kind == H3D:
             rc = self.L.orc_map_h3d(x, y, z, n, o)
+        elif kind == RB:
+            rc = self.L.orc_map_rb(x, y, n, o)
+        elif kind == LAMBDA:
+            rc = self.L.orc_map_lambda(x, n, o)
+        elif kind == PADDED:
+            rc = self.L.orc_map_padded(x, y, n, o)
         else:
             rc = self.L.orc_map_bb(x, y, z, n, m, o)
         self._ok(rc, "map_one")
         return tuple(int(v) for v in o)
 
+    def decompose_trapezoids(self, n: int, T: int) -> list[dict]:
+        out = np.zeros(9 * 64, np.int64)
+        c = C.c_int(0)
+        self._ok(self.L.orc_decompose_trapezoids(n, T, out, 64, C.byref(c)), "decompose_trapezoids")
+        keys = ("delta_x", "delta_y", "band", "h1", "h2", "grid_width", "valid_side", "ext_x", "ext_y")
+        return [dict(zip(keys, (int(v) for v in out[9 * i:9 * i + 9]))) for i in range(c.value)]
+
+    def map_trapezoid(self, n: int, T: int, band: int, x: int, y: int):
+        o = np.zeros(6, np.int64)
+        self._ok(self.L.orc_map_trapezoid(n, T, band, x, y, o), "map_trapezoid")
+        return tuple(int(v) for v in o)
+
     def sweep(self, kind: int, m: int, n: int, rho: int, coverage: bool = True,
-              cells: np.ndarray | None = None):
-        side = (n if kind == BB else n - 1) * rho
+              cells: np.ndarray | None = None, T: int = 1):
+        strict = kind in (H2D, TRAP, PADDED, H3D)
+        side = (n - 1 if strict else n) * rho
         cov = np.zeros(cells_of(m, side), np.uint32) if coverage else None
         cnt = np.zeros(4, np.uint64)
-        self._ok(self.L.orc_sweep(kind, m, n, rho,
-                                  cov.ctypes.data if cov is not None else None,
-                                  cells.ctypes.data if cells is not None else None, cnt), "sweep")
+        self._ok(self.L.orc_sweep_t(kind, m, n, rho, T,
+                                    cov.ctypes.data if cov is not None else None,
+                                    cells.ctypes.data if cells is not None else None, cnt), "sweep")
         return cov, [int(v) for v in cnt]
 
     def state_hash(self, m: int, side: int, arr: np.ndarray) -> int:
@@ -165,6 +199,9 @@ class Reference:
         L.ref_state_hash.restype = C.c_uint64
         L.ref_verify_exact_cover.argtypes = [C.c_int, C.c_int64, _u32p, C.c_uint64,
                                              C.POINTER(C.c_int), _i64p, _u64p]
+        L.ref_map_outcomes_t.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, _i64p, C.c_uint64]
+        L.ref_decompose_trapezoids.argtypes = [C.c_int64, C.c_int64, _i64p, C.c_int, C.POINTER(C.c_int)]
+        L.ref_map_trapezoid.argtypes = [C.c_int64, C.c_int64, C.c_int, C.c_int64, C.c_int64, _i64p]
         self.L = L
 
     def _ok(self, rc: int, what: str) -> None:
@@ -178,11 +215,29 @@ class Reference:
         self._ok(self.L.ref_make_grid(kind, m, n, rho, T, e, b, ds), "make_grid")
         return tuple(int(v) for v in e), int(b[0]), int(ds[0])
 
-    def map_outcomes(self, kind: int, m: int, n: int) -> np.ndarray:
-        (ex, ey, ez), blocks, _ = self.make_grid(kind, m, n)
+    def map_outcomes(self, kind: int, m: int, n: int, T: int = 1) -> np.ndarray:
+        (ex, ey, ez), blocks, _ = self.make_grid(kind, m, n, 1, T)
         out = np.zeros((blocks, 6), np.int64)
-        self._ok(self.L.ref_map_outcomes(kind, m, n, out, blocks), "map_outcomes")
+        self._ok(self.L.ref_map_outcomes_t(kind, m, n, T, out, blocks), "map_outcomes")
         return out
+
+    def decompose_trapezoids(self, n: int, T: int) -> list[dict]:
+        out = np.zeros(9 * 64, np.int64)
+        c = C.c_int(0)
+        rc = self.L.ref_decompose_trapezoids(n, T, out, 64, C.byref(c))
+        if rc == 1:
+            raise ValueError(self.L.ref_last_error().decode())
+        self._ok(rc, "decompose_trapezoids")
+        keys = ("delta_x", "delta_y", "band", "h1", "h2", "grid_width", "valid_side", "ext_x", "ext_y")
+        return [dict(zip(keys, (int(v) for v in out[9 * i:9 * i + 9]))) for i in range(c.value)]
+
+    def map_trapezoid(self, n: int, T: int, band: int, x: int, y: int):
+        o = np.zeros(6, np.int64)
+        rc = self.L.ref_map_trapezoid(n, T, band, x, y, o)
+        if rc == 1:
+            raise ValueError(self.L.ref_last_error().decode())
+        self._ok(rc, "map_trapezoid")
+        return tuple(int(v) for v in o)
 
     def map_one(self, kind: int, m: int, n: int, x: int, y: int, z: int = 0):
         o = np.zeros(6, np.int64)

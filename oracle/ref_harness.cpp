@@ -113,15 +113,64 @@ int ref_map_outcomes(int kind, int m, int64_t n, int64_t* out, uint64_t count) {
     });
 }
 
+// Every block of ANY grid kind in the reference's own emission order
+// (detail::for_each_block_outcome, simulator.hpp:109-158: natural z, y, x;
+// trapezoid bands one after another), 6 x int64 per block.
+int ref_map_outcomes_t(int kind, int m, int64_t n, int64_t T, int64_t* out, uint64_t count) {
+    return guarded([&] {
+        grid_spec g = make_grid(kind_of(kind), m, n, 1, T);
+        if (g.blocks() != count) throw std::invalid_argument("ref_map_outcomes_t: count mismatch");
+        uint64_t i = 0;
+        detail::for_each_block_outcome(g, 0, [&](block_coord, int, const map_outcome& o) {
+            int64_t* r = out + 6 * i++;
+            r[0] = o.is_void;
+            r[1] = o.target.x;
+            r[2] = o.target.y;
+            r[3] = o.target.z;
+            r[4] = o.level_b;
+            r[5] = o.index_q;
+        });
+    });
+}
+
+// decompose_trapezoids (maps.hpp:228-257): 9 x int64 per band
+// {delta_x, delta_y, band, h1, h2, grid_width, valid_side, ext_x, ext_y}.
+int ref_decompose_trapezoids(int64_t n, int64_t T, int64_t* out, int max, int* count) {
+    return guarded([&] {
+        auto traps = decompose_trapezoids(n, T);
+        *count = int(traps.size());
+        for (int i = 0; i < int(traps.size()) && i < max; ++i) {
+            const auto& t = traps[std::size_t(i)];
+            int64_t* r = out + 9 * i;
+            r[0] = t.delta_x; r[1] = t.delta_y; r[2] = t.band; r[3] = t.h1; r[4] = t.h2;
+            r[5] = t.grid_width; r[6] = t.valid_side; r[7] = t.ext_x; r[8] = t.ext_y;
+        }
+    });
+}
+
+// map_h2d_trapezoid (maps.hpp:269-281) on band `band` of decompose_trapezoids(n, T).
+int ref_map_trapezoid(int64_t n, int64_t T, int band, int64_t x, int64_t y, int64_t* out6) {
+    return guarded([&] {
+        auto traps = decompose_trapezoids(n, T);
+        if (band < 0 || band >= int(traps.size())) throw std::invalid_argument("ref_map_trapezoid: band");
+        map_outcome o = map_h2d_trapezoid({x, y, 0}, traps[std::size_t(band)]);
+        out6[0] = o.is_void; out6[1] = o.target.x; out6[2] = o.target.y; out6[3] = o.target.z;
+        out6[4] = o.level_b; out6[5] = o.index_q;
+    });
+}
+
 // Single-block map probes (maps.hpp:107,200,302), for pinned points + error behaviour.
 int ref_map_one(int kind, int m, int64_t n, int64_t x, int64_t y, int64_t z, int64_t* out6) {
     return guarded([&] {
         block_coord w{x, y, z};
         map_outcome o;
         if (kind == 0) o = map_bb(w, n, m);
+        else if (kind == 1) o = map_outcome{false, map_rb_2d(w, n), 1, 0};
+        else if (kind == 2) o = map_outcome{false, map_lambda_2d(u64(x), n), 1, 0};
         else if (kind == 3) o = map_h2d(w);
+        else if (kind == 5) o = map_h2d_padded(w, n);
         else if (kind == 6) o = map_h3d(w, n);
-        else throw std::invalid_argument("ref_map_one: bb/h2d/h3d only");
+        else throw std::invalid_argument("ref_map_one: use ref_map_trapezoid");
         out6[0] = o.is_void;
         out6[1] = o.target.x;
         out6[2] = o.target.y;

@@ -202,6 +202,218 @@ int orc_sweep(int kind, int m, i64 n, i64 rho, u32* coverage, u32* cells32, u64*
     return 0;
 }
 
+/* ---- general-n and comparison 2-D maps ---- */
+
+/* bits.hpp:28-40 */
+static u64 pow2_floor(u64 v) { return (u64)1 << floor_log2(v); }
+static u64 pow2_ceil(u64 v) { return v == 1 ? 1 : (u64)1 << (floor_log2(v - 1) + 1); }
+
+/* trapezoid_params (maps.hpp:49-60) */
+typedef struct { i64 dx, dy, band, h1, h2, gw, vside, ex, ey; } trap_t;
+
+/* decompose_trapezoids (maps.hpp:228-257): peel the largest power-of-two band
+ * from the left while padding the remainder from above would cost >= T rows;
+ * then pad the last remainder. */
+static int decompose(i64 n, i64 T, trap_t* t, int max) {
+    if (n < 2 || T < 1) return -1;
+    int cnt = 0;
+    i64 c = 0, r = n;
+    while (r >= 2) {
+        i64 pad = (i64)pow2_ceil((u64)r) - r;
+        trap_t b;
+        b.dx = b.dy = c;
+        if (pad < T) { b.band = (i64)pow2_ceil((u64)r); b.h2 = 0; b.vside = r; }
+        else { b.band = (i64)pow2_floor((u64)r); b.h2 = r - b.band; b.vside = b.band; }
+        b.h1 = b.band + b.h2 - 2;
+        b.gw = b.band / 2;
+        b.ex = b.gw;
+        b.ey = b.band - 1 + 2 * b.h2;
+        if (cnt == max) return -1;
+        t[cnt++] = b;
+        if (pad < T) break;
+        c += b.band;
+        r -= b.band;
+    }
+    return cnt;
+}
+
+int orc_decompose_trapezoids(i64 n, i64 T, i64* out9, int max, int* count) {
+    trap_t t[64];
+    int c = decompose(n, T, t, 64);
+    if (c < 0) return 1;
+    *count = c;
+    for (int i = 0; i < c && i < max; ++i) {
+        i64* r = out9 + 9 * i;
+        r[0] = t[i].dx; r[1] = t[i].dy; r[2] = t[i].band; r[3] = t[i].h1; r[4] = t[i].h2;
+        r[5] = t[i].gw; r[6] = t[i].vside; r[7] = t[i].ex; r[8] = t[i].ey;
+    }
+    return 0;
+}
+
+/* maps.hpp:133-141 — fold of the (n/2 x n+1) or ((n+1)/2 x n) rectangle onto T(n) */
+int orc_map_rb(i64 x, i64 y, i64 n, i64* o) {
+    if (n < 1) return 1;
+    i64 ex = n % 2 == 0 ? n / 2 : (n + 1) / 2, ey = n % 2 == 0 ? n + 1 : n;
+    if (x < 0 || x >= ex || y < 0 || y >= ey) return 1;
+    if (n % 2 == 0 && y == n) put(o, 0, n / 2, n / 2 + x, 0, 1, 0);
+    else if (x <= y) put(o, 0, x, y, 0, 1, 0);
+    else put(o, 0, n - x, n - 1 - y, 0, 1, 0);
+    return 0;
+}
+
+/* integer floor(sqrt(v)) by Newton steps (independent of the reference's
+ * floating-point root + fix-up, core.hpp:151-156; same result for all v) */
+static u64 isqrt_u64(u64 v) {
+    if (v < 2) return v;
+    u64 r = (u64)1 << ((64 - __builtin_clzll(v) + 1) / 2);
+    for (;;) {
+        u64 nr = (r + v / r) / 2;
+        if (nr >= r) break;
+        r = nr;
+    }
+    while (r * r > v) --r;
+    while ((r + 1) * (r + 1) <= v) ++r;
+    return r;
+}
+
+/* maps.hpp:156-159 — linear block index -> (x, y): y = floor((isqrt(8i+1)-1)/2) */
+int orc_map_lambda(u64 index, i64 n, i64* o) {
+    if (index >= orc_tri_cells(n)) return 1;
+    i64 y = (i64)((isqrt_u64(8 * index + 1) - 1) / 2);
+    put(o, 0, (i64)(index - tri_index(0, y)), y, 0, 1, 0);
+    return 0;
+}
+
+/* maps.hpp:219-222 — h2d of the power-of-two cover, rows beyond n-1 Void */
+int orc_map_padded(i64 x, i64 y, i64 n, i64* o) {
+    if (orc_map_h2d(x, y, o)) return 1;
+    if (o[2] > n - 1) put(o, 1, 0, 0, 0, 1, 0);
+    return 0;
+}
+
+/* maps.hpp:269-281 */
+static int map_trap(i64 x, i64 y, const trap_t* p, i64* o) {
+    if (x < 0 || x >= p->ex || y < 0 || y >= p->ey) return 1;
+    int lg = floor_log2((u64)y + 1);
+    i64 b = (i64)1 << lg, q = x >> lg, k = y > p->h1 ? 1 : 0;
+    i64 tx = p->dx + x + (q << lg) + k * p->gw;
+    i64 ty = p->dy + y - k * p->h2 + (q << (lg + 1)) + 1;
+    if (p->h2 == 0 && ty - p->dy > p->vside - 1) put(o, 1, 0, 0, 0, 1, 0);
+    else put(o, 0, tx, ty, 0, b, q);
+    return 0;
+}
+
+int orc_map_trapezoid(i64 n, i64 T, int band, i64 x, i64 y, i64* o) {
+    trap_t t[64];
+    int c = decompose(n, T, t, 64);
+    if (c < 0 || band < 0 || band >= c) return 1;
+    return map_trap(x, y, &t[band], o);
+}
+
+/* A grid as the reference walks it (simulator.hpp:109-158): one sub-grid, or
+ * one per trapezoid band in order. */
+typedef struct { i64 e[3]; int band; } sub_t;
+
+static int subs_of(int kind, int m, i64 n, i64 T, sub_t* s, trap_t* t, int* ns) {
+    if (kind == K_TRAP) {
+        if (m != 2) return 1;
+        int c = decompose(n, T, t, 64);
+        if (c < 0) return 1;
+        for (int i = 0; i < c; ++i) { s[i].e[0] = t[i].ex; s[i].e[1] = t[i].ey; s[i].e[2] = 1; s[i].band = i; }
+        *ns = c;
+        return 0;
+    }
+    s[0].band = -1;
+    *ns = 1;
+    if (kind == K_RB) {          /* maps.hpp:120-128 */
+        if (m != 2 || n < 1) return 1;
+        s[0].e[0] = n % 2 == 0 ? n / 2 : (n + 1) / 2; s[0].e[1] = n % 2 == 0 ? n + 1 : n; s[0].e[2] = 1;
+        return 0;
+    }
+    if (kind == K_LAMBDA) {      /* maps.hpp:145-152 */
+        if (m != 2 || n < 1) return 1;
+        s[0].e[0] = (i64)orc_tri_cells(n); s[0].e[1] = 1; s[0].e[2] = 1;
+        return 0;
+    }
+    if (kind == K_PADDED) {      /* maps.hpp:211-217 */
+        if (m != 2 || n < 2) return 1;
+        i64 p2 = (i64)pow2_ceil((u64)n);
+        s[0].e[0] = p2 / 2; s[0].e[1] = p2 - 1; s[0].e[2] = 1;
+        return 0;
+    }
+    return orc_grid(kind, m, n, s[0].e);
+}
+
+static int strict_kind(int kind) { return kind == K_H2D || kind == K_TRAP || kind == K_PADDED || kind == K_H3D; }
+
+static int map_at(int kind, int m, i64 n, const trap_t* t, int band, i64 x, i64 y, i64 z, i64* o) {
+    switch (kind) {
+        case K_RB: return orc_map_rb(x, y, n, o);
+        case K_LAMBDA: return orc_map_lambda((u64)x, n, o);
+        case K_PADDED: return orc_map_padded(x, y, n, o);
+        case K_TRAP: return map_trap(x, y, &t[band], o);
+        default: return map_any(kind, m, n, x, y, z, o);
+    }
+}
+
+u64 orc_grid_blocks(int kind, int m, i64 n, i64 T) {
+    sub_t s[64]; trap_t t[64]; int ns = 0;
+    if (subs_of(kind, m, n, T, s, t, &ns)) return 0;
+    u64 b = 0;
+    for (int i = 0; i < ns; ++i) b += (u64)(s[i].e[0] * s[i].e[1] * s[i].e[2]);
+    return b;
+}
+
+/* every block of any grid kind in the reference's emission order */
+int orc_map_outcomes_t(int kind, int m, i64 n, i64 T, i64* out, u64 count) {
+    sub_t s[64]; trap_t t[64]; int ns = 0;
+    if (subs_of(kind, m, n, T, s, t, &ns)) return 1;
+    u64 i = 0;
+    for (int k = 0; k < ns; ++k)
+        for (i64 z = 0; z < s[k].e[2]; ++z)
+            for (i64 y = 0; y < s[k].e[1]; ++y)
+                for (i64 x = 0; x < s[k].e[0]; ++x) {
+                    if (i >= count) return 1;
+                    if (map_at(kind, m, n, t, s[k].band, x, y, z, out + 6 * i++)) return 1;
+                }
+    return i == count ? 0 : 1;
+}
+
+/* detail::sweep (simulator.hpp:177-218) for any 2-D/3-D grid kind (see orc_sweep) */
+int orc_sweep_t(int kind, int m, i64 n, i64 rho, i64 T, u32* coverage, u32* cells32, u64* counters) {
+    sub_t s[64]; trap_t t[64]; int ns = 0;
+    if (rho < 1 || subs_of(kind, m, n, T, s, t, &ns)) return 1;
+    const int is3d = m == 3;
+    const int strict = strict_kind(kind);
+    const i64 side = (strict ? n - 1 : n) * rho;
+    const u64 tpb = is3d ? (u64)(rho * rho * rho) : (u64)(rho * rho);
+    u64 c[4] = {0, 0, 0, 0};
+    for (int k = 0; k < ns; ++k)
+        for (i64 wz = 0; wz < s[k].e[2]; ++wz)
+            for (i64 wy = 0; wy < s[k].e[1]; ++wy)
+                for (i64 wx = 0; wx < s[k].e[0]; ++wx) {
+                    i64 o[6];
+                    if (map_at(kind, m, n, t, s[k].band, wx, wy, wz, o)) return 1;
+                    c[0]++;
+                    c[2] += tpb;
+                    if (o[0]) { c[1]++; continue; }
+                    i64 dx = o[1], dy = o[2] - (strict ? 1 : 0), dz = o[3];
+                    for (i64 lz = 0; lz < (is3d ? rho : 1); ++lz)
+                        for (i64 ly = 0; ly < rho; ++ly)
+                            for (i64 lx = 0; lx < rho; ++lx) {
+                                i64 cx = dx * rho + lx, cy = dy * rho + ly, cz = dz * rho + lz;
+                                int member = is3d ? tet_contains(side, cx, cy, cz) : tri_contains(side, cx, cy);
+                                if (!member) continue;
+                                u64 idx = (is3d ? orc_tet_layer_prefix(side, cz) : 0) + tri_index(cx, cy);
+                                c[3]++;
+                                if (coverage) coverage[idx]++;
+                                if (cells32) cells32[idx]++;
+                            }
+                }
+    if (counters) memcpy(counters, c, sizeof c);
+    return 0;
+}
+
 /* bits.hpp:84-89, :96-109 */
 static u64 splitmix64(u64* s) {
     u64 z = (*s += 0x9e3779b97f4a7c15ull);

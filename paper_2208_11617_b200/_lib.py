@@ -49,6 +49,11 @@ class smx_outcome(C.Structure):
     ]
 
 
+class smx_trapezoid(C.Structure):
+    _fields_ = [(f, C.c_int64) for f in ("delta_x", "delta_y", "band", "h1", "h2", "grid_width", "valid_side",
+                                         "ext_x", "ext_y")]
+
+
 _G = C.POINTER(smx_grid)
 _VP = C.c_void_p
 _SIGS = {
@@ -78,6 +83,11 @@ _SIGS = {
     "smx_bits_step": ([_G, _VP, _VP, C.c_int64, C.c_int64, _VP], C.c_int),
     "smx_bits_unpack": ([_G, _VP, _VP, C.c_uint64, _VP], C.c_int),
     "smx_bits_run": ([_G, _VP, _VP, C.c_int64, _VP], C.c_int),
+    "smx_grid_blocks": ([_G], C.c_uint64),
+    "smx_decompose_trapezoids": ([C.c_int64, C.c_int64, C.POINTER(smx_trapezoid), C.c_int32,
+                                  C.POINTER(C.c_int32)], C.c_int),
+    "smx_map_trapezoid": ([C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.POINTER(smx_outcome)],
+                          C.c_int),
 }
 
 _lib = None

@@ -118,9 +118,16 @@ class grid_spec:
     def extents(self) -> tuple[int, int, int]:
         return tuple(int(v) for v in self._g.extents)
 
+    @property
+    def traps(self) -> list[trapezoid_params]:
+        """The bands of a trapezoid grid (maps.hpp:259-266), else []."""
+        if self.kind != map_kind.h2d_trapezoid:
+            return []
+        return decompose_trapezoids(self.n, self.threshold)
+
     def blocks(self) -> int:
-        ex, ey, ez = self.extents
-        return ex * ey * (ez if self.dims == 3 else 1)
+        """grid_spec::blocks (maps.hpp:73-82): summed over the bands for trapezoids."""
+        return int(lib().smx_grid_blocks(C.byref(self._g)))
 
     def threads(self) -> int:
         return self.blocks() * self.rho ** self.dims
@@ -160,6 +167,48 @@ def grid_h3d(n: int) -> grid_spec:
     return make_grid(map_kind.h3d, 3, n)
 
 
+def grid_rb(n: int) -> grid_spec:
+    return make_grid(map_kind.rb, 2, n)
+
+
+def grid_lambda(n: int) -> grid_spec:
+    return make_grid(map_kind.lambda2d, 2, n)
+
+
+def grid_h2d_padded(n: int) -> grid_spec:
+    return make_grid(map_kind.h2d_padded, 2, n)
+
+
+def grid_trapezoids(n: int, T: int) -> grid_spec:
+    return make_grid(map_kind.h2d_trapezoid, 2, n, 1, T)
+
+
+@dataclass(frozen=True)
+class trapezoid_params:
+    """maps.hpp:49-60"""
+    delta_x: int
+    delta_y: int
+    band: int
+    h1: int
+    h2: int
+    grid_width: int
+    valid_side: int
+    ext_x: int
+    ext_y: int
+
+    def blocks(self) -> int:
+        return self.ext_x * self.ext_y
+
+
+def decompose_trapezoids(n: int, T: int) -> list[trapezoid_params]:
+    """maps.hpp:228-257 (the shared arithmetic of include/smx_maps.hpp)."""
+    arr = (_lib.smx_trapezoid * 64)()
+    cnt = C.c_int32(0)
+    check(lib().smx_decompose_trapezoids(int(n), int(T), arr, 64, C.byref(cnt)))
+    return [trapezoid_params(*(int(getattr(arr[i], f)) for f, _ in _lib.smx_trapezoid._fields_))
+            for i in range(cnt.value)]
+
+
 def _map_one(kind: int, m: int, n: int, omega) -> map_outcome:
     o = _lib.smx_outcome()
     check(lib().smx_map_one(int(kind), int(m), int(n), int(omega.x), int(omega.y), int(omega.z), C.byref(o)))
@@ -178,9 +227,31 @@ def map_h3d(omega, n: int) -> map_outcome:
     return _map_one(map_kind.h3d, 3, n, omega)
 
 
+def map_rb_2d(omega, n: int) -> data_coord:
+    """maps.hpp:133-141 (returns the data coordinate, as the reference)."""
+    return _map_one(map_kind.rb, 2, n, omega).target
+
+
+def map_lambda_2d(index: int, n: int) -> data_coord:
+    """maps.hpp:156-159"""
+    return _map_one(map_kind.lambda2d, 2, n, data_coord(int(index), 0, 0)).target
+
+
+def map_h2d_padded(omega, n: int) -> map_outcome:
+    return _map_one(map_kind.h2d_padded, 2, n, omega)
+
+
+def map_h2d_trapezoid(omega, n: int, T: int, band: int) -> map_outcome:
+    """map_h2d_trapezoid (maps.hpp:269-281) on band `band` of decompose_trapezoids(n, T)."""
+    o = _lib.smx_outcome()
+    check(lib().smx_map_trapezoid(int(n), int(T), int(band), int(omega.x), int(omega.y), C.byref(o)))
+    return map_outcome(bool(o.is_void), data_coord(o.x, o.y, o.z), int(o.level_b), int(o.index_q))
+
+
 def map_outcomes(g: grid_spec) -> np.ndarray:
-    """Every block's map_outcome in natural z, y, x order as an (blocks, 8)
-    int32 array {is_void, x, y, z, level_b, index_q, 0, 0}, computed on the GPU."""
+    """Every block's map_outcome in natural z, y, x order (band after band for
+    trapezoid grids) as an (blocks, 8) int32 array {is_void, x, y, z, level_b,
+    index_q, 0, 0}, computed on the GPU."""
     out = np.empty((g.blocks(), 8), np.int32)
     check(lib().smx_map_outcomes(C.byref(g.raw), out.ctypes.data, out.shape[0], 0, None))
     return out

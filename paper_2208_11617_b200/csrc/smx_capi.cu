@@ -136,38 +136,91 @@ int sink_buf(unsigned** out) {
     return SMX_OK;
 }
 
+bool strict_kind_host(int k) { return k == SMX_H2D || k == SMX_PADDED || k == SMX_TRAP || k == SMX_H3D; }
+
 int64_t cell_side_of(const smx_grid* g) {
-    const int64_t ds = g->kind == SMX_BB ? g->n : g->n - 1;
+    const int64_t ds = strict_kind_host(g->kind) ? g->n - 1 : g->n;
     return ds * g->rho;
 }
 
-// Kernel-facing geometry; every coordinate must fit int32 and every CUDA grid
-// dimension the block scheme uses must fit the launch limits.
-int make_geom(const smx_grid* g, smx::Geom* out, bool need_prefix) {
+constexpr int kMaxTraps = 64;
+
+int trapezoids_of(int64_t n, int64_t T, smx::trapezoid<int64_t>* out, int* count) {
+    if (n < 2) return fail(SMX_EINVAL, "decompose_trapezoids: n must be >= 2");
+    if (T < 1) return fail(SMX_EINVAL, "decompose_trapezoids: T must be >= 1");
+    const int c = smx::decompose_trapezoids(n, T, out, kMaxTraps);
+    if (c < 0) return fail(SMX_ERANGE, "decompose_trapezoids: too many bands");
+    *count = c;
+    return SMX_OK;
+}
+
+uint64_t blocks_of(const smx_grid* g) {
+    if (g->kind == SMX_TRAP) {
+        smx::trapezoid<int64_t> t[kMaxTraps];
+        int c = 0;
+        if (trapezoids_of(g->n, g->threshold, t, &c)) return 0;
+        uint64_t b = 0;
+        for (int i = 0; i < c; ++i) b += uint64_t(t[i].ext_x) * uint64_t(t[i].ext_y);
+        return b;
+    }
+    return uint64_t(g->extents[0]) * uint64_t(g->extents[1]) * uint64_t(g->extents[2]);
+}
+
+// Kernel-facing geometry of one launch; every coordinate must fit int32 and
+// every CUDA grid dimension the block scheme uses must fit the launch limits.
+int make_geom_ext(const smx_grid* g, int64_t ex, int64_t ey, int64_t ez, smx::Geom* out, bool need_prefix) {
     if (!g) return fail(SMX_EINVAL, "null grid");
-    if (g->kind != SMX_BB && g->kind != SMX_H2D && g->kind != SMX_H3D)
-        return fail(SMX_EINVAL, std::string("map ") + kind_name(g->kind) +
-                                    " is outside the B200 hot path (bb, h2d, h3d)");
+    if (g->kind < SMX_BB || g->kind > SMX_H3D) return fail(SMX_EINVAL, "unknown map kind");
     if (g->rho < 1) return fail(SMX_EINVAL, "launch: rho must be >= 1");
     const int64_t side = cell_side_of(g);
-    if (side >= (int64_t(1) << 30) || g->extents[0] > 0x7fffffff || g->extents[1] > 65535 ||
-        g->extents[2] > 65535 || g->rho > 1024)
+    if (side >= (int64_t(1) << 30) || ex > 0x7fffffff || ey > 65535 || ez > 65535 || g->rho > 1024)
         return fail(SMX_ERANGE, "grid exceeds the device launch limits (extents.y,z <= 65535, side < 2^30)");
     smx::Geom k{};
     k.kind = g->kind;
     k.dims = g->dims;
     k.n = int(g->n);
     k.rho = int(g->rho);
-    k.ex = int(g->extents[0]);
-    k.ey = int(g->extents[1]);
-    k.ez = int(g->extents[2]);
-    k.strict = g->kind != SMX_BB;
+    k.ex = int(ex);
+    k.ey = int(ey);
+    k.ez = int(ez);
+    k.strict = strict_kind_host(g->kind);
     k.side = int(side);
     k.prefix = nullptr;
     if (need_prefix && g->dims == 3) {
         if (int rc = get_prefix(side, &k.prefix)) return rc;
     }
     *out = k;
+    return SMX_OK;
+}
+
+int make_geom(const smx_grid* g, smx::Geom* out, bool need_prefix) {
+    if (g && g->kind == SMX_TRAP) return fail(SMX_EINVAL, "trapezoid grids launch band by band");
+    if (!g) return fail(SMX_EINVAL, "null grid");
+    return make_geom_ext(g, g->extents[0], g->extents[1], g->extents[2], out, need_prefix);
+}
+
+// The launches of a grid: one for every kind but SMX_TRAP, one per band there
+// (the reference's concurrent trapezoid launches, maps.hpp:259-266).
+int sub_geoms(const smx_grid* g, std::vector<smx::Geom>& out, bool need_prefix) {
+    out.clear();
+    if (!g) return fail(SMX_EINVAL, "null grid");
+    if (g->kind != SMX_TRAP) {
+        smx::Geom k;
+        if (int rc = make_geom(g, &k, need_prefix)) return rc;
+        out.push_back(k);
+        return SMX_OK;
+    }
+    smx::trapezoid<int64_t> t[kMaxTraps];
+    int c = 0;
+    if (int rc = trapezoids_of(g->n, g->threshold, t, &c)) return rc;
+    for (int i = 0; i < c; ++i) {
+        smx::Geom k;
+        if (int rc = make_geom_ext(g, t[i].ext_x, t[i].ext_y, 1, &k, need_prefix)) return rc;
+        k.trap = smx::trapezoid<int>{int(t[i].delta_x), int(t[i].delta_y), int(t[i].band), int(t[i].h1),
+                                     int(t[i].h2), int(t[i].grid_width), int(t[i].valid_side), int(t[i].ext_x),
+                                     int(t[i].ext_y)};
+        out.push_back(k);
+    }
     return SMX_OK;
 }
 
@@ -179,14 +232,15 @@ int check_cells(const smx_grid* g, uint64_t ncells) {
     return SMX_OK;
 }
 
-int fill_counters(const smx_grid* g, const smx::Geom& k, smx_counters* c, cudaStream_t s,
-                  uint32_t* dev_cov) {
+int fill_counters(const smx_grid* g, smx_counters* c, cudaStream_t s, uint32_t* dev_cov) {
+    std::vector<smx::Geom> subs;
+    if (int rc = sub_geoms(g, subs, true)) return rc;
     smx::DevCounters* dc = nullptr;
     if (c) {
         if (int rc = counters_buf(&dc)) return rc;
         TRY(cudaMemsetAsync(dc, 0, sizeof(smx::DevCounters), s));
     }
-    smx::launch_map_block(k, dev_cov, dc, nullptr, s);
+    for (const auto& k : subs) smx::launch_map_block(k, dev_cov, dc, nullptr, s);
     TRY(cudaGetLastError());
     if (c) {
         smx::DevCounters h;
@@ -197,7 +251,7 @@ int fill_counters(const smx_grid* g, const smx::Geom& k, smx_counters* c, cudaSt
             v += h.blocks_void[i];
             u += h.threads_useful[i];
         }
-        const uint64_t blocks = uint64_t(g->extents[0]) * uint64_t(g->extents[1]) * uint64_t(g->extents[2]);
+        const uint64_t blocks = blocks_of(g);
         uint64_t tpb = uint64_t(g->rho) * uint64_t(g->rho);
         if (g->dims == 3) tpb *= uint64_t(g->rho);
         c->blocks_launched = blocks;
@@ -341,11 +395,65 @@ int smx_make_grid(int32_t kind, int32_t m, int64_t n, int64_t rho, int64_t thres
             g.extents[1] = n / 2;
             g.extents[2] = (3 * (n - 1) + 3) / 4;
             break;
+        case SMX_RB:  // maps.hpp:120-128
+            if (n < 1) return fail(SMX_EINVAL, "grid_rb: n must be >= 1");
+            g.extents[0] = n % 2 == 0 ? n / 2 : (n + 1) / 2;
+            g.extents[1] = n % 2 == 0 ? n + 1 : n;
+            g.extents[2] = 1;
+            break;
+        case SMX_LAMBDA:  // maps.hpp:145-152
+            if (n < 1) return fail(SMX_EINVAL, "grid_lambda: n must be >= 1");
+            g.extents[0] = int64_t(smx::tri_cells(n));
+            g.extents[1] = 1;
+            g.extents[2] = 1;
+            break;
+        case SMX_PADDED: {  // maps.hpp:211-217: grid_h2d(2^ceil(log2 n))
+            if (n < 2) return fail(SMX_EINVAL, "grid_h2d_padded: n must be >= 2");
+            const int64_t p2 = int64_t(smx::pow2_ceil(uint64_t(n)));
+            g.extents[0] = p2 / 2;
+            g.extents[1] = p2 - 1;
+            g.extents[2] = 1;
+            break;
+        }
+        case SMX_TRAP: {  // maps.hpp:259-266: extents stay {1,1,1}; the bands carry the grid
+            smx::trapezoid<int64_t> t[kMaxTraps];
+            int c = 0;
+            if (int rc = trapezoids_of(n, threshold, t, &c)) return rc;
+            g.extents[0] = g.extents[1] = g.extents[2] = 1;
+            break;
+        }
         default:
-            return fail(SMX_EINVAL, std::string("map ") + kind_name(kind) +
-                                        " is outside the B200 hot path (bb, h2d, h3d)");
+            return fail(SMX_EINVAL, "unknown map kind");
     }
     *out = g;
+    return SMX_OK;
+}
+
+uint64_t smx_grid_blocks(const smx_grid* g) { return g ? blocks_of(g) : 0; }
+
+int smx_decompose_trapezoids(int64_t n, int64_t T, smx_trapezoid* out, int32_t max, int32_t* count) {
+    smx::trapezoid<int64_t> t[kMaxTraps];
+    int c = 0;
+    if (int rc = trapezoids_of(n, T, t, &c)) return rc;
+    if (count) *count = c;
+    for (int i = 0; i < c && i < max && out; ++i)
+        out[i] = smx_trapezoid{t[i].delta_x, t[i].delta_y, t[i].band, t[i].h1, t[i].h2,
+                               t[i].grid_width, t[i].valid_side, t[i].ext_x, t[i].ext_y};
+    return SMX_OK;
+}
+
+int smx_map_trapezoid(int64_t n, int64_t T, int32_t band, int64_t wx, int64_t wy, smx_outcome* out) {
+    if (!out) return fail(SMX_EINVAL, "null output");
+    smx::trapezoid<int64_t> t[kMaxTraps];
+    int c = 0;
+    if (int rc = trapezoids_of(n, T, t, &c)) return rc;
+    if (band < 0 || band >= c) return fail(SMX_EINVAL, "map_h2d_trapezoid: no such band");
+    const smx::trapezoid<int64_t>& p = t[band];
+    if (wx < 0 || wx >= p.ext_x || wy < 0 || wy >= p.ext_y)
+        return fail(SMX_EINVAL, "map_h2d_trapezoid: omega outside the trapezoid grid");
+    const smx::outcome<int64_t> o = smx::map_h2d_trapezoid<int64_t>(wx, wy, p);
+    *out = smx_outcome{int32_t(o.is_void), int32_t(o.x), int32_t(o.y), int32_t(o.z),
+                       int32_t(o.level_b), int32_t(o.index_q), 0, 0};
     return SMX_OK;
 }
 
@@ -374,8 +482,22 @@ int smx_map_one(int32_t kind, int32_t m, int64_t n, int64_t wx, int64_t wy, int6
         if (wx < 0 || wx >= n / 2 || wy < 0 || wy >= n / 2 || wz < 0 || wz >= (3 * (n - 1) + 3) / 4)
             return fail(SMX_EINVAL, "map_h3d: omega outside the grid");
         o = smx::map_h3d<int64_t>(wx, wy, wz, n);
+    } else if (kind == SMX_PADDED) {  // maps.hpp:219-222
+        if (wx < 0 || wy < 0) return fail(SMX_EINVAL, "map_h2d: omega components must be >= 0");
+        if (wx >= (int64_t(1) << 31) || wy >= (int64_t(1) << 31))
+            return fail(SMX_ERANGE, "map_h2d: omega beyond the 2^31 block range of this build");
+        o = smx::map_h2d_padded<int64_t>(wx, wy, n);
+    } else if (kind == SMX_RB) {  // maps.hpp:133-141
+        if (n < 1) return fail(SMX_EINVAL, "grid_rb: n must be >= 1");
+        const int64_t ex = n % 2 == 0 ? n / 2 : (n + 1) / 2, ey = n % 2 == 0 ? n + 1 : n;
+        if (wx < 0 || wx >= ex || wy < 0 || wy >= ey) return fail(SMX_EINVAL, "map_rb_2d: omega outside the rectangle");
+        o = smx::map_rb<int64_t>(wx, wy, n);
+    } else if (kind == SMX_LAMBDA) {  // maps.hpp:156-159 (wx = linear index)
+        if (wx < 0 || uint64_t(wx) >= smx::tri_cells(n))
+            return fail(SMX_EINVAL, "map_lambda_2d: index out of range");
+        o = smx::map_lambda<int64_t>(uint64_t(wx));
     } else {
-        return fail(SMX_EINVAL, std::string("map ") + kind_name(kind) + " is outside the B200 hot path (bb, h2d, h3d)");
+        return fail(SMX_EINVAL, std::string("map ") + kind_name(kind) + ": use smx_map_trapezoid");
     }
     *out = smx_outcome{int32_t(o.is_void), int32_t(o.x), int32_t(o.y), int32_t(o.z),
                        int32_t(o.level_b), int32_t(o.index_q), 0, 0};
@@ -383,9 +505,9 @@ int smx_map_one(int32_t kind, int32_t m, int64_t n, int64_t wx, int64_t wy, int6
 }
 
 int smx_map_outcomes(const smx_grid* g, smx_outcome* out, uint64_t count, int device_ptr, void* stream) {
-    smx::Geom k;
-    if (int rc = make_geom(g, &k, false)) return rc;
-    const uint64_t blocks = uint64_t(g->extents[0]) * uint64_t(g->extents[1]) * uint64_t(g->extents[2]);
+    std::vector<smx::Geom> subs;
+    if (int rc = sub_geoms(g, subs, false)) return rc;
+    const uint64_t blocks = blocks_of(g);
     if (count != blocks) return fail(SMX_EINVAL, "map_outcomes: count != grid blocks");
     cudaStream_t s = (cudaStream_t)stream;
     smx_outcome* d = out;
@@ -394,7 +516,12 @@ int smx_map_outcomes(const smx_grid* g, smx_outcome* out, uint64_t count, int de
         if (int rc = pool_get(0, blocks * sizeof(smx_outcome), &p)) return rc;
         d = (smx_outcome*)p;
     }
-    smx::launch_outcomes(k, d, blocks, s);
+    uint64_t off = 0;
+    for (const auto& k : subs) {  // band after band for trapezoid grids (simulator.hpp:147-150)
+        const uint64_t nb = uint64_t(k.ex) * uint64_t(k.ey) * uint64_t(k.ez);
+        smx::launch_outcomes(k, d + off, nb, s);
+        off += nb;
+    }
     TRY(cudaGetLastError());
     if (!device_ptr) {
         TRY(cudaMemcpyAsync(out, d, blocks * sizeof(smx_outcome), cudaMemcpyDeviceToHost, s));
@@ -405,8 +532,8 @@ int smx_map_outcomes(const smx_grid* g, smx_outcome* out, uint64_t count, int de
 
 int smx_launch_map(const smx_grid* g, uint32_t* coverage, uint64_t ncells, int device_ptr,
                    smx_counters* counters, void* stream) {
-    smx::Geom k;
-    if (int rc = make_geom(g, &k, true)) return rc;
+    std::vector<smx::Geom> subs;
+    if (int rc = sub_geoms(g, subs, true)) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     uint32_t* dcov = coverage;
     if (coverage) {
@@ -418,7 +545,7 @@ int smx_launch_map(const smx_grid* g, uint32_t* coverage, uint64_t ncells, int d
             TRY(cudaMemcpyAsync(dcov, coverage, ncells * 4, cudaMemcpyHostToDevice, s));
         }
     }
-    if (int rc = fill_counters(g, k, counters, s, dcov)) return rc;
+    if (int rc = fill_counters(g, counters, s, dcov)) return rc;
     if (coverage && !device_ptr) {
         TRY(cudaMemcpyAsync(coverage, dcov, ncells * 4, cudaMemcpyDeviceToHost, s));
         TRY(cudaStreamSynchronize(s));
@@ -427,19 +554,19 @@ int smx_launch_map(const smx_grid* g, uint32_t* coverage, uint64_t ncells, int d
 }
 
 int smx_map_kernel(const smx_grid* g, void* stream) {
-    smx::Geom k;
-    if (int rc = make_geom(g, &k, true)) return rc;
+    std::vector<smx::Geom> subs;
+    if (int rc = sub_geoms(g, subs, true)) return rc;
     unsigned* sink;
     if (int rc = sink_buf(&sink)) return rc;
-    smx::launch_map_block(k, nullptr, nullptr, sink, (cudaStream_t)stream);
+    for (const auto& k : subs) smx::launch_map_block(k, nullptr, nullptr, sink, (cudaStream_t)stream);
     TRY(cudaGetLastError());
     return SMX_OK;
 }
 
 int smx_accum(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passes, int32_t exec,
               int device_ptr, uint32_t* coverage, smx_counters* counters, void* stream) {
-    smx::Geom k;
-    if (int rc = make_geom(g, &k, true)) return rc;
+    std::vector<smx::Geom> subs;
+    if (int rc = sub_geoms(g, subs, true)) return rc;
     if (g->dims != 2) return fail(SMX_EINVAL, "accum: the B200 ACCUM path is the 2-simplex kernel");
     if (int rc = check_cells(g, ncells)) return rc;
     if (passes < 0) return fail(SMX_EINVAL, "accum: passes must be >= 0");
@@ -460,8 +587,9 @@ int smx_accum(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passe
         }
     }
     if (coverage || counters)
-        if (int rc = fill_counters(g, k, counters, s, dcov)) return rc;
-    for (int64_t p = 0; p < passes; ++p) smx::launch_accum(k, d, exec, s);
+        if (int rc = fill_counters(g, counters, s, dcov)) return rc;
+    for (int64_t p = 0; p < passes; ++p)
+        for (const auto& k : subs) smx::launch_accum(k, d, exec, s);  // bands: disjoint cells
     TRY(cudaGetLastError());
     if (!device_ptr) {
         TRY(cudaMemcpyAsync(cells, d, ncells * 4, cudaMemcpyDeviceToHost, s));
@@ -577,7 +705,7 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
         b = (uint8_t*)p;
     }
     if ((coverage || counters) && steps > 0)
-        if (int rc = fill_counters(g, k, counters, s, dcov)) return rc;
+        if (int rc = fill_counters(g, counters, s, dcov)) return rc;
     uint8_t* cur = a;
     uint8_t* nxt = b;
     if (device_ptr)

@@ -19,17 +19,30 @@ struct Geom {
     int strict;           // h2d/h3d emit the strict view: data row = y - 1
     int side;             // cell side S
     const unsigned long long* prefix;  // 3-D: tet_layer_prefix(S, z), z = 0..S+1
+    trapezoid<int> trap;  // SMX_TRAP: the band this launch covers (one launch per band)
 };
+
+// strict_view (maps.hpp:35-38): outputs in { x < y }, shifted y - 1 by the sweep
+__host__ __device__ constexpr bool strict_kind(int k) { return k == SMX_H2D || k == SMX_PADDED || k == SMX_TRAP || k == SMX_H3D; }
+
+// The raw map_outcome of one block (maps.hpp), per kind.
+template <int KIND>
+__device__ __forceinline__ outcome<int> map_raw(const Geom& g, int wx, int wy, int wz) {
+    if (KIND == SMX_H2D) return map_h2d<int>(wx, wy);
+    if (KIND == SMX_H3D) return map_h3d<int>(wx, wy, wz, g.n);
+    if (KIND == SMX_PADDED) return map_h2d_padded<int>(wx, wy, g.n);
+    if (KIND == SMX_TRAP) return map_h2d_trapezoid<int>(wx, wy, g.trap);
+    if (KIND == SMX_RB) return map_rb<int>(wx, wy, g.n);
+    if (KIND == SMX_LAMBDA) return map_lambda<int>(uint64_t(wx));
+    return map_bb<int>(wx, wy, wz, g.n, g.dims);
+}
 
 // Per-block map dispatch; returns the with-diagonal tile coordinate (strict
 // shift already applied, simulator.hpp:202).
 template <int KIND>
 __device__ __forceinline__ outcome<int> map_block(const Geom& g, int wx, int wy, int wz) {
-    outcome<int> o;
-    if (KIND == SMX_H2D) o = map_h2d<int>(wx, wy);
-    else if (KIND == SMX_H3D) o = map_h3d<int>(wx, wy, wz, g.n);
-    else o = map_bb<int>(wx, wy, wz, g.n, g.dims);
-    if (KIND != SMX_BB) o.y -= 1;
+    outcome<int> o = map_raw<KIND>(g, wx, wy, wz);
+    if (strict_kind(KIND)) o.y -= 1;
     return o;
 }
 

@@ -23,10 +23,7 @@ __global__ void k_outcomes(Geom g, smx_outcome* out, unsigned long long count) {
         const unsigned long long r = b - (unsigned long long)wz * exy;
         const int wy = int(r / (unsigned long long)g.ex);
         const int wx = int(r - (unsigned long long)wy * g.ex);
-        outcome<int> o;
-        if (KIND == SMX_H2D) o = map_h2d<int>(wx, wy);
-        else if (KIND == SMX_H3D) o = map_h3d<int>(wx, wy, wz, g.n);
-        else o = map_bb<int>(wx, wy, wz, g.n, g.dims);
+        const outcome<int> o = map_raw<KIND>(g, wx, wy, wz);
         int4* dst = reinterpret_cast<int4*>(out + b);
         dst[0] = make_int4(o.is_void, o.x, o.y, o.z);
         dst[1] = make_int4(o.level_b, o.index_q, 0, 0);
@@ -354,11 +351,17 @@ static dim3 block_shape(const Geom& g) {
     return dim3(bx, by, bz);
 }
 
-#define SMX_DISPATCH_KIND(kind, F, ...)                       \
-    do {                                                      \
-        if ((kind) == SMX_H2D) F<SMX_H2D>(__VA_ARGS__);       \
-        else if ((kind) == SMX_H3D) F<SMX_H3D>(__VA_ARGS__);  \
-        else F<SMX_BB>(__VA_ARGS__);                          \
+#define SMX_DISPATCH_KIND(kind, F, ...)                             \
+    do {                                                            \
+        switch (kind) {                                             \
+            case SMX_H2D: F<SMX_H2D>(__VA_ARGS__); break;           \
+            case SMX_H3D: F<SMX_H3D>(__VA_ARGS__); break;           \
+            case SMX_PADDED: F<SMX_PADDED>(__VA_ARGS__); break;     \
+            case SMX_TRAP: F<SMX_TRAP>(__VA_ARGS__); break;         \
+            case SMX_RB: F<SMX_RB>(__VA_ARGS__); break;             \
+            case SMX_LAMBDA: F<SMX_LAMBDA>(__VA_ARGS__); break;     \
+            default: F<SMX_BB>(__VA_ARGS__); break;                 \
+        }                                                           \
     } while (0)
 
 template <int KIND>
@@ -424,7 +427,8 @@ static void launch_ca_k(const Geom& g, int wz0, int wz1, const uint8_t* cur, uin
 }
 // block scheme only; the x-run scheme is driven by the C ABI (pack + k_ca_bits)
 void launch_ca(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s) {
-    SMX_DISPATCH_KIND(g.kind, launch_ca_k, g, wz0, wz1, cur, next, exec, s);
+    if (g.kind == SMX_H3D) launch_ca_k<SMX_H3D>(g, wz0, wz1, cur, next, exec, s);
+    else launch_ca_k<SMX_BB>(g, wz0, wz1, cur, next, exec, s);
 }
 
 void launch_tiles_pack(const Geom& g, const uint8_t* cells, const int* tiles, unsigned long long ntiles,

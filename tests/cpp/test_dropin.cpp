@@ -27,7 +27,107 @@ static int g_fail = 0, g_pass = 0;
 
 static simplex_spec domain_of(const grid_spec& g) { return {g.dims, g.domain_side() * g.rho - 1}; }
 
+// strict-view cover of T(n - 1) (test_maps.cpp strict_cover2)
+struct strict_cover2 {
+    i64 n;
+    std::vector<u32> marks;
+    u64 total = 0, voids = 0;
+    bool outside = false;
+    explicit strict_cover2(i64 n_) : n(n_), marks(std::size_t(tri_cells(n_ - 1)), 0) {}
+    void add(const map_outcome& o) {
+        ++total;
+        if (o.is_void) { ++voids; return; }
+        const i64 x = o.target.x, y = o.target.y - 1;
+        if (!(0 <= x && x <= y && y <= n - 2)) { outside = true; return; }
+        ++marks[tri_linear_index(x, y)];
+    }
+    bool exact() const {
+        return !outside && std::all_of(marks.begin(), marks.end(), [](u32 v) { return v == 1; });
+    }
+};
+
+static void general_n_suite() {
+    // test_maps.cpp "h2d padded covers general n"
+    CHECK(grid_h2d_padded(8).extents == grid_h2d(8).extents);
+    CHECK((grid_h2d_padded(9).extents == std::array<i64, 3>{8, 15, 1}));
+    for (i64 n : {2, 3, 5, 27, 100, 255, 257}) {
+        grid_spec g = grid_h2d_padded(n);
+        strict_cover2 cover(n);
+        for (i64 oy = 0; oy < g.extents[1]; ++oy)
+            for (i64 ox = 0; ox < g.extents[0]; ++ox) cover.add(map_h2d_padded({ox, oy, 0}, n));
+        CHECK(cover.exact());
+        CHECK(cover.total == g.blocks());
+        CHECK(cover.total - cover.voids == u64(tri_cells(n - 1)));
+    }
+    {
+        grid_spec g = grid_h2d_padded(257);
+        double ratio = double(g.blocks()) / double(u64(tri_cells(256)));
+        CHECK(ratio > 3.9 && ratio < 4.1);
+    }
+    // "trapezoid decomposition"
+    for (i64 T : {1, 4, 16}) {
+        auto traps = decompose_trapezoids(16, T);
+        CHECK(traps.size() == 1);
+        CHECK(traps[0].band == 16 && traps[0].h2 == 0 && traps[0].valid_side == 16);
+        CHECK(traps[0].ext_x == grid_h2d(16).extents[0] && traps[0].ext_y == grid_h2d(16).extents[1]);
+    }
+    auto t27 = decompose_trapezoids(27, 1);
+    CHECK(t27.size() == 3);
+    CHECK(t27[0].delta_x == 0 && t27[0].band == 16 && t27[0].h2 == 11);
+    CHECK(t27[1].delta_x == 16 && t27[1].band == 8 && t27[1].h2 == 3);
+    CHECK(t27[2].delta_x == 24 && t27[2].band == 2 && t27[2].h2 == 1);
+    auto t27p = decompose_trapezoids(27, 4);
+    CHECK(t27p.size() == 3 && t27p[2].band == 4 && t27p[2].h2 == 0 && t27p[2].valid_side == 3);
+    for (auto& t : t27) CHECK(t.h1 + t.h2 == t.ext_y - 1);
+    // "trapezoid map pinned boundary blocks"
+    CHECK(map_h2d_trapezoid({0, 25, 0}, t27[0]).target == (data_coord{0, 26, 0}));
+    CHECK(map_h2d_trapezoid({0, 26, 0}, t27[0]).target == (data_coord{8, 16, 0}));
+    CHECK_THROWS_AS(map_h2d_trapezoid({0, 37, 0}, t27[0]), std::invalid_argument);
+    auto single = decompose_trapezoids(32, 1);
+    CHECK(single.size() == 1);
+    bool same = true;
+    for (i64 oy = 0; oy < single[0].ext_y; ++oy)
+        for (i64 ox = 0; ox < single[0].ext_x; ++ox)
+            same = same && map_h2d_trapezoid({ox, oy, 0}, single[0]).target == map_h2d({ox, oy, 0}).target;
+    CHECK(same);
+    // "trapezoid union tiles every n"
+    bool all_exact = true, counts = true;
+    for (i64 n = 2; n <= 512; ++n)
+        for (i64 T : {1, 4, 16}) {
+            auto traps = decompose_trapezoids(n, T);
+            counts = counts && i64(traps.size()) <= std::max<i64>(1, 64 - __builtin_clzll(u64(n - 1)));
+            strict_cover2 cover(n);
+            for (const auto& t : traps)
+                for (i64 oy = 0; oy < t.ext_y; ++oy)
+                    for (i64 ox = 0; ox < t.ext_x; ++ox) cover.add(map_h2d_trapezoid({ox, oy, 0}, t));
+            all_exact = all_exact && cover.exact();
+        }
+    CHECK(all_exact);
+    CHECK(counts);
+    CHECK(grid_trapezoids(27, 1).blocks() == 8 * 37 + 4 * 13 + 1 * 3);
+    // RB / lambda (maps.hpp:120-159): exact cover of T(n)
+    for (i64 n : {1, 2, 3, 8, 27, 64}) {
+        grid_spec g = grid_rb(n);
+        std::vector<u32> marks(std::size_t(tri_cells(n)), 0);
+        for (i64 oy = 0; oy < g.extents[1]; ++oy)
+            for (i64 ox = 0; ox < g.extents[0]; ++ox) {
+                data_coord d = map_rb_2d({ox, oy, 0}, n);
+                if (tri_contains(n, d.x, d.y)) ++marks[tri_linear_index(d.x, d.y)];
+            }
+        u64 ones = u64(std::count(marks.begin(), marks.end(), 1u));
+        CHECK(ones == tri_cells(n));
+        for (u64 i = 0; i < tri_cells(n); ++i) {
+            data_coord d = map_lambda_2d(i, n);
+            CHECK(tri_linear_index(d.x, d.y) == i);
+        }
+    }
+    CHECK_THROWS_AS(grid_rb(0), std::invalid_argument);
+    CHECK_THROWS_AS(grid_trapezoids(1, 1), std::invalid_argument);
+    CHECK_THROWS_AS(map_lambda_2d(15, 5), std::invalid_argument);
+}
+
 static void host_suite() {
+    general_n_suite();
     // test_maps.cpp "bounding box map"
     CHECK(map_bb({1, 3, 0}, 8, 2).target == (data_coord{1, 3, 0}));
     CHECK(!map_bb({1, 3, 0}, 8, 2).is_void);

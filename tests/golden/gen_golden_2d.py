@@ -1,0 +1,68 @@
+"""Generate tests/golden/maps2d.json from the REFERENCE ITSELF (oracle/_ref:
+the unmodified /root/reference headers compiled in place) for the general-n
+and comparison 2-D maps: RB, lambda, H padded,
+concurrent trapezoids.
+
+    make -C oracle && python tests/golden/gen_golden_2d.py
+
+Contents (hashes are the reference's fnv1a over the raw bytes, state_hash with
+m = 0, side = 0):
+  outcomes        per grid: blocks, voids, hash of the int64 map_outcome array
+                  (6 x i64 per block, the reference's own emission order:
+                  detail::for_each_block_outcome, bands one after another)
+  decompositions  decompose_trapezoids(n, T) band lists
+  launch_map      counters, exact space_overhead, coverage hash, all_one
+  launch_accum    one-pass state hash (and threads_useful)
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from oracle.oracle import LAMBDA, PADDED, RB, TRAP, Reference  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+OUTCOME_GRIDS = ([(RB, n, 1) for n in (1, 2, 3, 8, 27, 100, 1023, 1024)]
+                 + [(LAMBDA, n, 1) for n in (1, 2, 5, 64, 1000)]
+                 + [(PADDED, n, 1) for n in (2, 3, 5, 27, 100, 255, 257, 1000, 1025)]
+                 + [(TRAP, n, T) for T in (1, 4, 16) for n in (2, 3, 16, 27, 100, 257, 1000, 4095)])
+MAP_GRIDS = [(RB, 27, 3, 1), (RB, 1024, 16, 1), (RB, 1023, 16, 1), (LAMBDA, 50, 2, 1), (LAMBDA, 1023, 16, 1),
+             (PADDED, 100, 4, 1), (PADDED, 1025, 16, 1), (PADDED, 9, 1, 1), (TRAP, 100, 4, 4), (TRAP, 257, 2, 1),
+             (TRAP, 1000, 16, 16), (TRAP, 1000, 16, 1), (TRAP, 27, 5, 4)]
+ACCUM_GRIDS = [(RB, 27, 3, 1), (RB, 1024, 16, 1), (LAMBDA, 1023, 16, 1), (PADDED, 1025, 16, 1),
+               (PADDED, 100, 3, 1), (TRAP, 1000, 16, 16), (TRAP, 1000, 16, 1), (TRAP, 257, 2, 4),
+               (TRAP, 4095, 4, 1)]
+
+
+def main() -> None:
+    R = Reference()
+    h = lambda a: R.state_hash(0, 0, a)  # noqa: E731
+    out = {"hash_note": "state_hash(m=0, side=0, bytes) via the reference's fnv1a",
+           "outcomes": [], "decompositions": [], "launch_map": [], "launch_accum": []}
+    for kind, n, T in OUTCOME_GRIDS:
+        o = R.map_outcomes(kind, 2, n, T)
+        out["outcomes"].append({"kind": kind, "n": n, "T": T, "blocks": int(o.shape[0]),
+                                "voids": int(o[:, 0].sum()), "hash": h(o)})
+    for n in (16, 27, 100, 1000, 4095, 65535):
+        for T in (1, 4, 16):
+            out["decompositions"].append({"n": n, "T": T, "bands": R.decompose_trapezoids(n, T)})
+    for kind, n, rho, T in MAP_GRIDS:
+        cov, cnt = R.launch_map(kind, 2, n, rho, T)
+        out["launch_map"].append({"kind": kind, "n": n, "rho": rho, "T": T, "blocks_launched": cnt[0],
+                                  "blocks_void": cnt[1], "threads_launched": cnt[2], "threads_useful": cnt[3],
+                                  "space_overhead": [cnt[4], cnt[5]], "coverage_hash": h(cov),
+                                  "all_one": bool((cov == 1).all())})
+    for kind, n, rho, T in ACCUM_GRIDS:
+        cells, cnt, hh, _ = R.launch_accum(kind, 2, n, rho, passes=1, T=T)
+        out["launch_accum"].append({"kind": kind, "n": n, "rho": rho, "T": T, "hash": hh,
+                                    "threads_useful": cnt[3], "blocks_void": cnt[1]})
+    json.dump(out, open(os.path.join(OUT, "maps2d.json"), "w"), indent=1)
+    print("wrote", os.path.join(OUT, "maps2d.json"))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,88 @@
+"""GPU parity for the general-n and comparison 2-D maps:
+H padded, concurrent trapezoids (one launch per band), RB and lambda — block
+outcomes bit-exact against the reference goldens and the restated oracle;
+launch_map counters / exact space_overhead / coverage and launch_accum state
+hashes equal to the reference's (tests/golden/maps2d.json); every n up to 512
+tiled exactly by its trapezoid bands; general-n ACCUM at the C3 scale."""
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle.oracle import TRAP
+from paper_2208_11617_b200 import api
+
+pytestmark = pytest.mark.gpu
+G = golden("maps2d.json")
+
+
+def _grid(kind, n, rho=1, T=1):
+    return api.make_grid(kind, 2, n, rho, T)
+
+
+def test_outcomes_bit_exact(cuda, orc):
+    for row in G["outcomes"]:
+        got = api.map_outcomes(_grid(row["kind"], row["n"], 1, row["T"]))[:, :6].astype(np.int64)
+        assert got.shape[0] == row["blocks"], row
+        assert orc.state_hash(0, 0, np.ascontiguousarray(got)) == row["hash"], row
+        assert (got == orc.map_outcomes(row["kind"], 2, row["n"], row["T"])).all(), row
+
+
+def test_launch_map_vs_reference(cuda, orc):
+    for row in G["launch_map"]:
+        g = _grid(row["kind"], row["n"], row["rho"], row["T"])
+        dom = api.simplex_spec(2, g.cell_side() - 1)
+        rep = api.launch_map(g, dom)
+        assert [rep.blocks_launched, rep.blocks_void, rep.threads_launched, rep.threads_useful] == [
+            row["blocks_launched"], row["blocks_void"], row["threads_launched"], row["threads_useful"]], row
+        assert (rep.space_overhead.numerator, rep.space_overhead.denominator) == tuple(row["space_overhead"])
+        assert orc.state_hash(0, 0, rep.coverage) == row["coverage_hash"], row
+        assert api.verify_exact_cover(rep, dom).exact == row["all_one"]
+
+
+@pytest.mark.parametrize("ex", [api.EXEC_BLOCK, api.EXEC_RUNS])
+def test_launch_accum_vs_reference(cuda, ex):
+    for row in G["launch_accum"]:
+        g = _grid(row["kind"], row["n"], row["rho"], row["T"])
+        st = api.simplex_grid_state(2, g.cell_side())
+        rep = api.launch_accum(g, api.simplex_spec(2, g.cell_side() - 1), st,
+                               api.launch_opts(exec=ex, record_coverage=False))
+        assert st.hash() == row["hash"], (row, ex)
+        assert rep.threads_useful == row["threads_useful"] and rep.blocks_void == row["blocks_void"]
+
+
+def test_trapezoid_union_tiles_every_n(cuda):
+    # test_maps.cpp:222-234 on the GPU: every n in [2, 512], T in {1, 4, 16}
+    for n in range(2, 513):
+        for T in (1, 4, 16):
+            g = api.grid_trapezoids(n, T)
+            assert len(g.traps) <= max(1, (n - 1).bit_length())
+            dom = api.simplex_spec(2, g.cell_side() - 1)
+            rep = api.launch_map(g, dom)
+            assert api.verify_exact_cover(rep, dom).exact, (n, T)
+            assert rep.threads_useful == api.tri_cells(n - 1)
+
+
+def test_padded_general_n_exact(cuda):
+    # test_maps.cpp:146-165 on the GPU
+    for n in (2, 3, 5, 27, 100, 255, 257, 1000, 4097):
+        g = api.grid_h2d_padded(n)
+        dom = api.simplex_spec(2, g.cell_side() - 1)
+        rep = api.launch_map(g, dom)
+        assert api.verify_exact_cover(rep, dom).exact
+        assert rep.blocks_launched == g.blocks() and rep.blocks_launched - rep.blocks_void == api.tri_cells(n - 1)
+
+
+def test_general_n_accum_c3_scale(cuda, orc):
+    # a non-power-of-two side at the C3 scale: trapezoids n = 4097 (bands
+    # 4096 + padded tail), rho = 16 -> side 65536, 2,147,516,416 u32 cells;
+    # one pass must leave every cell at exactly 1 (exact cover), counters exact
+    import torch
+    g = api.make_grid(api.map_kind.h2d_trapezoid, 2, 4097, 16, 4)
+    side = g.cell_side()
+    cells = torch.zeros(api.tri_cells(side), dtype=torch.int32, device="cuda")
+    api.accum_device(g, cells, 1, api.EXEC_RUNS)
+    assert int((cells != 1).sum().item()) == 0
+    rep = api.launch_map_device(g)
+    _, cnt = orc.sweep(TRAP, 2, 4097, 1, coverage=False, T=4)
+    assert rep.blocks_launched == cnt[0] and rep.blocks_void == cnt[1]
+    assert rep.threads_useful == api.tri_cells(side)
