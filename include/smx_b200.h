@@ -161,13 +161,27 @@ int smx_accum(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passe
 int smx_life_init(int32_t m, int64_t side, uint64_t seed, uint8_t* cells, uint64_t ncells,
                   int device_ptr, void* stream);
 
+/* make_edm_points (simulator.hpp:333-343): count points, x then y drawn from
+ * one seed-keyed splitmix64 stream; out_xy holds 2*count doubles (host). */
+int smx_make_edm_points(int64_t count, uint64_t seed, double* out_xy);
+
+/* launch_edm (simulator.hpp:352-372), m = 2, any 2-D map: cell (x, y) = the
+ * distance between points x and y (f64, bit-identical to the reference's
+ * edm_distance). points_xy: npoints = cell side pairs. coverage/counters as
+ * for smx_accum. */
+int smx_edm(const smx_grid* g, const double* points_xy, int64_t npoints, double* cells, uint64_t ncells,
+            int32_t exec, int device_ptr, uint32_t* coverage, smx_counters* counters, void* stream);
+
 /* One dead-boundary 3-D Life step through the map (the body of launch_ca's step
  * loop, simulator.hpp:440-459, with alive_neighbors_3d_dead :242-253 and
  * life_next :220-223). Device pointers only; cur and next must not alias. */
 int smx_ca_step(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint64_t ncells,
                 int32_t exec, void* stream);
 
-/* launch_ca (simulator.hpp:431-463) for m = 3: `steps` steps in place.
+/* launch_ca (simulator.hpp:431-463): `steps` steps in place. m = 3: the
+ * dead boundary (bb / h3d grids); m = 2: the periodic boundary
+ * (alive_neighbors_2d_periodic, :227-239) through any 2-D map (smx_ca_step
+ * likewise).
  * scratch: optional device buffer of ncells bytes (device_ptr mode); NULL =
  * library-managed. coverage/counters as for smx_accum (first step). */
 int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, int32_t exec,

@@ -27,6 +27,7 @@ _u64p = np.ctypeslib.ndpointer(np.uint64, flags="C")
 _i64p = np.ctypeslib.ndpointer(np.int64, flags="C")
 _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C")
 _u8p = np.ctypeslib.ndpointer(np.uint8, flags="C")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C")
 
 
 def build() -> None:
@@ -87,6 +88,9 @@ class Restated:
         L.orc_map_rb.argtypes = [C.c_int64, C.c_int64, C.c_int64, _i64p]
         L.orc_map_lambda.argtypes = [C.c_uint64, C.c_int64, _i64p]
         L.orc_map_padded.argtypes = [C.c_int64, C.c_int64, C.c_int64, _i64p]
+        L.orc_make_edm_points.argtypes = [C.c_int64, C.c_uint64, _f64p]
+        L.orc_kernel_edm.argtypes = [C.c_int64, _f64p, _f64p]
+        L.orc_ca2d_run.argtypes = [C.c_int64, C.c_int64, _u8p, C.c_uint64]
         self.L = L
 
     @staticmethod
@@ -126,6 +130,21 @@ class Restated:
             rc = self.L.orc_map_bb(x, y, z, n, m, o)
         self._ok(rc, "map_one")
         return tuple(int(v) for v in o)
+
+    def make_edm_points(self, count: int, seed: int) -> np.ndarray:
+        out = np.zeros((count, 2), np.float64)
+        self.L.orc_make_edm_points(count, seed, out)
+        return out
+
+    def kernel_edm(self, side: int, seed: int) -> np.ndarray:
+        pts = self.make_edm_points(side, seed)
+        cells = np.zeros(tri_cells(side), np.float64)
+        self.L.orc_kernel_edm(side, pts, cells)
+        return cells
+
+    def ca2d_run(self, side: int, steps: int, cells: np.ndarray) -> np.ndarray:
+        self._ok(self.L.orc_ca2d_run(side, steps, cells, cells.size), "ca2d_run")
+        return cells
 
     def decompose_trapezoids(self, n: int, T: int) -> list[dict]:
         out = np.zeros(9 * 64, np.int64)
@@ -202,6 +221,10 @@ class Reference:
         L.ref_map_outcomes_t.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, _i64p, C.c_uint64]
         L.ref_decompose_trapezoids.argtypes = [C.c_int64, C.c_int64, _i64p, C.c_int, C.POINTER(C.c_int)]
         L.ref_map_trapezoid.argtypes = [C.c_int64, C.c_int64, C.c_int, C.c_int64, C.c_int64, _i64p]
+        L.ref_make_edm_points.argtypes = [C.c_int64, C.c_uint64, _f64p]
+        L.ref_kernel_edm.argtypes = [C.c_int64, C.c_uint64, _f64p, C.c_uint64, _u64p]
+        L.ref_launch_edm.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, _f64p, C.c_uint64,
+                                     _u64p, _u64p]
         self.L = L
 
     def _ok(self, rc: int, what: str) -> None:
@@ -220,6 +243,26 @@ class Reference:
         out = np.zeros((blocks, 6), np.int64)
         self._ok(self.L.ref_map_outcomes_t(kind, m, n, T, out, blocks), "map_outcomes")
         return out
+
+    def make_edm_points(self, count: int, seed: int) -> np.ndarray:
+        out = np.zeros((count, 2), np.float64)
+        self._ok(self.L.ref_make_edm_points(count, seed, out), "make_edm_points")
+        return out
+
+    def kernel_edm(self, side: int, seed: int):
+        cells = np.zeros(tri_cells(side), np.float64)
+        h = np.zeros(1, np.uint64)
+        self._ok(self.L.ref_kernel_edm(side, seed, cells, cells.size, h), "kernel_edm")
+        return cells, int(h[0])
+
+    def launch_edm(self, kind: int, n: int, rho: int, seed: int, T: int = 1):
+        _, _, ds = self.make_grid(kind, 2, n, rho, T)
+        side = ds * rho
+        cells = np.zeros(tri_cells(side), np.float64)
+        cnt = np.zeros(6, np.uint64)
+        h = np.zeros(1, np.uint64)
+        self._ok(self.L.ref_launch_edm(kind, n, rho, T, seed, cells, cells.size, cnt, h), "launch_edm")
+        return cells, [int(v) for v in cnt], int(h[0])
 
     def decompose_trapezoids(self, n: int, T: int) -> list[dict]:
         out = np.zeros(9 * 64, np.int64)

@@ -269,6 +269,45 @@ int ref_launch_ca(int kind, int m, int64_t n, int64_t rho, int64_t T, int64_t st
     });
 }
 
+// make_edm_points (simulator.hpp:333-343): 2 doubles per point.
+int ref_make_edm_points(int64_t count, uint64_t seed, double* out) {
+    return guarded([&] {
+        auto pts = make_edm_points(count, seed);
+        for (std::size_t i = 0; i < pts.size(); ++i) out[2 * i] = pts[i][0], out[2 * i + 1] = pts[i][1];
+    });
+}
+
+// kernel_edm (simulator.hpp:375-386): the sequential fill.
+int ref_kernel_edm(int64_t side, uint64_t seed, double* cells, uint64_t ncells, uint64_t* hash) {
+    return guarded([&] {
+        auto pts = make_edm_points(side, seed);
+        simplex_grid_state<double> s(2, side);
+        if (s.cells.size() != ncells) throw std::invalid_argument("ncells mismatch");
+        kernel_edm(pts, s);
+        std::memcpy(cells, s.cells.data(), ncells * sizeof(double));
+        if (hash) *hash = s.hash();
+    });
+}
+
+// launch_edm (simulator.hpp:352-372) over a map-driven grid.
+int ref_launch_edm(int kind, int64_t n, int64_t rho, int64_t T, uint64_t seed, double* cells, uint64_t ncells,
+                   uint64_t* counters, uint64_t* hash) {
+    return guarded([&] {
+        grid_spec g = make_grid(kind_of(kind), 2, n, rho, T);
+        simplex_spec dom = domain_of(g);
+        auto pts = make_edm_points(dom.n + 1, seed);
+        simplex_grid_state<double> s(2, dom.n + 1);
+        if (s.cells.size() != ncells) throw std::invalid_argument("ncells mismatch");
+        launch_opts o;
+        o.record_coverage = false;
+        o.seed = seed;
+        sim_report rep = launch_edm(g, dom, pts, s, o);
+        std::memcpy(cells, s.cells.data(), ncells * sizeof(double));
+        put_counters(rep, counters);
+        if (hash) *hash = rep.state_hash;
+    });
+}
+
 // simplex_grid_state<T>::hash (simulator.hpp:68-73) over raw cell bytes.
 uint64_t ref_state_hash(int m, int64_t side, const void* bytes, uint64_t nbytes) {
     u64 h = fnv1a_seed;

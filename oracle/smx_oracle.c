@@ -20,6 +20,7 @@
  * Status codes: 0 ok, 1 invalid argument (the reference throws
  * std::invalid_argument), 2 overflow.
  */
+#include <math.h>
 #include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -612,4 +613,48 @@ int orc_first_defect(int m, i64 side, const u32* cov, u64 n, i64* w3, u64* mult)
         return 0; /* not exact */
     }
     return 1; /* exact */
+}
+
+/* ---- EDM and the periodic 2-D Life ---- */
+
+/* make_edm_points (simulator.hpp:333-343) + splitmix64_unit (bits.hpp:92-94) */
+void orc_make_edm_points(i64 count, u64 seed, double* out) {
+    u64 st = seed;
+    for (i64 i = 0; i < 2 * count; ++i) out[i] = (double)(splitmix64(&st) >> 11) * 0x1.0p-53;
+}
+
+/* kernel_edm (simulator.hpp:375-386) with edm_distance (:345-350): mul, mul,
+ * add, sqrt, each rounded (this file is built with -ffp-contract=off) */
+void orc_kernel_edm(i64 side, const double* pts, double* cells) {
+    for (i64 y = 0; y < side; ++y)
+        for (i64 x = 0; x <= y; ++x) {
+            double dx = pts[2 * x] - pts[2 * y], dy = pts[2 * x + 1] - pts[2 * y + 1];
+            cells[tri_index(x, y)] = sqrt(dx * dx + dy * dy);
+        }
+}
+
+/* kernel_ca_run m = 2 (simulator.hpp:409-425) with alive_neighbors_2d_periodic
+ * (:227-239): Moore neighbourhood wrapped modulo the side, x > y reads dead */
+int orc_ca2d_run(i64 side, i64 steps, u8* cells, u64 ncells) {
+    if (ncells != orc_tri_cells(side) || steps < 0) return 1;
+    u8* next = (u8*)malloc(ncells ? ncells : 1);
+    if (!next) return 2;
+    for (i64 st = 0; st < steps; ++st) {
+        for (i64 y = 0; y < side; ++y)
+            for (i64 x = 0; x <= y; ++x) {
+                int count = 0;
+                for (i64 dy = -1; dy <= 1; ++dy)
+                    for (i64 dx = -1; dx <= 1; ++dx) {
+                        if (!dx && !dy) continue;
+                        i64 nx = x + dx, ny = y + dy;
+                        if (nx < 0) nx += side; else if (nx >= side) nx -= side;
+                        if (ny < 0) ny += side; else if (ny >= side) ny -= side;
+                        if (nx <= ny) count += cells[tri_index(nx, ny)];
+                    }
+                next[tri_index(x, y)] = life_next(cells[tri_index(x, y)], count);
+            }
+        memcpy(cells, next, ncells);
+    }
+    free(next);
+    return 0;
 }

@@ -455,6 +455,43 @@ def launch_ca(g: grid_spec, domain: simplex_spec, state: simplex_grid_state,
     return rep
 
 
+def make_edm_points(count: int, seed: int) -> np.ndarray:
+    """make_edm_points (simulator.hpp:333-343): (count, 2) float64, x then y
+    from one seed-keyed splitmix64 stream."""
+    out = np.empty((max(count, 0), 2), np.float64)
+    check(lib().smx_make_edm_points(int(count), int(seed) & 0xFFFFFFFFFFFFFFFF, out.ctypes.data))
+    return out
+
+
+def launch_edm(g: grid_spec, domain: simplex_spec, points: np.ndarray, state: simplex_grid_state,
+               opts: launch_opts | None = None) -> sim_report:
+    """launch_edm (simulator.hpp:352-372): cell (x, y) = |p_x - p_y|, f64."""
+    opts = opts or launch_opts()
+    validate_launch(g, domain)
+    if g.dims != 2:
+        raise InvalidArgument("launch_edm: 2-simplex domains only")
+    if state.m != 2 or state.side != g.cell_side():
+        raise InvalidArgument("launch: state does not match the domain")
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+    if pts.shape[0] != state.side:
+        raise InvalidArgument("launch_edm: need one point per domain side unit")
+    if state.cells.dtype != np.float64:
+        raise InvalidArgument("launch_edm: state cells must be f64")
+    rep = _make_report(g, opts)
+    cnt = _lib.smx_counters()
+    check(lib().smx_edm(C.byref(g.raw), pts.ctypes.data, pts.shape[0], state.cells.ctypes.data, state.cells.size,
+                        int(opts.exec), 0, _cov_ptr(rep), C.byref(cnt), None))
+    _finish(rep, cnt)
+    rep.state_hash = state.hash()
+    return rep
+
+
+def edm_device(g: grid_spec, points, cells, exec: int = EXEC_AUTO) -> None:
+    """Device-resident EDM: points a (side, 2) float64 CUDA tensor, cells f64."""
+    check(lib().smx_edm(C.byref(g.raw), _ptr(points), points.shape[0], _ptr(cells), cells.numel(), exec, 1,
+                        None, None, _stream()))
+
+
 def verify_exact_cover(rep: sim_report, domain: simplex_spec) -> cover_verdict:
     """simulator.hpp:467-478: first cell (linear order) whose multiplicity != 1."""
     if domain.m != rep.m or domain.n != rep.cell_side - 1:

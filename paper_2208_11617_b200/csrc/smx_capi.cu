@@ -634,9 +634,14 @@ static int check_align16(const void* a, const void* b) {
 constexpr uint64_t kFusedMaxCells = 48ull << 20;
 
 static int ca_validate(const smx_grid* g, uint64_t ncells, int32_t* exec) {
-    if (g->dims != 3)
-        return fail(SMX_EINVAL, "launch_ca: the B200 CA path is the dead-boundary 3-simplex kernel");
     if (int rc = check_cells(g, ncells)) return rc;
+    if (g->dims == 2) {  // periodic 2-D Life: BLOCK or RUNS (the x-run kernel), every 2-D map
+        if (*exec < 0 || *exec == SMX_EXEC_BITS) *exec = SMX_EXEC_RUNS;
+        if (*exec != SMX_EXEC_BLOCK && *exec != SMX_EXEC_RUNS) return fail(SMX_EINVAL, "ca: unknown exec scheme");
+        return SMX_OK;
+    }
+    if (g->kind != SMX_BB && g->kind != SMX_H3D)
+        return fail(SMX_EINVAL, "launch_ca: 3-simplex grids are bb or h3d");
     if (*exec < 0) *exec = smx::ca_runs_supported(int(g->rho)) ? SMX_EXEC_BITS : SMX_EXEC_BLOCK;
     if (*exec != SMX_EXEC_BLOCK && *exec != SMX_EXEC_RUNS && *exec != SMX_EXEC_BITS)
         return fail(SMX_EINVAL, "ca: unknown exec scheme");
@@ -645,9 +650,22 @@ static int ca_validate(const smx_grid* g, uint64_t ncells, int32_t* exec) {
     return SMX_OK;
 }
 
+static int ca2d_step(const smx_grid* g, const uint8_t* cur, uint8_t* next, int32_t exec, cudaStream_t s) {
+    std::vector<smx::Geom> subs;
+    if (int rc = sub_geoms(g, subs, false)) return rc;
+    for (const auto& k : subs) smx::launch_ca2d(k, cur, next, exec, s);  // bands: disjoint cells
+    TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
 int smx_ca_step(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint64_t ncells, int32_t exec,
                 void* stream) {
     const bool auto_exec = exec < 0;
+    if (g && g->dims == 2) {
+        if (int rc = ca_validate(g, ncells, &exec)) return rc;
+        if (cur == next) return fail(SMX_EINVAL, "ca_step: cur and next must not alias");
+        return ca2d_step(g, cur, next, exec, (cudaStream_t)stream);
+    }
     smx::Geom k;
     if (int rc = make_geom(g, &k, true)) return rc;
     if (int rc = ca_validate(g, ncells, &exec)) return rc;
@@ -682,7 +700,12 @@ int smx_ca_step_range(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint
 int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, int32_t exec, int device_ptr,
            uint8_t* scratch, uint32_t* coverage, smx_counters* counters, void* stream) {
     smx::Geom k;
-    if (int rc = make_geom(g, &k, true)) return rc;
+    if (g && g->dims == 2) {
+        k = smx::Geom{};
+        if (!g) return fail(SMX_EINVAL, "null grid");
+    } else if (int rc = make_geom(g, &k, true)) {
+        return rc;
+    }
     if (int rc = ca_validate(g, ncells, &exec)) return rc;
     if (steps < 0) return fail(SMX_EINVAL, "launch_ca: steps must be >= 0");
     cudaStream_t s = (cudaStream_t)stream;
@@ -710,7 +733,12 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
     uint8_t* nxt = b;
     if (device_ptr)
         if (int rc = check_align16(a, b)) return rc;
-    if (exec == SMX_EXEC_BITS && steps > 0) {
+    if (g->dims == 2) {
+        for (int64_t st = 0; st < steps; ++st) {
+            if (int rc = ca2d_step(g, cur, nxt, exec, s)) return rc;
+            std::swap(cur, nxt);
+        }
+    } else if (exec == SMX_EXEC_BITS && steps > 0) {
         // bit-shadow engine: pack once, steps x (bits -> bits), unpack once
         void *pa, *pb;
         if (int rc = pool_get(3, bits_bytes(k.side), &pa)) return rc;
@@ -796,6 +824,63 @@ int smx_bits_run(const smx_grid* g, uint32_t* bits_a, uint32_t* bits_b, int64_t 
     if (int rc = bits_tmap(bits_a, k.side, k.rho, &ta)) return rc;
     if (int rc = bits_tmap(bits_b, k.side, k.rho, &tb)) return rc;
     return bits_engine(g, k, bits_a, bits_b, ta, tb, steps, (cudaStream_t)stream);
+}
+
+int smx_make_edm_points(int64_t count, uint64_t seed, double* out_xy) {
+    if (count < 0) return fail(SMX_EINVAL, "make_edm_points: count must be >= 0");
+    if (count > 0 && !out_xy) return fail(SMX_EINVAL, "null output");
+    // make_edm_points (simulator.hpp:333-343): one splitmix64 stream, x then y
+    uint64_t st = seed;
+    auto unit = [&st]() {
+        uint64_t z = (st += 0x9e3779b97f4a7c15ull);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        z ^= z >> 31;
+        return double(z >> 11) * 0x1.0p-53;  // splitmix64_unit (bits.hpp:92-94)
+    };
+    for (int64_t i = 0; i < count; ++i) {
+        out_xy[2 * i] = unit();
+        out_xy[2 * i + 1] = unit();
+    }
+    return SMX_OK;
+}
+
+int smx_edm(const smx_grid* g, const double* points_xy, int64_t npoints, double* cells, uint64_t ncells,
+            int32_t exec, int device_ptr, uint32_t* coverage, smx_counters* counters, void* stream) {
+    std::vector<smx::Geom> subs;
+    if (int rc = sub_geoms(g, subs, false)) return rc;
+    if (g->dims != 2) return fail(SMX_EINVAL, "launch_edm: 2-simplex domains only");
+    if (int rc = check_cells(g, ncells)) return rc;
+    if (npoints != cell_side_of(g)) return fail(SMX_EINVAL, "launch_edm: need one point per domain side unit");
+    if (exec < 0 || exec == SMX_EXEC_BITS) exec = SMX_EXEC_RUNS;
+    if (exec != SMX_EXEC_BLOCK && exec != SMX_EXEC_RUNS) return fail(SMX_EINVAL, "edm: unknown exec scheme");
+    cudaStream_t s = (cudaStream_t)stream;
+    const double* dp = points_xy;
+    double* d = cells;
+    uint32_t* dcov = coverage;
+    if (!device_ptr) {
+        void *p, *q;
+        if (int rc = pool_get(1, ncells * 8, &p)) return rc;
+        if (int rc = pool_get(2, size_t(npoints) * 16, &q)) return rc;
+        d = (double*)p;
+        TRY(cudaMemcpyAsync(q, points_xy, size_t(npoints) * 16, cudaMemcpyHostToDevice, s));
+        dp = (const double*)q;
+        if (coverage) {
+            if (int rc = pool_get(0, ncells * 4, &p)) return rc;
+            dcov = (uint32_t*)p;
+            TRY(cudaMemcpyAsync(dcov, coverage, ncells * 4, cudaMemcpyHostToDevice, s));
+        }
+    }
+    if (coverage || counters)
+        if (int rc = fill_counters(g, counters, s, dcov)) return rc;
+    for (const auto& k : subs) smx::launch_edm(k, dp, d, exec, s);
+    TRY(cudaGetLastError());
+    if (!device_ptr) {
+        TRY(cudaMemcpyAsync(cells, d, ncells * 8, cudaMemcpyDeviceToHost, s));
+        if (coverage) TRY(cudaMemcpyAsync(coverage, dcov, ncells * 4, cudaMemcpyDeviceToHost, s));
+        TRY(cudaStreamSynchronize(s));
+    }
+    return SMX_OK;
 }
 
 uint64_t smx_state_hash(int32_t m, int64_t side, const void* bytes, uint64_t nbytes) {

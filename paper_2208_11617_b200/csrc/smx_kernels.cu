@@ -6,6 +6,7 @@
 // strict y-1 -> rho^m cells -> membership -> packed index -> body.
 #include "smx_common.cuh"
 #include "smx_launch.hpp"
+#include "smx_runs.cuh"
 
 namespace smx {
 
@@ -168,45 +169,10 @@ __device__ __forceinline__ void accum_rows(uint32_t* __restrict__ cells, const u
 
 template <int KIND, int KX, int RR, int NV>
 __global__ void __launch_bounds__(ACC_THREADS) k_accum_runs(Geom g, uint32_t* __restrict__ cells) {
-    static_assert(KX <= 32, "one warp maps the strip");
     __shared__ int s_run[KX][3];
     __shared__ int s_nruns;
-    const int x0 = blockIdx.x * KX, wy = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp == 0) {
-        const int wx = x0 + lane;
-        int valid = lane < KX && wx < g.ex;
-        outcome<int> o{1, 0, 0, 0, 1, 0};
-        if (valid) {
-            o = map_block<KIND>(g, wx, wy, 0);
-            valid = !o.is_void;
-        }
-        // x-adjacent chains in either direction (RB's reflected half maps
-        // consecutive blocks to descending x): a lane continues the run when
-        // its x step (+1 or -1) repeats the previous lane's step, or the
-        // previous lane had none (it is the run's first tile)
-        const int px = __shfl_up_sync(FULL_MASK, o.x, 1);
-        const int py = __shfl_up_sync(FULL_MASK, o.y, 1);
-        const int pv = __shfl_up_sync(FULL_MASK, valid, 1);
-        const int dx = o.x - px;
-        const int step = (lane > 0 && valid && pv && py == o.y && (dx == 1 || dx == -1)) ? dx : 0;
-        const int pstep = __shfl_up_sync(FULL_MASK, step, 1);
-        const bool head = valid && !(step != 0 && (lane == 0 || pstep == 0 || pstep == step));
-        const unsigned heads = __ballot_sync(FULL_MASK, head);
-        const unsigned vmask = __ballot_sync(FULL_MASK, valid);
-        const int nstep = __shfl_down_sync(FULL_MASK, step, 1);  // direction of the run from a head
-        if (head) {
-            const int r = __popc(heads & ((1u << lane) - 1u));
-            const unsigned above = lane == 31 ? 0u : ~((2u << lane) - 1u);
-            const unsigned stop = (heads | ~vmask) & above;
-            const int end = stop ? __ffs(stop) - 1 : 32;
-            const int len = end - lane;
-            s_run[r][0] = (len > 1 && lane < 31 && nstep < 0) ? o.x - (len - 1) : o.x;  // lowest x of the run
-            s_run[r][1] = o.y;
-            s_run[r][2] = len;
-        }
-        if (lane == 0) s_nruns = __popc(heads);
-    }
+    if (warp == 0) strip_runs<KIND, KX>(g, blockIdx.x * KX, blockIdx.y, s_run, &s_nruns);
     __syncthreads();
     const int nruns = s_nruns;
     const int rho = g.rho, S = g.side;

@@ -13,6 +13,9 @@ m = 0, side = 0):
   decompositions  decompose_trapezoids(n, T) band lists
   launch_map      counters, exact space_overhead, coverage hash, all_one
   launch_accum    one-pass state hash (and threads_useful)
+  edm             kernel_edm hashes and launch_edm through maps
+  ca2d            2-D periodic Life: make_life_state(2, ...) hashes, kernel_ca_run
+                  final hashes, launch_ca through maps
 """
 from __future__ import annotations
 
@@ -22,7 +25,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
-from oracle.oracle import LAMBDA, PADDED, RB, TRAP, Reference  # noqa: E402
+from oracle.oracle import BB, H2D, LAMBDA, PADDED, RB, TRAP, Reference  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 
@@ -60,6 +63,35 @@ def main() -> None:
         cells, cnt, hh, _ = R.launch_accum(kind, 2, n, rho, passes=1, T=T)
         out["launch_accum"].append({"kind": kind, "n": n, "rho": rho, "T": T, "hash": hh,
                                     "threads_useful": cnt[3], "blocks_void": cnt[1]})
+    out["edm"] = {"kernel_edm": [], "launch_edm": []}
+    for side in (14, 15, 63, 255, 1023):
+        for seed in (7, 42, 0xC0FFEE):
+            _, hh = R.kernel_edm(side, seed)
+            out["edm"]["kernel_edm"].append({"side": side, "seed": seed, "hash": hh})
+    for kind, n, rho, T in [(BB, 14, 1, 1), (RB, 14, 1, 1), (LAMBDA, 14, 1, 1), (PADDED, 15, 1, 1), (TRAP, 15, 1, 1),
+                            (BB, 15, 1, 1), (H2D, 16, 1, 1), (TRAP, 16, 1, 4), (H2D, 64, 4, 1), (BB, 63, 4, 1),
+                            (TRAP, 100, 3, 4), (RB, 85, 3, 1), (LAMBDA, 63, 4, 1), (PADDED, 100, 16, 1)]:
+        _, cnt, hh = R.launch_edm(kind, n, rho, 7, T)
+        out["edm"]["launch_edm"].append({"kind": kind, "n": n, "rho": rho, "T": T, "seed": 7, "hash": hh,
+                                         "threads_useful": cnt[3], "blocks_void": cnt[1]})
+    out["ca2d"] = {"life_init": [], "kernel_ca_run": [], "launch_ca": []}
+    for side, seed in [(24, 42), (15, 9), (63, 42), (1023, 42), (252, 5)]:
+        st = R.make_life_state(2, side, seed)
+        out["ca2d"]["life_init"].append({"side": side, "seed": seed, "hash": R.state_hash(2, side, st),
+                                         "alive": int(st.sum())})
+    for side, steps, seed in [(24, 8, 42), (15, 6, 9), (63, 64, 42), (255, 64, 42), (1023, 64, 42), (255, 64, 0xC0FFEE)]:
+        st = R.make_life_state(2, side, seed)
+        R.kernel_ca_run(2, side, steps, st)
+        out["ca2d"]["kernel_ca_run"].append({"side": side, "steps": steps, "seed": seed,
+                                             "hash": R.state_hash(2, side, st)})
+    for kind, n, rho, T, steps in [(BB, 24, 1, 1, 8), (RB, 24, 1, 1, 8), (LAMBDA, 24, 1, 1, 8), (TRAP, 25, 1, 1, 8),
+                                   (PADDED, 25, 1, 1, 8), (H2D, 16, 1, 1, 6), (TRAP, 16, 1, 4, 6),
+                                   (H2D, 64, 4, 1, 5), (BB, 63, 4, 1, 5), (TRAP, 100, 3, 4, 5), (RB, 85, 3, 1, 5)]:
+        side = (n - 1 if kind in (H2D, TRAP, PADDED) else n) * rho
+        st = R.make_life_state(2, side, 42)
+        st, cnt, hh, _ = R.launch_ca(kind, 2, n, rho, steps, st, T=T)
+        out["ca2d"]["launch_ca"].append({"kind": kind, "n": n, "rho": rho, "T": T, "steps": steps, "seed": 42,
+                                         "side": side, "hash": hh, "threads_useful": cnt[3]})
     json.dump(out, open(os.path.join(OUT, "maps2d.json"), "w"), indent=1)
     print("wrote", os.path.join(OUT, "maps2d.json"))
 

@@ -86,3 +86,77 @@ def test_general_n_accum_c3_scale(cuda, orc):
     _, cnt = orc.sweep(TRAP, 2, 4097, 1, coverage=False, T=4)
     assert rep.blocks_launched == cnt[0] and rep.blocks_void == cnt[1]
     assert rep.threads_useful == api.tri_cells(side)
+
+
+# ---- EDM and periodic 2-D Life (#3) through every 2-D map ----
+
+def _side(kind, n, rho):
+    return (n - 1 if api.strict_view(kind) else n) * rho
+
+
+@pytest.mark.parametrize("ex", [api.EXEC_BLOCK, api.EXEC_RUNS])
+def test_edm_bit_exact_vs_reference(cuda, ex):
+    # test_simulator.cpp:199-228: launch_edm through every map == the sequential fill
+    E = G["edm"]
+    for row in E["launch_edm"]:
+        g = _grid(row["kind"], row["n"], row["rho"], row["T"])
+        side = g.cell_side()
+        pts = api.make_edm_points(side, row["seed"])
+        st = api.simplex_grid_state(2, side, np.float64)
+        rep = api.launch_edm(g, api.simplex_spec(2, side - 1), pts, st,
+                             api.launch_opts(exec=ex, record_coverage=False))
+        assert st.hash() == row["hash"] and rep.state_hash == row["hash"], (row, ex)
+        assert rep.threads_useful == row["threads_useful"]
+    # acceptance.cpp:182-200 (criterion 7): sides 63, 255, 1023, two seeds, the five maps
+    seq = {(r["side"], r["seed"]): r["hash"] for r in E["kernel_edm"]}
+    for side in (63, 255, 1023):
+        for seed in (42, 0xC0FFEE):
+            pts = api.make_edm_points(side, seed)
+            for g in (api.grid_bb(side, 2), api.grid_rb(side), api.grid_lambda(side), api.grid_h2d(side + 1)
+                      if side + 1 in (64, 256, 1024) else None, api.grid_trapezoids(side + 1, 1)):
+                if g is None:
+                    continue
+                st = api.simplex_grid_state(2, side, np.float64)
+                api.launch_edm(g, api.simplex_spec(2, side - 1), pts, st, api.launch_opts(exec=ex,
+                                                                                           record_coverage=False))
+                assert st.hash() == seq[(side, seed)], (side, seed, g, ex)
+
+
+def test_edm_c1_scale_vs_restated(cuda, orc):
+    # H2D(1024), rho = 16: side 16368, 133,963,896 f64 cells (1.07 GB), bit-exact
+    import torch
+    g = api.make_grid(api.map_kind.h2d, 2, 1024, 16)
+    side = g.cell_side()
+    pts = torch.from_numpy(api.make_edm_points(side, 42)).cuda()
+    cells = torch.empty(api.tri_cells(side), dtype=torch.float64, device="cuda")
+    api.edm_device(g, pts, cells, api.EXEC_RUNS)
+    want = orc.kernel_edm(side, 42)
+    assert orc.state_hash(2, side, cells.cpu().numpy()) == orc.state_hash(2, side, want)
+
+
+@pytest.mark.parametrize("ex", [api.EXEC_BLOCK, api.EXEC_RUNS])
+def test_ca2d_periodic_vs_reference(cuda, ex):
+    C2 = G["ca2d"]
+    for row in C2["life_init"]:
+        st = api.make_life_state(2, row["side"], row["seed"])
+        assert st.hash() == row["hash"] and int(st.cells.sum()) == row["alive"]
+    for row in C2["launch_ca"]:
+        g = _grid(row["kind"], row["n"], row["rho"], row["T"])
+        st = api.make_life_state(2, row["side"], row["seed"])
+        rep = api.launch_ca(g, api.simplex_spec(2, row["side"] - 1), st,
+                            api.launch_opts(steps=row["steps"], boundary=api.ca_boundary.periodic2d, exec=ex,
+                                            record_coverage=False))
+        assert rep.state_hash == row["hash"], (row, ex)
+        assert rep.threads_useful == row["threads_useful"]
+    # acceptance.cpp:182-205 + SURVEY Appendix A: 64 steps, every map, sides 63..1023
+    seq = {(r["side"], r["steps"], r["seed"]): r["hash"] for r in C2["kernel_ca_run"]}
+    for side, seed in ((63, 42), (255, 42), (1023, 42), (255, 0xC0FFEE)):
+        for g in (api.grid_bb(side, 2), api.grid_rb(side), api.grid_lambda(side), api.grid_h2d(side + 1)
+                  if side + 1 in (64, 256, 1024) else None, api.grid_trapezoids(side + 1, 1)):
+            if g is None:
+                continue
+            st = api.make_life_state(2, side, seed)
+            api.launch_ca(g, api.simplex_spec(2, side - 1), st,
+                          api.launch_opts(steps=64, boundary=api.ca_boundary.periodic2d, exec=ex,
+                                          record_coverage=False))
+            assert st.hash() == seq[(side, 64, seed)], (side, seed, g, ex)

@@ -8,14 +8,14 @@ import numpy as np
 import pytest
 
 from conftest import golden
-from oracle.oracle import LAMBDA, PADDED, RB, TRAP
+from oracle.oracle import H2D, LAMBDA, PADDED, RB, TRAP
 from paper_2208_11617_b200 import api
 
 G = golden("maps2d.json")
 
 
 def _side(kind, n, rho):
-    return (n - 1 if kind in (PADDED, TRAP) else n) * rho
+    return (n - 1 if kind in (PADDED, TRAP, H2D) else n) * rho
 
 
 def test_restated_outcomes_vs_reference_goldens(orc):
@@ -132,3 +132,36 @@ def test_trapezoid_union_tiles_every_n(orc):
             assert len(orc.decompose_trapezoids(n, T)) <= max(1, (n - 1).bit_length())
             cov, _ = orc.sweep(TRAP, 2, n, 1, T=T)
             assert (cov == 1).all(), (n, T)
+
+
+def test_restated_edm_and_ca2d_vs_reference_goldens(orc):
+    E = G["edm"]
+    for row in E["kernel_edm"]:
+        if row["side"] <= 255:
+            assert orc.state_hash(2, row["side"], orc.kernel_edm(row["side"], row["seed"])) == row["hash"], row
+    # every map's launch_edm equals the sequential fill (test_simulator.cpp:199-228)
+    seq = {r["side"]: r["hash"] for r in E["kernel_edm"] if r["seed"] == 7}
+    for row in E["launch_edm"]:
+        side = _side(row["kind"], row["n"], row["rho"])
+        want = seq.get(side, orc.state_hash(2, side, orc.kernel_edm(side, 7)))
+        assert row["hash"] == want, row
+    C2 = G["ca2d"]
+    for row in C2["kernel_ca_run"]:
+        if row["side"] > 255:
+            continue
+        st = np.zeros(row["side"] * (row["side"] + 1) // 2, np.uint8)
+        init = [r for r in C2["life_init"] if (r["side"], r["seed"]) == (row["side"], row["seed"])]
+        st = orc.make_life_state(2, row["side"], row["seed"])
+        if init:
+            assert orc.state_hash(2, row["side"], st) == init[0]["hash"]
+        orc.ca2d_run(row["side"], row["steps"], st)
+        assert orc.state_hash(2, row["side"], st) == row["hash"], row
+    # 2-D periodic, seed 42, 64 steps
+    hashes = {(r["side"], r["steps"], r["seed"]): r["hash"] for r in C2["kernel_ca_run"]}
+    assert hashes[(63, 64, 42)] == 8247929562437622423
+    assert hashes[(1023, 64, 42)] == 17772433350676739252
+
+
+def test_edm_points_abi_matches_restated(orc):
+    for count, seed in ((14, 7), (1000, 42), (5, 0xC0FFEE)):
+        assert (api.make_edm_points(count, seed) == orc.make_edm_points(count, seed)).all()
