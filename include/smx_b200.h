@@ -161,6 +161,12 @@ int smx_accum(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passe
 int smx_life_init(int32_t m, int64_t side, uint64_t seed, uint8_t* cells, uint64_t ncells,
                   int device_ptr, void* stream);
 
+/* verify_exact_cover (simulator.hpp:467-478) on the device: *first_bad = the
+ * first packed index whose coverage is not 1 (ncells when exact),
+ * *multiplicity = its coverage. Synchronises `stream`. */
+int smx_verify_cover(const uint32_t* coverage, uint64_t ncells, int device_ptr, uint64_t* first_bad,
+                     uint32_t* multiplicity, void* stream);
+
 /* make_edm_points (simulator.hpp:333-343): count points, x then y drawn from
  * one seed-keyed splitmix64 stream; out_xy holds 2*count doubles (host). */
 int smx_make_edm_points(int64_t count, uint64_t seed, double* out_xy);

@@ -225,6 +225,8 @@ class Reference:
         L.ref_kernel_edm.argtypes = [C.c_int64, C.c_uint64, _f64p, C.c_uint64, _u64p]
         L.ref_launch_edm.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, _f64p, C.c_uint64,
                                      _u64p, _u64p]
+        L.ref_csv_sweep.argtypes = [C.c_int, C.c_int, C.c_char_p, C.c_int64, C.c_int64, C.c_int, C.c_char_p,
+                                    C.c_uint64, C.POINTER(C.c_uint64), C.c_char_p, C.c_uint64]
         self.L = L
 
     def _ok(self, rc: int, what: str) -> None:
@@ -243,6 +245,16 @@ class Reference:
         out = np.zeros((blocks, 6), np.int64)
         self._ok(self.L.ref_map_outcomes_t(kind, m, n, T, out, blocks), "map_outcomes")
         return out
+
+    def csv_sweep(self, kind: int, m: int, nrange: str, rho: int = 1, T: int = 1, analyze: bool = False):
+        """verify_sweep + csv_measure (or analyze_sweep + csv_analyze); -> (text, witnesses)"""
+        cap = 1 << 24
+        buf = C.create_string_buffer(cap)
+        wbuf = C.create_string_buffer(1 << 16)
+        n = C.c_uint64(0)
+        self._ok(self.L.ref_csv_sweep(kind, m, nrange.encode(), rho, T, 1 if analyze else 0, buf, cap, C.byref(n),
+                                      wbuf, 1 << 16), "csv_sweep")
+        return buf.raw[:n.value].decode(), wbuf.value.decode()
 
     def make_edm_points(self, count: int, seed: int) -> np.ndarray:
         out = np.zeros((count, 2), np.float64)

@@ -308,6 +308,29 @@ int ref_launch_edm(int kind, int64_t n, int64_t rho, int64_t T, uint64_t seed, d
     });
 }
 
+// verify_sweep + csv_measure (mode 0) or analyze_sweep + csv_analyze (mode 1)
+// over an n-range literal (report.hpp:73-110, 324-412). Writes up to cap bytes,
+// *len = the full text length; witnesses of failed rows as "n:(x,y[,z])xM;".
+int ref_csv_sweep(int kind, int m, const char* nrange, int64_t rho, int64_t T, int mode, char* out,
+                  uint64_t cap, uint64_t* len, char* witnesses, uint64_t wcap) {
+    return guarded([&] {
+        auto ns = expand_n_range(parse_n_range(nrange));
+        auto rows = mode == 0 ? verify_sweep(kind_of(kind), m, ns, rho, T) : analyze_sweep(kind_of(kind), m, ns, rho, T);
+        std::string text = mode == 0 ? csv_measure(rows) : csv_analyze(rows);
+        *len = text.size();
+        std::memcpy(out, text.data(), std::min<uint64_t>(cap, text.size()));
+        std::string w;
+        if (mode == 0)
+            for (const auto& r : rows)
+                if (!r.exact) w += std::to_string(r.n) + ":" + witness_text(r) + "x" + std::to_string(r.multiplicity) + ";";
+        if (witnesses && wcap) {
+            std::size_t k = std::min<std::size_t>(wcap - 1, w.size());
+            std::memcpy(witnesses, w.data(), k);
+            witnesses[k] = 0;
+        }
+    });
+}
+
 // simplex_grid_state<T>::hash (simulator.hpp:68-73) over raw cell bytes.
 uint64_t ref_state_hash(int m, int64_t side, const void* bytes, uint64_t nbytes) {
     u64 h = fnv1a_seed;

@@ -826,6 +826,38 @@ int smx_bits_run(const smx_grid* g, uint32_t* bits_a, uint32_t* bits_b, int64_t 
     return bits_engine(g, k, bits_a, bits_b, ta, tb, steps, (cudaStream_t)stream);
 }
 
+int smx_verify_cover(const uint32_t* coverage, uint64_t ncells, int device_ptr, uint64_t* first_bad,
+                     uint32_t* multiplicity, void* stream) {
+    if (!first_bad) return fail(SMX_EINVAL, "null output");
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint32_t* d = coverage;
+    if (!device_ptr) {
+        void* p;
+        if (int rc = pool_get(0, ncells * 4, &p)) return rc;
+        TRY(cudaMemcpyAsync(p, coverage, ncells * 4, cudaMemcpyHostToDevice, s));
+        d = (const uint32_t*)p;
+    }
+    void* pctl;
+    if (int rc = pool_get(6, 64, &pctl)) return rc;
+    unsigned long long* first = (unsigned long long*)pctl + 4;  // words 0..3: the CA engine's control
+    const unsigned long long init = ncells;
+    TRY(cudaMemcpyAsync(first, &init, 8, cudaMemcpyHostToDevice, s));
+    if (ncells) smx::launch_first_defect(d, ncells, first, s);
+    TRY(cudaGetLastError());
+    unsigned long long h = ncells;
+    TRY(cudaMemcpyAsync(&h, first, 8, cudaMemcpyDeviceToHost, s));
+    TRY(cudaStreamSynchronize(s));
+    *first_bad = h;
+    if (multiplicity) {
+        *multiplicity = 1;
+        if (h < ncells) {
+            if (device_ptr) TRY(cudaMemcpy(multiplicity, d + h, 4, cudaMemcpyDeviceToHost));
+            else *multiplicity = coverage[h];
+        }
+    }
+    return SMX_OK;
+}
+
 int smx_make_edm_points(int64_t count, uint64_t seed, double* out_xy) {
     if (count < 0) return fail(SMX_EINVAL, "make_edm_points: count must be >= 0");
     if (count > 0 && !out_xy) return fail(SMX_EINVAL, "null output");

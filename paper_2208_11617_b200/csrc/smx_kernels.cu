@@ -312,6 +312,27 @@ __global__ void k_tiles_unpack(Geom g, uint8_t* __restrict__ cells, const int* _
 }
 
 // ---------------------------------------------------------------------------
+// verify_exact_cover on the device (simulator.hpp:467-478): the first packed
+// index whose multiplicity is not 1 (ncells when the cover is exact).
+__global__ void k_first_defect(const uint32_t* __restrict__ cov, unsigned long long n,
+                               unsigned long long* __restrict__ first) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        if (__ldg(cov + i) != 1u) {
+            atomicMin(first, i);
+            return;  // later indices of this thread cannot be smaller
+        }
+    }
+}
+
+void launch_first_defect(const uint32_t* cov, unsigned long long n, unsigned long long* first, cudaStream_t s) {
+    unsigned long long blocks = (n + 255) / 256;
+    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    if (blocks == 0) blocks = 1;
+    k_first_defect<<<(unsigned)blocks, 256, 0, s>>>(cov, n, first);
+}
+
+// ---------------------------------------------------------------------------
 // Launchers.
 static dim3 block_shape(const Geom& g) {
     const int bx = g.rho < 1024 ? g.rho : 1024;

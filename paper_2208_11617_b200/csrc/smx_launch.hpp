@@ -35,6 +35,8 @@ cudaError_t launch_ca_bits_run(const Geom& g, const void* tmA, const void* tmB, 
 // 2-simplex EDM (f64 points as x, y pairs) and periodic 2-D Life (smx_kernels2d.cu)
 void launch_edm(const Geom& g, const double* pts, double* cells, int exec, cudaStream_t s);
 void launch_ca2d(const Geom& g, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s);
+// first packed index with coverage != 1 (atomicMin into *first, preset to n)
+void launch_first_defect(const uint32_t* cov, unsigned long long n, unsigned long long* first, cudaStream_t s);
 void launch_tiles_pack(const Geom& g, const uint8_t* cells, const int* tiles, unsigned long long ntiles,
                        uint8_t* out, cudaStream_t s);
 void launch_tiles_unpack(const Geom& g, uint8_t* cells, const int* tiles, unsigned long long ntiles,
