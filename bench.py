@@ -482,6 +482,70 @@ def extra_configs(api, flush, sampler, peak, args):
     del c5r4
     torch.cuda.empty_cache()
     out["map_kernel_3d"] = map_pair(3, 256)
+    out.update(next_rows(api, flush, peak, K))
+    return out
+
+
+def next_rows(api, flush, peak, K):
+    """SURVEY 8(f) rows at 1 GPU: general-n H (trapezoid bands / padded) ACCUM
+    at the C3 scale, EDM (f64, 8 B written per cell) and the periodic 2-D Life
+    step through H2D vs BB, and the GPU cover-verification sweep."""
+    import torch
+    out = {}
+
+    def timed(fn, iters):
+        timed_steps(lambda i: fn(), 2, flush)
+        return statistics.mean(timed_steps(lambda i: fn(), iters, flush))
+
+    acc = {}
+    for name, g in (("trapezoid_n4097_T4", api.make_grid(api.map_kind.h2d_trapezoid, 2, 4097, 16, 4)),
+                    ("padded_n3000", api.make_grid(api.map_kind.h2d_padded, 2, 3000, 16)),
+                    ("bb_n3000", api.make_grid(api.map_kind.bb, 2, 3000, 16))):
+        cells = api.tri_cells(g.cell_side())
+        a = torch.zeros(cells, dtype=torch.int32, device="cuda")
+        ms = timed(lambda: api.accum_device(g, a, 1, api.EXEC_RUNS), K)
+        acc[name] = {"side": g.cell_side(), "cells": cells, "gcells_s": round(gcells(cells, ms), 2),
+                     "roofline_frac": round(8.0 * cells / (ms * 1e-3) / 1e9 / peak, 4)}
+        del a
+        torch.cuda.empty_cache()
+    out["F1_general_n_accum"] = acc
+
+    gh, gb = api.make_grid(api.map_kind.h2d, 2, 1024, 16), api.make_grid(api.map_kind.bb, 2, 1023, 16)
+    side = gh.cell_side()
+    cells = api.tri_cells(side)
+    pts = torch.from_numpy(api.make_edm_points(side, 7)).cuda()
+    e = torch.empty(cells, dtype=torch.float64, device="cuda")
+    edm = {"side": side, "cells": cells}
+    for ex_name, ex in (("runs", api.EXEC_RUNS), ("block", api.EXEC_BLOCK)):
+        mh = timed(lambda: api.edm_device(gh, pts, e, ex), K)
+        mb = timed(lambda: api.edm_device(gb, pts, e, ex), K)
+        edm[ex_name] = {"h_gcells_s": round(gcells(cells, mh), 2), "bb_gcells_s": round(gcells(cells, mb), 2),
+                        "h_vs_bb": round(mb / mh, 3),
+                        "h_roofline_frac": round(8.0 * cells / (mh * 1e-3) / 1e9 / peak, 4)}
+    del e
+    torch.cuda.empty_cache()
+    out["F2_edm_n1024"] = edm
+
+    a = torch.empty(cells, dtype=torch.uint8, device="cuda")
+    b = torch.empty_like(a)
+    api.life_init_device(2, side, SEED, a)
+    ca = {"side": side, "cells": cells}
+    for ex_name, ex in (("runs", api.EXEC_RUNS), ("block", api.EXEC_BLOCK)):
+        mh = timed(lambda: api.ca_step_device(gh, a, b, ex), K)
+        mb = timed(lambda: api.ca_step_device(gb, a, b, ex), K)
+        ca[ex_name] = {"h_gcells_s": round(gcells(cells, mh), 2), "bb_gcells_s": round(gcells(cells, mb), 2),
+                       "h_vs_bb": round(mb / mh, 3),
+                       "h_roofline_frac": round(2.0 * cells / (mh * 1e-3) / 1e9 / peak, 4)}
+    del a, b
+    torch.cuda.empty_cache()
+    out["F3_ca2d_periodic_n1024"] = ca
+
+    from paper_2208_11617_b200 import report as rp
+    t0 = time.perf_counter()
+    rows = rp.verify_sweep(api.map_kind.h2d_trapezoid, 2, list(range(2, 4097)), 1, 4)
+    out["F4_verify_sweep"] = {"sweep": "verify_sweep(trapezoid, m=2, n=2..4096, T=4) on the GPU",
+                              "grids": len(rows), "all_exact": all(r.exact for r in rows),
+                              "seconds": round(time.perf_counter() - t0, 2)}
     return out
 
 
