@@ -389,8 +389,10 @@ __global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_
 // the steps over that list (every warp takes items round-robin, so consecutive
 // items — spatial neighbours — run concurrently) with a grid barrier between
 // steps. No per-step launch or re-mapping; the chain-building cost is paid once.
+constexpr int PLAN_THREADS = 512;
+
 template <int KIND, int RHO>
-__global__ void __launch_bounds__(NTHR) k_ca_plan(Geom g, int wz0, int wz1, int P, int NZ, Chunk* __restrict__ out,
+__global__ void __launch_bounds__(PLAN_THREADS) k_ca_plan(Geom g, int wz0, int wz1, int P, int NZ, Chunk* __restrict__ out,
                                                   unsigned* __restrict__ count) {
     using C = Cfg<RHO>;
     const int NBP = P * P * NZ;
@@ -483,10 +485,14 @@ void launch_t(const Geom& g, int wz0, int wz1, const CUtensorMap& tmap, uint32_t
 template <int KIND, int RHO>
 void launch_plan_t(const Geom& g, void* chunks, unsigned* count, cudaStream_t s) {
     using C = Cfg<RHO>;
-    const int P = C::LMAX, NZ = 1;  // longest chains; the plan kernel is cheap
+    // Chains stop at patch edges. H3D: 32 x 32 patches (32 divides the n/2
+    // extents, so the hinge fold and the slab levels fragment least: H3D(128)
+    // 36.3 K chunks vs 40.7 K at P = 12); BB: P = LMAX (rows of the box are
+    // unbroken chains, cut every LMAX tiles anyway). 512 threads map a patch.
+    const int P = KIND == SMX_H3D ? 32 : C::LMAX, NZ = 1;
     const dim3 grid((g.ex + P - 1) / P, (g.ey + P - 1) / P, g.ez);
-    k_ca_plan<KIND, RHO><<<grid, NTHR, 2 * P * P * NZ * 16 + 16, s>>>(g, 0, g.ez, P, NZ,
-                                                                      reinterpret_cast<Chunk*>(chunks), count);
+    k_ca_plan<KIND, RHO><<<grid, PLAN_THREADS, 2 * P * P * NZ * 16 + 16, s>>>(g, 0, g.ez, P, NZ,
+                                                                              reinterpret_cast<Chunk*>(chunks), count);
 }
 
 template <int RHO>
