@@ -483,7 +483,37 @@ def extra_configs(api, flush, sampler, peak, args):
     torch.cuda.empty_cache()
     out["map_kernel_3d"] = map_pair(3, 256)
     out.update(next_rows(api, flush, peak, K))
+    out["cpu_reference"] = cpu_reference_rows()
     return out
+
+
+def cpu_reference_rows():
+    """The reference's own launch_* (oracle/_ref, Release flags) on one host
+    core, bounded samples beside the GPU configs (Gcells/s per call)."""
+    try:
+        from oracle.oracle import H2D, H3D, Reference, reference_available
+        if not reference_available():
+            return {"unavailable": "oracle/_ref not built"}
+        R = Reference()
+        out = {}
+        _, cnt, _, secs = R.launch_accum(H2D, 2, 1024, 16, passes=1)
+        out["accum_C1_h2d1024_rho16"] = {"gcells_s": round(cnt[3] / secs / 1e9, 4), "seconds": round(secs, 3)}
+        t0 = time.perf_counter()
+        _, cnt, _ = R.launch_edm(H2D, 1024, 4, 7)
+        dt = time.perf_counter() - t0
+        out["edm_h2d1024_rho4"] = {"gcells_s": round(cnt[3] / dt / 1e9, 4), "seconds": round(dt, 3),
+                                   "note": "side 4092 sample (the GPU row is side 16368)"}
+        s = R.make_life_state(2, 1023, SEED)
+        _, cnt, _, secs = R.launch_ca(H2D, 2, 1024, 1, 1, s)
+        out["ca2d_periodic_h2d1024_1step"] = {"gcells_s": round(cnt[3] / secs / 1e9, 4), "seconds": round(secs, 3),
+                                              "note": "side 1023 sample"}
+        s = R.make_life_state(3, 252, SEED)
+        _, cnt, _, secs = R.launch_ca(H3D, 3, 64, 4, 1, s)
+        out["ca3d_C2_1step"] = {"gcells_s": round(cnt[3] / secs / 1e9, 6), "seconds": round(secs, 3)}
+        out["cores"] = 1
+        return out
+    except Exception as e:  # pragma: no cover
+        return {"unavailable": str(e)}
 
 
 def next_rows(api, flush, peak, K):
