@@ -105,6 +105,39 @@ __global__ void k_ca2d_block(Geom g, const uint8_t* __restrict__ cur, uint8_t* _
         }
 }
 
+// bytes [a, a + 4) of a u8 array through aligned 32-bit loads (the packed rows
+// have arbitrary byte alignment)
+__device__ __forceinline__ void load8(const uint8_t* __restrict__ p, unsigned long long a, uint32_t& lo,
+                                      uint32_t& hi) {
+    const unsigned long long b = a & ~3ull;
+    const uint32_t* q = reinterpret_cast<const uint32_t*>(p + b);
+    const uint32_t w0 = __ldg(q), w1 = __ldg(q + 1), w2 = __ldg(q + 2);
+    const int sh = int(a - b) * 8;
+    lo = __funnelshift_r(w0, w1, sh);
+    hi = __funnelshift_r(w1, w2, sh);
+}
+
+// exact per-byte "== 0" for bytes < 0x80: bit 7 of each byte
+__device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {
+    return ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;
+}
+
+// 3 cells' horizontal sums of one row, for the 4 cells x .. x+3 (bytes x-1 .. x+4
+// at packed index a = row + x - 1): left + centre + right, <= 3 per byte
+__device__ __forceinline__ uint32_t hsum4(const uint8_t* __restrict__ cur, unsigned long long a, uint32_t* centre) {
+    uint32_t L, H;
+    load8(cur, a, L, H);
+    const uint32_t C = __funnelshift_r(L, H, 8), R = __funnelshift_r(L, H, 16);
+    if (centre) *centre = C;
+    return L + C + R;
+}
+
+// periodic 2-D Life, x-run scheme: a warp per cell row of a run; lane per
+// 4-byte-aligned output word. Interior words (no wrap, every neighbour row
+// long enough) are computed SWAR: three rows' horizontal sums added bytewise
+// (<= 9 per byte), B3/S23 as (S == 3) | (alive & S == 4) with an exact
+// per-byte zero test; wrap-around, row-end and partial words fall back to the
+// per-cell rule.
 template <int KIND>
 __global__ void __launch_bounds__(T2_THREADS) k_ca2d_runs(Geom g, const uint8_t* __restrict__ cur,
                                                           uint8_t* __restrict__ next) {
@@ -117,8 +150,32 @@ __global__ void __launch_bounds__(T2_THREADS) k_ca2d_runs(Geom g, const uint8_t*
     for (int rr = warp; rr < rows; rr += T2_THREADS / 32) {
         int cy, xlo, xhi;
         if (!run_row(s_run, rr, g.rho, S, &cy, &xlo, &xhi)) continue;
-        const unsigned long long base = tri_idx(0, cy);
-        for (int x = xlo + lane; x < xhi; x += 32) next[base + x] = life2d_cell(cur, S, x, cy);
+        const unsigned long long R = tri_idx(0, cy);
+        const unsigned long long E0 = R + xlo, E1 = R + xhi;
+        const unsigned long long A0 = (E0 + 3) & ~3ull, A1 = E1 & ~3ull;
+        const bool yin = cy >= 1 && cy <= S - 2;  // no vertical wrap
+        const unsigned long long Rm = yin ? tri_idx(0, cy - 1) : 0, Rp = yin ? tri_idx(0, cy + 1) : 0;
+        if (A0 < A1) {
+            for (unsigned long long A = A0 + 4ull * lane; A < A1; A += 128) {
+                const int x = int(A - R);
+                if (yin && x >= 1 && x + 4 <= cy - 1) {
+                    uint32_t self;
+                    const uint32_t t = hsum4(cur, Rm + x - 1, nullptr) + hsum4(cur, R + x - 1, &self) +
+                                       hsum4(cur, Rp + x - 1, nullptr);
+                    const uint32_t eq3 = zero_bytes(t ^ 0x03030303u), eq4 = zero_bytes(t ^ 0x04040404u);
+                    *reinterpret_cast<uint32_t*>(next + A) = ((eq3 | (eq4 & (self << 7))) >> 7) & 0x01010101u;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) next[A + j] = life2d_cell(cur, S, x + j, cy);
+                }
+            }
+            // head [E0, A0) and tail [A1, E1): at most 3 + 3 cells
+            const int nh = int(A0 - E0), nt = int(E1 - A1);
+            if (lane < nh) next[E0 + lane] = life2d_cell(cur, S, xlo + lane, cy);
+            else if (lane >= 8 && lane - 8 < nt) next[A1 + lane - 8] = life2d_cell(cur, S, int(A1 - R) + lane - 8, cy);
+        } else {
+            for (int x = xlo + lane; x < xhi; x += 32) next[R + x] = life2d_cell(cur, S, x, cy);
+        }
     }
 }
 
