@@ -52,7 +52,9 @@ constexpr int BOXW = 12;
 constexpr int NWARP = 4;  // warps per CTA
 constexpr int NTHR = NWARP * 32;
 
-template <int RHO>
+// CPIX: chunks per warp item (default: as many as the 32 lanes can march, 32 /
+// (4 rho)); the persistent small-grid runs use 1 to halve an item's latency.
+template <int RHO, int CPIX = 32 / (RHO * 4)>
 struct Cfg {
     static constexpr int LMAX = OWN / RHO;              // tiles per chunk
     static constexpr int P = LMAX;                      // patch edge (blocks)
@@ -60,7 +62,8 @@ struct Cfg {
     static constexpr int NB = P * P * NZ;               // max blocks per CTA
     static constexpr int HL = RHO + 2;                  // halo layers == halo rows per layer
     static constexpr int LPC = RHO * 4;                 // compute lanes per chunk
-    static constexpr int CPI = 32 / LPC;                // chunks per warp item
+    static constexpr int CPI = CPIX;                    // chunks per warp item
+    static_assert(CPI >= 1 && CPI * LPC <= 32, "an item's chunks must fit the warp's lanes");
     static constexpr int BOXB = HL * HL * BOXW * 4;     // bytes per TMA box (one per chunk)
     static constexpr int SLOT = (BOXB + 127) & ~127;    // 128B-aligned slot per box
     static constexpr int BUF = CPI * SLOT;              // one buffer: the boxes of an item
@@ -236,10 +239,10 @@ __global__ void __launch_bounds__(256) k_unpack_bits(const uint32_t* __restrict_
 
 // TMA issue for one warp item (lane 0): one 3-D box (12 words x rho+2 rows x
 // rho+2 layers) per chunk; out-of-range coordinates land as zeros.
-template <int RHO>
+template <int RHO, int CPIX>
 __device__ __forceinline__ void issue_item(const CUtensorMap* tm, const Chunk* s_chunk, int nchunks, int item,
                                            uint8_t* buf, uint32_t mbar) {
-    using C = Cfg<RHO>;
+    using C = Cfg<RHO, CPIX>;
     const int nc = min(C::CPI, nchunks - item * C::CPI);
     mbar_expect_tx(mbar, uint32_t(nc * C::BOXB));
     for (int c = 0; c < nc; ++c) {
@@ -257,11 +260,11 @@ __device__ __forceinline__ void issue_item(const CUtensorMap* tm, const Chunk* s
 // form the horizontal 3-sums as bit-planes, then lane (ly, w) marches z and
 // writes whole 32-bit words of the next bit shadow. `phases` carries the two
 // mbarriers' parities across calls (the persistent kernel reuses them).
-template <int RHO>
+template <int RHO, int CPIX = 32 / (RHO * 4)>
 __device__ __forceinline__ void run_items(const Chunk* __restrict__ s_chunk, int nchunks, int item0, int istride,
                                           const CUtensorMap* tm, uint32_t* __restrict__ nbits, int S, int WP,
                                           uint8_t* wbase, uint32_t mbar0, uint32_t& phases) {
-    using C = Cfg<RHO>;
+    using C = Cfg<RHO, CPIX>;
     constexpr int HL = C::HL;
     const int lane = threadIdx.x & 31;
     uint32_t* sH = reinterpret_cast<uint32_t*>(wbase + 2 * C::BUF);  // [HROWS][8]: h0 w0..3, h1 w0..3
@@ -269,13 +272,13 @@ __device__ __forceinline__ void run_items(const Chunk* __restrict__ s_chunk, int
     int item = item0, b = 0;
     if (item < nitems && lane == 0) {
         fence_proxy_async();
-        issue_item<RHO>(tm, s_chunk, nchunks, item, wbase, mbar0);
+        issue_item<RHO, CPIX>(tm, s_chunk, nchunks, item, wbase, mbar0);
     }
     for (; item < nitems; item += istride, b ^= 1) {
         const int nxt = item + istride;
         if (nxt < nitems && lane == 0) {
             fence_proxy_async();
-            issue_item<RHO>(tm, s_chunk, nchunks, nxt, wbase + (b ^ 1) * C::BUF, mbar0 + 8 * (b ^ 1));
+            issue_item<RHO, CPIX>(tm, s_chunk, nchunks, nxt, wbase + (b ^ 1) * C::BUF, mbar0 + 8 * (b ^ 1));
         }
         while (!mbar_try_wait(mbar0 + 8 * b, (phases >> b) & 1u)) {
         }
@@ -326,10 +329,11 @@ __device__ __forceinline__ void run_items(const Chunk* __restrict__ s_chunk, int
             const int cl = lane / C::LPC, l = lane % C::LPC;
             const int ly = l >> 2, w = l & 3;
             const int ci = item * C::CPI + cl;
-            const bool cvalid = ci < nchunks;
+            const bool cvalid = cl < C::CPI && ci < nchunks;
             const Chunk ch = cvalid ? s_chunk[ci] : Chunk{0, 0, 0, 0};
-            const uint32_t* H = sH + 8 * (cl * HL * HL);
-            const uint8_t* cbuf = buf + cl * C::SLOT;
+            const int cs = cl < C::CPI ? cl : 0;  // idle lanes (cl >= CPI) read slot 0, never store
+            const uint32_t* H = sH + 8 * (cs * HL * HL);
+            const uint8_t* cbuf = buf + cs * C::SLOT;
             auto vsum = [&](int zi) {
                 const int r0 = zi * HL + ly;
                 return add3x2(H[8 * r0 + w], H[8 * r0 + 4 + w], H[8 * (r0 + 1) + w], H[8 * (r0 + 1) + 4 + w],
@@ -407,38 +411,50 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_ca_plan(Geom g, int wz0, int w
     for (int i = threadIdx.x; i < n; i += blockDim.x) out[s_base + i] = s_chunk[i];
 }
 
-// all CTAs co-resident (cooperative launch); bar[0] = arrivals, bar[1] = generation
+// all CTAs co-resident (cooperative launch); bar[0] = arrivals, bar[1] = generation.
+// One thread per CTA: a release add on the arrival counter (orders this CTA's
+// step writes, made visible to the async proxy first); the last arriver resets
+// the counter and bumps the generation with release; the others spin with
+// acquire loads. Then the CTA re-syncs and fences toward the async proxy so
+// the next step's TMA loads see every CTA's writes.
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
-    // generic-proxy writes of this step must be visible to the next step's TMA reads
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned* gen = bar + 1;
-        const unsigned g0 = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == nblocks - 1) {
-            bar[0] = 0;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
+        unsigned g0, old;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(g0) : "l"(bar + 1) : "memory");
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;\n" : "=r"(old) : "l"(bar) : "memory");
+        if (old == nblocks - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;\n" ::"l"(bar) : "memory");
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar + 1) : "memory");
         } else {
-            while (*gen == g0) {
-            }
+            unsigned g;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(g) : "l"(bar + 1) : "memory");
+            } while (g == g0);
         }
-        __threadfence();
     }
     __syncthreads();
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
 
-constexpr int RUN_NWARP = 16;  // persistent kernel: one 16-warp CTA per SM (fewer barrier arrivals)
+// persistent kernel: one 16-warp CTA per SM (fewer barrier arrivals), the
+// default chunks per item (measured: 1 chunk per item with 32 warps per SM is
+// 8 % slower at C2 — the per-item fixed costs dominate there)
+template <int RHO>
+struct RunCfg {
+    static constexpr int NW = 16;
+    static constexpr int CPIX = 32 / (RHO * 4);
+};
 
 template <int RHO>
-__global__ void __launch_bounds__(RUN_NWARP * 32) k_ca_bits_run(const __grid_constant__ CUtensorMap tmA,
+__global__ void __launch_bounds__(RunCfg<RHO>::NW * 32) k_ca_bits_run(const __grid_constant__ CUtensorMap tmA,
                                                       const __grid_constant__ CUtensorMap tmB, uint32_t* bitsA,
                                                       uint32_t* bitsB, const Chunk* __restrict__ chunks,
                                                       const unsigned* __restrict__ count, int steps, int S, int WP,
                                                       unsigned* bar) {
-    using C = Cfg<RHO>;
+    using C = Cfg<RHO, RunCfg<RHO>::CPIX>;
+    constexpr int RUN_NWARP = RunCfg<RHO>::NW;
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint8_t* wbase = smem + warp * C::WARP_BYTES;
@@ -454,7 +470,7 @@ __global__ void __launch_bounds__(RUN_NWARP * 32) k_ca_bits_run(const __grid_con
     uint32_t phases = 0u;
     for (int st = 0; st < steps; ++st) {
         const bool even = (st & 1) == 0;
-        run_items<RHO>(chunks, nchunks, gwarp, nwarps, even ? &tmA : &tmB, even ? bitsB : bitsA, S, WP, wbase,
+        run_items<RHO, RunCfg<RHO>::CPIX>(chunks, nchunks, gwarp, nwarps, even ? &tmA : &tmB, even ? bitsB : bitsA, S, WP, wbase,
                        mbar0, phases);
         if (st + 1 < steps) grid_barrier(bar, gridDim.x);
     }
@@ -498,7 +514,8 @@ void launch_plan_t(const Geom& g, void* chunks, unsigned* count, cudaStream_t s)
 template <int RHO>
 cudaError_t launch_run_t(const Geom& g, const CUtensorMap& tA, const CUtensorMap& tB, uint32_t* A, uint32_t* B,
                          const void* chunks, const unsigned* count, int steps, unsigned* bar, cudaStream_t s) {
-    using C = Cfg<RHO>;
+    using C = Cfg<RHO, RunCfg<RHO>::CPIX>;
+    constexpr int RUN_NWARP = RunCfg<RHO>::NW;
     const int smem = RUN_NWARP * C::WARP_BYTES;
     static int grid = [&] {
         cudaFuncSetAttribute(k_ca_bits_run<RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
