@@ -342,10 +342,16 @@ int ca_runs_step(const smx_grid* g, const smx::Geom& k, int64_t wz0, int64_t wz1
     void *pa, *pb;
     if (int rc = pool_get(3, bits_bytes(k.side), &pa)) return rc;
     if (int rc = pool_get(4, bits_bytes(k.side), &pb)) return rc;
-    const CUtensorMap* tm;
-    if (int rc = bits_tmap((const uint32_t*)pa, k.side, k.rho, &tm)) return rc;
+    const CUtensorMap *ta, *tb;
+    if (int rc = bits_tmap((const uint32_t*)pa, k.side, k.rho, &ta)) return rc;
     smx::launch_pack_bits(k, cur, (uint32_t*)pa, s);
-    smx::launch_ca_bits(k, g->kind, int(wz0), int(wz1), tm, (uint32_t*)pb, s);
+    if (wz0 == 0 && wz1 == k.ez) {
+        // the whole grid: the engine's plan + one persistent launch of 1 step
+        if (int rc = bits_tmap((const uint32_t*)pb, k.side, k.rho, &tb)) return rc;
+        if (int rc = bits_engine(g, k, (uint32_t*)pa, (uint32_t*)pb, ta, tb, 1, s)) return rc;
+    } else {
+        smx::launch_ca_bits(k, g->kind, int(wz0), int(wz1), ta, (uint32_t*)pb, s);
+    }
     smx::launch_unpack_bits(k, (const uint32_t*)pb, next, s);
     TRY(cudaGetLastError());
     return SMX_OK;
