@@ -476,6 +476,13 @@ def extra_configs(api, flush, sampler, peak, args):
     # rho sweep at the same n = 2048 cell scale (trade map
     # amortisation against the BB/H block ratio); r/beta are fixed at (2, 2)
     # by the executable map
+    from paper_2208_11617_b200 import analysis as A
+    ranked = A.optimize_params(3, 8, 8, 256)
+    out["C5_r_beta_sweep"] = {
+        "note": "analytical (analysis.hpp restated, exact): optimize_params(m=3, 1/r<=8, beta<=8, n_eval=256); "
+                "the executable H3D is the (2, 2) family — every other family under-covers (alpha < 0)",
+        "top": [{"inv_r": p.inv_r, "beta": p.beta, "alpha": str(r.alpha), "n0": r.n0 if r.found else None}
+                for p, r in ranked[:6]], "families": len(ranked)}
     c5r4 = engine_case(api, "h3d", 512, 4, 20, 3, 1, flush)
     out["C5_rho4_engine"] = {"grid": "h3d(512) rho=4", "side": c5r4["side"], "cells": c5r4["cells"],
                              "h_gcell_steps_s": round(gcells(c5r4["cells"] * 20, statistics.mean(c5r4["ms"])), 2)}

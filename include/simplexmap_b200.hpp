@@ -186,6 +186,24 @@ inline grid_spec grid_bb(i64 n, int m) {
 }
 inline grid_spec grid_h2d(i64 n) { return make_grid(map_kind::h2d, 2, n); }
 inline grid_spec grid_h3d(i64 n) { return make_grid(map_kind::h3d, 3, n); }
+// self_similar_params (analysis.hpp:21-33): the executable H maps are the
+// halving family; the r/beta overload accepts (1/r, beta) = (2, 2) only
+// (SURVEY 8(b)); the analysis itself is paper_2208_11617_b200/analysis.py.
+struct self_similar_params {
+    i64 inv_r = 2, beta = 2;
+    int m = 2;
+    self_similar_params() = default;
+    self_similar_params(i64 inv_r_, i64 beta_, int m_) : inv_r(inv_r_), beta(beta_), m(m_) {
+        if (m < 1) throw std::invalid_argument("self_similar_params: m must be >= 1");
+        if (beta <= 1) throw std::invalid_argument("self_similar_params: beta must be > 1");
+        if (inv_r < beta) throw std::invalid_argument("self_similar_params: 1/r must be >= beta");
+    }
+};
+inline grid_spec grid_h3d(i64 n, const self_similar_params& p) {
+    if (p.inv_r != 2 || p.beta != 2)
+        throw std::invalid_argument("map_h3d: the executable map is the halving family (1/r, beta) = (2, 2)");
+    return grid_h3d(n);
+}
 inline grid_spec grid_rb(i64 n) { return make_grid(map_kind::rb, 2, n); }
 inline grid_spec grid_lambda(i64 n) { return make_grid(map_kind::lambda2d, 2, n); }
 inline grid_spec grid_h2d_padded(i64 n) { return make_grid(map_kind::h2d_padded, 2, n); }

@@ -225,6 +225,8 @@ class Reference:
         L.ref_kernel_edm.argtypes = [C.c_int64, C.c_uint64, _f64p, C.c_uint64, _u64p]
         L.ref_launch_edm.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, _f64p, C.c_uint64,
                                      _u64p, _u64p]
+        L.ref_csv_optimize.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_char_p, C.c_uint64,
+                                       C.POINTER(C.c_uint64)]
         L.ref_csv_sweep.argtypes = [C.c_int, C.c_int, C.c_char_p, C.c_int64, C.c_int64, C.c_int, C.c_char_p,
                                     C.c_uint64, C.POINTER(C.c_uint64), C.c_char_p, C.c_uint64]
         self.L = L
@@ -245,6 +247,16 @@ class Reference:
         out = np.zeros((blocks, 6), np.int64)
         self._ok(self.L.ref_map_outcomes_t(kind, m, n, T, out, blocks), "map_outcomes")
         return out
+
+    def csv_optimize(self, m: int, inv_r_max: int, beta_max: int, n_eval: int) -> str:
+        cap = 1 << 20
+        buf = C.create_string_buffer(cap)
+        n = C.c_uint64(0)
+        rc = self.L.ref_csv_optimize(m, inv_r_max, beta_max, n_eval, buf, cap, C.byref(n))
+        if rc == 1:
+            raise ValueError(self.L.ref_last_error().decode())
+        self._ok(rc, "csv_optimize")
+        return buf.raw[:n.value].decode()
 
     def csv_sweep(self, kind: int, m: int, nrange: str, rho: int = 1, T: int = 1, analyze: bool = False):
         """verify_sweep + csv_measure (or analyze_sweep + csv_analyze); -> (text, witnesses)"""

@@ -331,6 +331,16 @@ int ref_csv_sweep(int kind, int m, const char* nrange, int64_t rho, int64_t T, i
     });
 }
 
+// csv_optimize(optimize_params(m, inv_r_max, beta_max, n_eval), n_eval) (report.hpp:448-472)
+int ref_csv_optimize(int m, int64_t inv_r_max, int64_t beta_max, int64_t n_eval, char* out, uint64_t cap,
+                     uint64_t* len) {
+    return guarded([&] {
+        std::string text = csv_optimize(optimize_params(m, inv_r_max, beta_max, n_eval), n_eval);
+        *len = text.size();
+        std::memcpy(out, text.data(), std::min<uint64_t>(cap, text.size()));
+    });
+}
+
 // simplex_grid_state<T>::hash (simulator.hpp:68-73) over raw cell bytes.
 uint64_t ref_state_hash(int m, int64_t side, const void* bytes, uint64_t nbytes) {
     u64 h = fnv1a_seed;

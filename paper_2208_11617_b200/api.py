@@ -163,7 +163,13 @@ def grid_h2d(n: int) -> grid_spec:
     return make_grid(map_kind.h2d, 2, n)
 
 
-def grid_h3d(n: int) -> grid_spec:
+def grid_h3d(n: int, params=None) -> grid_spec:
+    """grid_h3d (maps.hpp:285-295). `params` (analysis.self_similar_params,
+    optional): the executable map is the (1/r, beta) = (2, 2) family; any other
+    raises InvalidArgument."""
+    if params is not None:
+        from .analysis import check_executable
+        check_executable(params)
     return make_grid(map_kind.h3d, 3, n)
 
 

@@ -128,6 +128,10 @@ static void general_n_suite() {
 
 static void host_suite() {
     general_n_suite();
+    // self_similar_params on the 3-D path (analysis.hpp:27-32)
+    CHECK(grid_h3d(64, self_similar_params(2, 2, 3)).blocks() == 49152);
+    CHECK_THROWS_AS(grid_h3d(64, self_similar_params(3, 3, 3)), std::invalid_argument);
+    CHECK_THROWS_AS(self_similar_params(2, 3, 3), std::invalid_argument);
     // test_maps.cpp "bounding box map"
     CHECK(map_bb({1, 3, 0}, 8, 2).target == (data_coord{1, 3, 0}));
     CHECK(!map_bb({1, 3, 0}, 8, 2).is_void);
