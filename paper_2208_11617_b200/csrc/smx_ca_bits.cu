@@ -68,7 +68,11 @@ struct Cfg {
     static constexpr int SLOT = (BOXB + 127) & ~127;    // 128B-aligned slot per box
     static constexpr int BUF = CPI * SLOT;              // one buffer: the boxes of an item
     static constexpr int HROWS = CPI * HL * HL;         // halo rows per item
-    static constexpr int WARP_BYTES = (2 * BUF + HROWS * 32 + 64 + 127) & ~127;  // TMA dst: 128B aligned
+    // per warp: 2 TMA buffers | h-sums | mbarriers (64 B) | a cached chunk list
+    // (the persistent kernel's items when a warp owns <= LIST_ITEMS of them)
+    static constexpr int LIST_ITEMS = 8;
+    static constexpr int LIST_OFF = 2 * BUF + HROWS * 32 + 64;
+    static constexpr int WARP_BYTES = (LIST_OFF + LIST_ITEMS * CPI * 16 + 127) & ~127;  // TMA dst: 128B aligned
     static int smem(int nb) { return NWARP * WARP_BYTES + nb * 32 + 128; }
 };
 
@@ -467,11 +471,36 @@ __global__ void __launch_bounds__(RunCfg<RHO>::NW * 32) k_ca_bits_run(const __gr
     __syncthreads();
     const int nchunks = int(*count);
     const int gwarp = blockIdx.x * RUN_NWARP + warp, nwarps = gridDim.x * RUN_NWARP;
+    // A warp runs the same items every step. When it owns few (small grids),
+    // copy their chunks once into its smem list, so no step waits on a global
+    // read of a chunk before issuing its TMA box.
+    const Chunk* src = chunks;
+    int nsrc = nchunks, i0 = gwarp, istr = nwarps;
+    {
+        const int nitems = (nchunks + C::CPI - 1) / C::CPI;
+        const int mine = gwarp < nitems ? (nitems - 1 - gwarp) / nwarps + 1 : 0;
+        if (mine <= C::LIST_ITEMS) {
+            Chunk* loc = reinterpret_cast<Chunk*>(wbase + C::LIST_OFF);
+            int nloc = 0;
+            for (int k = 0; k < mine * C::CPI; ++k) {
+                const int ci = (gwarp + (k / C::CPI) * nwarps) * C::CPI + k % C::CPI;
+                if (ci < nchunks) {
+                    if (lane == 0) loc[k] = chunks[ci];
+                    nloc = k + 1;
+                }
+            }
+            __syncwarp();
+            src = loc;
+            nsrc = nloc;
+            i0 = 0;
+            istr = 1;
+        }
+    }
     uint32_t phases = 0u;
     for (int st = 0; st < steps; ++st) {
         const bool even = (st & 1) == 0;
-        run_items<RHO, RunCfg<RHO>::CPIX>(chunks, nchunks, gwarp, nwarps, even ? &tmA : &tmB, even ? bitsB : bitsA, S, WP, wbase,
-                       mbar0, phases);
+        run_items<RHO, RunCfg<RHO>::CPIX>(src, nsrc, i0, istr, even ? &tmA : &tmB, even ? bitsB : bitsA, S, WP,
+                                          wbase, mbar0, phases);
         if (st + 1 < steps) grid_barrier(bar, gridDim.x);
     }
 }
