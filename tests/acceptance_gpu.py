@@ -1,0 +1,250 @@
+"""GPU acceptance gate — the reference's ten end-to-end criteria
+(tests/acceptance.cpp:38-120) run through this build's public
+API on the B200, one [PASS]/[FAIL] line apiece with the reference's budgets.
+Exits nonzero if any criterion fails.
+
+    python tests/acceptance_gpu.py
+
+TEST INFRASTRUCTURE: criterion 7 compares against the sequential CPU oracle
+(oracle/), as the reference's gate compares against kernel_edm / kernel_ca_run.
+Criterion 10 drops the SVG check (render.hpp is out of scope).
+"""
+from __future__ import annotations
+
+import os
+import sys
+import time
+from fractions import Fraction
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2208_11617_b200 import analysis as A  # noqa: E402
+from paper_2208_11617_b200 import api  # noqa: E402
+from paper_2208_11617_b200 import report as rp  # noqa: E402
+
+failures = 0
+
+
+def run(cid: int, label: str, budget: float, body) -> None:
+    global failures
+    t0 = time.perf_counter()
+    try:
+        ok, note = body()
+    except Exception as e:  # the reference's "unexpected exception" path
+        ok, note = False, f"unexpected exception: {type(e).__name__}: {e}"
+    dt = time.perf_counter() - t0
+    in_budget = budget <= 0 or dt < budget
+    passed = ok and in_budget
+    failures += 0 if passed else 1
+    line = f"[{'PASS' if passed else 'FAIL'}] criterion {cid}: {label} ({dt:.2f}s"
+    if budget > 0:
+        line += f", budget {budget:.0f}s"
+    line += ")"
+    if note:
+        line += " " + note
+    if not in_budget:
+        line += " [over budget]"
+    print(line, flush=True)
+
+
+def dom(g):
+    return api.simplex_spec(g.dims, g.cell_side() - 1)
+
+
+def c1():
+    r = rp.measure_grid(api.make_grid(api.map_kind.bb, 2, 1024))
+    want = Fraction(1023, 1025)
+    if not r.exact:
+        return False, "bb cover not exact"
+    if r.overhead != want:
+        return False, f"overhead {r.overhead} != {want}"
+    gap = abs(float(r.overhead) - 1.0)
+    return gap <= 0.01, f"overhead == {want}, {gap * 100:.3f}% from limit 1"
+
+
+def c2():
+    r = rp.measure_grid(api.make_grid(api.map_kind.bb, 3, 256))
+    if not r.exact:
+        return False, "bb cover not exact"
+    rel = abs(float(r.overhead) - 5.0) / 5.0
+    return rel <= 0.03, f"overhead {r.overhead} ~= {float(r.overhead):.6f}, {rel * 100:.3f}% from 5"
+
+
+def c3():
+    for k in range(1, 13):
+        n = 1 << k
+        g = api.grid_h2d(n)
+        st = api.simplex_grid_state(2, n - 1)
+        rep = api.launch_accum(g, dom(g), st, api.launch_opts(record_coverage=False))
+        if rep.blocks_void != 0:
+            return False, f"n={n}: void blocks present"
+        if rep.blocks_launched != n * (n - 1) // 2:
+            return False, f"n={n}: blocks_launched != n(n-1)/2"
+        if not (st.cells == 1).all():
+            return False, f"n={n}: cell != 1 after accum"
+    return True, "n = 2^1..2^12: every cell 1, blocks n(n-1)/2, zero void"
+
+
+def c4():
+    for T in (1, 4, 16):
+        rows = rp.verify_sweep(api.map_kind.h2d_trapezoid, 2, list(range(2, 4097)), 1, T)
+        for r in rows:
+            if len(api.decompose_trapezoids(r.n, T)) > max(1, (r.n - 1).bit_length()):
+                return False, f"n={r.n} T={T}: trapezoid count exceeds ceil(log2 n)"
+            if not r.exact:
+                return False, f"n={r.n} T={T}: cover not exact, witness {rp.witness_text(r)} x{r.multiplicity}"
+    return True, "all n in [2,4096], T in {1,4,16}: exact, count <= ceil(log2 n)"
+
+
+def c5():
+    prev, last = None, None
+    for n in (4, 8, 16, 32, 64, 128):
+        r = rp.measure_grid(api.grid_h3d(n))
+        if not r.exact:
+            return False, f"n={n}: cover not exact"
+        ratio = Fraction(r.threads_launched, r.threads_useful)
+        if not ratio > Fraction(9, 8):
+            return False, f"n={n}: ratio not above 9/8"
+        if prev is not None and not ratio < prev:
+            return False, f"n={n}: ratio not strictly decreasing"
+        prev = last = ratio
+    gap = abs(float(last) - 1.125) / 1.125
+    return gap <= 0.10, f"exact at all n; ratio(128) = {last} ~= {float(last):.6f}, decreasing toward 9/8"
+
+
+def c6():
+    P = A.self_similar_params
+    for k in range(1, 41):
+        n = 1 << k
+        if A.self_similar_volume(n, P(2, 2, 2)) != Fraction(n * (n - 1), 2):
+            return False, f"m=2 volume mismatch at n=2^{k}"
+        if A.self_similar_volume(n, P(2, 2, 3)) != Fraction(n ** 3 - n, 6):
+            return False, f"m=3 volume mismatch at n=2^{k}"
+    for m, want in ((2, 0), (3, 0), (4, Fraction(5, 7)), (5, 3), (7, 39)):
+        if A.extra_fraction_limit(m) != want:
+            return False, f"extra_fraction_limit({m}) != {want}"
+    return True, "volumes n(n-1)/2 and (n^3-n)/6 exact for n = 2^1..2^40; limits 0, 0, 5/7, 3, 39"
+
+
+def c7():
+    from oracle.oracle import Restated
+    orc = Restated()
+    for seed in (42, 0xC0FFEE):
+        for side in (63, 255, 1023):
+            want_edm = orc.kernel_edm(side, seed)
+            want_ca = orc.make_life_state(2, side, seed)
+            orc.ca2d_run(side, 64, want_ca)
+            pts = api.make_edm_points(side, seed)
+            for g in (api.make_grid(api.map_kind.bb, 2, side), api.make_grid(api.map_kind.rb, 2, side),
+                      api.make_grid(api.map_kind.lambda2d, 2, side), api.make_grid(api.map_kind.h2d, 2, side + 1),
+                      api.make_grid(api.map_kind.h2d_trapezoid, 2, side + 1, 1, 1)):
+                st = api.simplex_grid_state(2, side, np.float64)
+                api.launch_edm(g, dom(g), pts, st, api.launch_opts(record_coverage=False))
+                if not (st.cells == want_edm).all():
+                    return False, f"edm mismatch, side {side} map {api.map_kind_name(g.kind)}"
+                ca = api.make_life_state(2, side, seed)
+                api.launch_ca(g, dom(g), ca, api.launch_opts(steps=64, record_coverage=False))
+                if not (ca.cells == want_ca).all():
+                    return False, f"ca mismatch, side {side} map {api.map_kind_name(g.kind)}"
+        for side in (15, 31, 63):
+            want = orc.make_life_state(3, side, seed)
+            orc.ca3d_run(side, 64, want)
+            for g in (api.make_grid(api.map_kind.bb, 3, side), api.make_grid(api.map_kind.h3d, 3, side + 1)):
+                ca = api.make_life_state(3, side, seed)
+                api.launch_ca(g, dom(g), ca, api.launch_opts(steps=64, boundary=api.ca_boundary.dead3d,
+                                                             record_coverage=False))
+                if not (ca.cells == want).all():
+                    return False, f"3d ca mismatch, side {side} map {api.map_kind_name(g.kind)}"
+    return True, "edm + 64-step ca bit-equal to sequential oracle across maps, 2 seeds (edm is 2-simplex-only)"
+
+
+def c8():
+    for n in range(2, 4097, 2):
+        r = rp.measure_grid(api.make_grid(api.map_kind.rb, 2, n))
+        if not r.exact or r.blocks_void != 0 or r.threads_launched != r.threads_useful:
+            return False, f"rb not bijective at n={n}"
+    # the lambda map over every block of T(4096) on the GPU: block i -> the
+    # coordinate whose linear index is i
+    out = api.map_outcomes(api.grid_lambda(4096))
+    x, y = out[:, 1].astype(np.int64), out[:, 2].astype(np.int64)
+    if not ((0 <= x) & (x <= y) & (y < 4096)).all() or not (y * (y + 1) // 2 + x == np.arange(out.shape[0])).all():
+        return False, "linear-index round trip broken"
+    for n in (1, 2, 63, 64, 4095, 4096):
+        last = api.map_lambda_2d(api.tri_cells(n) - 1, n)
+        if (last.x, last.y) != (n - 1, n - 1):
+            return False, f"lambda top cell wrong at n={n}"
+        try:
+            api.map_lambda_2d(api.tri_cells(n), n)
+            return False, f"lambda accepted an out-of-range index at n={n}"
+        except api.InvalidArgument:
+            pass
+    return True, f"rb bijective for even n <= 4096; lambda round trip exact over all {out.shape[0]} indices at n=4096"
+
+
+def c9():
+    n, seen = 1024, []
+    for rho in (2, 4, 8, 16):
+        r = rp.measure_grid(api.make_grid(api.map_kind.h2d, 2, n, rho))
+        if not r.exact:
+            return False, f"h2d cover not exact at rho={rho}"
+        slack = r.threads_launched - r.threads_useful
+        if slack != (n - 1) * rho * (rho - 1) // 2:
+            return False, f"slack formula mismatch at rho={rho}"
+        if slack > 2 * n * rho * rho:
+            return False, f"slack exceeds 2 n rho^2 at rho={rho}"
+        seen.append(str(slack))
+    return True, f"slack threads {', '.join(seen)} for rho 2,4,8,16: each == (n-1)rho(rho-1)/2 <= 2 n rho^2"
+
+
+def c10():
+    ns = rp.expand_n_range(rp.parse_n_range("2..128"))
+    a = rp.csv_measure(rp.verify_sweep(api.map_kind.h2d_trapezoid, 2, ns, 1, 1))
+    b = rp.csv_measure(rp.verify_sweep(api.map_kind.h2d_trapezoid, 2, ns, 1, 1))
+    if a != b:
+        return False, "verify csv differs across runs"
+
+    def ca_csv():
+        g = api.make_grid(api.map_kind.h2d, 2, 64)
+        st = api.make_life_state(2, 63, 7)
+        rep = api.launch_ca(g, dom(g), st, api.launch_opts(steps=16, seed=7))
+        row = rp.measure_row(g.kind, g.dims, g.n, g.rho, rep.blocks_launched, rep.blocks_void, rep.threads_launched,
+                             rep.threads_useful, rep.space_overhead)
+        return rp.csv_simulate([rp.simulate_row(row, "ca", 16, 7, rep.state_hash)])
+
+    if ca_csv() != ca_csv():
+        return False, "simulate csv differs across runs"
+
+    def an_csv():
+        return rp.csv_analyze(rp.analyze_sweep(api.map_kind.h3d, 3, [8, 16, 32]))
+
+    if an_csv() != an_csv():
+        return False, "analyze csv differs across runs"
+    if A.csv_optimize(A.optimize_params(2, 2, 2, 4096), 4096) != A.csv_optimize(A.optimize_params(2, 2, 2, 4096), 4096):
+        return False, "optimize csv differs across runs"
+    return True, "verify/simulate/analyze/optimize csv byte-identical on repeat (svg: out of scope)"
+
+
+def main() -> int:
+    import torch
+    torch.cuda.set_device(0)
+    rp.measure_grid(api.grid_h2d(8))  # CUDA context + module load outside the budgets
+    print("acceptance gate (B200): the reference's ten criteria through the GPU path", flush=True)
+    run(1, "bb waste m=2: overhead at n=1024 equals 1023/1025, within 1% of limit 1", 1, c1)
+    run(2, "bb waste m=3: overhead at n=256 within 3% of 5", 10, c2)
+    run(3, "h2d exactness under accum kernel, n = 2^1..2^12", 30, c3)
+    run(4, "trapezoid exactness, n in [2,4096] x T in {1,4,16}", 300, c4)
+    run(5, "h3d exactness and ratio convergence toward 9/8, n = 4..128", 120, c5)
+    run(6, "self-similar closed forms and extra-fraction limits", 1, c6)
+    run(7, "map/kernel orthogonality: edm + ca vs sequential oracle", 120, c7)
+    run(8, "bijectivity: rb rectangle<->triangle, linear-index round trip", 60, c8)
+    run(9, "thread-level slack bound at n=1024, rho in {2,4,8,16}", 60, c9)
+    run(10, "determinism: repeated runs yield byte-identical reports", 0, c10)
+    print(f"{10 - failures}/10 passed", flush=True)
+    return 1 if failures else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
