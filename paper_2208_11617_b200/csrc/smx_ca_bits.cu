@@ -1,37 +1,40 @@
-// 3-D Life, x-run scheme (SMX_EXEC_RUNS), sm_100a: bit-shadow engine.
-//
-// Three kernels, the packed u8 state (reference layout) at both ends:
+// 3-D Life, sm_100a: the bit-shadow engine (SMX_EXEC_BITS; what launch_ca runs).
 //
 // k_pack_bits    u8 state -> "bit shadow": one bit per cell in a PITCHED layout,
 //                every packed row (y, z) padded to WP 32-bit words at word row
 //                z*S + y (a full S x S square per layer stack, so (w, y, z) is
-//                an affine 3-D tensor for TMA; rows y > S-1-z are never used). A warp walks 32 rows, 8 lanes per row, streaming each row's bytes as
-//                32-byte aligned chunks (2 x 16B loads per lane), packing them
-//                (IMAD gather + PRMT) and realigning at the bit level.
-// k_ca_bits      bit shadow -> next bit shadow. Work assignment is the map: a CTA
-//                owns a P x P patch of map blocks at one wz; its threads map the
-//                blocks lane-parallel and chain x-adjacent tiles (predecessor at
-//                patch neighbour (wx-1, wy) for unfolded H tiles / wall plane / BB
-//                rows, (wx, wy-1) for the hinge fold, maps.hpp:334-336) into
-//                chunks of <= 96 cells. A warp takes a chunk: one 3-D TMA tensor
-//                box (12 words x rho+2 rows x rho+2 layers) lands its halo in
-//                shared memory (double-buffered across chunks, mbarrier
-//                completion), lanes form the horizontal 3-sums as bit-planes, and
-//                lane (ly, w) marches along z with carry-save adders: 32 cells per
-//                LOP3. Output is whole 32-bit words: a word shared by two chunks
-//                gets identical values from both (every cell of a computed word is
-//                computed from the same input), so the writes are idempotent.
+//                an affine 3-D tensor for TMA; rows y > S-1-z are never used).
+//                A warp walks up to 32 rows, 8 lanes per row, streaming each
+//                row's bytes as 32-byte aligned chunks (2 x 16B loads per lane),
+//                packing them (IMAD gather + PRMT) and realigning at the bit level.
+// k_ca_plan      the map, applied ONCE per launch_ca: a CTA maps a P x P patch of
+//                map blocks lane-parallel and chains x-adjacent tiles
+//                (ca::build_chunks) into chunks of <= 96 cells, appended to one
+//                global chunk list.
+// k_ca_bits_run  ONE persistent cooperative launch (one 16-warp CTA per SM) runs
+//                every step over the chunk list: warps take items (1-2 chunks)
+//                round-robin; per chunk one 3-D TMA tensor box (12 words x rho+2
+//                rows x rho+2 layers) lands its halo in shared memory
+//                (double-buffered across items, mbarrier completion), lanes form
+//                the horizontal 3-sums as bit-planes, and lane (ly, w) marches z
+//                with carry-save adders (32 cells per LOP3). Output is whole
+//                32-bit words: a word shared by two chunks gets identical values
+//                from both (same input), so the writes are idempotent. A grid
+//                barrier separates the steps.
+// k_ca_bits      one step with the map evaluated inside the launch (per-CTA patch
+//                -> chunks in smem -> the same item loop): smx_bits_step and the
+//                multi-GPU range steps.
 // k_unpack_bits  bit shadow -> u8 state: 16-byte vector stores over each row's
-//                aligned interior, one byte store per lane for its two ends.
+//                aligned interior, byte stores for its two ends.
 //
-// A single step (smx_ca_step) is pack -> ca -> unpack; a multi-step run
-// (smx_ca) packs once and then runs ca -> unpack per step, so every step still
-// materialises the full u8 state in the reference layout.
+// launch_ca = pack -> plan -> run (all steps) -> unpack; one full-grid u8 step
+// (smx_ca_step, large states) is the same with one step.
 //
 // Semantics: alive_neighbors_3d_dead + life_next (simulator.hpp:220-253) for
 // every cell of every tile the map emits; each tile is processed by exactly one
 // chunk. Bits for x > y of a row (not cells) are never trusted: every reader
 // masks them.
+#include <cooperative_groups.h>
 #include <cuda.h>
 
 #include "smx_ca_common.cuh"
@@ -415,30 +418,15 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_ca_plan(Geom g, int wz0, int w
     for (int i = threadIdx.x; i < n; i += blockDim.x) out[s_base + i] = s_chunk[i];
 }
 
-// all CTAs co-resident (cooperative launch); bar[0] = arrivals, bar[1] = generation.
-// One thread per CTA: a release add on the arrival counter (orders this CTA's
-// step writes, made visible to the async proxy first); the last arriver resets
-// the counter and bumps the generation with release; the others spin with
-// acquire loads. Then the CTA re-syncs and fences toward the async proxy so
-// the next step's TMA loads see every CTA's writes.
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+// Between steps: every CTA's generic-proxy stores of this step must be visible
+// to the next step's TMA (async-proxy) loads in other CTAs: a proxy fence,
+// then the cooperative-groups grid barrier (cumulative gpu-scope release /
+// acquire), then a proxy fence before the next TMA issue. Measured per-step
+// floor on B200 (tools/step_floor.py): 3.1 us with grid.sync() vs 3.4 us with
+// a hand-rolled acq_rel counter barrier; 5.1 vs 5.9 us at C2.
+__device__ __forceinline__ void step_barrier() {
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned g0, old;
-        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(g0) : "l"(bar + 1) : "memory");
-        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;\n" : "=r"(old) : "l"(bar) : "memory");
-        if (old == nblocks - 1) {
-            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;\n" ::"l"(bar) : "memory");
-            asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar + 1) : "memory");
-        } else {
-            unsigned g;
-            do {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(g) : "l"(bar + 1) : "memory");
-            } while (g == g0);
-        }
-    }
-    __syncthreads();
+    cooperative_groups::this_grid().sync();
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
 
@@ -455,8 +443,8 @@ template <int RHO>
 __global__ void __launch_bounds__(RunCfg<RHO>::NW * 32) k_ca_bits_run(const __grid_constant__ CUtensorMap tmA,
                                                       const __grid_constant__ CUtensorMap tmB, uint32_t* bitsA,
                                                       uint32_t* bitsB, const Chunk* __restrict__ chunks,
-                                                      const unsigned* __restrict__ count, int steps, int S, int WP,
-                                                      unsigned* bar) {
+                                                      const unsigned* __restrict__ count, int steps, int S,
+                                                      int WP) {
     using C = Cfg<RHO, RunCfg<RHO>::CPIX>;
     constexpr int RUN_NWARP = RunCfg<RHO>::NW;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -501,7 +489,7 @@ __global__ void __launch_bounds__(RunCfg<RHO>::NW * 32) k_ca_bits_run(const __gr
         const bool even = (st & 1) == 0;
         run_items<RHO, RunCfg<RHO>::CPIX>(src, nsrc, i0, istr, even ? &tmA : &tmB, even ? bitsB : bitsA, S, WP,
                                           wbase, mbar0, phases);
-        if (st + 1 < steps) grid_barrier(bar, gridDim.x);
+        if (st + 1 < steps) step_barrier();
     }
 }
 
@@ -542,7 +530,7 @@ void launch_plan_t(const Geom& g, void* chunks, unsigned* count, cudaStream_t s)
 
 template <int RHO>
 cudaError_t launch_run_t(const Geom& g, const CUtensorMap& tA, const CUtensorMap& tB, uint32_t* A, uint32_t* B,
-                         const void* chunks, const unsigned* count, int steps, unsigned* bar, cudaStream_t s) {
+                         const void* chunks, const unsigned* count, int steps, cudaStream_t s) {
     using C = Cfg<RHO, RunCfg<RHO>::CPIX>;
     constexpr int RUN_NWARP = RunCfg<RHO>::NW;
     const int smem = RUN_NWARP * C::WARP_BYTES;
@@ -557,7 +545,7 @@ cudaError_t launch_run_t(const Geom& g, const CUtensorMap& tA, const CUtensorMap
     const Chunk* ch = reinterpret_cast<const Chunk*>(chunks);
     int S = g.side, WP = bits_pitch_words(g.side);
     void* args[] = {const_cast<CUtensorMap*>(&tA), const_cast<CUtensorMap*>(&tB), &A, &B, &ch,
-                    const_cast<unsigned**>(&count), &steps, &S, &WP, &bar};
+                    const_cast<unsigned**>(&count), &steps, &S, &WP};
     return cudaLaunchCooperativeKernel((const void*)k_ca_bits_run<RHO>, dim3(grid), dim3(RUN_NWARP * 32), args, smem,
                                        s);
 }
@@ -623,11 +611,11 @@ void launch_ca_plan(const Geom& g, int kind, void* chunks, unsigned* count, cuda
 }
 
 cudaError_t launch_ca_bits_run(const Geom& g, const void* tmA, const void* tmB, uint32_t* A, uint32_t* B,
-                               const void* chunks, const unsigned* count, int steps, unsigned* bar, cudaStream_t s) {
+                               const void* chunks, const unsigned* count, int steps, cudaStream_t s) {
     const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(tmA);
     const CUtensorMap& tb = *reinterpret_cast<const CUtensorMap*>(tmB);
-    if (g.rho == 4) return launch_run_t<4>(g, ta, tb, A, B, chunks, count, steps, bar, s);
-    return launch_run_t<8>(g, ta, tb, A, B, chunks, count, steps, bar, s);
+    if (g.rho == 4) return launch_run_t<4>(g, ta, tb, A, B, chunks, count, steps, s);
+    return launch_run_t<8>(g, ta, tb, A, B, chunks, count, steps, s);
 }
 
 void launch_ca_bits(const Geom& g, int kind, int wz0, int wz1, const void* tmap_ptr, uint32_t* nbits, cudaStream_t s) {

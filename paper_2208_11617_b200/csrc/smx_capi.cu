@@ -324,10 +324,9 @@ int bits_engine(const smx_grid* g, const smx::Geom& k, uint32_t* A, uint32_t* B,
     if (int rc = pool_get(5, size_t(smx::ca_plan_capacity(k)) * 16, &pch)) return rc;
     if (int rc = pool_get(6, 64, &pctl)) return rc;
     unsigned* count = (unsigned*)pctl;
-    unsigned* bar = count + 4;
     TRY(cudaMemsetAsync(pctl, 0, 64, s));
     smx::launch_ca_plan(k, g->kind, pch, count, s);
-    TRY(smx::launch_ca_bits_run(k, ta, tb, A, B, pch, count, int(steps), bar, s));
+    TRY(smx::launch_ca_bits_run(k, ta, tb, A, B, pch, count, int(steps), s));
     return SMX_OK;
 }
 

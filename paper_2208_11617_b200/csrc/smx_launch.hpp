@@ -27,11 +27,10 @@ void launch_ca_bits(const Geom& g, int kind, int wz0, int wz1, const void* tmap,
 // multi-step engine: the map applied once (chunk list, 16 B per chunk, at most
 // ca_plan_capacity entries; *count must be zero), then ONE persistent
 // cooperative launch runs `steps` bit-sliced steps A -> B -> A ...
-// (bar: two zeroed u32 for the grid barrier)
 unsigned long long ca_plan_capacity(const Geom& g);
 void launch_ca_plan(const Geom& g, int kind, void* chunks, unsigned* count, cudaStream_t s);
 cudaError_t launch_ca_bits_run(const Geom& g, const void* tmA, const void* tmB, uint32_t* A, uint32_t* B,
-                               const void* chunks, const unsigned* count, int steps, unsigned* bar, cudaStream_t s);
+                               const void* chunks, const unsigned* count, int steps, cudaStream_t s);
 // 2-simplex EDM (f64 points as x, y pairs) and periodic 2-D Life (smx_kernels2d.cu)
 void launch_edm(const Geom& g, const double* pts, double* cells, int exec, cudaStream_t s);
 void launch_ca2d(const Geom& g, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s);
