@@ -262,7 +262,7 @@ int fill_counters(const smx_grid* g, smx_counters* c, cudaStream_t s, uint32_t* 
     return SMX_OK;
 }
 
-int resolve_exec(int exec, const smx_grid* g) {
+int resolve_exec(int exec) {
     if (exec == SMX_EXEC_BLOCK || exec == SMX_EXEC_RUNS) return exec;
     return -1;
 }
@@ -576,7 +576,7 @@ int smx_accum(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passe
     if (int rc = check_cells(g, ncells)) return rc;
     if (passes < 0) return fail(SMX_EINVAL, "accum: passes must be >= 0");
     if (exec < 0) exec = SMX_EXEC_RUNS;
-    if (resolve_exec(exec, g) < 0) return fail(SMX_EINVAL, "accum: unknown exec scheme");
+    if (resolve_exec(exec) < 0) return fail(SMX_EINVAL, "accum: unknown exec scheme");
     cudaStream_t s = (cudaStream_t)stream;
     uint32_t* d = cells;
     uint32_t* dcov = coverage;

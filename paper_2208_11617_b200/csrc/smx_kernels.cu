@@ -416,15 +416,15 @@ void launch_life_init(unsigned long long seed, uint8_t* cells, unsigned long lon
 }
 
 template <int KIND>
-static void launch_ca_k(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t* next, int exec,
-                        cudaStream_t s) {
+static void launch_ca_k(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t* next, cudaStream_t s) {
     if (wz1 <= wz0) return;
     k_ca_block<KIND><<<dim3(g.ex, g.ey, wz1 - wz0), block_shape(g), 0, s>>>(g, wz0, cur, next);
 }
 // block scheme only; the x-run scheme is driven by the C ABI (pack + k_ca_bits)
 void launch_ca(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s) {
-    if (g.kind == SMX_H3D) launch_ca_k<SMX_H3D>(g, wz0, wz1, cur, next, exec, s);
-    else launch_ca_k<SMX_BB>(g, wz0, wz1, cur, next, exec, s);
+    (void)exec;  // the block scheme is the only per-cell CA kernel here
+    if (g.kind == SMX_H3D) launch_ca_k<SMX_H3D>(g, wz0, wz1, cur, next, s);
+    else launch_ca_k<SMX_BB>(g, wz0, wz1, cur, next, s);
 }
 
 void launch_tiles_pack(const Geom& g, const uint8_t* cells, const int* tiles, unsigned long long ntiles,
