@@ -233,6 +233,15 @@ int smx_tiles_pack(const smx_grid* g, const uint8_t* cells, const int32_t* tiles
 int smx_tiles_unpack(const smx_grid* g, uint8_t* cells, const int32_t* tiles, uint64_t ntiles,
                      const uint8_t* in, void* stream);
 
+/* The same exchange on bit shadows (the sharded bit-shadow engine): tile k
+ * occupies smx_bits_tile_bytes(g, 1) bytes (rho = 8: 64, rho = 4: 8) — rho^2
+ * rows of rho bits, lz, ly order. Device pointers; rho in {4, 8}. */
+uint64_t smx_bits_tile_bytes(const smx_grid* g, uint64_t ntiles);
+int smx_bits_tiles_pack(const smx_grid* g, const uint32_t* bits, const int32_t* tiles, uint64_t ntiles, uint8_t* out,
+                        void* stream);
+int smx_bits_tiles_unpack(const smx_grid* g, uint32_t* bits, const int32_t* tiles, uint64_t ntiles,
+                          const uint8_t* in, void* stream);
+
 /* cudaDeviceSynchronize on the current device. */
 int smx_device_sync(void);
 

@@ -580,6 +580,19 @@ def tiles_unpack_device(g: grid_spec, cells, tiles, buf) -> None:
     check(lib().smx_tiles_unpack(C.byref(g.raw), _ptr(cells), _ptr(tiles), tiles.shape[0], _ptr(buf), _stream()))
 
 
+def bits_tiles_pack_device(g: grid_spec, bits, tiles, out) -> None:
+    check(lib().smx_bits_tiles_pack(C.byref(g.raw), _ptr(bits), _ptr(tiles), tiles.shape[0], _ptr(out), _stream()))
+
+
+def bits_tiles_unpack_device(g: grid_spec, bits, tiles, buf) -> None:
+    check(lib().smx_bits_tiles_unpack(C.byref(g.raw), _ptr(bits), _ptr(tiles), tiles.shape[0], _ptr(buf),
+                                      _stream()))
+
+
+def bits_tile_bytes(g: grid_spec) -> int:
+    return int(lib().smx_bits_tile_bytes(C.byref(g.raw), 1))
+
+
 def bits_buffer(g: grid_spec):
     """A device bit shadow for the x-run engine stages (with TMA-read slack)."""
     import torch

@@ -558,7 +558,75 @@ void launch_kind(const Geom& g, int wz0, int wz1, const CUtensorMap& tmap, uint3
 
 }  // namespace
 
+// Halo exchange in bits (the sharded engine): tile (X, Y, Z) of side rho is
+// rho^2 rows of rho bits at bit offset (rho X) % 32 of word (rho X) / 32 of
+// pitched row (z, y). Packed: per tile, rows in lz, ly order, rho bits each
+// (rho = 8: one byte per row, 64 bytes per tile; rho = 4: a nibble per row,
+// 8 bytes per tile). Unpack writes whole bytes for rho = 8 and nibbles through
+// 32-bit atomics for rho = 4 (two tiles share a byte), so tiles unpacked
+// concurrently never clobber each other. Rows outside the square shadow are skipped.
+template <int RHO>
+__device__ __forceinline__ uint32_t tile_row_bits(const uint32_t* __restrict__ bits, int S, int WP, int X, int Y,
+                                                  int Z, int r) {
+    const int z = Z * RHO + r / RHO, y = Y * RHO + r % RHO;
+    if (z >= S || y >= S) return 0u;
+    return (bits[((long long)z * S + y) * WP + ((RHO * X) >> 5)] >> ((RHO * X) & 31)) & ((1u << RHO) - 1u);
+}
+
+template <int RHO>
+__global__ void k_bits_tiles_pack(const uint32_t* __restrict__ bits, int S, int WP, const int* __restrict__ tiles,
+                                  uint8_t* __restrict__ out) {
+    const int k = blockIdx.x;
+    const int X = tiles[3 * k], Y = tiles[3 * k + 1], Z = tiles[3 * k + 2];
+    if (RHO == 8) {
+        for (int r = threadIdx.x; r < 64; r += blockDim.x)
+            out[(long long)k * 64 + r] = (uint8_t)tile_row_bits<RHO>(bits, S, WP, X, Y, Z, r);
+    } else {  // two rows per byte: low nibble = even row
+        for (int t = threadIdx.x; t < 8; t += blockDim.x)
+            out[(long long)k * 8 + t] = (uint8_t)(tile_row_bits<RHO>(bits, S, WP, X, Y, Z, 2 * t) |
+                                                  (tile_row_bits<RHO>(bits, S, WP, X, Y, Z, 2 * t + 1) << 4));
+    }
+}
+
+template <int RHO>
+__global__ void k_bits_tiles_unpack(uint32_t* __restrict__ bits, int S, int WP, const int* __restrict__ tiles,
+                                    const uint8_t* __restrict__ in) {
+    const int k = blockIdx.x;
+    const int X = tiles[3 * k], Y = tiles[3 * k + 1], Z = tiles[3 * k + 2];
+    const int bit = (RHO * X) & 31, word = (RHO * X) >> 5;
+    for (int r = threadIdx.x; r < RHO * RHO; r += blockDim.x) {
+        const int z = Z * RHO + r / RHO, y = Y * RHO + r % RHO;
+        if (z >= S || y >= S) continue;
+        uint32_t* w = bits + ((long long)z * S + y) * WP + word;
+        if (RHO == 8) {
+            reinterpret_cast<uint8_t*>(w)[bit >> 3] = in[(long long)k * 64 + r];
+        } else {
+            const uint32_t v = (in[(long long)k * 8 + r / 2] >> (4 * (r & 1))) & 0xfu;
+            atomicAnd(w, ~(0xfu << bit));
+            atomicOr(w, v << bit);
+        }
+    }
+}
+
 bool ca_runs_supported(int rho) { return rho == 4 || rho == 8; }
+
+unsigned long long bits_tile_bytes(int rho) { return rho == 8 ? 64ull : 8ull; }
+
+void launch_bits_tiles_pack(const Geom& g, const uint32_t* bits, const int* tiles, unsigned long long ntiles,
+                            uint8_t* out, cudaStream_t s) {
+    if (ntiles == 0) return;
+    const int WP = bits_pitch_words(g.side);
+    if (g.rho == 8) k_bits_tiles_pack<8><<<(unsigned)ntiles, 64, 0, s>>>(bits, g.side, WP, tiles, out);
+    else k_bits_tiles_pack<4><<<(unsigned)ntiles, 32, 0, s>>>(bits, g.side, WP, tiles, out);
+}
+
+void launch_bits_tiles_unpack(const Geom& g, uint32_t* bits, const int* tiles, unsigned long long ntiles,
+                              const uint8_t* in, cudaStream_t s) {
+    if (ntiles == 0) return;
+    const int WP = bits_pitch_words(g.side);
+    if (g.rho == 8) k_bits_tiles_unpack<8><<<(unsigned)ntiles, 64, 0, s>>>(bits, g.side, WP, tiles, in);
+    else k_bits_tiles_unpack<4><<<(unsigned)ntiles, 32, 0, s>>>(bits, g.side, WP, tiles, in);
+}
 
 // words per pitched row: >= 8, multiple of 4 (16-byte row stride for TMA)
 int bits_pitch_words(int side) {

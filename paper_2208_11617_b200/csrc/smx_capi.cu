@@ -943,6 +943,33 @@ uint64_t smx_tile_bytes(const smx_grid* g, uint64_t ntiles) {
     return r3 * ntiles;
 }
 
+uint64_t smx_bits_tile_bytes(const smx_grid* g, uint64_t ntiles) {
+    if (!g || g->dims != 3 || !smx::ca_runs_supported(int(g->rho))) return 0;
+    return ntiles * smx::bits_tile_bytes(int(g->rho));
+}
+
+int smx_bits_tiles_pack(const smx_grid* g, const uint32_t* bits, const int32_t* tiles, uint64_t ntiles, uint8_t* out,
+                        void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, false)) return rc;
+    if (g->dims != 3 || !smx::ca_runs_supported(int(g->rho)))
+        return fail(SMX_EINVAL, "bits_tiles: 3-simplex grids with rho in {4, 8}");
+    smx::launch_bits_tiles_pack(k, bits, tiles, ntiles, out, (cudaStream_t)stream);
+    TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
+int smx_bits_tiles_unpack(const smx_grid* g, uint32_t* bits, const int32_t* tiles, uint64_t ntiles,
+                          const uint8_t* in, void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, false)) return rc;
+    if (g->dims != 3 || !smx::ca_runs_supported(int(g->rho)))
+        return fail(SMX_EINVAL, "bits_tiles: 3-simplex grids with rho in {4, 8}");
+    smx::launch_bits_tiles_unpack(k, bits, tiles, ntiles, in, (cudaStream_t)stream);
+    TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
 int smx_tiles_pack(const smx_grid* g, const uint8_t* cells, const int32_t* tiles, uint64_t ntiles, uint8_t* out,
                    void* stream) {
     smx::Geom k;

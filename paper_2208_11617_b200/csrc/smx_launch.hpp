@@ -36,6 +36,12 @@ void launch_edm(const Geom& g, const double* pts, double* cells, int exec, cudaS
 void launch_ca2d(const Geom& g, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s);
 // first packed index with coverage != 1 (atomicMin into *first, preset to n)
 void launch_first_defect(const uint32_t* cov, unsigned long long n, unsigned long long* first, cudaStream_t s);
+// bit-shadow tiles for the sharded engine's halo (rho in {4, 8})
+unsigned long long bits_tile_bytes(int rho);
+void launch_bits_tiles_pack(const Geom& g, const uint32_t* bits, const int* tiles, unsigned long long ntiles,
+                            uint8_t* out, cudaStream_t s);
+void launch_bits_tiles_unpack(const Geom& g, uint32_t* bits, const int* tiles, unsigned long long ntiles,
+                              const uint8_t* in, cudaStream_t s);
 void launch_tiles_pack(const Geom& g, const uint8_t* cells, const int* tiles, unsigned long long ntiles,
                        uint8_t* out, cudaStream_t s);
 void launch_tiles_unpack(const Geom& g, uint8_t* cells, const int* tiles, unsigned long long ntiles,

@@ -138,7 +138,7 @@ class ShardedLife:
         self.dist = dist
         self.plan, self.rank, self.rho, self.ops, self.group = plan, rank, rho, ops, group
         self.lo, self.hi = plan.wz_ranges[rank]
-        r3 = rho ** 3
+        r3 = getattr(ops, "tile_bytes", rho ** 3)  # u8 tiles: rho^3 bytes; bit tiles: rho^3 / 8
         self.send_t = {q: ops.tiles(t) for q, t in plan.send[rank].items()}
         self.recv_t = {q: ops.tiles(t) for q, t in plan.recv(rank).items()}
         self.send_b = {q: ops.empty(t.shape[0] * r3) for q, t in plan.send[rank].items()}
@@ -212,12 +212,44 @@ class CudaOps:
         return torch.from_numpy(np.ascontiguousarray(t, dtype=np.int32).reshape(-1, 3)).cuda()
 
 
+class BitsOps(CudaOps):
+    """The sharded bit-shadow engine: the state lives as bit shadows on every
+    rank (pack once, unpack once), a step is the map-driven bit-sliced kernel
+    over the rank's wz range (smx_bits_step), and the halo travels as bit tiles
+    (rho^3 / 8 bytes: 64 B at rho = 8, vs 512 B as u8). A rank's whole-word
+    stores may dirty cells of x-adjacent foreign tiles (all in its halo plan, so
+    they are overwritten by the exchange) or of tiles it never reads."""
+
+    def __init__(self, grid):
+        super().__init__(grid)
+        self.tile_bytes = self.api.bits_tile_bytes(grid)
+
+    def step_range(self, cur, nxt, lo, hi):
+        self.api.bits_step_device(self.g, cur, nxt, lo, hi)
+
+    def pack(self, bits, tiles, out):
+        self.api.bits_tiles_pack_device(self.g, bits, tiles, out)
+
+    def unpack(self, bits, tiles, buf):
+        self.api.bits_tiles_unpack_device(self.g, bits, tiles, buf)
+
+
+def run_bits(sh: "ShardedLife", api, g, cells, steps: int):
+    """launch_ca sharded: pack -> steps x (range step + bit-tile exchange) ->
+    unpack into `cells` (valid on the rank's own tiles; gather_owned collects)."""
+    a, b = api.bits_buffer(g), api.bits_buffer(g)
+    api.bits_pack_device(g, cells, a)
+    res = sh.run(a, b, steps)
+    api.bits_unpack_device(g, res, cells)
+    return cells
+
+
 def bench_sharded(args, api):
     """bench.py --gpus N under torchrun: the C2 launch_ca (100 CA steps per
-    bench step) sharded over N GPUs: each rank steps its H wz range with the
-    fused u8 kernel and exchanges halo tiles over NCCL after every CA step."""
+    bench step) sharded over N GPUs with the bit-shadow engine: each rank packs
+    its replica once, steps its H wz range (map-driven bit-sliced kernel) and
+    exchanges bit halo tiles over NCCL after every CA step, unpacks once."""
     import os
-    import statistics  # noqa: F401
 
     import torch
     import torch.distributed as dist
@@ -234,15 +266,14 @@ def bench_sharded(args, api):
     cells = api.tet_cells(side)
     out = api.map_outcomes(g)
     plan = build_plan(g.extents, out, True, g.domain_side(), world)
-    ops = CudaOps(g, api.EXEC_RUNS)
+    ops = BitsOps(g)
     sh = ShardedLife(plan, rank, rho, ops)
     a = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
-    b = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
     api.life_init_device(3, side, SEED, a)
     flush = Flusher()
 
     def step(i):
-        sh.run(a, b, nsteps)
+        run_bits(sh, api, g, a, nsteps)
 
     dist.barrier()
     timed_steps(step, args.warmup, flush)
@@ -262,10 +293,11 @@ def bench_sharded(args, api):
             "data": "synthetic (make_life_state seed 42)", "impl": "ours",
             "config": {"workload": desc, "map": kind, "n_b": n, "rho": rho, "side": side, "cells": cells,
                        "ca_steps_per_call": nsteps,
-                       "parallelism": f"H wz-range shards x{world}, tile halo over NCCL after every CA step",
+                       "parallelism": f"H wz-range shards x{world}: bit-shadow engine, bit-tile halo "
+                                      f"({ops.tile_bytes} B/tile) over NCCL after every CA step",
                        "wz_ranges": plan.wz_ranges, "halo_tiles_per_rank": [plan.halo_tiles(r) for r in
                                                                             range(world)]},
-            "gpu_launches": args.steps * nsteps * 3,
+            "gpu_launches": args.steps * (2 + nsteps * (1 + 2 * len(plan.send[rank]) + len(plan.recv(rank)))),
         }
     dist.destroy_process_group()
     return line

@@ -22,7 +22,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, kind, n, rho, ex, steps, q):
+def _worker(rank, world, port, kind, n, rho, ex, steps, q, bits=False):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from oracle.oracle import Restated
@@ -45,6 +45,18 @@ def _worker(rank, world, port, kind, n, rho, ex, steps, q):
         def unpack(self, cells, tiles, buf):
             super().unpack(cells, tiles, buf.cuda())
 
+    class StagedBitsOps(D.BitsOps):
+        def empty(self, n_):
+            return torch.zeros(max(n_, 1), dtype=torch.uint8)
+
+        def pack(self, bits_, tiles, out):
+            tmp = torch.empty(out.numel(), dtype=torch.uint8, device="cuda")
+            super().pack(bits_, tiles, tmp)
+            out.copy_(tmp.cpu())
+
+        def unpack(self, bits_, tiles, buf):
+            super().unpack(bits_, tiles, buf.cuda())
+
     g = api.make_grid(api.map_kind[kind], 3, n, rho)
     side = g.cell_side()
     cells = api.tet_cells(side)
@@ -54,7 +66,11 @@ def _worker(rank, world, port, kind, n, rho, ex, steps, q):
     b = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
     api.life_init_device(3, side, 42, a)
     b.fill_(1)  # garbage outside owned + halo tiles must never matter
-    res = sh.run(a, b, steps)
+    if bits:
+        shb = D.ShardedLife(plan, rank, rho, StagedBitsOps(g))
+        res = D.run_bits(shb, api, g, a, steps)
+    else:
+        res = sh.run(a, b, steps)
     torch.cuda.synchronize()
     sh.gather_owned(res, 0)
     if rank == 0:
@@ -74,6 +90,22 @@ def test_sharded_step_on_one_gpu(cuda, kind, n, rho, ex):
     port = _free_port()
     world = 2
     procs = [ctx.Process(target=_worker, args=(r, world, port, kind, n, rho, ex, 4, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert ok
+
+
+@pytest.mark.parametrize("kind,n,rho", [("h3d", 32, 4), ("h3d", 32, 8), ("bb", 31, 4), ("h3d", 64, 8)])
+def test_sharded_bits_engine_on_one_gpu(cuda, kind, n, rho):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 2
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, n, rho, 1, 6, q, True)) for r in range(world)]
     for p in procs:
         p.start()
     ok = q.get(timeout=600)
