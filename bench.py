@@ -268,10 +268,10 @@ def run_ours(args):
 
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
     local = env_int("LOCAL_RANK", 0)
-    torch.cuda.set_device(local)
     if world > 1:
         from paper_2208_11617_b200 import dist as D
-        return D.bench_sharded(args, api)
+        return D.bench_sharded(args, api)  # picks the device per backend
+    torch.cuda.set_device(local)
 
     peak, peak_src = load_peaks()
     flush = Flusher()

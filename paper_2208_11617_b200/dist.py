@@ -234,6 +234,23 @@ class BitsOps(CudaOps):
         self.api.bits_tiles_unpack_device(self.g, bits, tiles, buf)
 
 
+class StagedBitsOps(BitsOps):
+    """BitsOps with host-staged halo buffers (gloo on one GPU; smoke tests)."""
+
+    def empty(self, n):
+        import torch
+        return torch.zeros(max(n, 1), dtype=torch.uint8)
+
+    def pack(self, bits, tiles, out):
+        import torch
+        tmp = torch.empty(out.numel(), dtype=torch.uint8, device="cuda")
+        super().pack(bits, tiles, tmp)
+        out.copy_(tmp.cpu())
+
+    def unpack(self, bits, tiles, buf):
+        super().unpack(bits, tiles, buf.cuda())
+
+
 def run_bits(sh: "ShardedLife", api, g, cells, steps: int):
     """launch_ca sharded: pack -> steps x (range step + bit-tile exchange) ->
     unpack into `cells` (valid on the rank's own tiles; gather_owned collects)."""
@@ -256,8 +273,15 @@ def bench_sharded(args, api):
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", 0))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # SMX_DIST_BACKEND=gloo: a smoke path for one-GPU boxes (every rank on
+    # cuda:0, halo staged through host memory); the product path is NCCL
+    backend = os.environ.get("SMX_DIST_BACKEND", "nccl")
+    if backend == "gloo":
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from bench import METRIC, SEED, WORKLOADS, Flusher, timed_steps  # noqa: E402
 
     desc, kind, n, rho, nsteps = WORKLOADS["c2"]
@@ -266,7 +290,7 @@ def bench_sharded(args, api):
     cells = api.tet_cells(side)
     out = api.map_outcomes(g)
     plan = build_plan(g.extents, out, True, g.domain_side(), world)
-    ops = BitsOps(g)
+    ops = BitsOps(g) if backend != "gloo" else StagedBitsOps(g)
     sh = ShardedLife(plan, rank, rho, ops)
     a = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
     api.life_init_device(3, side, SEED, a)
@@ -280,7 +304,7 @@ def bench_sharded(args, api):
     torch.cuda.synchronize()
     dist.barrier()
     ms = timed_steps(step, args.steps, flush)
-    tot = torch.tensor([sum(ms)], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([sum(ms)], dtype=torch.float64, device="cuda" if backend != "gloo" else "cpu")
     dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms_step = float(tot.item()) / args.steps
     line = None

@@ -113,3 +113,20 @@ def test_sharded_bits_engine_on_one_gpu(cuda, kind, n, rho):
         p.join(timeout=120)
         assert p.exitcode == 0
     assert ok
+
+
+def test_bench_sharded_smoke(cuda):
+    # bench.py --gpus 2 through torchrun: the sharded bit-shadow engine bench
+    # path end to end (gloo + host-staged halo: one GPU cannot host two NCCL ranks)
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SMX_DIST_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus",
+                          "2", "--steps", "2", "--warmup", "3"], cwd=root, env=env, capture_output=True, text=True,
+                         timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and "bit-shadow engine" in line["config"]["parallelism"]
