@@ -168,7 +168,7 @@ __device__ __forceinline__ void accum_rows(uint32_t* __restrict__ cells, const u
 }
 
 template <int KIND, int KX, int RR, int NV>
-__global__ void __launch_bounds__(ACC_THREADS) k_accum_runs(Geom g, uint32_t* __restrict__ cells) {
+__global__ void __launch_bounds__(ACC_THREADS, 4) k_accum_runs(Geom g, uint32_t* __restrict__ cells) {
     __shared__ int s_run[KX][3];
     __shared__ int s_nruns;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -399,8 +399,9 @@ static void launch_accum_k(const Geom& g, uint32_t* cells, int exec, cudaStream_
         k_accum_block<KIND><<<dim3(g.ex, g.ey, 1), block_shape(g), 0, s>>>(g, cells);
         return;
     }
-    // 32 blocks per CTA strip, 2 rows x 4 vectors in flight per lane: C3 at
-    // 0.80 of the measured HBM peak (profiles/r1/accum_sweep.txt)
+    // 32 blocks per CTA strip, 2 rows x 4 vectors in flight per lane, 4 CTAs
+    // per SM (<= 64 registers): C3 at 0.85 of the HBM peak
+    // (profiles/r1/accum_sweep.txt; 3 CTAs: 0.78, 5 CTAs: spills, 0.60)
     launch_runs_t<KIND, 32, 2, 4>(g, cells, s);
 }
 void launch_accum(const Geom& g, uint32_t* cells, int exec, cudaStream_t s) {
