@@ -9,9 +9,12 @@
 // launch_accum, launch_ca (dead3d), make_life_state, verify_exact_cover; and
 // the general-n / comparison 2-D maps: grid_rb,
 // grid_lambda, grid_h2d_padded, grid_trapezoids, decompose_trapezoids,
-// map_rb_2d, map_lambda_2d, map_h2d_padded, map_h2d_trapezoid.
-// Out of scope (not declared here): EDM, the 2-D periodic CA, analysis,
-// reports, rendering.
+// map_rb_2d, map_lambda_2d, map_h2d_padded, map_h2d_trapezoid; the EDM and
+// 2-D periodic Life kernels (make_edm_points, launch_edm, launch_ca m=2); and
+// the report layer (report.hpp: measure_grid, verify_sweep, analyze_sweep,
+// parse_n_range, csv_measure / csv_analyze / csv_simulate, text_report).
+// Out of scope (not declared here): the r/beta analysis (Python:
+// paper_2208_11617_b200.analysis), rendering.
 //
 // Switching from the reference: include this header instead of
 // <simplexmap/simulator.hpp> and define SMX_B200_AS_SIMPLEXMAP to get the
@@ -84,10 +87,51 @@ struct rational {
         if (a > 1) num /= a, den /= a;
     }
     bool operator==(const rational& o) const { return num == o.num && den == o.den; }
+    bool operator!=(const rational& o) const { return !(*this == o); }
+
+    static std::string int_text(i128 v) {
+        if (v == 0) return "0";
+        const bool neg = v < 0;
+        unsigned __int128 u = neg ? (unsigned __int128)(-(v + 1)) + 1 : (unsigned __int128)v;
+        std::string d;
+        while (u) d.insert(d.begin(), char('0' + int(u % 10))), u /= 10;
+        return neg ? "-" + d : d;
+    }
+    // rational.hpp:123-126
+    std::string to_string() const { return den == 1 ? int_text(num) : int_text(num) + "/" + int_text(den); }
+    // rational.hpp:129-144: fixed point, round half up on the magnitude
+    std::string to_decimal_string(int digits = 6) const {
+        unsigned __int128 mag = num < 0 ? (unsigned __int128)(-num) : (unsigned __int128)num, scale = 1;
+        for (int i = 0; i < digits; ++i) scale *= 10;
+        const unsigned __int128 d = (unsigned __int128)den;
+        unsigned __int128 q = mag / d * scale, r = mag % d;
+        q += r * scale / d;
+        if ((r * scale % d) * 2 >= d) q += 1;
+        std::string out = (num < 0 && q != 0) ? "-" : "";
+        out += int_text(i128(q / scale));
+        if (digits > 0) {
+            std::string f = int_text(i128(q % scale));
+            out += "." + std::string(std::size_t(digits) - f.size(), '0') + f;
+        }
+        return out;
+    }
 };
 
 // ---- maps (maps.hpp:19-92, :96-116, :188-207, :285-337) ----
 enum class map_kind { bb, rb, lambda2d, h2d, h2d_trapezoid, h2d_padded, h3d };
+
+inline const char* map_kind_name(map_kind k) {
+    switch (k) {
+        case map_kind::bb: return "bb";
+        case map_kind::rb: return "rb";
+        case map_kind::lambda2d: return "lambda";
+        case map_kind::h2d: return "h2d";
+        case map_kind::h2d_trapezoid: return "trapezoid";
+        case map_kind::h2d_padded: return "h2d-padded";
+        case map_kind::h3d: return "h3d";
+    }
+    return "?";
+}
 
 inline bool strict_view(map_kind k) {
     return k == map_kind::h2d || k == map_kind::h2d_padded || k == map_kind::h2d_trapezoid || k == map_kind::h3d;
@@ -234,7 +278,18 @@ inline map_outcome map_h2d_trapezoid(block_coord omega, const trapezoid_params& 
 }
 
 // ---- simulator (simulator.hpp:37-96, :257-478) ----
+enum class kernel_kind { map, accum, edm, ca_life };
 enum class ca_boundary { periodic2d, dead3d };
+
+inline const char* kernel_kind_name(kernel_kind k) {
+    switch (k) {
+        case kernel_kind::map: return "map";
+        case kernel_kind::accum: return "accum";
+        case kernel_kind::edm: return "edm";
+        case kernel_kind::ca_life: return "ca";
+    }
+    return "?";
+}
 
 template <class T>
 struct simplex_grid_state {
@@ -368,6 +423,35 @@ inline sim_report launch_ca(const grid_spec& g, const simplex_spec& domain, simp
     return rep;
 }
 
+// make_edm_points (simulator.hpp:333-343): seeded splitmix64 points in [0,1)^2
+inline std::vector<std::array<double, 2>> make_edm_points(i64 count, u64 seed) {
+    if (count < 0) throw std::invalid_argument("make_edm_points: count must be >= 0");
+    std::vector<std::array<double, 2>> pts(static_cast<std::size_t>(count));
+    if (count) check(smx_make_edm_points(count, seed, pts.front().data()));
+    return pts;
+}
+
+// launch_edm (simulator.hpp:352-372): cell (x, y) = |p_x - p_y| in f64, bit-identical
+// to the reference's edm_distance
+inline sim_report launch_edm(const grid_spec& g, const simplex_spec& domain,
+                             const std::vector<std::array<double, 2>>& points, simplex_grid_state<double>& state,
+                             const launch_opts& opts = {}) {
+    validate_launch(g, domain);
+    if (g.dims != 2) throw std::invalid_argument("launch_edm: 2-simplex domains only");
+    if (state.m != 2 || state.side != g.domain_side() * g.rho)
+        throw std::invalid_argument("launch: state does not match the domain");
+    if (i64(points.size()) != state.side)
+        throw std::invalid_argument("launch_edm: need one point per domain side unit");
+    sim_report rep = detail::make_report(g, opts);
+    smx_grid r = g.raw();
+    smx_counters c{};
+    check(smx_edm(&r, points.front().data(), i64(points.size()), state.cells.data(), state.cells.size(), opts.exec,
+                  0, rep.coverage_recorded ? rep.coverage.data() : nullptr, &c, nullptr));
+    detail::finish(rep, c);
+    rep.state_hash = state.hash();
+    return rep;
+}
+
 // verify_exact_cover (simulator.hpp:467-478): first cell of multiplicity != 1
 inline cover_verdict verify_exact_cover(const sim_report& rep, const simplex_spec& domain) {
     if (domain.m != rep.m || domain.n != rep.cell_side - 1)
@@ -386,6 +470,222 @@ inline cover_verdict verify_exact_cover(const sim_report& rep, const simplex_spe
         return {false, {i64(rem - tri_linear_index(0, y)), y, z}, rep.coverage[i]};
     }
     return {};
+}
+
+// ---- report layer (report.hpp) ----
+constexpr const char* csv_schema_measure = "slx-1";
+constexpr const char* csv_schema_simulate = "slx-sim-1";
+constexpr const char* csv_schema_analyze = "slx-an-1";
+constexpr const char* csv_measure_columns =
+    "map,m,n,rho,blocks_launched,blocks_void,threads_launched,threads_useful,overhead_num,overhead_den,"
+    "overhead_decimal";
+
+// report.hpp:158-171
+struct measure_row {
+    map_kind kind = map_kind::bb;
+    int m = 2;
+    i64 n = 1;
+    i64 rho = 1;
+    u64 blocks_launched = 0, blocks_void = 0, threads_launched = 0, threads_useful = 0;
+    rational overhead;
+    bool exact = false;
+    data_coord witness{};
+    u64 multiplicity = 0;
+};
+
+// report.hpp:173-186
+inline measure_row row_from_report(const grid_spec& g, const sim_report& rep) {
+    measure_row row;
+    row.kind = g.kind;
+    row.m = g.dims;
+    row.n = g.n;
+    row.rho = g.rho;
+    row.blocks_launched = rep.blocks_launched;
+    row.blocks_void = rep.blocks_void;
+    row.threads_launched = rep.threads_launched;
+    row.threads_useful = rep.threads_useful;
+    row.overhead = rep.space_overhead;
+    return row;
+}
+
+// report.hpp:190-203: one map-kernel launch on the GPU; the coverage multiset
+// is reduced to the first non-1 cell on the device (smx_verify_cover), so only
+// the verdict crosses PCIe.
+inline measure_row measure_grid(const grid_spec& g, bool check_cover = true) {
+    const simplex_spec dom(g.dims, g.domain_side() * g.rho - 1);
+    validate_launch(g, dom);
+    const i64 side = dom.n + 1;
+    const u64 cells = g.dims == 2 ? tri_cells(side) : tet_cells(side);
+    smx_grid r = g.raw();
+    smx_counters c{};
+    u64 first = cells;
+    u32 mult = 0;
+    check(smx_measure_grid(&r, check_cover ? 1 : 0, &c, &first, &mult, nullptr));
+    sim_report rep;
+    rep.m = g.dims;
+    rep.cell_side = side;
+    detail::finish(rep, c);
+    measure_row row = row_from_report(g, rep);
+    if (check_cover) {
+        row.exact = first == cells;
+        if (!row.exact) {
+            u64 rem = first;
+            i64 z = 0;
+            if (g.dims == 3) {
+                while (z + 1 < side && tet_layer_prefix(side, z + 1) <= first) ++z;
+                rem = first - tet_layer_prefix(side, z);
+            }
+            i64 y = 0;
+            while (tri_linear_index(0, y + 1) <= rem) ++y;
+            row.witness = {i64(rem - tri_linear_index(0, y)), y, z};
+            row.multiplicity = mult;
+        }
+    }
+    return row;
+}
+
+// report.hpp:68-110
+struct n_range {
+    i64 lo = 1, hi = 1;
+    bool pow2_only = false;
+};
+
+inline n_range parse_n_range(const std::string& text) {
+    auto parse_int = [](const std::string& s) -> i64 {
+        if (s.empty() || s.find_first_not_of("0123456789") != std::string::npos)
+            throw std::invalid_argument("bad n-range literal: " + s);
+        return i64(std::stoll(s));
+    };
+    const auto dots = text.find("..");
+    if (dots == std::string::npos) {
+        const i64 v = parse_int(text);
+        return {v, v, false};
+    }
+    const i64 lo = parse_int(text.substr(0, dots));
+    std::string rest = text.substr(dots + 2);
+    const std::string tag = "(pow2)";
+    const bool pow2 = rest.size() > tag.size() && rest.compare(rest.size() - tag.size(), tag.size(), tag) == 0;
+    if (pow2) rest.resize(rest.size() - tag.size());
+    const i64 hi = parse_int(rest);
+    if (lo < 1 || hi < lo) throw std::invalid_argument("bad n-range: " + text);
+    return {lo, hi, pow2};
+}
+
+inline std::vector<i64> expand_n_range(const n_range& r) {
+    std::vector<i64> out;
+    if (!r.pow2_only) {
+        for (i64 n = r.lo; n <= r.hi; ++n) out.push_back(n);
+        return out;
+    }
+    for (i64 n = 1; n <= r.hi; n *= 2) {
+        if (n >= r.lo) out.push_back(n);
+        if (n > r.hi / 2) break;
+    }
+    return out;
+}
+
+// report.hpp:324-342. Rows in input order; verify_sweep caps the multiplicity
+// at 255 like the reference's byte-mark walk (measure_grid_compact :287-321).
+inline std::vector<measure_row> verify_sweep(map_kind k, int m, const std::vector<i64>& ns, i64 rho = 1,
+                                             i64 threshold = 1) {
+    std::vector<measure_row> rows;
+    rows.reserve(ns.size());
+    for (i64 n : ns) {
+        measure_row row = measure_grid(make_grid(k, m, n, rho, threshold), true);
+        if (row.multiplicity > 255) row.multiplicity = 255;
+        rows.push_back(row);
+    }
+    return rows;
+}
+
+inline std::vector<measure_row> analyze_sweep(map_kind k, int m, const std::vector<i64>& ns, i64 rho = 1,
+                                              i64 threshold = 1) {
+    std::vector<measure_row> rows;
+    rows.reserve(ns.size());
+    for (i64 n : ns) rows.push_back(measure_grid(make_grid(k, m, n, rho, threshold), false));
+    return rows;
+}
+
+// report.hpp:345-352 (bb: m! - 1, core.hpp:125-128)
+inline rational scheme_overhead_limit(map_kind k, int m) {
+    switch (k) {
+        case map_kind::bb: {
+            i128 f = 1;
+            for (int i = 2; i <= m; ++i) f *= i;
+            return rational(f - 1);
+        }
+        case map_kind::h2d_padded: return rational(3);
+        case map_kind::h3d: return rational(1, 8);
+        default: return rational(0);
+    }
+}
+
+namespace detail {
+inline std::string csv_rational(const rational& r) {
+    return rational::int_text(r.num) + "," + rational::int_text(r.den) + "," + r.to_decimal_string(9);
+}
+inline std::string csv_fields(const measure_row& r) {
+    return std::string(map_kind_name(r.kind)) + "," + std::to_string(r.m) + "," + std::to_string(r.n) + "," +
+           std::to_string(r.rho) + "," + std::to_string(r.blocks_launched) + "," + std::to_string(r.blocks_void) +
+           "," + std::to_string(r.threads_launched) + "," + std::to_string(r.threads_useful) + "," +
+           csv_rational(r.overhead);
+}
+}  // namespace detail
+
+// report.hpp:386-446
+inline std::string csv_measure(const std::vector<measure_row>& rows) {
+    std::string out = std::string("schema,") + csv_measure_columns + "\n";
+    for (const auto& r : rows) out += std::string(csv_schema_measure) + "," + detail::csv_fields(r) + "\n";
+    return out;
+}
+
+inline std::string csv_analyze(const std::vector<measure_row>& rows) {
+    std::string out = std::string("schema,") + csv_measure_columns + ",limit_num,limit_den,limit_decimal\n";
+    for (const auto& r : rows)
+        out += std::string(csv_schema_analyze) + "," + detail::csv_fields(r) + "," +
+               detail::csv_rational(scheme_overhead_limit(r.kind, r.m)) + "\n";
+    return out;
+}
+
+struct simulate_row {
+    measure_row base;
+    kernel_kind kernel = kernel_kind::map;
+    i64 steps = 0;
+    u64 seed = 0;
+    u64 state_hash = 0;
+};
+
+inline std::string csv_simulate(const std::vector<simulate_row>& rows) {
+    std::string out = std::string("schema,") + csv_measure_columns + ",kernel,steps,seed,state_hash\n";
+    for (const auto& r : rows)
+        out += std::string(csv_schema_simulate) + "," + detail::csv_fields(r.base) + "," +
+               kernel_kind_name(r.kernel) + "," + std::to_string(r.steps) + "," + std::to_string(r.seed) + "," +
+               std::to_string(r.state_hash) + "\n";
+    return out;
+}
+
+// report.hpp:475-480
+inline std::string witness_text(const measure_row& r) {
+    std::string out = "(" + std::to_string(r.witness.x) + "," + std::to_string(r.witness.y);
+    if (r.m == 3) out += "," + std::to_string(r.witness.z);
+    return out + ")";
+}
+
+// report.hpp:483-511: one line per row
+inline std::string text_report(const std::vector<measure_row>& rows, bool verified) {
+    std::string out;
+    for (const auto& r : rows) {
+        out += std::string("map=") + map_kind_name(r.kind) + " m=" + std::to_string(r.m) +
+               " n=" + std::to_string(r.n) + " rho=" + std::to_string(r.rho) +
+               " blocks=" + std::to_string(r.blocks_launched) + " void=" + std::to_string(r.blocks_void) +
+               " threads=" + std::to_string(r.threads_launched) + " useful=" + std::to_string(r.threads_useful) +
+               " overhead=" + r.overhead.to_string() + " (" + r.overhead.to_decimal_string(6) + ")";
+        if (verified)
+            out += r.exact ? std::string(" Exact")
+                           : " NotExact witness=" + witness_text(r) + " mult=" + std::to_string(r.multiplicity);
+        out += '\n';
+    }
+    return out;
 }
 
 }  // namespace simplexmap_b200

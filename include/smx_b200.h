@@ -167,6 +167,13 @@ int smx_life_init(int32_t m, int64_t side, uint64_t seed, uint8_t* cells, uint64
 int smx_verify_cover(const uint32_t* coverage, uint64_t ncells, int device_ptr, uint64_t* first_bad,
                      uint32_t* multiplicity, void* stream);
 
+/* measure_grid (report.hpp:190-203) entirely on the device: one map launch
+ * into a zeroed device coverage multiset (pool-owned) and, when check_cover,
+ * the verify_exact_cover reduction above; only counters and the verdict come
+ * back. check_cover = 0 is analyze_sweep's count-only launch. */
+int smx_measure_grid(const smx_grid* g, int check_cover, smx_counters* counters, uint64_t* first_bad,
+                     uint32_t* multiplicity, void* stream);
+
 /* make_edm_points (simulator.hpp:333-343): count points, x then y drawn from
  * one seed-keyed splitmix64 stream; out_xy holds 2*count doubles (host). */
 int smx_make_edm_points(int64_t count, uint64_t seed, double* out_xy);

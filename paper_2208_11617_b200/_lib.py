@@ -88,6 +88,7 @@ _SIGS = {
     "smx_bits_tile_bytes": ([_G, C.c_uint64], C.c_uint64),
     "smx_bits_tiles_pack": ([_G, _VP, _VP, C.c_uint64, _VP, _VP], C.c_int),
     "smx_bits_tiles_unpack": ([_G, _VP, _VP, C.c_uint64, _VP, _VP], C.c_int),
+    "smx_measure_grid": ([_G, C.c_int, _VP, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), _VP], C.c_int),
     "smx_verify_cover": ([_VP, C.c_uint64, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), _VP], C.c_int),
     "smx_edm": ([_G, _VP, C.c_int64, _VP, C.c_uint64, C.c_int32, C.c_int, _VP, _VP, _VP], C.c_int),
     "smx_decompose_trapezoids": ([C.c_int64, C.c_int64, C.POINTER(smx_trapezoid), C.c_int32,

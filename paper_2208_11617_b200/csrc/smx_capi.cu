@@ -863,6 +863,21 @@ int smx_verify_cover(const uint32_t* coverage, uint64_t ncells, int device_ptr, 
     return SMX_OK;
 }
 
+int smx_measure_grid(const smx_grid* g, int check_cover, smx_counters* counters, uint64_t* first_bad,
+                     uint32_t* multiplicity, void* stream) {
+    std::vector<smx::Geom> subs;
+    if (int rc = sub_geoms(g, subs, true)) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!check_cover) return fill_counters(g, counters, s, nullptr);
+    if (!first_bad) return fail(SMX_EINVAL, "null output");
+    const uint64_t ncells = cells_of(g->dims, cell_side_of(g));
+    void* p;
+    if (int rc = pool_get(0, ncells * 4, &p)) return rc;
+    TRY(cudaMemsetAsync(p, 0, ncells * 4, s));
+    if (int rc = fill_counters(g, counters, s, (uint32_t*)p)) return rc;
+    return smx_verify_cover((const uint32_t*)p, ncells, 1, first_bad, multiplicity, stream);
+}
+
 int smx_make_edm_points(int64_t count, uint64_t seed, double* out_xy) {
     if (count < 0) return fail(SMX_EINVAL, "make_edm_points: count must be >= 0");
     if (count > 0 && !out_xy) return fail(SMX_EINVAL, "null output");

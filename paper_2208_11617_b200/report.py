@@ -118,19 +118,20 @@ def _row(g: api.grid_spec, rep: api.sim_report) -> measure_row:
 
 
 def measure_grid(g: api.grid_spec, check_cover: bool = True, _cap: int | None = None) -> measure_row:
-    """report.hpp:190-203: one launch of the map kernel on the GPU; the cover
-    check runs on the device (no coverage copy to the host)."""
-    import torch
+    """report.hpp:190-203: one launch of the map kernel on the GPU into a
+    device-resident coverage multiset, the cover verdict reduced there
+    (smx_measure_grid); only the counters and the verdict reach the host."""
     side = g.cell_side()
     cells = api.tri_cells(side) if g.dims == 2 else api.tet_cells(side)
-    cov = torch.zeros(max(cells, 1), dtype=torch.int32, device="cuda")[:cells] if check_cover else None
-    rep = api.launch_map_device(g, cov)
+    cnt = _lib.smx_counters()
+    first = C.c_uint64(cells)
+    mult = C.c_uint32(0)
+    check(lib().smx_measure_grid(C.byref(g.raw), 1 if check_cover else 0, C.byref(cnt), C.byref(first),
+                                 C.byref(mult), api._stream()))
+    rep = api.sim_report(m=g.dims, cell_side=side)
+    api._finish(rep, cnt)
     row = _row(g, rep)
     if check_cover:
-        first = C.c_uint64(0)
-        mult = C.c_uint32(0)
-        check(lib().smx_verify_cover(api._ptr(cov) if cells else None, cells, 1, C.byref(first), C.byref(mult),
-                                     api._stream()))
         row.exact = first.value == cells
         if not row.exact:
             row.witness = _coord_at(g.dims, side, int(first.value))
@@ -224,6 +225,21 @@ def csv_simulate(rows: list[simulate_row]) -> str:
     return out
 
 
+def text_report(rows: list[measure_row], verified: bool) -> str:
+    """report.hpp:483-511: one human-readable line per row."""
+    out = ""
+    for r in rows:
+        ov = Fraction(r.overhead)
+        frac = str(ov.numerator) if ov.denominator == 1 else f"{ov.numerator}/{ov.denominator}"
+        out += (f"map={api.map_kind_name(r.kind)} m={r.m} n={r.n} rho={r.rho} blocks={r.blocks_launched} "
+                f"void={r.blocks_void} threads={r.threads_launched} useful={r.threads_useful} "
+                f"overhead={frac} ({decimal_string(ov, 6)})")
+        if verified:
+            out += " Exact" if r.exact else f" NotExact witness={witness_text(r)} mult={r.multiplicity}"
+        out += "\n"
+    return out
+
+
 def witness_text(r: measure_row) -> str:
     """report.hpp:475-480"""
     out = f"({r.witness.x},{r.witness.y}"
@@ -234,5 +250,5 @@ def witness_text(r: measure_row) -> str:
 
 __all__ = ["measure_row", "n_range", "parse_n_range", "expand_n_range", "measure_grid", "verify_sweep",
            "analyze_sweep", "scheme_overhead_limit", "decimal_string", "csv_measure", "csv_analyze",
-           "simulate_row", "csv_simulate", "witness_text", "CSV_SCHEMA_MEASURE", "CSV_SCHEMA_SIMULATE",
+           "simulate_row", "csv_simulate", "witness_text", "text_report", "CSV_SCHEMA_MEASURE", "CSV_SCHEMA_SIMULATE",
            "CSV_SCHEMA_ANALYZE", "CSV_MEASURE_COLUMNS", "_lib"]

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <cmath>
 #include <functional>
 
 using namespace simplexmap;
@@ -300,11 +301,106 @@ static void gpu_suite() {
     CHECK_THROWS_AS(launch_ca(g16, domain_of(g16), life, bad), std::invalid_argument);
 }
 
+// report layer (test_report.cpp:128-200), EDM (test_simulator.cpp:199-230),
+// 2-D periodic Life
+static void report_suite() {
+    auto rows = verify_sweep(map_kind::bb, 2, {2, 4});
+    CHECK(csv_measure(rows) ==
+          "schema,map,m,n,rho,blocks_launched,blocks_void,threads_launched,threads_useful,overhead_num,"
+          "overhead_den,overhead_decimal\n"
+          "slx-1,bb,2,2,1,4,1,4,3,1,3,0.333333333\n"
+          "slx-1,bb,2,4,1,16,6,16,10,3,5,0.600000000\n");
+    CHECK(rows[0].exact && rows[1].exact);
+    auto an = csv_analyze(analyze_sweep(map_kind::bb, 3, {4}));
+    CHECK(an.find(",limit_num,limit_den,limit_decimal\n") != std::string::npos);
+    CHECK(an.find("slx-an-1,bb,3,4,1,64,44,64,20,11,5,2.200000000,5,1,5.000000000\n") != std::string::npos);
+    CHECK(csv_analyze(analyze_sweep(map_kind::h3d, 3, {16})).find(",1,8,0.125000000\n") != std::string::npos);
+    CHECK(csv_analyze(analyze_sweep(map_kind::h2d, 2, {16})).find(",0,1,0.000000000,0,1,0.000000000\n") !=
+          std::string::npos);
+    CHECK(scheme_overhead_limit(map_kind::bb, 3) == rational(5));
+    CHECK(scheme_overhead_limit(map_kind::h2d_padded, 2) == rational(3));
+    CHECK(scheme_overhead_limit(map_kind::h2d_trapezoid, 2) == rational(0));
+    // every map family verifies exact over a small n range
+    for (i64 n : expand_n_range(parse_n_range("2..40"))) {
+        CHECK(measure_grid(make_grid(map_kind::h2d_trapezoid, 2, n, 1, 4)).exact);
+        CHECK(measure_grid(make_grid(map_kind::rb, 2, n)).exact);
+        CHECK(measure_grid(make_grid(map_kind::lambda2d, 2, n)).exact);
+        CHECK(measure_grid(make_grid(map_kind::h2d_padded, 2, n)).exact);
+        CHECK(measure_grid(make_grid(map_kind::bb, 3, n)).exact);
+    }
+    CHECK(expand_n_range(parse_n_range("3..40(pow2)")) == (std::vector<i64>{4, 8, 16, 32}));
+    CHECK_THROWS_AS(parse_n_range("5..2"), std::invalid_argument);
+    // text report
+    auto h = verify_sweep(map_kind::h2d, 2, {16});
+    auto text = text_report(h, true);
+    CHECK(text.find("map=h2d m=2 n=16 rho=1 blocks=120 void=0") != std::string::npos);
+    CHECK(text.find(" Exact\n") != std::string::npos);
+    measure_row bad = h[0];
+    bad.exact = false;
+    bad.witness = {2, 5, 0};
+    bad.multiplicity = 0;
+    CHECK(text_report({bad}, true).find("NotExact witness=(2,5) mult=0") != std::string::npos);
+    // simulate CSV over a 2-D Life run on trapezoids
+    auto run = [] {
+        auto g = make_grid(map_kind::h2d_trapezoid, 2, 16, 1, 4);
+        auto state = make_life_state(2, g.domain_side(), 3);
+        launch_opts o;
+        o.steps = 5;
+        o.seed = 3;
+        auto rep = launch_ca(g, domain_of(g), state, o);
+        simulate_row row;
+        row.base = measure_grid(g, true);
+        row.kernel = kernel_kind::ca_life;
+        row.steps = 5;
+        row.seed = 3;
+        row.state_hash = rep.state_hash;
+        return csv_simulate({row});
+    };
+    const std::string a = run();
+    CHECK(a == run());
+    CHECK(a.find(",kernel,steps,seed,state_hash\n") != std::string::npos);
+    CHECK(a.find("slx-sim-1,trapezoid,2,16,1,") != std::string::npos);
+    CHECK(a.find(",ca,5,3,") != std::string::npos);
+    // EDM: every 2-D map gives the same cells; cell (2, 9) is the fixed-order distance
+    for (i64 side : {14, 15}) {
+        auto pts = make_edm_points(side, 7);
+        std::vector<grid_spec> grids = {grid_bb(side, 2), grid_rb(side), grid_lambda(side),
+                                        grid_h2d_padded(side + 1), grid_trapezoids(side + 1, side == 14 ? 1 : 4)};
+        if (side == 15) grids.push_back(grid_h2d(16));
+        std::vector<double> first;
+        for (const auto& g : grids) {
+            simplex_grid_state<double> st(2, side);
+            auto rep = launch_edm(g, domain_of(g), pts, st);
+            CHECK(verify_exact_cover(rep, domain_of(g)).exact);
+            if (first.empty()) first = st.cells;
+            CHECK(st.cells == first);
+            const double dx = pts[2][0] - pts[9][0], dy = pts[2][1] - pts[9][1];
+            CHECK(st.at(2, 9) == std::sqrt(dx * dx + dy * dy));
+            CHECK(st.at(3, 3) == 0.0);
+        }
+    }
+    {
+        auto g = grid_h2d(16);
+        auto pts = make_edm_points(14, 1);
+        simplex_grid_state<double> st(2, 15);
+        CHECK_THROWS_AS(launch_edm(g, domain_of(g), pts, st), std::invalid_argument);
+    }
+    // 2-D periodic Life, seed 42, 64 steps
+    for (auto g : {grid_h2d(64), grid_bb(63, 2), grid_rb(63), grid_lambda(63), grid_trapezoids(64, 4)}) {
+        auto st = make_life_state(2, 63, 42);
+        launch_opts o;
+        o.steps = 64;
+        auto rep = launch_ca(g, domain_of(g), st, o);
+        CHECK(rep.state_hash == 8247929562437622423ull);
+    }
+}
+
 int main(int argc, char** argv) {
     const bool gpu = argc > 1 && std::strcmp(argv[1], "--gpu") == 0;
     try {
         host_suite();
         if (gpu) gpu_suite();
+        if (gpu) report_suite();
     } catch (const std::exception& e) {
         std::printf("FAIL unexpected exception: %s\n", e.what());
         ++g_fail;

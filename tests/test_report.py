@@ -36,3 +36,16 @@ def test_decimals_match_reference_csv(ref):
                                                              [f[1]]], int(f[2])) == Fraction(int(f[12]), int(f[13]))
     assert rp.decimal_string(Fraction(-1, 3), 2) == "-0.33"
     assert rp.decimal_string(Fraction(1, 2), 0) == "1"
+
+
+def test_text_report_lines():
+    """text_report (report.hpp:483-511) on host rows (test_report.cpp:190-200)."""
+    row = rp.measure_row(kind=api.map_kind.h2d, m=2, n=16, rho=1, blocks_launched=120, blocks_void=0,
+                         threads_launched=120, threads_useful=120, overhead=Fraction(0), exact=True)
+    text = rp.text_report([row], True)
+    assert text == ("map=h2d m=2 n=16 rho=1 blocks=120 void=0 threads=120 useful=120 overhead=0 (0.000000)"
+                    " Exact\n")
+    bad = rp.measure_row(kind=api.map_kind.bb, m=3, n=4, blocks_launched=64, blocks_void=44, threads_launched=64,
+                         threads_useful=20, overhead=Fraction(11, 5), witness=api.data_coord(2, 5, 1))
+    assert rp.text_report([bad], True).endswith("overhead=11/5 (2.200000) NotExact witness=(2,5,1) mult=0\n")
+    assert "Exact" not in rp.text_report([bad], False)
