@@ -1,6 +1,7 @@
 // The C ABI (include/smx_b200.h): argument validation with the reference's
 // contract messages, host<->device staging for host-buffer calls, the per-side
 // layer-prefix tables, and dispatch to the sm_100a kernels.
+#include <algorithm>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -107,11 +108,16 @@ int pool_get(int slot, size_t bytes, void** out) {
     if (int rc = device_res(&r)) return rc;
     std::lock_guard<std::mutex> lk(g_mu);
     if (r->pool_bytes[slot] < bytes) {
+        // sweeps grow a slot grid after grid: below 256 MiB reserve 2x so a
+        // monotone sweep reallocates O(log) times (cudaFree synchronises)
+        constexpr size_t kGeom = size_t(256) << 20;
+        size_t want = bytes;
+        if (bytes < kGeom) want = std::max(bytes, std::min(2 * r->pool_bytes[slot], kGeom));
         if (r->pool[slot]) TRY(cudaFree(r->pool[slot]));
         r->pool[slot] = nullptr;
         r->pool_bytes[slot] = 0;
-        TRY(cudaMalloc(&r->pool[slot], bytes + 256));  // 16B-granule reads past the end stay inside
-        r->pool_bytes[slot] = bytes;
+        TRY(cudaMalloc(&r->pool[slot], want + 256));  // 16B-granule reads past the end stay inside
+        r->pool_bytes[slot] = want;
     }
     *out = r->pool[slot];
     return SMX_OK;
@@ -669,6 +675,7 @@ int smx_ca_step(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint64_t n
     if (g && g->dims == 2) {
         if (int rc = ca_validate(g, ncells, &exec)) return rc;
         if (cur == next) return fail(SMX_EINVAL, "ca_step: cur and next must not alias");
+        if (int rc = check_align16(cur, next)) return rc;
         return ca2d_step(g, cur, next, exec, (cudaStream_t)stream);
     }
     smx::Geom k;

@@ -12,11 +12,12 @@
 //    coordinates outside T(S) (x > y) read as dead; B3/S23.
 //
 // Each in two execution schemes: BLOCK (the paper's launch model: one CTA per
-// map block, rho^2 threads) and RUNS (a warp maps 32 blocks, merges x-adjacent
-// tiles, and each warp streams whole cell rows of the runs: coalesced 8-byte
-// (EDM) / 1-byte (Life) stores, lane-consecutive cells).
+// map block, rho^2 threads) and RUNS (a warp maps 32 blocks and merges
+// x-adjacent tiles into runs; EDM streams whole cell rows of the runs with
+// lane-consecutive 8-byte stores, Life cuts them into 32-cell bit-sliced items).
 #include "smx_common.cuh"
 #include "smx_launch.hpp"
+#include "smx_ca_common.cuh"
 #include "smx_runs.cuh"
 
 namespace smx {
@@ -105,76 +106,108 @@ __global__ void k_ca2d_block(Geom g, const uint8_t* __restrict__ cur, uint8_t* _
         }
 }
 
-// bytes [a, a + 4) of a u8 array through aligned 32-bit loads (the packed rows
-// have arbitrary byte alignment)
-__device__ __forceinline__ void load8(const uint8_t* __restrict__ p, unsigned long long a, uint32_t& lo,
-                                      uint32_t& hi) {
-    const unsigned long long b = a & ~3ull;
-    const uint32_t* q = reinterpret_cast<const uint32_t*>(p + b);
-    const uint32_t w0 = __ldg(q), w1 = __ldg(q + 1), w2 = __ldg(q + 2);
-    const int sh = int(a - b) * 8;
-    lo = __funnelshift_r(w0, w1, sh);
-    hi = __funnelshift_r(w1, w2, sh);
+// 16 cells of a u8 state at 16-aligned packed index q; zero past the end
+// (and for q < 0), so windows that run off the array read dead cells
+__device__ __forceinline__ uint4 load_cells16(const uint8_t* __restrict__ cur, long long q, long long ncells) {
+    if (q < 0 || q >= ncells) return make_uint4(0, 0, 0, 0);
+    uint4 v = __ldg(reinterpret_cast<const uint4*>(cur + q));
+    if (q + 16 > ncells) {  // bytes past the last cell are not state: clear them
+        const int keep = int(ncells - q);
+        uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int k = keep - 4 * i;
+            w[i] = k >= 4 ? w[i] : (k <= 0 ? 0u : (w[i] & (0xffffffffu >> (32 - 8 * k))));
+        }
+    }
+    return v;
 }
 
-// exact per-byte "== 0" for bytes < 0x80: bit 7 of each byte
-__device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {
-    return ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;
+// One row's contribution to the 3x3 sums of the 32 cells x0 .. x0+31: bits of
+// cells x0-1 .. x0+32 of row (start index Rr, length len; cells outside
+// [0, len) are dead) -> the horizontal 3-sum as two bit-planes (s0, s1).
+__device__ __forceinline__ void row_hsum(const uint8_t* __restrict__ cur, long long ncells, long long Rr, int len,
+                                         int x0, uint32_t& s0, uint32_t& s1, uint32_t* centre) {
+    const long long p = Rr + x0 - 1;
+    const long long q = p & ~15ll;
+    const int d = int(p - q);
+    const uint32_t lo = ca::pack32(load_cells16(cur, q, ncells), load_cells16(cur, q + 16, ncells));
+    const uint32_t hi = ca::pack32(load_cells16(cur, q + 32, ncells), load_cells16(cur, q + 48, ncells));
+    uint32_t M = __funnelshift_r(lo, hi, d);  // bit j = cell x0 - 1 + j
+    uint32_t T = (hi >> d) & 3u;              // cells x0 + 31, x0 + 32
+    M &= ca::range_mask(1 - x0, len - x0);
+    T &= ((x0 + 31 >= 0 && x0 + 31 < len) ? 1u : 0u) | ((x0 + 32 >= 0 && x0 + 32 < len) ? 2u : 0u);
+    const uint32_t l = M, c = (M >> 1) | (T << 31), r = (M >> 2) | (T << 30);
+    s0 = l ^ c ^ r;
+    s1 = (l & c) | (l & r) | (c & r);
+    if (centre) *centre = c;
 }
 
-// 3 cells' horizontal sums of one row, for the 4 cells x .. x+3 (bytes x-1 .. x+4
-// at packed index a = row + x - 1): left + centre + right, <= 3 per byte
-__device__ __forceinline__ uint32_t hsum4(const uint8_t* __restrict__ cur, unsigned long long a, uint32_t* centre) {
-    uint32_t L, H;
-    load8(cur, a, L, H);
-    const uint32_t C = __funnelshift_r(L, H, 8), R = __funnelshift_r(L, H, 16);
-    if (centre) *centre = C;
-    return L + C + R;
-}
-
-// periodic 2-D Life, x-run scheme: a warp per cell row of a run; lane per
-// 4-byte-aligned output word. Interior words (no wrap, every neighbour row
-// long enough) are computed SWAR: three rows' horizontal sums added bytewise
-// (<= 9 per byte), B3/S23 as (S == 3) | (alive & S == 4) with an exact
-// per-byte zero test; wrap-around, row-end and partial words fall back to the
-// per-cell rule.
+// periodic 2-D Life, x-run scheme, bit-sliced: the CTA's warp 0 maps a strip
+// of KX blocks and merges runs; the run rows are cut into 32-cell items
+// aligned in the packed array (one lane each: 3 rows x 64 bytes of 16-byte
+// loads -> bit windows -> 3x3 sum as bit-planes -> B3/S23 for 32 cells at
+// once -> two 16-byte stores). Rows 1 .. S-3 never wrap (a wrapped neighbour
+// of theirs lies outside T(S) and reads dead), so the windows only mask the
+// row ends; rows 0, S-2, S-1 take the per-cell rule. An item writes only the
+// bytes of its own run row (whole 16-byte halves where it owns them).
 template <int KIND>
 __global__ void __launch_bounds__(T2_THREADS) k_ca2d_runs(Geom g, const uint8_t* __restrict__ cur,
                                                           uint8_t* __restrict__ next) {
     __shared__ int s_run[T2_KX][3];
     __shared__ int s_nruns;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ int s_pre[T2_KX + 1];
+    const int warp = threadIdx.x >> 5;
     if (warp == 0) strip_runs<KIND, T2_KX>(g, blockIdx.x * T2_KX, blockIdx.y, s_run, &s_nruns);
     __syncthreads();
-    const int rows = s_nruns * g.rho, S = g.side;
-    for (int rr = warp; rr < rows; rr += T2_THREADS / 32) {
+    const int rho = g.rho, S = g.side;
+    if (threadIdx.x == 0) {  // items per run: rho rows x (chunks per row + 1 for misalignment)
+        int t = 0;
+        for (int r = 0; r < s_nruns; ++r) {
+            s_pre[r] = t;
+            t += rho * ((s_run[r][2] * rho + 31) / 32 + 1);
+        }
+        s_pre[s_nruns] = t;
+    }
+    __syncthreads();
+    const long long ncells = (long long)tri_idx(0, S);  // T(S) cells
+    const int total = s_pre[s_nruns];
+    for (int it = threadIdx.x; it < total; it += T2_THREADS) {
+        int r = 0;
+        while (s_pre[r + 1] <= it) ++r;
+        const int cpr = (s_run[r][2] * rho + 31) / 32 + 1;
+        const int k = it - s_pre[r], row = k / cpr, c = k - row * cpr;
         int cy, xlo, xhi;
-        if (!run_row(s_run, rr, g.rho, S, &cy, &xlo, &xhi)) continue;
-        const unsigned long long R = tri_idx(0, cy);
-        const unsigned long long E0 = R + xlo, E1 = R + xhi;
-        const unsigned long long A0 = (E0 + 3) & ~3ull, A1 = E1 & ~3ull;
-        const bool yin = cy >= 1 && cy <= S - 2;  // no vertical wrap
-        const unsigned long long Rm = yin ? tri_idx(0, cy - 1) : 0, Rp = yin ? tri_idx(0, cy + 1) : 0;
-        if (A0 < A1) {
-            for (unsigned long long A = A0 + 4ull * lane; A < A1; A += 128) {
-                const int x = int(A - R);
-                if (yin && x >= 1 && x + 4 <= cy - 1) {
-                    uint32_t self;
-                    const uint32_t t = hsum4(cur, Rm + x - 1, nullptr) + hsum4(cur, R + x - 1, &self) +
-                                       hsum4(cur, Rp + x - 1, nullptr);
-                    const uint32_t eq3 = zero_bytes(t ^ 0x03030303u), eq4 = zero_bytes(t ^ 0x04040404u);
-                    *reinterpret_cast<uint32_t*>(next + A) = ((eq3 | (eq4 & (self << 7))) >> 7) & 0x01010101u;
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) next[A + j] = life2d_cell(cur, S, x + j, cy);
-                }
-            }
-            // head [E0, A0) and tail [A1, E1): at most 3 + 3 cells
-            const int nh = int(A0 - E0), nt = int(E1 - A1);
-            if (lane < nh) next[E0 + lane] = life2d_cell(cur, S, xlo + lane, cy);
-            else if (lane >= 8 && lane - 8 < nt) next[A1 + lane - 8] = life2d_cell(cur, S, int(A1 - R) + lane - 8, cy);
+        if (!run_row(s_run, r * rho + row, rho, S, &cy, &xlo, &xhi)) continue;
+        const long long R = (long long)tri_idx(0, cy);
+        const long long E0 = R + xlo, E1 = R + xhi;
+        const long long A = (E0 & ~31ll) + 32ll * c;
+        if (A >= E1) continue;
+        const int x0 = int(A - R);
+        uint32_t res = 0;
+        if (cy >= 1 && cy <= S - 3) {
+            uint32_t a0, a1, b0, b1, c0, c1, alive;
+            row_hsum(cur, ncells, R - cy, cy, x0, a0, a1, nullptr);
+            row_hsum(cur, ncells, R, cy + 1, x0, b0, b1, &alive);
+            row_hsum(cur, ncells, R + cy + 1, cy + 2, x0, c0, c1, nullptr);
+            const ca::Planes4 t = ca::add3x2(a0, a1, b0, b1, c0, c1);  // 9-sum incl. the cell
+            const uint32_t eq3 = ~t.b3 & ~t.b2 & t.b1 & t.b0, eq4 = ~t.b3 & t.b2 & ~t.b1 & ~t.b0;
+            res = eq3 | (eq4 & alive);
         } else {
-            for (int x = xlo + lane; x < xhi; x += 32) next[R + x] = life2d_cell(cur, S, x, cy);
+            for (int j = 0; j < 32; ++j)
+                if (A + j >= E0 && A + j < E1) res |= uint32_t(life2d_cell(cur, S, x0 + j, cy)) << j;
+        }
+        const uint4 v0 = ca::spread16(res & 0xffffu), v1 = ca::spread16(res >> 16);
+        uint4* o = reinterpret_cast<uint4*>(next + A);
+        if (A >= E0 && A + 16 <= E1) o[0] = v0;
+        if (A + 16 >= E0 && A + 32 <= E1) o[1] = v1;
+        if (A < E0 || A + 32 > E1) {  // the run row's first / last item: its own bytes of a shared half
+            const bool h0 = A >= E0 && A + 16 <= E1, h1 = A + 16 >= E0 && A + 32 <= E1;
+            for (int j = 0; j < 32; ++j) {
+                const long long e = A + j;
+                if (e < E0 || e >= E1 || (j < 16 ? h0 : h1)) continue;
+                next[e] = uint8_t((res >> j) & 1u);
+            }
         }
     }
 }
