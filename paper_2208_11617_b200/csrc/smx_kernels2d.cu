@@ -106,33 +106,50 @@ __global__ void k_ca2d_block(Geom g, const uint8_t* __restrict__ cur, uint8_t* _
         }
 }
 
-// 16 cells of a u8 state at 16-aligned packed index q; zero past the end
-// (and for q < 0), so windows that run off the array read dead cells
-__device__ __forceinline__ uint4 load_cells16(const uint8_t* __restrict__ cur, long long q, long long ncells) {
-    if (q < 0 || q >= ncells) return make_uint4(0, 0, 0, 0);
-    uint4 v = __ldg(reinterpret_cast<const uint4*>(cur + q));
-    if (q + 16 > ncells) {  // bytes past the last cell are not state: clear them
-        const int keep = int(ncells - q);
-        uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+// The bit-sliced 2-D Life kernel indexes the packed state with IDX: int when
+// T(S) < 2^31 (every 2-D configuration up to side ~65K), else long long.
+
+// 16 cells of a u8 state at 16-aligned packed index q. GUARD: zero outside
+// [0, ncells) (bytes past the last cell are not state), for windows that run
+// off either end of the array.
+template <bool GUARD, typename IDX>
+__device__ __forceinline__ uint4 load_cells16(const uint8_t* __restrict__ cur, IDX q, IDX ncells) {
+    if (GUARD) {
+        if (q < 0 || q >= ncells) return make_uint4(0, 0, 0, 0);
+        uint4 v = __ldg(reinterpret_cast<const uint4*>(cur + q));
+        if (q + 16 > ncells) {
+            const int keep = int(ncells - q);
+            uint32_t* w = reinterpret_cast<uint32_t*>(&v);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int k = keep - 4 * i;
-            w[i] = k >= 4 ? w[i] : (k <= 0 ? 0u : (w[i] & (0xffffffffu >> (32 - 8 * k))));
+            for (int i = 0; i < 4; ++i) {
+                const int k = keep - 4 * i;
+                w[i] = k >= 4 ? w[i] : (k <= 0 ? 0u : (w[i] & (0xffffffffu >> (32 - 8 * k))));
+            }
         }
+        return v;
     }
-    return v;
+    return __ldg(reinterpret_cast<const uint4*>(cur + q));
 }
 
 // One row's contribution to the 3x3 sums of the 32 cells x0 .. x0+31: bits of
-// cells x0-1 .. x0+32 of row (start index Rr, length len; cells outside
-// [0, len) are dead) -> the horizontal 3-sum as two bit-planes (s0, s1).
-__device__ __forceinline__ void row_hsum(const uint8_t* __restrict__ cur, long long ncells, long long Rr, int len,
-                                         int x0, uint32_t& s0, uint32_t& s1, uint32_t* centre) {
-    const long long p = Rr + x0 - 1;
-    const long long q = p & ~15ll;
+// cells x0-1 .. x0+32 of the row starting at packed index Rr with len cells
+// (cells outside [0, len) are dead) -> the horizontal 3-sum as two bit-planes.
+template <bool GUARD, typename IDX>
+__device__ __forceinline__ void row_hsum(const uint8_t* __restrict__ cur, IDX ncells, IDX Rr, int len, int x0,
+                                         uint32_t& s0, uint32_t& s1, uint32_t* centre) {
+    const IDX p = Rr + x0 - 1;
+    const IDX q = p & ~IDX(15);
     const int d = int(p - q);
-    const uint32_t lo = ca::pack32(load_cells16(cur, q, ncells), load_cells16(cur, q + 16, ncells));
-    const uint32_t hi = ca::pack32(load_cells16(cur, q + 32, ncells), load_cells16(cur, q + 48, ncells));
+    const uint8_t* b = cur + q;
+    uint32_t lo, hi;
+    if (GUARD) {
+        lo = ca::pack32(load_cells16<true>(cur, q, ncells), load_cells16<true>(cur, q + 16, ncells));
+        hi = ca::pack32(load_cells16<true>(cur, q + 32, ncells), load_cells16<true>(cur, q + 48, ncells));
+    } else {
+        const uint4* v = reinterpret_cast<const uint4*>(b);
+        lo = ca::pack32(__ldg(v), __ldg(v + 1));
+        hi = ca::pack32(__ldg(v + 2), __ldg(v + 3));
+    }
     uint32_t M = __funnelshift_r(lo, hi, d);  // bit j = cell x0 - 1 + j
     uint32_t T = (hi >> d) & 3u;              // cells x0 + 31, x0 + 32
     M &= ca::range_mask(1 - x0, len - x0);
@@ -143,71 +160,113 @@ __device__ __forceinline__ void row_hsum(const uint8_t* __restrict__ cur, long l
     if (centre) *centre = c;
 }
 
-// periodic 2-D Life, x-run scheme, bit-sliced: the CTA's warp 0 maps a strip
-// of KX blocks and merges runs; the run rows are cut into 32-cell items
-// aligned in the packed array (one lane each: 3 rows x 64 bytes of 16-byte
-// loads -> bit windows -> 3x3 sum as bit-planes -> B3/S23 for 32 cells at
-// once -> two 16-byte stores). Rows 1 .. S-3 never wrap (a wrapped neighbour
-// of theirs lies outside T(S) and reads dead), so the windows only mask the
-// row ends; rows 0, S-2, S-1 take the per-cell rule. An item writes only the
-// bytes of its own run row (whole 16-byte halves where it owns them).
-template <int KIND>
+// next-state bits of cells x0 .. x0+31 of row cy (start R), 1 <= cy <= S-3
+// (bits past the row end are junk; callers mask them)
+template <typename IDX>
+__device__ __forceinline__ uint32_t life2d_bits(const uint8_t* __restrict__ cur, IDX ncells, IDX R, int cy, int x0) {
+    uint32_t a0, a1, b0, b1, c0, c1, alive;
+    if (R - cy + x0 - 1 < 16 || R + cy + 1 + x0 + 63 >= ncells) {  // a window runs off the array
+        row_hsum<true>(cur, ncells, R - cy, cy, x0, a0, a1, nullptr);
+        row_hsum<true>(cur, ncells, R, cy + 1, x0, b0, b1, &alive);
+        row_hsum<true>(cur, ncells, R + cy + 1, cy + 2, x0, c0, c1, nullptr);
+    } else {
+        row_hsum<false>(cur, ncells, R - cy, cy, x0, a0, a1, nullptr);
+        row_hsum<false>(cur, ncells, R, cy + 1, x0, b0, b1, &alive);
+        row_hsum<false>(cur, ncells, R + cy + 1, cy + 2, x0, c0, c1, nullptr);
+    }
+    const ca::Planes4 t = ca::add3x2(a0, a1, b0, b1, c0, c1);  // 9-sum incl. the cell
+    return (~t.b3 & ~t.b2 & t.b1 & t.b0) | (~t.b3 & t.b2 & ~t.b1 & ~t.b0 & alive);
+}
+
+// Strips per CTA for the 2-D x-run Life kernel: ~256+ chunks per CTA at rho >= 8,
+// bounded by shared memory below.
+__host__ __device__ constexpr int ca2d_strips(int rho) { return rho >= 16 ? 2 : (rho >= 8 ? 8 : 32); }
+
+// periodic 2-D Life, x-run scheme, bit-sliced. The CTA's warps map NS strips
+// of KX blocks (NS consecutive grid rows) and merge x-adjacent tiles into runs.
+// Work is cut into 32-cell chunks aligned in the packed array; a chunk belongs
+// to the run row holding its first cell (the maps tile T(S) exactly, so every
+// chunk has one owner), and one thread computes all 32 cells, across a row end
+// if need be: 3 rows x 64 bytes of 16-byte loads -> bit windows -> the 3x3
+// sum as bit-planes -> B3/S23 for 32 cells at once -> two 16-byte stores.
+// Rows 1 .. S-3 never wrap (their wrapped neighbours lie outside T(S) and read
+// dead), so windows only mask row ends; chunks touching rows 0, S-2, S-1 (or
+// more than two rows, near the apex) take the per-cell rule.
+template <int KIND, int NS, typename IDX>
 __global__ void __launch_bounds__(T2_THREADS) k_ca2d_runs(Geom g, const uint8_t* __restrict__ cur,
                                                           uint8_t* __restrict__ next) {
-    __shared__ int s_run[T2_KX][3];
-    __shared__ int s_nruns;
-    __shared__ int s_pre[T2_KX + 1];
+    constexpr int NR = NS * T2_KX;
+    __shared__ int s_run[NR][3];
+    __shared__ int s_nr[NS];
+    __shared__ int s_pre[NR + 1];
+    __shared__ int s_cpr[NR];
     const int warp = threadIdx.x >> 5;
-    if (warp == 0) strip_runs<KIND, T2_KX>(g, blockIdx.x * T2_KX, blockIdx.y, s_run, &s_nruns);
-    __syncthreads();
     const int rho = g.rho, S = g.side;
-    if (threadIdx.x == 0) {  // items per run: rho rows x (chunks per row + 1 for misalignment)
-        int t = 0;
-        for (int r = 0; r < s_nruns; ++r) {
-            s_pre[r] = t;
-            t += rho * ((s_run[r][2] * rho + 31) / 32 + 1);
-        }
-        s_pre[s_nruns] = t;
+    for (int st = warp; st < NS; st += T2_THREADS / 32) {
+        const int wy = blockIdx.y * NS + st;
+        if (wy < g.ey) strip_runs<KIND, T2_KX>(g, blockIdx.x * T2_KX, wy, s_run + st * T2_KX, &s_nr[st]);
+        else if ((threadIdx.x & 31) == 0) s_nr[st] = 0;
     }
     __syncthreads();
-    const long long ncells = (long long)tri_idx(0, S);  // T(S) cells
-    const int total = s_pre[s_nruns];
-    for (int it = threadIdx.x; it < total; it += T2_THREADS) {
-        int r = 0;
-        while (s_pre[r + 1] <= it) ++r;
-        const int cpr = (s_run[r][2] * rho + 31) / 32 + 1;
-        const int k = it - s_pre[r], row = k / cpr, c = k - row * cpr;
-        int cy, xlo, xhi;
-        if (!run_row(s_run, r * rho + row, rho, S, &cy, &xlo, &xhi)) continue;
-        const long long R = (long long)tri_idx(0, cy);
-        const long long E0 = R + xlo, E1 = R + xhi;
-        const long long A = (E0 & ~31ll) + 32ll * c;
-        if (A >= E1) continue;
-        const int x0 = int(A - R);
-        uint32_t res = 0;
-        if (cy >= 1 && cy <= S - 3) {
-            uint32_t a0, a1, b0, b1, c0, c1, alive;
-            row_hsum(cur, ncells, R - cy, cy, x0, a0, a1, nullptr);
-            row_hsum(cur, ncells, R, cy + 1, x0, b0, b1, &alive);
-            row_hsum(cur, ncells, R + cy + 1, cy + 2, x0, c0, c1, nullptr);
-            const ca::Planes4 t = ca::add3x2(a0, a1, b0, b1, c0, c1);  // 9-sum incl. the cell
-            const uint32_t eq3 = ~t.b3 & ~t.b2 & t.b1 & t.b0, eq4 = ~t.b3 & t.b2 & ~t.b1 & ~t.b0;
-            res = eq3 | (eq4 & alive);
-        } else {
-            for (int j = 0; j < 32; ++j)
-                if (A + j >= E0 && A + j < E1) res |= uint32_t(life2d_cell(cur, S, x0 + j, cy)) << j;
-        }
-        const uint4 v0 = ca::spread16(res & 0xffffu), v1 = ca::spread16(res >> 16);
-        uint4* o = reinterpret_cast<uint4*>(next + A);
-        if (A >= E0 && A + 16 <= E1) o[0] = v0;
-        if (A + 16 >= E0 && A + 32 <= E1) o[1] = v1;
-        if (A < E0 || A + 32 > E1) {  // the run row's first / last item: its own bytes of a shared half
-            const bool h0 = A >= E0 && A + 16 <= E1, h1 = A + 16 >= E0 && A + 32 <= E1;
-            for (int j = 0; j < 32; ++j) {
-                const long long e = A + j;
-                if (e < E0 || e >= E1 || (j < 16 ? h0 : h1)) continue;
-                next[e] = uint8_t((res >> j) & 1u);
+    if (threadIdx.x == 0) {  // compact the strips' runs; chunks per run: rho rows x chunk starts per row
+        int n = 0, t = 0;
+        for (int st = 0; st < NS; ++st)
+            for (int r = 0; r < s_nr[st]; ++r, ++n) {
+                const int* src = s_run[st * T2_KX + r];
+                s_run[n][0] = src[0], s_run[n][1] = src[1], s_run[n][2] = src[2];
+                const int cpr = (src[2] * rho + 31) / 32;  // >= the chunk starts in any of its rows
+                s_cpr[n] = cpr;
+                s_pre[n] = t;
+                t += rho * cpr;
             }
+        s_pre[n] = t;
+        s_nr[0] = n;
+    }
+    __syncthreads();
+    const int nruns = s_nr[0];
+    const IDX ncells = IDX((unsigned long long)S * (S + 1) / 2);  // T(S) cells
+    const int total = s_pre[nruns];
+    for (int it = threadIdx.x; it < total; it += T2_THREADS) {
+        int lo = 0, hi = nruns - 1;  // run r: s_pre[r] <= it < s_pre[r + 1]
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_pre[mid] <= it) lo = mid;
+            else hi = mid - 1;
+        }
+        const int r = lo, cpr = s_cpr[r], k = it - s_pre[r];
+        int ly = int(__fdividef(float(k) + 0.5f, float(cpr)));  // k / cpr (exact after the fix-up)
+        ly -= ly * cpr > k;
+        ly += (ly + 1) * cpr <= k;
+        const int cy = s_run[r][1] * rho + ly, xlo = s_run[r][0] * rho;
+        const int xhi = min((s_run[r][0] + s_run[r][2]) * rho, cy + 1);
+        if (cy > S - 1 || xlo >= xhi) continue;
+        const IDX R = IDX(((unsigned long long)cy * (cy + 1)) >> 1);
+        const IDX A = ((R + xlo + 31) & ~IDX(31)) + 32 * (k - ly * cpr);  // chunk starts inside [E0, E1)
+        if (A >= R + xhi) continue;
+        const int x0 = int(A - R);
+        uint32_t res;
+        if (cy >= 1 && cy <= S - 3 && x0 + 31 <= cy) {  // wholly inside row cy
+            res = life2d_bits(cur, ncells, R, cy, x0);
+        } else if (cy >= 1 && cy + 1 <= S - 3 && A + 32 <= R + 2 * cy + 3) {  // rows cy, cy + 1
+            const int n0 = cy - x0 + 1;  // cells of row cy in the chunk
+            const uint32_t m0 = (1u << n0) - 1u;
+            res = (life2d_bits(cur, ncells, R, cy, x0) & m0) |
+                  (life2d_bits(cur, ncells, IDX(R + cy + 1), cy + 1, x0 - cy - 1) & ~m0);
+        } else {  // per cell, rows found by walking down from cy
+            res = 0;
+            IDX Ry = R;
+            int y = cy;
+            for (int b = 0; b < 32 && A + b < ncells; ++b) {
+                while (A + b >= Ry + y + 1) Ry += y + 1, ++y;
+                res |= uint32_t(life2d_cell(cur, S, int(A + b - Ry), y)) << b;
+            }
+        }
+        if (A + 32 <= ncells) {
+            uint4* o = reinterpret_cast<uint4*>(next + A);
+            o[0] = ca::spread16(res & 0xffffu);
+            o[1] = ca::spread16(res >> 16);
+        } else {
+            for (int b = 0; A + b < ncells; ++b) next[A + b] = uint8_t((res >> b) & 1u);
         }
     }
 }
@@ -241,7 +300,22 @@ void launch_edm_k(const Geom& g, const double* pts, double* cells, int exec, cud
 template <int KIND>
 void launch_ca2d_k(const Geom& g, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s) {
     if (exec == SMX_EXEC_BLOCK) k_ca2d_block<KIND><<<dim3(g.ex, g.ey, 1), block2(g), 0, s>>>(g, cur, next);
-    else k_ca2d_runs<KIND><<<dim3((g.ex + T2_KX - 1) / T2_KX, g.ey, 1), T2_THREADS, 0, s>>>(g, cur, next);
+    else {
+        const dim3 grid((g.ex + T2_KX - 1) / T2_KX, (g.ey + ca2d_strips(g.rho) - 1) / ca2d_strips(g.rho), 1);
+        if ((unsigned long long)g.side * (g.side + 1) / 2 + 64 < (1ull << 31)) {
+            switch (ca2d_strips(g.rho)) {
+                case 2: k_ca2d_runs<KIND, 2, int><<<grid, T2_THREADS, 0, s>>>(g, cur, next); break;
+                case 8: k_ca2d_runs<KIND, 8, int><<<grid, T2_THREADS, 0, s>>>(g, cur, next); break;
+                default: k_ca2d_runs<KIND, 32, int><<<grid, T2_THREADS, 0, s>>>(g, cur, next); break;
+            }
+        } else {
+            switch (ca2d_strips(g.rho)) {
+                case 2: k_ca2d_runs<KIND, 2, long long><<<grid, T2_THREADS, 0, s>>>(g, cur, next); break;
+                case 8: k_ca2d_runs<KIND, 8, long long><<<grid, T2_THREADS, 0, s>>>(g, cur, next); break;
+                default: k_ca2d_runs<KIND, 32, long long><<<grid, T2_THREADS, 0, s>>>(g, cur, next); break;
+            }
+        }
+    }
 }
 
 }  // namespace

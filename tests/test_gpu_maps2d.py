@@ -160,3 +160,52 @@ def test_ca2d_periodic_vs_reference(cuda, ex):
                           api.launch_opts(steps=64, boundary=api.ca_boundary.periodic2d, exec=ex,
                                           record_coverage=False))
             assert st.hash() == seq[(side, 64, seed)], (side, seed, g, ex)
+
+
+def test_ca2d_runs_every_small_side_vs_restated(cuda, orc):
+    """The bit-sliced x-run 2-D Life kernel against the restated oracle for every
+    side 1..80 and rho in {1, 3, 16} (odd alignments of every packed row, the
+    wrap rows 0 / S-2 / S-1, runs shorter and longer than one 32-cell item),
+    through H, BB, RB and trapezoid grids; 3 steps each."""
+    import torch
+    def run(g, init):
+        a = torch.from_numpy(init.copy()).cuda()
+        b = torch.empty_like(a)
+        for _ in range(3):
+            api.ca_step_device(g, a, b, api.EXEC_RUNS)
+            a, b = b, a
+        return a.cpu().numpy()
+
+    for side in range(1, 81):
+        init = orc.make_life_state(2, side, 1000 + side)
+        want = orc.ca2d_run(side, 3, init.copy())
+        for rho in (1, 3, 16):
+            if side % rho == 0:
+                for kind in (api.map_kind.bb, api.map_kind.rb):
+                    g = api.make_grid(kind, 2, side // rho, rho)
+                    assert np.array_equal(run(g, init), want), (side, rho, g)
+    for side in range(1, 81):
+        init = orc.make_life_state(2, side, 7 * side)
+        want = orc.ca2d_run(side, 3, init.copy())
+        grids = [api.grid_trapezoids(side + 1, 4), api.grid_lambda(side)]
+        n = side + 1
+        if n & (n - 1) == 0 and n >= 2:
+            grids.append(api.grid_h2d(n))
+        for g in grids:
+            assert np.array_equal(run(g, init), want), (side, g)
+
+
+def test_ca2d_runs_large_rho16_vs_block(cuda):
+    """F3's shape (H2D n=1024, rho=16, side 16368): one RUNS step equals one
+    BLOCK step cell for cell, and the same for BB over the same domain."""
+    import torch
+    gh = api.make_grid(api.map_kind.h2d, 2, 1024, 16)
+    gb = api.make_grid(api.map_kind.bb, 2, 1023, 16)
+    side = gh.cell_side()
+    a = torch.empty(api.tri_cells(side), dtype=torch.uint8, device="cuda")
+    api.life_init_device(2, side, 42, a)
+    r1, r2, r3 = torch.empty_like(a), torch.empty_like(a), torch.empty_like(a)
+    api.ca_step_device(gh, a, r1, api.EXEC_RUNS)
+    api.ca_step_device(gh, a, r2, api.EXEC_BLOCK)
+    api.ca_step_device(gb, a, r3, api.EXEC_RUNS)
+    assert torch.equal(r1, r2) and torch.equal(r1, r3)

@@ -3,6 +3,7 @@
     python tools/prof_case.py ca  h3d 256 8 [runs|block] [iters]
     python tools/prof_case.py accum h2d 4096 16 [runs|block] [iters]
     python tools/prof_case.py map h3d 256 1
+    python tools/prof_case.py ca2d h2d 4096 16 [runs|block] [iters]
 """
 import os
 import statistics
@@ -20,7 +21,7 @@ def main():
     what, kind, n, rho = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4])
     ex = {"runs": api.EXEC_RUNS, "block": api.EXEC_BLOCK, "bits": api.EXEC_BITS}[sys.argv[5] if len(sys.argv) > 5 else "runs"]
     iters = int(sys.argv[6]) if len(sys.argv) > 6 else 5
-    m = 2 if what == "accum" or (what == "map" and kind == "h2d") else 3
+    m = 2 if what in ("accum", "ca2d") or (what == "map" and kind == "h2d") else 3
     if what == "map" and kind == "bb" and len(sys.argv) > 7:
         m = int(sys.argv[7])
     g = api.make_grid(api.map_kind[kind], m, n, rho)
@@ -42,6 +43,14 @@ def main():
         K = 10
         fn = lambda i: api.ca_device(g, a, K, ex, scratch)  # noqa: E731
         cells_done = cells * K
+    elif what == "ca2d":
+        cells = api.tri_cells(side)
+        a = torch.empty(cells, dtype=torch.uint8, device="cuda")
+        b = torch.empty_like(a)
+        api.life_init_device(2, side, 42, a)
+        bufs = [a, b]
+        fn = lambda i: api.ca_step_device(g, bufs[i % 2], bufs[(i + 1) % 2], ex)  # noqa: E731
+        cells_done = cells
     elif what == "accum":
         cells = api.tri_cells(side)
         a = torch.zeros(cells, dtype=torch.int32, device="cuda")
