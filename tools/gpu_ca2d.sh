@@ -22,4 +22,4 @@ for g in (api.make_grid(api.map_kind.h2d, 2, 1024, 16), api.make_grid(api.map_ki
           api.make_grid(api.map_kind.h2d, 2, 65536, 1), api.make_grid(api.map_kind.rb, 2, 4095, 16)):
     t(g, api.EXEC_RUNS)
 PY
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_ca2d_runs" -s 2 -c 1 -o gpurun_out/ca2d python tools/prof_case.py ca2d h2d 4096 16 runs 3 > /dev/null 2>&1; echo "ncu rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_ca2d_" -s 2 -c 1 -o gpurun_out/ca2d python tools/prof_case.py ca2d h2d 4096 16 runs 3 > /dev/null 2>&1; echo "ncu rc=$?"
