@@ -34,10 +34,22 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", OUT + ".tmp", *sources()]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.run(cmd, check=True)
+    # one nvcc per translation unit, in parallel, then one link
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    comp = [f for f in FLAGS if f != "-shared"]
+    procs, objs = [], []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *ARCH, *comp, "-c", "-o", obj, src]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        procs.append((src, subprocess.Popen(cmd)))
+        objs.append(obj)
+    bad = [src for src, p in procs if p.wait() != 0]
+    if bad:
+        raise subprocess.CalledProcessError(1, f"nvcc {' '.join(os.path.basename(b) for b in bad)}")
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs], check=True)
     os.replace(OUT + ".tmp", OUT)
     return OUT
 

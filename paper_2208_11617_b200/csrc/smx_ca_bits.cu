@@ -457,8 +457,15 @@ __global__ void __launch_bounds__(RunCfg<RHO>::NW * 32) k_ca_bits_run(const __gr
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
     const int nchunks = int(*count);
-    const int gwarp = blockIdx.x * RUN_NWARP + warp, nwarps = gridDim.x * RUN_NWARP;
+    // items go to SMs first (warp w of CTA b is global warp w * grid + b): a grid
+    // with fewer items than warps spreads them over every SM instead of filling
+    // the first CTAs' 16 warps and leaving the rest idle
+    const int gwarp = warp * gridDim.x + blockIdx.x, nwarps = gridDim.x * RUN_NWARP;
     // A warp runs the same items every step. When it owns few (small grids),
     // copy their chunks once into its smem list, so no step waits on a global
     // read of a chunk before issuing its TMA box.
