@@ -351,17 +351,22 @@ __device__ __forceinline__ void run_items(const Chunk* __restrict__ s_chunk, int
             const int w0 = ch.x0 >> 5;
             const int xw = 32 * (w0 + w);  // x of this lane's word
             const int lastw = (ch.x0 + ch.w - 1) >> 5;
+            // layers z0 .. zmax-1 of this lane's word are cells (y + z <= S - 1);
+            // the output pointer steps one layer (S rows) per z
+            const int zmax = (cvalid && ch.x0 <= y && w0 + w <= lastw && xw <= y) ? min(ch.z0 + RHO, S - y) : 0;
+            uint32_t* optr = nbits + ((long long)ch.z0 * S + y) * WP + w0 + w;
+            const long long zstep = (long long)S * WP;
+            const uint32_t* arow = reinterpret_cast<const uint32_t*>(cbuf + (HL + ly + 1) * BOXW * 4) +
+                                   ((w0 - 1) & 3) + 1 + w;
 #pragma unroll 2
             for (int lz = 0; lz < RHO; ++lz) {
                 const Planes4 vc = vsum(lz + 2);
-                const uint32_t alive = reinterpret_cast<const uint32_t*>(
-                    cbuf + ((lz + 1) * HL + ly + 1) * BOXW * 4)[((w0 - 1) & 3) + 1 + w];
+                const uint32_t alive = arow[lz * HL * BOXW];
                 const uint32_t O = life_planes(va, vb, vc, alive);
                 va = vb;
                 vb = vc;
-                const int z = ch.z0 + lz;
-                if (!cvalid || y + z > S - 1 || ch.x0 > y || w0 + w > lastw || xw > y) continue;
-                nbits[((long long)z * S + y) * WP + w0 + w] = O;
+                if (ch.z0 + lz < zmax) *optr = O;
+                optr += zstep;
             }
         }
         __syncwarp();

@@ -164,9 +164,9 @@ def test_ca2d_periodic_vs_reference(cuda, ex):
 
 def test_ca2d_runs_every_small_side_vs_restated(cuda, orc):
     """The bit-sliced x-run 2-D Life kernel against the restated oracle for every
-    side 1..80 and rho in {1, 3, 16} (odd alignments of every packed row, the
-    wrap rows 0 / S-2 / S-1, runs shorter and longer than one 32-cell item),
-    through H, BB, RB and trapezoid grids; 3 steps each."""
+    side 1..80 and rho in {1, 3, 8, 16, 32} (odd alignments of every packed
+    row, the wrap rows 0 / S-2 / S-1, runs shorter and longer than one 32-cell
+    item), through H, BB, RB and trapezoid grids; 3 steps each."""
     import torch
     def run(g, init):
         a = torch.from_numpy(init.copy()).cuda()
@@ -179,7 +179,7 @@ def test_ca2d_runs_every_small_side_vs_restated(cuda, orc):
     for side in range(1, 81):
         init = orc.make_life_state(2, side, 1000 + side)
         want = orc.ca2d_run(side, 3, init.copy())
-        for rho in (1, 3, 16):
+        for rho in (1, 3, 8, 16, 32):
             if side % rho == 0:
                 for kind in (api.map_kind.bb, api.map_kind.rb):
                     g = api.make_grid(kind, 2, side // rho, rho)
