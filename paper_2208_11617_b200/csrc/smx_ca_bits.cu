@@ -274,7 +274,7 @@ __device__ __forceinline__ void run_items(const Chunk* __restrict__ s_chunk, int
     using C = Cfg<RHO, CPIX>;
     constexpr int HL = C::HL;
     const int lane = threadIdx.x & 31;
-    uint32_t* sH = reinterpret_cast<uint32_t*>(wbase + 2 * C::BUF);  // [HROWS][8]: h0 w0..3, h1 w0..3
+    uint32_t* sH = reinterpret_cast<uint32_t*>(wbase + 2 * C::BUF);  // [HROWS][4][2]: (h0, h1) of words 0..3
     const int nitems = (nchunks + C::CPI - 1) / C::CPI;
     int item = item0, b = 0;
     if (item < nitems && lane == 0) {
@@ -326,8 +326,8 @@ __device__ __forceinline__ void run_items(const Chunk* __restrict__ s_chunk, int
                     h1 = make_uint4(bb[0], bb[1], bb[2], bb[3]);
                 }
             }
-            reinterpret_cast<uint4*>(sH + 8 * r)[0] = h0;
-            reinterpret_cast<uint4*>(sH + 8 * r)[1] = h1;
+            reinterpret_cast<uint4*>(sH + 8 * r)[0] = make_uint4(h0.x, h1.x, h0.y, h1.y);
+            reinterpret_cast<uint4*>(sH + 8 * r)[1] = make_uint4(h0.z, h1.z, h0.w, h1.w);
         }
         __syncwarp();
 
@@ -343,8 +343,10 @@ __device__ __forceinline__ void run_items(const Chunk* __restrict__ s_chunk, int
             const uint8_t* cbuf = buf + cs * C::SLOT;
             auto vsum = [&](int zi) {
                 const int r0 = zi * HL + ly;
-                return add3x2(H[8 * r0 + w], H[8 * r0 + 4 + w], H[8 * (r0 + 1) + w], H[8 * (r0 + 1) + 4 + w],
-                              H[8 * (r0 + 2) + w], H[8 * (r0 + 2) + 4 + w]);
+                const uint2 p = reinterpret_cast<const uint2*>(H + 8 * r0)[w];
+                const uint2 q = reinterpret_cast<const uint2*>(H + 8 * (r0 + 1))[w];
+                const uint2 u = reinterpret_cast<const uint2*>(H + 8 * (r0 + 2))[w];
+                return add3x2(p.x, p.y, q.x, q.y, u.x, u.y);
             };
             Planes4 va = vsum(0), vb = vsum(1);
             const int y = ch.y0 + ly;
