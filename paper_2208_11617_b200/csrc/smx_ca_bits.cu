@@ -76,7 +76,7 @@ struct Cfg {
     static constexpr int LIST_ITEMS = 8;
     static constexpr int LIST_OFF = 2 * BUF + HROWS * 32 + 64;
     static constexpr int WARP_BYTES = (LIST_OFF + LIST_ITEMS * CPI * 16 + 127) & ~127;  // TMA dst: 128B aligned
-    static int smem(int nb) { return NWARP * WARP_BYTES + nb * 32 + 128; }
+    static int smem(int nb) { return NWARP * WARP_BYTES + nb * 40 + 128; }
 };
 
 __device__ __forceinline__ int layer_row(int z, int S) { return z * S - (z * (z - 1)) / 2; }
@@ -387,6 +387,7 @@ __global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_
     int4* s_tile = reinterpret_cast<int4*>(smem + NWARP * C::WARP_BYTES);
     Chunk* s_chunk = reinterpret_cast<Chunk*>(smem + NWARP * C::WARP_BYTES + NBP * 16);
     int* s_nchunks = reinterpret_cast<int*>(smem + NWARP * C::WARP_BYTES + 2 * NBP * 16);
+    uint32_t* s_link = reinterpret_cast<uint32_t*>(smem + NWARP * C::WARP_BYTES + 2 * NBP * 16 + 16);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint8_t* wbase = smem + warp * C::WARP_BYTES;
     const uint32_t mbar0 = smem_u32(wbase + 2 * C::BUF + C::HROWS * 32);
@@ -395,7 +396,8 @@ __global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_
         mbar_init(mbar0 + 8, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    const int nchunks = build_chunks<KIND>(g, wz0 + blockIdx.z * NZ, wz1, P, NZ, C::LMAX, s_tile, s_chunk, s_nchunks);
+    const int nchunks =
+        build_chunks<KIND>(g, wz0 + blockIdx.z * NZ, wz1, P, NZ, C::LMAX, s_tile, s_chunk, s_nchunks, s_link);
     uint32_t phases = 0u;
     run_items<RHO>(s_chunk, nchunks, warp, NWARP, &tmap, nbits, g.side, WP, wbase, mbar0, phases);
 }
@@ -418,8 +420,9 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_ca_plan(Geom g, int wz0, int w
     int4* s_tile = reinterpret_cast<int4*>(smem);
     Chunk* s_chunk = reinterpret_cast<Chunk*>(smem + NBP * 16);
     int* s_nchunks = reinterpret_cast<int*>(smem + 2 * NBP * 16);
+    uint32_t* s_link = reinterpret_cast<uint32_t*>(smem + 2 * NBP * 16 + 16);
     __shared__ unsigned s_base;
-    const int n = build_chunks<KIND>(g, wz0 + blockIdx.z * NZ, wz1, P, NZ, C::LMAX, s_tile, s_chunk, s_nchunks);
+    const int n = build_chunks<KIND>(g, wz0 + blockIdx.z * NZ, wz1, P, NZ, C::LMAX, s_tile, s_chunk, s_nchunks, s_link);
     if (threadIdx.x == 0) s_base = atomicAdd(count, unsigned(n));
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) out[s_base + i] = s_chunk[i];
@@ -538,7 +541,7 @@ void launch_plan_t(const Geom& g, void* chunks, unsigned* count, cudaStream_t s)
     // unbroken chains, cut every LMAX tiles anyway). 512 threads map a patch.
     const int P = KIND == SMX_H3D ? 32 : C::LMAX, NZ = 1;
     const dim3 grid((g.ex + P - 1) / P, (g.ey + P - 1) / P, g.ez);
-    k_ca_plan<KIND, RHO><<<grid, PLAN_THREADS, 2 * P * P * NZ * 16 + 16, s>>>(g, 0, g.ez, P, NZ,
+    k_ca_plan<KIND, RHO><<<grid, PLAN_THREADS, 2 * P * P * NZ * 16 + 16 + 2 * P * P * NZ * 4, s>>>(g, 0, g.ez, P, NZ,
                                                                               reinterpret_cast<Chunk*>(chunks), count);
 }
 

@@ -88,12 +88,21 @@ __device__ __forceinline__ uint32_t life_planes(const Planes4& a, const Planes4&
 // wzb .. wzb+NZ-1 (< wz1). Its threads map the blocks lane-parallel, then chain
 // tiles that are x-adjacent in the data: a tile's predecessor is at patch
 // neighbour (wx-1, wy) (unfolded H tiles, the wall plane, BB rows) or
-// (wx, wy-1) (the hinge fold, maps.hpp:334-336). Chains are cut into chunks of
-// at most LMAX tiles. Every useful tile lands in exactly one chunk.
+// (wx, wy-1) (the hinge fold, maps.hpp:334-336); its successor is at
+// (wx+1, wy) or (wx, wy+1). The map is an exact cover, so a data tile has at
+// most one predecessor and one successor: chains are disjoint paths. Every
+// tile finds its distance to its chain's head and tail by pointer jumping
+// (log2 of the chain length rounds, all tiles in parallel; s_link holds a
+// (pointer, distance) pair per tile and direction in one 32-bit word, so the
+// in-place updates stay consistent without double buffering), and the tiles
+// at head distance 0, LMAX, 2 LMAX, ... emit the chunks of at most LMAX tiles.
+// Every useful tile lands in exactly one chunk. s_link: 2 * P * P * NZ words.
 // Returns the chunk count (after a __syncthreads).
+constexpr uint32_t LINK_END = 0xffffu;
+
 template <int KIND>
 __device__ __forceinline__ int build_chunks(const Geom& g, int wzb, int wz1, int P, int NZ, int lmax, int4* s_tile,
-                                            Chunk* s_chunk, int* s_nchunks) {
+                                            Chunk* s_chunk, int* s_nchunks, uint32_t* s_link) {
     const int PP = P * P, NBP = PP * NZ;
     const int rho = g.rho;
     const int tid = threadIdx.x, nthr = blockDim.x;
@@ -109,31 +118,46 @@ __device__ __forceinline__ int build_chunks(const Geom& g, int wzb, int wz1, int
         s_tile[t] = v;
     }
     __syncthreads();
+    // links: (neighbour, 1) or (END, 0) toward the head (word t) and the tail (word NBP + t)
+    for (int t = tid; t < NBP; t += nthr) {
+        const int4 me = s_tile[t];
+        uint32_t pl = LINK_END, sl = LINK_END;
+        if (me.w) {
+            const int px = (me.w >> 8) & 0xff, py = me.w >> 16;
+            auto is_tile = [&](int i, int x) {
+                const int4 o = s_tile[i];
+                return o.w && o.x == x && o.y == me.y && o.z == me.z;
+            };
+            if (px > 0 && is_tile(t - 1, me.x - 1)) pl = uint32_t(t - 1) | (1u << 16);
+            else if (py > 0 && is_tile(t - P, me.x - 1)) pl = uint32_t(t - P) | (1u << 16);
+            if (px + 1 < P && is_tile(t + 1, me.x + 1)) sl = uint32_t(t + 1) | (1u << 16);
+            else if (py + 1 < P && is_tile(t + P, me.x + 1)) sl = uint32_t(t + P) | (1u << 16);
+        }
+        s_link[t] = pl;
+        s_link[NBP + t] = sl;
+    }
+    __syncthreads();
+    for (;;) {
+        int more = 0;
+        for (int k = tid; k < 2 * NBP; k += nthr) {
+            const uint32_t v = s_link[k];
+            const uint32_t q = v & 0xffffu;
+            if (q == LINK_END) continue;
+            const int base = k < NBP ? 0 : NBP;
+            const uint32_t w = s_link[base + int(q)];  // a consistent (pointer, distance) pair
+            const uint32_t nv = (w & 0xffffu) | ((v & 0xffff0000u) + (w & 0xffff0000u));
+            s_link[k] = nv;
+            more |= (nv & 0xffffu) != LINK_END;
+        }
+        if (!__syncthreads_or(more)) break;
+    }
     for (int t = tid; t < NBP; t += nthr) {
         const int4 me = s_tile[t];
         if (!me.w) continue;
-        const int px = (me.w >> 8) & 0xff, py = me.w >> 16;
-        auto is_tile = [&](int i, int x) {
-            const int4 o = s_tile[i];
-            return o.w && o.x == x && o.y == me.y && o.z == me.z;
-        };
-        if ((px > 0 && is_tile(t - 1, me.x - 1)) || (py > 0 && is_tile(t - P, me.x - 1))) continue;
-        int u = t, len = 1, x0 = me.x;
-        for (;;) {
-            const int uw = s_tile[u].w, ux = (uw >> 8) & 0xff, uy = uw >> 16;
-            const int xn = s_tile[u].x + 1;
-            int nxt = -1;
-            if (ux + 1 < P && is_tile(u + 1, xn)) nxt = u + 1;
-            else if (uy + 1 < P && is_tile(u + P, xn)) nxt = u + P;
-            if (nxt < 0 || len == lmax) {
-                const int c = atomicAdd(s_nchunks, 1);
-                s_chunk[c] = Chunk{x0 * rho, me.y * rho, me.z * rho, len * rho};
-                if (nxt < 0) break;
-                x0 = s_tile[nxt].x;
-                len = 0;
-            }
-            u = nxt;
-            ++len;
+        const int dh = int(s_link[t] >> 16), dt = int(s_link[NBP + t] >> 16);
+        if (dh % lmax == 0) {
+            const int c = atomicAdd(s_nchunks, 1);
+            s_chunk[c] = Chunk{me.x * rho, me.y * rho, me.z * rho, min(lmax, dt + 1) * rho};
         }
     }
     __syncthreads();

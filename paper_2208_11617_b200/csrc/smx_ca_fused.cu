@@ -65,7 +65,7 @@ struct FCfg {
     static constexpr int O_OFF = H_OFF + HROWS * HW * 4;
     static constexpr int D_OFF = (O_OFF + (RHO * OSTR + 1) * 4 + 15) & ~15;
     static constexpr int WARP_BYTES = (D_OFF + HROWS * 16 + 127) & ~127;
-    static int smem(int nb) { return F_NWARP * WARP_BYTES + nb * 32 + 16; }
+    static int smem(int nb) { return F_NWARP * WARP_BYTES + nb * 40 + 16; }
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -100,6 +100,7 @@ __global__ void __launch_bounds__(F_NTHR) k_ca_fused(Geom g, int wz0, int wz1, i
     int4* s_tile = reinterpret_cast<int4*>(fsm + F_NWARP * C::WARP_BYTES);
     Chunk* s_chunk = reinterpret_cast<Chunk*>(s_tile + NBP);
     int* s_nchunks = reinterpret_cast<int*>(s_chunk + NBP);
+    uint32_t* s_link = reinterpret_cast<uint32_t*>(s_chunk + NBP) + 4;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane >> 3, gl = lane & 7;
@@ -110,7 +111,8 @@ __global__ void __launch_bounds__(F_NTHR) k_ca_fused(Geom g, int wz0, int wz1, i
     uint32_t* sO = reinterpret_cast<uint32_t*>(sR + C::O_OFF);     // [RHO][OSTR] (+1 pad word)
     int4* sD = reinterpret_cast<int4*>(sR + C::D_OFF);             // [HROWS] row descriptors
 
-    const int nchunks = build_chunks<KIND>(g, wz0 + blockIdx.z * NZ, wz1, P, NZ, C::LMAX, s_tile, s_chunk, s_nchunks);
+    const int nchunks =
+        build_chunks<KIND>(g, wz0 + blockIdx.z * NZ, wz1, P, NZ, C::LMAX, s_tile, s_chunk, s_nchunks, s_link);
     const int nitems = (nchunks + C::CPI - 1) / C::CPI;
 
     for (int item = warp; item < nitems; item += F_NWARP) {
