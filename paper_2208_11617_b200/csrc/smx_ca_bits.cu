@@ -139,8 +139,8 @@ struct RowCursor {
 // layer_row(z) = z (2S + 1 - z) / 2; z = floor of the smaller root of
 // z^2 - (2S+1) z + 2r = 0, corrected by one either way (no dependent loads)
 __device__ __forceinline__ RowCursor row_at(int row, int S, const unsigned long long* __restrict__ PZ) {
-    const double b = 2.0 * S + 1.0;
-    int z = int((b - sqrt(b * b - 8.0 * row)) * 0.5);
+    const float b = 2.0f * S + 1.0f;  // fp32 root: off by at most a few, fixed below
+    int z = int((b - sqrtf(fmaxf(b * b - 8.0f * float(row), 0.0f))) * 0.5f);
     if (z < 0) z = 0;
     if (z > S - 1) z = S - 1;
     while (z > 0 && layer_row(z, S) > row) --z;

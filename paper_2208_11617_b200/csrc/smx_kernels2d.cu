@@ -178,40 +178,6 @@ __device__ __forceinline__ uint32_t life2d_bits(const uint8_t* __restrict__ cur,
     return (~t.b3 & ~t.b2 & t.b1 & t.b0) | (~t.b3 & t.b2 & ~t.b1 & ~t.b0 & alive);
 }
 
-// Next states of the 32 cells at packed A .. A+31 (A 32-aligned; cell A is
-// (A - R, cy), R = the start of row cy), across row ends if need be.
-template <typename IDX>
-__device__ __forceinline__ uint32_t life2d_chunk(const uint8_t* __restrict__ cur, IDX ncells, int S, IDX R, int cy,
-                                                 IDX A) {
-    const int x0 = int(A - R);
-    if (cy >= 1 && cy <= S - 3 && x0 + 31 <= cy) return life2d_bits(cur, ncells, R, cy, x0);  // inside row cy
-    if (cy >= 1 && cy + 1 <= S - 3 && A + 32 <= R + 2 * cy + 3) {  // rows cy, cy + 1
-        const int n0 = cy - x0 + 1;  // cells of row cy in the chunk
-        const uint32_t m0 = (1u << n0) - 1u;
-        return (life2d_bits(cur, ncells, R, cy, x0) & m0) |
-               (life2d_bits(cur, ncells, IDX(R + cy + 1), cy + 1, x0 - cy - 1) & ~m0);
-    }
-    uint32_t res = 0;  // per cell, rows found by walking down from cy
-    IDX Ry = R;
-    int y = cy;
-    for (int b = 0; b < 32 && A + b < ncells; ++b) {
-        while (A + b >= Ry + y + 1) Ry += y + 1, ++y;
-        res |= uint32_t(life2d_cell(cur, S, int(A + b - Ry), y)) << b;
-    }
-    return res;
-}
-
-template <typename IDX>
-__device__ __forceinline__ void store_chunk(uint8_t* __restrict__ next, IDX ncells, IDX A, uint32_t res) {
-    if (A + 32 <= ncells) {
-        uint4* o = reinterpret_cast<uint4*>(next + A);
-        o[0] = ca::spread16(res & 0xffffu);
-        o[1] = ca::spread16(res >> 16);
-    } else {
-        for (int b = 0; A + b < ncells; ++b) next[A + b] = uint8_t((res >> b) & 1u);
-    }
-}
-
 // Strips per CTA for the 2-D x-run Life kernel: ~256+ chunks per CTA at rho >= 8,
 // bounded by shared memory below.
 __host__ __device__ constexpr int ca2d_strips(int rho) { return rho >= 16 ? 2 : (rho >= 8 ? 8 : 32); }
@@ -277,7 +243,31 @@ __global__ void __launch_bounds__(T2_THREADS) k_ca2d_runs(Geom g, const uint8_t*
         const IDX R = IDX(((unsigned long long)cy * (cy + 1)) >> 1);
         const IDX A = ((R + xlo + 31) & ~IDX(31)) + 32 * (k - ly * cpr);  // chunk starts inside [E0, E1)
         if (A >= R + xhi) continue;
-        store_chunk(next, ncells, A, life2d_chunk(cur, ncells, S, R, cy, A));
+        const int x0 = int(A - R);
+        uint32_t res;
+        if (cy >= 1 && cy <= S - 3 && x0 + 31 <= cy) {  // wholly inside row cy
+            res = life2d_bits(cur, ncells, R, cy, x0);
+        } else if (cy >= 1 && cy + 1 <= S - 3 && A + 32 <= R + 2 * cy + 3) {  // rows cy, cy + 1
+            const int n0 = cy - x0 + 1;  // cells of row cy in the chunk
+            const uint32_t m0 = (1u << n0) - 1u;
+            res = (life2d_bits(cur, ncells, R, cy, x0) & m0) |
+                  (life2d_bits(cur, ncells, IDX(R + cy + 1), cy + 1, x0 - cy - 1) & ~m0);
+        } else {  // per cell, rows found by walking down from cy
+            res = 0;
+            IDX Ry = R;
+            int y = cy;
+            for (int b = 0; b < 32 && A + b < ncells; ++b) {
+                while (A + b >= Ry + y + 1) Ry += y + 1, ++y;
+                res |= uint32_t(life2d_cell(cur, S, int(A + b - Ry), y)) << b;
+            }
+        }
+        if (A + 32 <= ncells) {
+            uint4* o = reinterpret_cast<uint4*>(next + A);
+            o[0] = ca::spread16(res & 0xffffu);
+            o[1] = ca::spread16(res >> 16);
+        } else {
+            for (int b = 0; A + b < ncells; ++b) next[A + b] = uint8_t((res >> b) & 1u);
+        }
     }
 }
 
