@@ -13,9 +13,10 @@ the 2.7 MB state is L2-resident, as it is for the reference workload.
 `e2e` is the same call through the reference-facing C ABI with host (pinned)
 buffers: H2D + 100 steps + D2H per bench step.
 
-`roofline` is for the dominant kernel, k_ca_bits (one bit-sliced step over the
-whole map grid), timed per launch with CUDA events on the launching stream,
-on SURVEY §8(d)'s basis of 2 B per useful cell per step.
+`roofline` is for the dominant kernel, k_ca_bits_run (the persistent launch
+running all 100 bit-sliced steps over the map-built chunk list), timed per
+launch with CUDA events on the launching stream, on SURVEY §8(d)'s basis of
+2 B per useful cell per step.
 
 Also reported (`configs`), per BASELINE config at 1 GPU: H and BB Gcells/s,
 H-vs-BB speedup, HBM roofline fraction, J/cell from NVML — ACCUM C1/C3 (x-run
