@@ -76,7 +76,7 @@ struct Cfg {
     static constexpr int LIST_ITEMS = 8;
     static constexpr int LIST_OFF = 2 * BUF + HROWS * 32 + 64;
     static constexpr int WARP_BYTES = (LIST_OFF + LIST_ITEMS * CPI * 16 + 127) & ~127;  // TMA dst: 128B aligned
-    static int smem(int nb) { return NWARP * WARP_BYTES + nb * 40 + 128; }
+    static int smem(int nb) { return NWARP * WARP_BYTES + nb * 48 + 128; }
 };
 
 __device__ __forceinline__ int layer_row(int z, int S) { return z * S - (z * (z - 1)) / 2; }
@@ -540,8 +540,14 @@ void launch_plan_t(const Geom& g, void* chunks, unsigned* count, cudaStream_t s)
     // 36.3 K chunks vs 40.7 K at P = 12); BB: P = LMAX (rows of the box are
     // unbroken chains, cut every LMAX tiles anyway). 512 threads map a patch.
     const int P = KIND == SMX_H3D ? 32 : C::LMAX, NZ = 1;
+    const int smem = 2 * P * P * NZ * 16 + 16 + 4 * P * P * NZ * 4;  // tiles | chunks | count | links
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_ca_plan<KIND, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr_set = true;
+    }
     const dim3 grid((g.ex + P - 1) / P, (g.ey + P - 1) / P, g.ez);
-    k_ca_plan<KIND, RHO><<<grid, PLAN_THREADS, 2 * P * P * NZ * 16 + 16 + 2 * P * P * NZ * 4, s>>>(g, 0, g.ez, P, NZ,
+    k_ca_plan<KIND, RHO><<<grid, PLAN_THREADS, smem, s>>>(g, 0, g.ez, P, NZ,
                                                                               reinterpret_cast<Chunk*>(chunks), count);
 }
 

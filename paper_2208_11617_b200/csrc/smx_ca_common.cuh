@@ -93,10 +93,11 @@ __device__ __forceinline__ uint32_t life_planes(const Planes4& a, const Planes4&
 // most one predecessor and one successor: chains are disjoint paths. Every
 // tile finds its distance to its chain's head and tail by pointer jumping
 // (log2 of the chain length rounds, all tiles in parallel; s_link holds a
-// (pointer, distance) pair per tile and direction in one 32-bit word, so the
-// in-place updates stay consistent without double buffering), and the tiles
-// at head distance 0, LMAX, 2 LMAX, ... emit the chunks of at most LMAX tiles.
-// Every useful tile lands in exactly one chunk. s_link: 2 * P * P * NZ words.
+// (pointer, distance) pair per tile and direction in one 32-bit word, ping-
+// ponged between two halves so every round reads only the previous round's
+// pairs), and the tiles at head distance 0, LMAX, 2 LMAX, ... emit the chunks
+// of at most LMAX tiles. Every useful tile lands in exactly one chunk.
+// s_link: 4 * P * P * NZ words.
 // Returns the chunk count (after a __syncthreads).
 constexpr uint32_t LINK_END = 0xffffu;
 
@@ -137,24 +138,30 @@ __device__ __forceinline__ int build_chunks(const Geom& g, int wzb, int wz1, int
         s_link[NBP + t] = sl;
     }
     __syncthreads();
+    uint32_t* cur = s_link;
+    uint32_t* nxt = s_link + 2 * NBP;
     for (;;) {
         int more = 0;
         for (int k = tid; k < 2 * NBP; k += nthr) {
-            const uint32_t v = s_link[k];
+            const uint32_t v = cur[k];
             const uint32_t q = v & 0xffffu;
-            if (q == LINK_END) continue;
-            const int base = k < NBP ? 0 : NBP;
-            const uint32_t w = s_link[base + int(q)];  // a consistent (pointer, distance) pair
-            const uint32_t nv = (w & 0xffffu) | ((v & 0xffff0000u) + (w & 0xffff0000u));
-            s_link[k] = nv;
-            more |= (nv & 0xffffu) != LINK_END;
+            uint32_t nv = v;
+            if (q != LINK_END) {
+                const uint32_t w = cur[(k < NBP ? 0 : NBP) + int(q)];
+                nv = (w & 0xffffu) | ((v & 0xffff0000u) + (w & 0xffff0000u));
+                more |= (nv & 0xffffu) != LINK_END;
+            }
+            nxt[k] = nv;
         }
+        uint32_t* t = cur;
+        cur = nxt;
+        nxt = t;
         if (!__syncthreads_or(more)) break;
     }
     for (int t = tid; t < NBP; t += nthr) {
         const int4 me = s_tile[t];
         if (!me.w) continue;
-        const int dh = int(s_link[t] >> 16), dt = int(s_link[NBP + t] >> 16);
+        const int dh = int(cur[t] >> 16), dt = int(cur[NBP + t] >> 16);
         if (dh % lmax == 0) {
             const int c = atomicAdd(s_nchunks, 1);
             s_chunk[c] = Chunk{me.x * rho, me.y * rho, me.z * rho, min(lmax, dt + 1) * rho};

@@ -65,7 +65,7 @@ struct FCfg {
     static constexpr int O_OFF = H_OFF + HROWS * HW * 4;
     static constexpr int D_OFF = (O_OFF + (RHO * OSTR + 1) * 4 + 15) & ~15;
     static constexpr int WARP_BYTES = (D_OFF + HROWS * 16 + 127) & ~127;
-    static int smem(int nb) { return F_NWARP * WARP_BYTES + nb * 40 + 16; }
+    static int smem(int nb) { return F_NWARP * WARP_BYTES + nb * 48 + 16; }
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
