@@ -310,8 +310,11 @@ __device__ __forceinline__ void run_items(const Chunk* __restrict__ s_chunk, int
                     for (int j = 0; j < 6; ++j) T[j] = src[j];
                     const int xb = ((ch.x0 >> 5) - 1) * 32;  // x of T[0] bit 0
                     if (xb + 191 > yy) {
+                        // keep cells x <= yy (x < 0 words are TMA zero-fill): the low
+                        // yy - x + 1 bits, clamped to [0, 32] by the funnel shift
 #pragma unroll
-                        for (int j = 0; j < 6; ++j) T[j] &= range_mask(-(xb + 32 * j), yy - (xb + 32 * j));
+                        for (int j = 0; j < 6; ++j)
+                            T[j] &= __funnelshift_lc(0xffffffffu, 0u, max(yy - (xb + 32 * j) + 1, 0));
                     }
                     uint32_t a[4], bb[4];
 #pragma unroll
