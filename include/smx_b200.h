@@ -18,6 +18,12 @@
  *    device pool, runs, copies results back and synchronises `stream`
  *    (the reference's mutate-in-place semantics, simulator.hpp:313-326,431-463).
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).
+ *  - Threads: the library's scratch (staging pool, bit shadows, CA chunk list,
+ *    the side stream the CA plan runs on) is per (device, host thread), so
+ *    calls on distinct states from distinct threads may run concurrently, as
+ *    the reference's launches may. Device-resident calls from ONE thread share
+ *    that thread's scratch: issue them on one stream (or synchronise between
+ *    streams); host-buffer calls synchronise before returning.
  *  - Cell state is the reference's packed layout: 2-D row-major triangle
  *    index y(y+1)/2 + x (core.hpp:136-138); 3-D layer prefix tet(S)-tet(S-z)
  *    plus the triangle index (core.hpp:140-149). u32 cells for ACCUM, u8 for CA.

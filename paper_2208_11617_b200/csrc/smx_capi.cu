@@ -12,6 +12,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -53,9 +54,15 @@ std::string valid_pairs() {
 
 bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 
-// Device-side resources, per device: layer-prefix tables keyed by side, a
-// grow-only staging pool for host-buffer calls, counters and the MAP sink.
+// Device-side resources, per (device, host thread): layer-prefix tables keyed
+// by side, a grow-only scratch pool (staging for host-buffer calls, bit
+// shadows, the CA chunk list), counters, the MAP sink and the side stream the
+// CA plan runs on. Per host thread, so launches on distinct states from
+// distinct threads never share scratch (the reference's functions are
+// reentrant); calls from one thread are ordered on the stream they pass.
 struct DeviceRes {
+    cudaStream_t side = nullptr;  // CA plan, concurrent with staging + pack
+    cudaEvent_t ev_in = nullptr, ev_plan = nullptr;
     std::map<int64_t, unsigned long long*> prefix;
     // 0 cov, 1/2 u8, 3/4 bit shadows, 5 CA chunk list, 6 engine control words
     void* pool[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -65,7 +72,7 @@ struct DeviceRes {
     unsigned* sink = nullptr;
 };
 std::mutex g_mu;
-std::map<int, DeviceRes> g_res;
+std::map<std::pair<int, std::thread::id>, DeviceRes> g_res;
 
 int cuda_fail(cudaError_t e, const char* what) {
     return fail(SMX_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -80,7 +87,7 @@ int device_res(DeviceRes** out) {
     int dev = 0;
     TRY(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(g_mu);
-    *out = &g_res[dev];
+    *out = &g_res[{dev, std::this_thread::get_id()}];
     return SMX_OK;
 }
 
@@ -322,18 +329,49 @@ int ca_fused_step(const smx::Geom& k, int64_t wz0, int64_t wz1, const uint8_t* c
 }
 
 // plan (map once -> chunk list) + persistent multi-step run, A -> B -> A ...
+//
+// The plan depends on the grid only, so it is issued first, on a side stream
+// ordered after the caller's prior work: it runs concurrently with whatever
+// the caller stream does next (host staging, pack) until engine_run joins it.
+int engine_plan(const smx_grid* g, const smx::Geom& k, int64_t steps, cudaStream_t s, void** pch, unsigned** count) {
+    if (steps > INT32_MAX) return fail(SMX_ERANGE, "launch_ca: steps must fit int32");
+    void* pctl;
+    if (int rc = pool_get(5, size_t(smx::ca_plan_capacity(k)) * 16, pch)) return rc;
+    if (int rc = pool_get(6, 64, &pctl)) return rc;
+    *count = (unsigned*)pctl;
+    DeviceRes* r;
+    if (int rc = device_res(&r)) return rc;
+    if (!r->side) {
+        TRY(cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking));
+        TRY(cudaEventCreateWithFlags(&r->ev_in, cudaEventDisableTiming));
+        TRY(cudaEventCreateWithFlags(&r->ev_plan, cudaEventDisableTiming));
+    }
+    TRY(cudaEventRecord(r->ev_in, s));
+    TRY(cudaStreamWaitEvent(r->side, r->ev_in, 0));
+    TRY(cudaMemsetAsync(pctl, 0, 64, r->side));
+    smx::launch_ca_plan(k, g->kind, *pch, *count, r->side);
+    TRY(cudaGetLastError());
+    TRY(cudaEventRecord(r->ev_plan, r->side));
+    return SMX_OK;
+}
+
+// join the plan, then ONE persistent launch for all steps
+int engine_run(const smx::Geom& k, uint32_t* A, uint32_t* B, const CUtensorMap* ta, const CUtensorMap* tb,
+               int64_t steps, cudaStream_t s, void* pch, unsigned* count) {
+    DeviceRes* r;
+    if (int rc = device_res(&r)) return rc;
+    TRY(cudaStreamWaitEvent(s, r->ev_plan, 0));
+    TRY(smx::launch_ca_bits_run(k, ta, tb, A, B, pch, count, int(steps), s));
+    return SMX_OK;
+}
+
 int bits_engine(const smx_grid* g, const smx::Geom& k, uint32_t* A, uint32_t* B, const CUtensorMap* ta,
                 const CUtensorMap* tb, int64_t steps, cudaStream_t s) {
     if (steps <= 0) return SMX_OK;
-    if (steps > INT32_MAX) return fail(SMX_ERANGE, "launch_ca: steps must fit int32");
-    void *pch, *pctl;
-    if (int rc = pool_get(5, size_t(smx::ca_plan_capacity(k)) * 16, &pch)) return rc;
-    if (int rc = pool_get(6, 64, &pctl)) return rc;
-    unsigned* count = (unsigned*)pctl;
-    TRY(cudaMemsetAsync(pctl, 0, 64, s));
-    smx::launch_ca_plan(k, g->kind, pch, count, s);
-    TRY(smx::launch_ca_bits_run(k, ta, tb, A, B, pch, count, int(steps), s));
-    return SMX_OK;
+    void* pch;
+    unsigned* count;
+    if (int rc = engine_plan(g, k, steps, s, &pch, &count)) return rc;
+    return engine_run(k, A, B, ta, tb, steps, s, pch, count);
 }
 
 size_t bits_bytes(int64_t side) {
@@ -725,6 +763,13 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
     uint8_t* b = scratch;
     uint32_t* dcov = coverage;
     void* p;
+    // bit-shadow engine: the plan (map -> chunk list) needs only the grid, so
+    // it is issued first and overlaps the input staging and the pack
+    const bool engine = g->dims == 3 && exec == SMX_EXEC_BITS && steps > 0;
+    void* plan = nullptr;
+    unsigned* plan_count = nullptr;
+    if (engine)
+        if (int rc = engine_plan(g, k, steps, s, &plan, &plan_count)) return rc;
     if (!device_ptr) {
         if (int rc = pool_get(1, ncells, &p)) return rc;
         a = (uint8_t*)p;
@@ -750,7 +795,7 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
             if (int rc = ca2d_step(g, cur, nxt, exec, s)) return rc;
             std::swap(cur, nxt);
         }
-    } else if (exec == SMX_EXEC_BITS && steps > 0) {
+    } else if (engine) {
         // bit-shadow engine: pack once, steps x (bits -> bits), unpack once
         void *pa, *pb;
         if (int rc = pool_get(3, bits_bytes(k.side), &pa)) return rc;
@@ -761,7 +806,7 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
         // the map applied once (chunk list), then ONE persistent launch for all
         // steps, A -> B -> A ..., and the final shadow unpacked in place
         smx::launch_pack_bits(k, cur, (uint32_t*)pa, s);
-        if (int rc = bits_engine(g, k, (uint32_t*)pa, (uint32_t*)pb, ta, tb, steps, s)) return rc;
+        if (int rc = engine_run(k, (uint32_t*)pa, (uint32_t*)pb, ta, tb, steps, s, plan, plan_count)) return rc;
         smx::launch_unpack_bits(k, (steps & 1) ? (const uint32_t*)pb : (const uint32_t*)pa, cur, s);
     } else {
         for (int64_t st = 0; st < steps; ++st) {
