@@ -387,12 +387,17 @@ int ca_runs_step(const smx_grid* g, const smx::Geom& k, int64_t wz0, int64_t wz1
     if (int rc = pool_get(4, bits_bytes(k.side), &pb)) return rc;
     const CUtensorMap *ta, *tb;
     if (int rc = bits_tmap((const uint32_t*)pa, k.side, k.rho, &ta)) return rc;
-    smx::launch_pack_bits(k, cur, (uint32_t*)pa, s);
     if (wz0 == 0 && wz1 == k.ez) {
-        // the whole grid: the engine's plan + one persistent launch of 1 step
+        // the whole grid: the engine's plan (issued first, on the side stream,
+        // concurrent with the pack) + one persistent launch of 1 step
+        void* plan;
+        unsigned* count;
+        if (int rc = engine_plan(g, k, 1, s, &plan, &count)) return rc;
+        smx::launch_pack_bits(k, cur, (uint32_t*)pa, s);
         if (int rc = bits_tmap((const uint32_t*)pb, k.side, k.rho, &tb)) return rc;
-        if (int rc = bits_engine(g, k, (uint32_t*)pa, (uint32_t*)pb, ta, tb, 1, s)) return rc;
+        if (int rc = engine_run(k, (uint32_t*)pa, (uint32_t*)pb, ta, tb, 1, s, plan, count)) return rc;
     } else {
+        smx::launch_pack_bits(k, cur, (uint32_t*)pa, s);
         smx::launch_ca_bits(k, g->kind, int(wz0), int(wz1), ta, (uint32_t*)pb, s);
     }
     smx::launch_unpack_bits(k, (const uint32_t*)pb, next, s);
@@ -676,11 +681,14 @@ static int check_align16(const void* a, const void* b) {
     return SMX_OK;
 }
 
-// EXEC_AUTO for ONE step: the fused u8 -> u8 kernel up to this many cells
-// (L2-resident states, where one launch beats pack + step + unpack), the
-// bit-shadow path above it. Multi-step launch_ca always uses the bit shadow
-// (pack once, unpack once). Measured on B200: profiles/r1/ca_exec_sweep.txt.
-constexpr uint64_t kFusedMaxCells = 48ull << 20;
+// EXEC_AUTO for ONE step: the fused u8 -> u8 kernel only for small rho = 4
+// states (C2 size: it ties the bit-shadow path on H3D and wins on BB); the
+// bit-shadow path (pack || plan, one persistent step, unpack) everywhere else
+// (2x the fused kernel at H3D(64) rho = 8, 21 M cells). Multi-step launch_ca
+// always uses the bit shadow (pack once, unpack once). Measured on B200:
+// profiles/r1/ca_exec_sweep.txt.
+constexpr uint64_t kFusedMaxCells = 4ull << 20;
+static bool prefer_fused(const smx_grid* g, uint64_t ncells) { return g->rho == 4 && ncells <= kFusedMaxCells; }
 
 static int ca_validate(const smx_grid* g, uint64_t ncells, int32_t* exec) {
     if (int rc = check_cells(g, ncells)) return rc;
@@ -721,7 +729,7 @@ int smx_ca_step(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint64_t n
     if (int rc = ca_validate(g, ncells, &exec)) return rc;
     if (cur == next) return fail(SMX_EINVAL, "ca_step: cur and next must not alias");
     if (int rc = check_align16(cur, next)) return rc;
-    if (auto_exec && exec == SMX_EXEC_BITS && ncells <= kFusedMaxCells) exec = SMX_EXEC_RUNS;
+    if (auto_exec && exec == SMX_EXEC_BITS && prefer_fused(g, ncells)) exec = SMX_EXEC_RUNS;
     if (exec == SMX_EXEC_BITS) return ca_runs_step(g, k, 0, k.ez, cur, next, (cudaStream_t)stream);
     if (exec == SMX_EXEC_RUNS) return ca_fused_step(k, 0, k.ez, cur, next, (cudaStream_t)stream);
     smx::launch_ca(k, 0, k.ez, cur, next, exec, (cudaStream_t)stream);
@@ -739,7 +747,7 @@ int smx_ca_step_range(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint
         return fail(SMX_EINVAL, "ca_step_range: wz range outside the grid");
     if (cur == next) return fail(SMX_EINVAL, "ca_step_range: cur and next must not alias");
     if (int rc = check_align16(cur, next)) return rc;
-    if (auto_exec && exec == SMX_EXEC_BITS && ncells <= kFusedMaxCells) exec = SMX_EXEC_RUNS;
+    if (auto_exec && exec == SMX_EXEC_BITS && prefer_fused(g, ncells)) exec = SMX_EXEC_RUNS;
     if (exec == SMX_EXEC_BITS) return ca_runs_step(g, k, wz_lo, wz_hi, cur, next, (cudaStream_t)stream);
     if (exec == SMX_EXEC_RUNS) return ca_fused_step(k, wz_lo, wz_hi, cur, next, (cudaStream_t)stream);
     smx::launch_ca(k, int(wz_lo), int(wz_hi), cur, next, exec, (cudaStream_t)stream);
