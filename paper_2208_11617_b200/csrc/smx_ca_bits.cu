@@ -336,8 +336,16 @@ __device__ __forceinline__ void run_items(const Chunk* __restrict__ s_chunk, int
 
         // ---- 4. march along z: vertical sums, rule, stores ----
         {
-            const int cl = lane / C::LPC, l = lane % C::LPC;
+            // ZS lane groups split the z-march of a chunk when an item's chunks
+            // leave lanes free (rho = 4, one chunk per item: 2 x 16 lanes, each
+            // marching rho / 2 layers): shorter per-item latency
+            constexpr int ZS = 32 / (C::LPC * C::CPI) >= 2 && RHO % 2 == 0 ? 2 : 1;
+            constexpr int LZN = RHO / ZS;  // layers per lane
+            const int zg = ZS > 1 ? lane / (C::LPC * C::CPI) : 0;
+            const int lane_c = ZS > 1 ? lane % (C::LPC * C::CPI) : lane;
+            const int cl = lane_c / C::LPC, l = lane_c % C::LPC;
             const int ly = l >> 2, w = l & 3;
+            const int lz0 = zg * LZN;
             const int ci = item * C::CPI + cl;
             const bool cvalid = cl < C::CPI && ci < nchunks;
             const Chunk ch = cvalid ? s_chunk[ci] : Chunk{0, 0, 0, 0};
@@ -351,7 +359,7 @@ __device__ __forceinline__ void run_items(const Chunk* __restrict__ s_chunk, int
                 const uint2 u = reinterpret_cast<const uint2*>(H + 8 * (r0 + 2))[w];
                 return add3x2(p.x, p.y, q.x, q.y, u.x, u.y);
             };
-            Planes4 va = vsum(0), vb = vsum(1);
+            Planes4 va = vsum(lz0), vb = vsum(lz0 + 1);
             const int y = ch.y0 + ly;
             const int w0 = ch.x0 >> 5;
             const int xw = 32 * (w0 + w);  // x of this lane's word
@@ -359,12 +367,12 @@ __device__ __forceinline__ void run_items(const Chunk* __restrict__ s_chunk, int
             // layers z0 .. zmax-1 of this lane's word are cells (y + z <= S - 1);
             // the output pointer steps one layer (S rows) per z
             const int zmax = (cvalid && ch.x0 <= y && w0 + w <= lastw && xw <= y) ? min(ch.z0 + RHO, S - y) : 0;
-            uint32_t* optr = nbits + ((long long)ch.z0 * S + y) * WP + w0 + w;
             const long long zstep = (long long)S * WP;
+            uint32_t* optr = nbits + ((long long)(ch.z0 + lz0) * S + y) * WP + w0 + w;
             const uint32_t* arow = reinterpret_cast<const uint32_t*>(cbuf + (HL + ly + 1) * BOXW * 4) +
                                    ((w0 - 1) & 3) + 1 + w;
 #pragma unroll 2
-            for (int lz = 0; lz < RHO; ++lz) {
+            for (int lz = lz0; lz < lz0 + LZN; ++lz) {
                 const Planes4 vc = vsum(lz + 2);
                 const uint32_t alive = arow[lz * HL * BOXW];
                 const uint32_t O = life_planes(va, vb, vc, alive);
@@ -446,20 +454,20 @@ __device__ __forceinline__ void step_barrier() {
 // persistent kernel: one 16-warp CTA per SM (fewer barrier arrivals), the
 // default chunks per item (measured: 1 chunk per item with 32 warps per SM is
 // 8 % slower at C2 — the per-item fixed costs dominate there)
-template <int RHO>
+template <int RHO, int NWX = 16, int CPIY = 32 / (RHO * 4)>
 struct RunCfg {
-    static constexpr int NW = 16;
-    static constexpr int CPIX = 32 / (RHO * 4);
+    static constexpr int NW = NWX;
+    static constexpr int CPIX = CPIY;
 };
 
-template <int RHO>
-__global__ void __launch_bounds__(RunCfg<RHO>::NW * 32) k_ca_bits_run(const __grid_constant__ CUtensorMap tmA,
+template <int RHO, int NWX = 16, int CPIY = 32 / (RHO * 4)>
+__global__ void __launch_bounds__(NWX * 32) k_ca_bits_run(const __grid_constant__ CUtensorMap tmA,
                                                       const __grid_constant__ CUtensorMap tmB, uint32_t* bitsA,
                                                       uint32_t* bitsB, const Chunk* __restrict__ chunks,
                                                       const unsigned* __restrict__ count, int steps, int S,
                                                       int WP) {
-    using C = Cfg<RHO, RunCfg<RHO>::CPIX>;
-    constexpr int RUN_NWARP = RunCfg<RHO>::NW;
+    using C = Cfg<RHO, CPIY>;
+    constexpr int RUN_NWARP = NWX;
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint8_t* wbase = smem + warp * C::WARP_BYTES;
@@ -507,7 +515,7 @@ __global__ void __launch_bounds__(RunCfg<RHO>::NW * 32) k_ca_bits_run(const __gr
     uint32_t phases = 0u;
     for (int st = 0; st < steps; ++st) {
         const bool even = (st & 1) == 0;
-        run_items<RHO, RunCfg<RHO>::CPIX>(src, nsrc, i0, istr, even ? &tmA : &tmB, even ? bitsB : bitsA, S, WP,
+        run_items<RHO, CPIY>(src, nsrc, i0, istr, even ? &tmA : &tmB, even ? bitsB : bitsA, S, WP,
                                           wbase, mbar0, phases);
         if (st + 1 < steps) step_barrier();
     }
@@ -554,16 +562,15 @@ void launch_plan_t(const Geom& g, void* chunks, unsigned* count, cudaStream_t s)
                                                                               reinterpret_cast<Chunk*>(chunks), count);
 }
 
-template <int RHO>
+template <int RHO, int NWX, int CPIY>
 cudaError_t launch_run_t(const Geom& g, const CUtensorMap& tA, const CUtensorMap& tB, uint32_t* A, uint32_t* B,
                          const void* chunks, const unsigned* count, int steps, cudaStream_t s) {
-    using C = Cfg<RHO, RunCfg<RHO>::CPIX>;
-    constexpr int RUN_NWARP = RunCfg<RHO>::NW;
-    const int smem = RUN_NWARP * C::WARP_BYTES;
+    using C = Cfg<RHO, CPIY>;
+    const int smem = NWX * C::WARP_BYTES;
     static int grid = [&] {
-        cudaFuncSetAttribute(k_ca_bits_run<RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_ca_bits_run<RHO, NWX, CPIY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 0, dev = 0, nsm = 148;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ca_bits_run<RHO>, RUN_NWARP * 32, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ca_bits_run<RHO, NWX, CPIY>, NWX * 32, smem);
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         return (per_sm > 0 ? per_sm : 1) * nsm;
@@ -572,8 +579,8 @@ cudaError_t launch_run_t(const Geom& g, const CUtensorMap& tA, const CUtensorMap
     int S = g.side, WP = bits_pitch_words(g.side);
     void* args[] = {const_cast<CUtensorMap*>(&tA), const_cast<CUtensorMap*>(&tB), &A, &B, &ch,
                     const_cast<unsigned**>(&count), &steps, &S, &WP};
-    return cudaLaunchCooperativeKernel((const void*)k_ca_bits_run<RHO>, dim3(grid), dim3(RUN_NWARP * 32), args, smem,
-                                       s);
+    return cudaLaunchCooperativeKernel((const void*)k_ca_bits_run<RHO, NWX, CPIY>, dim3(grid), dim3(NWX * 32), args,
+                                       smem, s);
 }
 
 template <int KIND>
@@ -708,8 +715,15 @@ cudaError_t launch_ca_bits_run(const Geom& g, const void* tmA, const void* tmB, 
                                const void* chunks, const unsigned* count, int steps, cudaStream_t s) {
     const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(tmA);
     const CUtensorMap& tb = *reinterpret_cast<const CUtensorMap*>(tmB);
-    if (g.rho == 4) return launch_run_t<4>(g, ta, tb, A, B, chunks, count, steps, s);
-    return launch_run_t<8>(g, ta, tb, A, B, chunks, count, steps, s);
+    if (g.rho == 4) {
+        // few items per warp (latency-bound, C2: 4.38 -> 4.00 us per step):
+        // one chunk per item, its z-march split over both half-warps; many
+        // items (>= 177 M cells: 4-6 % faster): two chunks per item, fewer
+        // idle h-sum lanes. 32 warps per SM measured no better than 16.
+        if (tet_cells(g.side) <= (32ull << 20)) return launch_run_t<4, 16, 1>(g, ta, tb, A, B, chunks, count, steps, s);
+        return launch_run_t<4, 16, 2>(g, ta, tb, A, B, chunks, count, steps, s);
+    }
+    return launch_run_t<8, 16, 1>(g, ta, tb, A, B, chunks, count, steps, s);
 }
 
 void launch_ca_bits(const Geom& g, int kind, int wz0, int wz1, const void* tmap_ptr, uint32_t* nbits, cudaStream_t s) {
