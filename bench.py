@@ -84,7 +84,7 @@ def ncu_kernel_traffic(key: str):
 class ClockSampler:
     """nvidia-smi-equivalent clock / throttle-reason sampling through NVML."""
 
-    def __init__(self, index=0, period=0.05):
+    def __init__(self, index=0, period=0.002):
         self.index, self.period = index, period
         self.samples, self.reasons = [], set()
         self.max_mhz = None
