@@ -55,14 +55,19 @@ constexpr int BOXW = 12;
 constexpr int NWARP = 4;  // warps per CTA
 constexpr int NTHR = NWARP * 32;
 
-// CPIX: chunks per warp item (default: as many as the 32 lanes can march, 32 /
-// (4 rho)); the persistent small-grid runs use 1 to halve an item's latency.
-template <int RHO, int CPIX = 32 / (RHO * 4)>
-struct Cfg {
+// chunking: tiles per chunk and the per-launch scheme's patch (blocks per CTA)
+template <int RHO>
+struct PlanCfg {
     static constexpr int LMAX = OWN / RHO;              // tiles per chunk
     static constexpr int P = LMAX;                      // patch edge (blocks)
     static constexpr int NZ = 4;                        // max wz layers per CTA
     static constexpr int NB = P * P * NZ;               // max blocks per CTA
+};
+
+// CPIX: chunks per warp item (default: as many as the 32 lanes can march, 32 /
+// (4 rho)); the persistent small-grid runs use 1 to halve an item's latency.
+template <int RHO, int CPIX = 32 / (RHO * 4)>
+struct Cfg {
     static constexpr int HL = RHO + 2;                  // halo layers == halo rows per layer
     static constexpr int LPC = RHO * 4;                 // compute lanes per chunk
     static constexpr int CPI = CPIX;                    // chunks per warp item
@@ -408,7 +413,7 @@ __global__ void __launch_bounds__(NTHR) k_ca_bits(Geom g, int wz0, const __grid_
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     const int nchunks =
-        build_chunks<KIND>(g, wz0 + blockIdx.z * NZ, wz1, P, NZ, C::LMAX, s_tile, s_chunk, s_nchunks, s_link);
+        build_chunks<KIND>(g, wz0 + blockIdx.z * NZ, wz1, P, NZ, PlanCfg<RHO>::LMAX, s_tile, s_chunk, s_nchunks, s_link);
     uint32_t phases = 0u;
     run_items<RHO>(s_chunk, nchunks, warp, NWARP, &tmap, nbits, g.side, WP, wbase, mbar0, phases);
 }
@@ -433,7 +438,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_ca_plan(Geom g, int wz0, int w
     int* s_nchunks = reinterpret_cast<int*>(smem + 2 * NBP * 16);
     uint32_t* s_link = reinterpret_cast<uint32_t*>(smem + 2 * NBP * 16 + 16);
     __shared__ unsigned s_base;
-    const int n = build_chunks<KIND>(g, wz0 + blockIdx.z * NZ, wz1, P, NZ, C::LMAX, s_tile, s_chunk, s_nchunks, s_link);
+    const int n = build_chunks<KIND>(g, wz0 + blockIdx.z * NZ, wz1, P, NZ, PlanCfg<RHO>::LMAX, s_tile, s_chunk, s_nchunks, s_link);
     if (threadIdx.x == 0) s_base = atomicAdd(count, unsigned(n));
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) out[s_base + i] = s_chunk[i];
@@ -526,14 +531,14 @@ void launch_t(const Geom& g, int wz0, int wz1, const CUtensorMap& tmap, uint32_t
     using C = Cfg<RHO>;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_ca_bits<KIND, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(C::NB));
+        cudaFuncSetAttribute(k_ca_bits<KIND, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(PlanCfg<RHO>::NB));
         attr_set = true;
     }
     // patch edge: the largest that still gives >= 4 CTAs per SM (small grids
     // trade chunk length for parallelism)
     // and up to NZ wz layers per CTA (more chunks per warp keep the TMA
     // double buffer busy) while the grid still gives >= 4 CTAs per SM
-    int P = C::P, NZ = C::NZ;
+    int P = PlanCfg<RHO>::P, NZ = PlanCfg<RHO>::NZ;
     auto ctas = [&](int p, int nz) {
         return (long long)((g.ex + p - 1) / p) * ((g.ey + p - 1) / p) * ((wz1 - wz0 + nz - 1) / nz);
     };
@@ -550,7 +555,7 @@ void launch_plan_t(const Geom& g, void* chunks, unsigned* count, cudaStream_t s)
     // extents, so the hinge fold and the slab levels fragment least: H3D(128)
     // 36.3 K chunks vs 40.7 K at P = 12); BB: P = LMAX (rows of the box are
     // unbroken chains, cut every LMAX tiles anyway). 512 threads map a patch.
-    const int P = KIND == SMX_H3D ? 32 : C::LMAX, NZ = 1;
+    const int P = KIND == SMX_H3D ? 32 : PlanCfg<RHO>::LMAX, NZ = 1;
     const int smem = 2 * P * P * NZ * 16 + 16 + 4 * P * P * NZ * 4;  // tiles | chunks | count | links
     static bool attr_set = false;
     if (!attr_set) {
