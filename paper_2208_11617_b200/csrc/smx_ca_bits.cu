@@ -96,10 +96,12 @@ __device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
 }
+// the waiting thread is suspended (up to the hint, 10 ms) until the phase
+// completes instead of spinning: no issue slots burnt while the box lands
 __device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t parity) {
     uint32_t ok;
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 10000000;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok)
         : "r"(a), "r"(parity)
         : "memory");
@@ -298,8 +300,11 @@ __device__ __forceinline__ void run_items(const Chunk* __restrict__ s_chunk, int
         const uint8_t* buf = wbase + b * C::BUF;
 
         // ---- 3. horizontal 3-sums (bit-planes), lane per halo row ----
-        for (int r = lane; r < C::HROWS; r += 32) {
-            const int c = r / (HL * HL), rr = r % (HL * HL);
+#pragma unroll
+        for (int pass = 0; pass < (C::HROWS + 31) / 32; ++pass) {
+            const int r = lane + 32 * pass;
+            if (r >= C::HROWS) break;
+            const int c = r / (HL * HL), rr = r % (HL * HL);  // lane/pass constants, hoisted by the unroll
             const int zi = rr / HL, yi = rr % HL;
             const int ci = item * C::CPI + c;
             uint4 h0 = make_uint4(0, 0, 0, 0), h1 = h0;
