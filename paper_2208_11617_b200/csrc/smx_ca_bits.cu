@@ -455,9 +455,30 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_ca_plan(Geom g, int wz0, int w
 // acquire), then a proxy fence before the next TMA issue. Measured per-step
 // floor on B200 (tools/step_floor.py): 3.1 us with grid.sync() vs 3.4 us with
 // a hand-rolled acq_rel counter barrier; 5.1 vs 5.9 us at C2.
-__device__ __forceinline__ void step_barrier() {
+//
+// The barrier is the cooperative-groups algorithm (one arrival counter; the
+// master's arrival flips its top bit) with a nanosleep back-off in the poll:
+// same latency (1.19 vs 1.20 us, tools/barrier_probe.cu), but a CTA that
+// arrives early no longer burns the issue slots a co-resident CTA still
+// computing its items needs (the spin was 10 % of all C2 instructions). `bar`
+// is a zeroed word of the launch's control block; cooperative launch keeps
+// every CTA resident.
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void step_barrier(unsigned* bar) {
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
-    cooperative_groups::this_grid().sync();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned nb = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+        __threadfence();
+        const unsigned old = atomicAdd(bar, nb);
+        while (((old ^ ld_acquire_gpu(bar)) & 0x80000000u) == 0) __nanosleep(64);
+    }
+    __syncthreads();
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
 
@@ -474,8 +495,7 @@ template <int RHO, int NWX = 16, int CPIY = 32 / (RHO * 4)>
 __global__ void __launch_bounds__(NWX * 32) k_ca_bits_run(const __grid_constant__ CUtensorMap tmA,
                                                       const __grid_constant__ CUtensorMap tmB, uint32_t* bitsA,
                                                       uint32_t* bitsB, const Chunk* __restrict__ chunks,
-                                                      const unsigned* __restrict__ count, int steps, int S,
-                                                      int WP) {
+                                                      unsigned* count, int steps, int S, int WP) {
     using C = Cfg<RHO, CPIY>;
     constexpr int RUN_NWARP = NWX;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -527,7 +547,7 @@ __global__ void __launch_bounds__(NWX * 32) k_ca_bits_run(const __grid_constant_
         const bool even = (st & 1) == 0;
         run_items<RHO, CPIY>(src, nsrc, i0, istr, even ? &tmA : &tmB, even ? bitsB : bitsA, S, WP,
                                           wbase, mbar0, phases);
-        if (st + 1 < steps) step_barrier();
+        if (st + 1 < steps) step_barrier(count + 8);  // count: word 0 of the zeroed 64-byte control block
     }
 }
 
@@ -587,8 +607,8 @@ cudaError_t launch_run_t(const Geom& g, const CUtensorMap& tA, const CUtensorMap
     }();
     const Chunk* ch = reinterpret_cast<const Chunk*>(chunks);
     int S = g.side, WP = bits_pitch_words(g.side);
-    void* args[] = {const_cast<CUtensorMap*>(&tA), const_cast<CUtensorMap*>(&tB), &A, &B, &ch,
-                    const_cast<unsigned**>(&count), &steps, &S, &WP};
+    unsigned* ctl = const_cast<unsigned*>(count);
+    void* args[] = {const_cast<CUtensorMap*>(&tA), const_cast<CUtensorMap*>(&tB), &A, &B, &ch, &ctl, &steps, &S, &WP};
     return cudaLaunchCooperativeKernel((const void*)k_ca_bits_run<RHO, NWX, CPIY>, dim3(grid), dim3(NWX * 32), args,
                                        smem, s);
 }

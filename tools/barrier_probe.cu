@@ -59,14 +59,35 @@ __global__ void k_tree(int iters, unsigned* ctr) {
     }
 }
 
+// the cooperative-groups algorithm (one arrival counter, the master's flip bit)
+// with a nanosleep back-off in the poll: the polling warp stops competing for
+// issue slots with co-resident CTAs that are still computing
+template <int NS>
+__global__ void k_cgsleep(int iters, unsigned* ctr) {
+    const unsigned expected = gridDim.x;
+    for (int i = 0; i < iters; ++i) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned nb = blockIdx.x == 0 ? 0x80000000u - (expected - 1) : 1u;
+            __threadfence();
+            const unsigned old = atomicAdd(ctr, nb);
+            while (((old ^ ld_acquire(ctr)) & 0x80000000u) == 0) {
+                if (NS > 0) __nanosleep(NS);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 int main() {
     unsigned* buf;
     cudaMalloc(&buf, 1 << 20);
     int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    const char* names[3] = {"cg", "flags", "tree"};
-    void* fns[3] = {(void*)k_cg, (void*)k_flags, (void*)k_tree};
-    for (int v = 0; v < 3; ++v) {
+    const char* names[7] = {"cg", "flags", "tree", "cgs0", "cgs32", "cgs100", "cgs250"};
+    void* fns[7] = {(void*)k_cg, (void*)k_flags, (void*)k_tree, (void*)k_cgsleep<0>, (void*)k_cgsleep<32>,
+                    (void*)k_cgsleep<100>, (void*)k_cgsleep<250>};
+    for (int v = 0; v < 7; ++v) {
         float t[2];
         int its[2] = {10, 1010};
         for (int k = 0; k < 2; ++k) {
