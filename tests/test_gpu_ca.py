@@ -122,3 +122,38 @@ def test_c4_100_steps_vs_restated_oracle(cuda, orc):
     api.life_init_device(3, side, 42, cur)
     api.ca_device(gb, cur, 100, api.EXEC_RUNS)
     assert (cur.cpu().numpy() == want).all()
+    # and the product path: the bit-shadow engine (pack, plan, one persistent
+    # launch of all 100 steps, unpack), H and BB
+    for grid in (g, gb):
+        api.life_init_device(3, side, 42, cur)
+        api.ca_device(grid, cur, 100, api.EXEC_BITS)
+        assert (cur.cpu().numpy() == want).all(), grid
+
+
+@pytest.mark.slow
+def test_c5_full_size_engine_vs_block_scheme(cuda):
+    """C5: H3D(256), rho = 8, side 2040 (1,417,025,480 cells). The engine's
+    3 steps (H3D and BB) equal 3 steps of the paper's one-thread-per-cell block
+    scheme (an independent kernel: 26 byte neighbours through L1), and one
+    single-step u8 -> u8 call equals one block step; compared on the device."""
+    import torch
+    g = api.make_grid(api.map_kind.h3d, 3, 256, 8)
+    gb = api.make_grid(api.map_kind.bb, 3, 255, 8)
+    side = g.cell_side()
+    n = api.tet_cells(side)
+    a = torch.empty(n + 256, dtype=torch.uint8, device="cuda")[:n]
+    b = torch.empty(n + 256, dtype=torch.uint8, device="cuda")[:n]
+    ref = torch.empty(n + 256, dtype=torch.uint8, device="cuda")[:n]
+    api.life_init_device(3, side, 42, ref)
+    for _ in range(3):  # block scheme, u8 -> u8 per step
+        api.ca_step_device(g, ref, b, api.EXEC_BLOCK)
+        ref, b = b, ref
+    for grid in (g, gb):
+        api.life_init_device(3, side, 42, a)
+        api.ca_device(grid, a, 3, api.EXEC_BITS)
+        assert torch.equal(a, ref), grid
+    api.life_init_device(3, side, 42, a)
+    api.ca_step_device(g, a, b, api.EXEC_AUTO)
+    api.life_init_device(3, side, 42, ref)
+    api.ca_step_device(gb, ref, a, api.EXEC_BLOCK)
+    assert torch.equal(a, b)
