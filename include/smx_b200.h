@@ -162,6 +162,14 @@ int smx_map_kernel(const smx_grid* g, void* stream);
 int smx_accum(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passes, int32_t exec,
               int device_ptr, uint32_t* coverage, smx_counters* counters, void* stream);
 
+/* launch_accum over the grid rows wy in [wy_lo, wy_hi) only (device pointers,
+ * 2-D non-trapezoid grids): the multi-GPU shard of ACCUM (blocks
+ * are independent, so a rank runs a contiguous range of grid rows and no cell
+ * data moves; only the counters are summed). counters (nullable): this range's
+ * blocks_launched / blocks_void / threads_launched / threads_useful. */
+int smx_accum_range(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passes, int32_t exec,
+                    int64_t wy_lo, int64_t wy_hi, smx_counters* counters, void* stream);
+
 /* make_life_state (simulator.hpp:390-398) for m = 3 (and m = 2): writes
  * smx_cell_count(m, side) bytes. */
 int smx_life_init(int32_t m, int64_t side, uint64_t seed, uint8_t* cells, uint64_t ncells,

@@ -68,6 +68,8 @@ _SIGS = {
     "smx_map_kernel": ([_G, _VP], C.c_int),
     "smx_accum": ([_G, _VP, C.c_uint64, C.c_int64, C.c_int32, C.c_int, _VP,
                    C.POINTER(smx_counters), _VP], C.c_int),
+    "smx_accum_range": ([_G, _VP, C.c_uint64, C.c_int64, C.c_int32, C.c_int64, C.c_int64,
+                         C.POINTER(smx_counters), _VP], C.c_int),
     "smx_life_init": ([C.c_int32, C.c_int64, C.c_uint64, _VP, C.c_uint64, C.c_int, _VP], C.c_int),
     "smx_ca_step": ([_G, _VP, _VP, C.c_uint64, C.c_int32, _VP], C.c_int),
     "smx_ca": ([_G, _VP, C.c_uint64, C.c_int64, C.c_int32, C.c_int, _VP, _VP,

@@ -541,6 +541,17 @@ def accum_device(g: grid_spec, cells, passes: int = 1, exec: int = EXEC_RUNS) ->
     check(lib().smx_accum(C.byref(g.raw), _ptr(cells), cells.numel(), passes, exec, 1, None, None, _stream()))
 
 
+def accum_range_device(g: grid_spec, cells, passes: int, wy_lo: int, wy_hi: int,
+                       exec: int = EXEC_RUNS) -> dict:
+    """ACCUM over grid rows [wy_lo, wy_hi) only (a multi-GPU shard, SURVEY 8(e));
+    returns that range's launch counters."""
+    cnt = _lib.smx_counters()
+    check(lib().smx_accum_range(C.byref(g.raw), _ptr(cells), cells.numel(), passes, exec, wy_lo, wy_hi,
+                                C.byref(cnt), _stream()))
+    return {"blocks_launched": int(cnt.blocks_launched), "blocks_void": int(cnt.blocks_void),
+            "threads_launched": int(cnt.threads_launched), "threads_useful": int(cnt.threads_useful)}
+
+
 def life_init_device(m: int, side: int, seed: int, cells) -> None:
     check(lib().smx_life_init(m, side, seed, _ptr(cells), cells.numel(), 1, _stream()))
 

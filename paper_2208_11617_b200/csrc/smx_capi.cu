@@ -653,6 +653,44 @@ int smx_accum(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passe
     return SMX_OK;
 }
 
+int smx_accum_range(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passes, int32_t exec,
+                    int64_t wy_lo, int64_t wy_hi, smx_counters* counters, void* stream) {
+    if (!g) return fail(SMX_EINVAL, "null grid");
+    if (g->dims != 2 || g->kind == SMX_TRAP)
+        return fail(SMX_EINVAL, "accum_range: row ranges shard the 2-simplex grids other than trapezoid bands");
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    if (int rc = check_cells(g, ncells)) return rc;
+    if (passes < 0) return fail(SMX_EINVAL, "accum: passes must be >= 0");
+    if (wy_lo < 0 || wy_hi > k.ey || wy_lo > wy_hi) return fail(SMX_EINVAL, "accum_range: rows outside the grid");
+    if (exec < 0) exec = SMX_EXEC_RUNS;
+    if (resolve_exec(exec) < 0) return fail(SMX_EINVAL, "accum: unknown exec scheme");
+    cudaStream_t s = (cudaStream_t)stream;
+    k.wy0 = int(wy_lo);
+    k.ey = int(wy_hi - wy_lo);
+    if (counters) {
+        smx::DevCounters* dc;
+        if (int rc = counters_buf(&dc)) return rc;
+        TRY(cudaMemsetAsync(dc, 0, sizeof(smx::DevCounters), s));
+        if (k.ey > 0) smx::launch_map_block(k, nullptr, dc, nullptr, s);
+        TRY(cudaGetLastError());
+        smx::DevCounters h;
+        TRY(cudaMemcpyAsync(&h, dc, sizeof h, cudaMemcpyDeviceToHost, s));
+        TRY(cudaStreamSynchronize(s));
+        uint64_t v = 0, u = 0;
+        for (int i = 0; i < smx::NSLOT; ++i) v += h.blocks_void[i], u += h.threads_useful[i];
+        const uint64_t blocks = uint64_t(k.ex) * uint64_t(k.ey);
+        counters->blocks_launched = blocks;
+        counters->blocks_void = v;
+        counters->threads_launched = blocks * uint64_t(g->rho) * uint64_t(g->rho);
+        counters->threads_useful = u;
+    }
+    if (k.ey > 0)
+        for (int64_t p = 0; p < passes; ++p) smx::launch_accum(k, cells, exec, s);
+    TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
 int smx_life_init(int32_t m, int64_t side, uint64_t seed, uint8_t* cells, uint64_t ncells, int device_ptr,
                   void* stream) {
     if (m != 2 && m != 3) return fail(SMX_EINVAL, "simplex_grid_state: m must be 2 or 3");

@@ -20,6 +20,7 @@ struct Geom {
     int side;             // cell side S
     const unsigned long long* prefix;  // 3-D: tet_layer_prefix(S, z), z = 0..S+1
     trapezoid<int> trap;  // SMX_TRAP: the band this launch covers (one launch per band)
+    int wy0;              // first grid row of this launch (row-range shards: wy = wy0 + blockIdx.y)
 };
 
 // strict_view (maps.hpp:35-38): outputs in { x < y }, shifted y - 1 by the sweep

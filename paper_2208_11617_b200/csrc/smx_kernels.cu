@@ -63,7 +63,7 @@ __device__ __forceinline__ int flat_tid() {
 template <int KIND, int MODE>
 __global__ void k_map_block(Geom g, int wz0, uint32_t* __restrict__ cov, DevCounters* cnt,
                             unsigned* sink) {
-    const int wx = blockIdx.x, wy = blockIdx.y, wz = blockIdx.z + wz0;
+    const int wx = blockIdx.x, wy = g.wy0 + blockIdx.y, wz = blockIdx.z + wz0;
     const BlockTarget t = warp_map<KIND>(g, wx, wy, wz);
     const int slot = (wx + 7 * wy + 13 * wz) & (NSLOT - 1);
     if (t.is_void) {
@@ -99,7 +99,7 @@ __global__ void k_map_block(Geom g, int wz0, uint32_t* __restrict__ cov, DevCoun
 // ACCUM, block scheme (the paper's launch model): ++cells[idx] per useful thread.
 template <int KIND>
 __global__ void k_accum_block(Geom g, uint32_t* __restrict__ cells) {
-    const int wx = blockIdx.x, wy = blockIdx.y;
+    const int wx = blockIdx.x, wy = g.wy0 + blockIdx.y;
     const BlockTarget t = warp_map<KIND>(g, wx, wy, 0);
     if (t.is_void) return;
     const int rho = g.rho, S = g.side;
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(ACC_THREADS, 4) k_accum_runs(Geom g, uint32_t*
     __shared__ int s_run[KX][3];
     __shared__ int s_nruns;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp == 0) strip_runs<KIND, KX>(g, blockIdx.x * KX, blockIdx.y, s_run, &s_nruns);
+    if (warp == 0) strip_runs<KIND, KX>(g, blockIdx.x * KX, g.wy0 + blockIdx.y, s_run, &s_nruns);
     __syncthreads();
     const int nruns = s_nruns;
     const int rho = g.rho, S = g.side;

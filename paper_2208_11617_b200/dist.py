@@ -82,6 +82,52 @@ _OFFSETS = np.array([(dx, dy, dz) for dz in (-1, 0, 1) for dy in (-1, 0, 1) for 
                      if (dx, dy, dz) != (0, 0, 0)], np.int64)
 
 
+def partition_rows(useful_per_wy: np.ndarray, world: int) -> list[tuple[int, int]]:
+    """ACCUM / MAP sharding: blocks are independent, so each rank
+    takes a contiguous range of grid rows [lo, hi), balanced by useful (non-Void)
+    block count; no cell data is exchanged, only the u64 counters are summed."""
+    u = np.asarray(useful_per_wy, dtype=np.int64)
+    ey = u.shape[0]
+    csum = np.concatenate([[0], np.cumsum(u)])
+    total = int(csum[-1])
+    cuts = [0]
+    for r in range(1, world):
+        cuts.append(int(np.searchsorted(csum, total * r / world, side="left")))
+    cuts.append(ey)
+    cuts = [min(max(c, cuts[i - 1] if i else 0), ey) for i, c in enumerate(cuts)]
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def useful_per_row(outcomes: np.ndarray, ex: int, ey: int) -> np.ndarray:
+    """Non-Void blocks per grid row from a map_outcomes dump (wx fastest)."""
+    o = np.asarray(outcomes).reshape(-1, ex, np.asarray(outcomes).shape[-1])[:ey]
+    return (o[:, :, 0] == 0).sum(axis=1)
+
+
+class ShardedAccum:
+    """launch_accum sharded by grid rows: rank r accumulates rows
+    wy_ranges[r] into its own device state (the cells its blocks map to); the
+    counters are all-reduced (sum). `run` returns the job's counters."""
+
+    def __init__(self, grid, wy_ranges: list[tuple[int, int]], rank: int, group=None, counters_device="cpu"):
+        import torch.distributed as dist
+
+        self.dist, self.g, self.rank, self.group = dist, grid, rank, group
+        self.lo, self.hi = wy_ranges[rank]
+        self.dev = counters_device
+
+    def run(self, cells, passes: int, exec_=None) -> dict:
+        import torch
+
+        from . import api
+        c = api.accum_range_device(self.g, cells, passes, self.lo, self.hi,
+                                   api.EXEC_RUNS if exec_ is None else exec_)
+        keys = ("blocks_launched", "blocks_void", "threads_launched", "threads_useful")
+        t = torch.tensor([c[k] for k in keys], dtype=torch.int64, device=self.dev)
+        self.dist.all_reduce(t, group=self.group)
+        return dict(zip(keys, (int(v) for v in t.tolist())))
+
+
 def build_plan(extents: tuple[int, int, int], outcomes: np.ndarray, strict: bool, domain_blocks: int,
                world: int) -> HaloPlan:
     """outcomes: one row per block in natural z, y, x order, columns

@@ -132,3 +132,19 @@ def test_partition_balanced_whole_levels():
         for r in range(world):
             for q, t in plan.recv(r).items():
                 assert (plan.send[q][r] == t).all()
+
+
+def test_partition_rows_balanced_and_contiguous():
+    """ACCUM / MAP row sharding: contiguous row ranges covering
+    the grid, balanced by useful blocks within one row's weight."""
+    from oracle.oracle import BB, H2D, Restated
+    from paper_2208_11617_b200 import dist as D
+    o = Restated()
+    for kind, n, ex, ey in ((H2D, 64, 32, 63), (BB, 63, 63, 63), (H2D, 1024, 512, 1023)):
+        u = D.useful_per_row(o.map_outcomes(kind, 2, n), ex, ey)
+        for world in (1, 2, 3, 8):
+            r = D.partition_rows(u, world)
+            assert r[0][0] == 0 and r[-1][1] == ey
+            assert all(r[i][1] == r[i + 1][0] for i in range(world - 1))
+            loads = [int(u[lo:hi].sum()) for lo, hi in r]
+            assert max(loads) - int(u.sum()) / world <= int(u.max()), (kind, n, world, loads)
