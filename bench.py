@@ -349,11 +349,14 @@ def run_ours(args):
         "single_step": single,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "k_ca_bits_run<4> (+ its k_ca_plan): 100 map-driven bit-sliced steps per launch",
+                     "frac_vs_nominal_8tbs": round(achieved / 8000.0, 4),
+                     "kernel": "k_ca_bits_run<4,16,1> (+ its k_ca_plan): 100 map-driven bit-sliced steps per launch",
                      "kernel_ms": round(kms, 6), "launches_per_call": 1,
                      "basis": "2 B per useful cell per step (u8 read + u8 write, SURVEY 8(d)) x 100 steps; "
                               "CUDA events around the launch; C2's 2.7 MB state is L2-resident, so HBM is "
-                              "not the binding roof here (see configs.C5 for the HBM-bound size)",
+                              "not the binding roof here (see configs.C4/C5 for the HBM-bound sizes: engine "
+                              "1.0-1.06 of this peak on the u8 basis); a step is barrier (1.2 us) + one item's "
+                              "TMA + compute latency",
                      "peak_source": peak_src},
         "e2e": {"value": round(gcells(cells * nsteps, e2e_ms), 3), "unit": "Gcell-steps/s",
                 "h2d_bytes_per_step": cells, "d2h_bytes_per_step": cells, "ms_per_step": round(e2e_ms, 4),
