@@ -134,3 +134,12 @@ def test_library_has_sm100a_code():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_missing_library_fails_loudly(monkeypatch):
+    """No CPU fallback: without the sm_100a library every entry point raises."""
+    from paper_2208_11617_b200 import _lib
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", "/nonexistent/libsmx_b200.so")
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        _lib.lib()
