@@ -143,3 +143,12 @@ def test_missing_library_fails_loudly(monkeypatch):
     monkeypatch.setattr(_lib, "LIB_PATH", "/nonexistent/libsmx_b200.so")
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         _lib.lib()
+
+
+def test_accum_range_contract_checked_before_device_work():
+    """smx_accum_range shards 2-D non-trapezoid grids by rows; other grids are
+    rejected with the contract message before any CUDA call."""
+    L = _lib.lib()
+    for g in (api.grid_h3d(8), api.grid_trapezoids(9, 1)):
+        rc = L.smx_accum_range(C.byref(g.raw), None, 0, 1, api.EXEC_RUNS, 0, 1, None, None)
+        assert rc == 1 and b"row ranges" in L.smx_last_error()
