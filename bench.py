@@ -318,6 +318,11 @@ def run_ours(args):
 
     timed_steps(e2e_call, args.warmup, flush)
     e2e_ms = statistics.mean(timed_steps(e2e_call, args.steps, flush))
+    # where the e2e time goes: the two PCIe copies of the state alone
+    dev = torch.empty(cells, dtype=torch.uint8, device="cuda")
+    h2d_ms = statistics.median(timed_steps(lambda i: dev.copy_(host, non_blocking=True), 5, flush))
+    d2h_ms = statistics.median(timed_steps(lambda i: host.copy_(dev, non_blocking=True), 5, flush))
+    del dev
 
     j_h = energy_per_cell(sampler, h["call"], cells * nsteps)
     j_bb = energy_per_cell(sampler, bb["call"], cells * nsteps)
@@ -360,7 +365,9 @@ def run_ours(args):
                      "peak_source": peak_src},
         "e2e": {"value": round(gcells(cells * nsteps, e2e_ms), 3), "unit": "Gcell-steps/s",
                 "h2d_bytes_per_step": cells, "d2h_bytes_per_step": cells, "ms_per_step": round(e2e_ms, 4),
-                "path": "smx_ca(host buffer, steps=100, EXEC_AUTO) through the C ABI"},
+                "path": "smx_ca(host buffer, steps=100, EXEC_AUTO) through the C ABI",
+                "h2d_ms": round(h2d_ms, 4), "d2h_ms": round(d2h_ms, 4),
+                "pcie_gb_s": round(2.0 * cells / ((h2d_ms + d2h_ms) * 1e-3) / 1e9, 1)},
         "energy": {"j_per_cell_step_h": j_h, "j_per_cell_step_bb": j_bb},
         "cpu_baseline": cpu,
         "gpu_launches": 4 * args.steps,  # pack, plan, persistent run, unpack (+1 memset) per call
