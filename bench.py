@@ -373,6 +373,7 @@ def run_ours(args):
         "gpu_launches": 4 * args.steps,  # pack, plan, persistent run, unpack (+1 memset) per call
         "clocks": sampler.summary(),
         "configs": configs,
+        "h_vs_bb_summary": h_vs_bb_summary(configs, single, round(ms_bb / ms_h, 3)),
     }
     return line
 
@@ -392,6 +393,24 @@ def cpu_baseline_c2(kind, n, rho, side):
     except Exception as e:  # pragma: no cover
         return {"value": None, "unit": "Gcell-steps/s", "cores": 1, "kind": "reference",
                 "sample": f"unavailable: {e}"}
+
+
+def h_vs_bb_summary(configs, single, engine_c2):
+    """The paper's headline comparison in one place: where the work is per
+    launched block (the MAP kernel, the one-CTA-per-block launch model) H's
+    fewer blocks show as the block ratio; the x-run schemes make BB's Void
+    blocks nearly free, so the streaming kernels run at the same roof."""
+    out = {"engine_c2_launch_ca": engine_c2, "single_step_block_model_c2": single.get("block", {}).get("h_vs_bb")}
+    pick = {"map_kernel_2d": ("C1_map_kernel_2d", None), "map_kernel_3d": ("map_kernel_3d", None),
+            "accum_block_model_c3": ("C3_accum_n65536", "block"), "accum_xrun_c3": ("C3_accum_n65536", "runs"),
+            "ca_block_model_c5_1step": ("C5_ca_n2048_1gpu", "single_block"),
+            "ca_engine_c5": ("C5_ca_n2048_1gpu", "engine")}
+    for k, (cfg, sub) in pick.items():
+        c = configs.get(cfg)
+        if c is not None:
+            c = c.get(sub) if sub else c
+            out[k] = c.get("h_vs_bb") if isinstance(c, dict) else None
+    return out
 
 
 def extra_configs(api, flush, sampler, peak, args):
