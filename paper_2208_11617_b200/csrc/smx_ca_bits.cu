@@ -554,11 +554,12 @@ __global__ void __launch_bounds__(NWX * 32) k_ca_bits_run(const __grid_constant_
 template <int KIND, int RHO>
 void launch_t(const Geom& g, int wz0, int wz1, const CUtensorMap& tmap, uint32_t* nbits, int WP, cudaStream_t s) {
     using C = Cfg<RHO>;
-    static bool attr_set = false;
-    if (!attr_set) {
+    // once per process, thread-safe (a function-local static's initialiser)
+    static const bool attr_set = [&] {
         cudaFuncSetAttribute(k_ca_bits<KIND, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(PlanCfg<RHO>::NB));
-        attr_set = true;
-    }
+        return true;
+    }();
+    (void)attr_set;
     // patch edge: the largest that still gives >= 4 CTAs per SM (small grids
     // trade chunk length for parallelism)
     // and up to NZ wz layers per CTA (more chunks per warp keep the TMA
@@ -582,11 +583,12 @@ void launch_plan_t(const Geom& g, void* chunks, unsigned* count, cudaStream_t s)
     // unbroken chains, cut every LMAX tiles anyway). 512 threads map a patch.
     const int P = KIND == SMX_H3D ? 32 : PlanCfg<RHO>::LMAX, NZ = 1;
     const int smem = 2 * P * P * NZ * 16 + 16 + 4 * P * P * NZ * 4;  // tiles | chunks | count | links
-    static bool attr_set = false;
-    if (!attr_set) {
+    // once per process, thread-safe (a function-local static's initialiser)
+    static const bool attr_set = [&] {
         cudaFuncSetAttribute(k_ca_plan<KIND, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr_set = true;
-    }
+        return true;
+    }();
+    (void)attr_set;
     const dim3 grid((g.ex + P - 1) / P, (g.ey + P - 1) / P, g.ez);
     k_ca_plan<KIND, RHO><<<grid, PLAN_THREADS, smem, s>>>(g, 0, g.ez, P, NZ,
                                                                               reinterpret_cast<Chunk*>(chunks), count);

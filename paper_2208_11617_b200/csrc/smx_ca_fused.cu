@@ -271,12 +271,13 @@ template <int KIND, int RHO>
 void launch_fused_t(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t* next, cudaStream_t s) {
     using C = FCfg<RHO>;
     constexpr int NZMAX = 2;
-    static bool attr_set = false;
-    if (!attr_set) {
+    // once per process, thread-safe (a function-local static's initialiser)
+    static const bool attr_set = [&] {
         cudaFuncSetAttribute(k_ca_fused<KIND, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::smem(C::LMAX * C::LMAX * NZMAX));
-        attr_set = true;
-    }
+                                    C::smem(C::LMAX * C::LMAX * NZMAX));
+        return true;
+    }();
+    (void)attr_set;
     // patch edge and layers per CTA: as large as possible while the grid still
     // has >= 2 CTAs per SM (small grids trade chunk length for parallelism)
     int P = C::LMAX, NZ = NZMAX;
