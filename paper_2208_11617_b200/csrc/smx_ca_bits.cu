@@ -579,9 +579,12 @@ void launch_plan_t(const Geom& g, void* chunks, unsigned* count, cudaStream_t s)
     using C = Cfg<RHO>;
     // Chains stop at patch edges. H3D: 32 x 32 patches (32 divides the n/2
     // extents, so the hinge fold and the slab levels fragment least: H3D(128)
-    // 36.3 K chunks vs 40.7 K at P = 12); BB: P = LMAX (rows of the box are
-    // unbroken chains, cut every LMAX tiles anyway). 512 threads map a patch.
-    const int P = KIND == SMX_H3D ? 32 : PlanCfg<RHO>::LMAX, NZ = 1;
+    // 36.3 K chunks vs 40.7 K at P = 12); BB: P = 2-3 LMAX (rows of the box are
+    // unbroken chains cut every LMAX tiles from wx = 0, so any multiple of LMAX
+    // gives the same chunks): rho = 8, 3 LMAX = 36 keeps the 512 threads busy
+    // (BB plan 61 -> 32 us at C4, 463 -> 199 us at C5); rho = 4, LMAX (more
+    // CTAs win at C2: 8.6 vs 13.8 us at 2 LMAX).
+    const int P = KIND == SMX_H3D ? 32 : PlanCfg<RHO>::LMAX * (RHO == 8 ? 3 : 1), NZ = 1;
     const int smem = 2 * P * P * NZ * 16 + 16 + 4 * P * P * NZ * 4;  // tiles | chunks | count | links
     // once per process, thread-safe (a function-local static's initialiser)
     static const bool attr_set = [&] {
