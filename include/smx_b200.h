@@ -19,7 +19,8 @@
  *    (the reference's mutate-in-place semantics, simulator.hpp:313-326,431-463).
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).
  *  - Threads: the library's scratch (staging pool, bit shadows, CA chunk list,
- *    the side stream the CA plan runs on) is per (device, host thread), so
+ *    the side stream the CA plan runs on) is per (device, host thread) — freed
+ *    by smx_release() or when the thread exits — so
  *    calls on distinct states from distinct threads may run concurrently, as
  *    the reference's launches may. Device-resident calls from ONE thread share
  *    that thread's scratch: issue them on one stream (or synchronise between
@@ -240,7 +241,11 @@ uint64_t smx_state_hash(int32_t m, int64_t side, const void* bytes, uint64_t nby
 
 /* ---- multi-GPU shard support (H block-space partitioner) ----
  * One Life step restricted to H-grid blocks with wz in [wz_lo, wz_hi) (a
- * contiguous sub-box of whole sub-orthotope levels). Device pointers. */
+ * contiguous sub-box of whole sub-orthotope levels). Device pointers. Cells
+ * of `next` outside the range keep their prior values on every exec scheme,
+ * except that the x-run schemes (RUNS, BITS) may also store the correctly
+ * stepped value of cells sharing a 32-cell word / 32-byte sector with a
+ * range tile. */
 int smx_ca_step_range(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint64_t ncells,
                       int64_t wz_lo, int64_t wz_hi, int32_t exec, void* stream);
 
@@ -262,6 +267,16 @@ int smx_bits_tiles_pack(const smx_grid* g, const uint32_t* bits, const int32_t* 
                         void* stream);
 int smx_bits_tiles_unpack(const smx_grid* g, uint32_t* bits, const int32_t* tiles, uint64_t ntiles,
                           const uint8_t* in, void* stream);
+
+/* Frees the calling host thread's library scratch on every device (staging
+ * pools, bit shadows, chunk lists, prefix tables, tensor maps, the side
+ * stream); the next call re-creates what it needs. Synchronises the devices
+ * (cudaFree). A thread's scratch is also freed automatically when the thread
+ * exits. No reference counterpart: the reference holds no device state. */
+int smx_release(void);
+
+/* Bytes of pooled scratch the calling thread currently holds (all devices). */
+uint64_t smx_scratch_bytes(void);
 
 /* cudaDeviceSynchronize on the current device. */
 int smx_device_sync(void);

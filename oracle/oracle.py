@@ -210,6 +210,8 @@ class Reference:
         L.ref_launch_accum.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                        _u32p, C.c_uint64, _u64p, _u64p, C.POINTER(C.c_double)]
         L.ref_make_life_state.argtypes = [C.c_int, C.c_int64, C.c_uint64, _u8p, C.c_uint64]
+        L.ref_accum_sample.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int,
+                                       C.c_int, _f64p, _u64p]
         L.ref_kernel_ca_run.argtypes = [C.c_int, C.c_int64, C.c_int64, _u8p, C.c_uint64,
                                         C.POINTER(C.c_double)]
         L.ref_launch_ca.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
@@ -337,6 +339,17 @@ class Reference:
         self._ok(self.L.ref_launch_accum(kind, m, n, rho, T, passes, cells, cells.size, cnt, h,
                                          C.byref(secs)), "launch_accum")
         return cells, [int(v) for v in cnt], int(h[0]), secs.value
+
+    def accum_sample(self, kind: int, m: int, n: int, rho: int, rows: int, threads: int, warm: int = 1,
+                     reps: int = 1):
+        """ref_accum_sample: the reference's launch_accum sweep over the first
+        `rows` block rows of the grid, `threads` concurrent replicas. Returns
+        (seconds per rep [reps], useful cells per replica per rep)."""
+        secs = np.zeros(reps, np.float64)
+        useful = np.zeros(1, np.uint64)
+        self._ok(self.L.ref_accum_sample(kind, m, n, rho, rows, threads, warm, reps, secs, useful),
+                 "accum_sample")
+        return secs.tolist(), int(useful[0])
 
     def make_life_state(self, m: int, side: int, seed: int) -> np.ndarray:
         out = np.empty(cells_of(m, side), np.uint8)

@@ -14,9 +14,13 @@
 #include <simplexmap/report.hpp>
 #include <simplexmap/simulator.hpp>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <thread>
+#include <vector>
 #include <string>
 
 using namespace simplexmap;
@@ -347,6 +351,56 @@ uint64_t ref_state_hash(int m, int64_t side, const void* bytes, uint64_t nbytes)
     h = fnv1a_append_u64(h, u64(m));
     h = fnv1a_append_u64(h, u64(side));
     return fnv1a_append(h, bytes, nbytes);
+}
+
+// A bounded, multi-core sample of launch_accum (simulator.hpp:313-327) for the
+// bench's reference arm at the full-size grids (C3: 2.1 G cells, ~12 s per
+// pass on one core): the reference's own accounted_sweep (:277-291) with
+// launch_accum's body `++cells[idx]`, over the first `rows` block rows (2-D) or
+// block layers (3-D) of the grid in its natural walk order (:113-118) — the
+// grid itself is untouched, so map, Void filter, thread expansion, membership
+// and packed index are the reference's at that grid. `threads` replicas run
+// concurrently (the reference is single-threaded within a launch,
+// report.hpp:125-156), each on its own zero state (calloc: only the pages the
+// sample touches are materialised). launch_accum's trailing state.hash() (a
+// serial FNV over the whole state) is not part of the sample. Times `reps`
+// repetitions after `warm` untimed ones: seconds[i] = wall time of rep i (all
+// replicas); *useful = cells incremented per replica per rep.
+int ref_accum_sample(int kind, int m, int64_t n, int64_t rho, int64_t rows, int threads, int warm, int reps,
+                     double* seconds, uint64_t* useful) {
+    return guarded([&] {
+        grid_spec g = make_grid(kind_of(kind), m, n, rho, 1);
+        if (g.kind == map_kind::h2d_trapezoid) throw std::invalid_argument("accum_sample: not for trapezoids");
+        if (rows < 1 || threads < 1 || reps < 1 || warm < 0) throw std::invalid_argument("accum_sample: bad sizes");
+        if (g.dims == 2) g.extents[1] = std::min<i64>(g.extents[1], rows);
+        else g.extents[2] = std::min<i64>(g.extents[2], rows);
+        const i64 side = g.domain_side() * g.rho;
+        const std::size_t ncells = std::size_t(g.dims == 2 ? tri_cells(side) : tet_cells(side));
+        std::vector<u32*> states(std::size_t(threads), nullptr);
+        for (auto& p : states) {
+            p = static_cast<u32*>(std::calloc(ncells, sizeof(u32)));
+            if (!p) throw std::runtime_error("accum_sample: out of host memory");
+        }
+        launch_opts o;
+        o.record_coverage = false;
+        std::vector<u64> counts(std::size_t(threads), 0);
+        for (int it = 0; it < warm + reps; ++it) {
+            auto t0 = std::chrono::steady_clock::now();
+            std::vector<std::thread> pool;
+            for (int t = 0; t < threads; ++t)
+                pool.emplace_back([&, t] {
+                    sim_report rep = make_report(g, o);
+                    u32* cells = states[std::size_t(t)];
+                    accounted_sweep(g, rep, 0, [cells](i64, i64, i64, u64 idx) { ++cells[idx]; });
+                    counts[std::size_t(t)] = rep.threads_useful;
+                });
+            for (auto& th : pool) th.join();
+            auto t1 = std::chrono::steady_clock::now();
+            if (it >= warm) seconds[it - warm] = std::chrono::duration<double>(t1 - t0).count();
+        }
+        for (auto* p : states) std::free(p);
+        *useful = counts[0];
+    });
 }
 
 // Cell counts (core.hpp:125-133).

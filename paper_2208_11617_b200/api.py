@@ -416,7 +416,7 @@ def launch_map(g: grid_spec, domain: simplex_spec, opts: launch_opts | None = No
 
 
 def launch_accum(g: grid_spec, domain: simplex_spec, state: simplex_grid_state,
-                 opts: launch_opts | None = None) -> sim_report:
+                 opts: launch_opts | None = None, stream=None) -> sim_report:
     opts = opts or launch_opts()
     validate_launch(g, domain)
     if state.m != g.dims or state.side != g.cell_side():
@@ -426,10 +426,20 @@ def launch_accum(g: grid_spec, domain: simplex_spec, state: simplex_grid_state,
     rep = _make_report(g, opts)
     cnt = _lib.smx_counters()
     check(lib().smx_accum(C.byref(g.raw), state.cells.ctypes.data, state.cells.size, 1, int(opts.exec), 0,
-                          _cov_ptr(rep), C.byref(cnt), None))
+                          _cov_ptr(rep), C.byref(cnt), _raw_stream(stream)))
     _finish(rep, cnt)
     rep.state_hash = state.hash()
     return rep
+
+
+def release_scratch() -> None:
+    """Free the calling thread's library scratch on every device (smx_release)."""
+    check(lib().smx_release())
+
+
+def scratch_bytes() -> int:
+    """Pooled scratch bytes the calling thread holds (smx_scratch_bytes)."""
+    return int(lib().smx_scratch_bytes())
 
 
 def make_life_state(m: int, side: int, seed: int) -> simplex_grid_state:
@@ -438,8 +448,21 @@ def make_life_state(m: int, side: int, seed: int) -> simplex_grid_state:
     return s
 
 
+def _raw_stream(stream):
+    """A cudaStream_t for the C ABI: None (legacy default stream), a raw
+    handle (int), or a torch.cuda.Stream."""
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
 def launch_ca(g: grid_spec, domain: simplex_spec, state: simplex_grid_state,
-              opts: launch_opts | None = None) -> sim_report:
+              opts: launch_opts | None = None, stream=None) -> sim_report:
+    """launch_ca (simulator.hpp:431-463) on a host state. `stream` (optional,
+    B200 extension): the CUDA stream the call's copies and kernels run on
+    (the call still synchronises it before returning)."""
     opts = opts or launch_opts()
     validate_launch(g, domain)
     if state.m != g.dims or state.side != g.cell_side():
@@ -454,7 +477,7 @@ def launch_ca(g: grid_spec, domain: simplex_spec, state: simplex_grid_state,
     cnt = _lib.smx_counters()
     check(lib().smx_ca(C.byref(g.raw), state.cells.ctypes.data, state.cells.size, int(opts.steps),
                        int(opts.exec), 0, None, _cov_ptr(rep) if opts.steps > 0 else None,
-                       C.byref(cnt) if opts.steps > 0 else None, None))
+                       C.byref(cnt) if opts.steps > 0 else None, _raw_stream(stream)))
     if opts.steps > 0:
         _finish(rep, cnt)
     rep.state_hash = state.hash()

@@ -554,12 +554,10 @@ __global__ void __launch_bounds__(NWX * 32) k_ca_bits_run(const __grid_constant_
 template <int KIND, int RHO>
 void launch_t(const Geom& g, int wz0, int wz1, const CUtensorMap& tmap, uint32_t* nbits, int WP, cudaStream_t s) {
     using C = Cfg<RHO>;
-    // once per process, thread-safe (a function-local static's initialiser)
-    static const bool attr_set = [&] {
+    static std::once_flag once[kMaxDevices];  // once per device (thread-safe)
+    once_per_device(once, current_device(), [] {
         cudaFuncSetAttribute(k_ca_bits<KIND, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(PlanCfg<RHO>::NB));
-        return true;
-    }();
-    (void)attr_set;
+    });
     // patch edge: the largest that still gives >= 4 CTAs per SM (small grids
     // trade chunk length for parallelism)
     // and up to NZ wz layers per CTA (more chunks per warp keep the TMA
@@ -586,12 +584,9 @@ void launch_plan_t(const Geom& g, void* chunks, unsigned* count, cudaStream_t s)
     // CTAs win at C2: 8.6 vs 13.8 us at 2 LMAX).
     const int P = KIND == SMX_H3D ? 32 : PlanCfg<RHO>::LMAX * (RHO == 8 ? 3 : 1), NZ = 1;
     const int smem = 2 * P * P * NZ * 16 + 16 + 4 * P * P * NZ * 4;  // tiles | chunks | count | links
-    // once per process, thread-safe (a function-local static's initialiser)
-    static const bool attr_set = [&] {
-        cudaFuncSetAttribute(k_ca_plan<KIND, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        return true;
-    }();
-    (void)attr_set;
+    static std::once_flag once[kMaxDevices];  // once per device (thread-safe)
+    once_per_device(once, current_device(),
+                    [&] { cudaFuncSetAttribute(k_ca_plan<KIND, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
     const dim3 grid((g.ex + P - 1) / P, (g.ey + P - 1) / P, g.ez);
     k_ca_plan<KIND, RHO><<<grid, PLAN_THREADS, smem, s>>>(g, 0, g.ez, P, NZ,
                                                                               reinterpret_cast<Chunk*>(chunks), count);
@@ -602,14 +597,20 @@ cudaError_t launch_run_t(const Geom& g, const CUtensorMap& tA, const CUtensorMap
                          const void* chunks, const unsigned* count, int steps, cudaStream_t s) {
     using C = Cfg<RHO, CPIY>;
     const int smem = NWX * C::WARP_BYTES;
-    static int grid = [&] {
+    // attribute + persistent grid (co-resident CTAs x SMs) once per device
+    static std::once_flag once[kMaxDevices];
+    static int grids[kMaxDevices];
+    const int dev = current_device();
+    int grid_local = 0;
+    once_per_device(once, dev, [&] {
         cudaFuncSetAttribute(k_ca_bits_run<RHO, NWX, CPIY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        int per_sm = 0, dev = 0, nsm = 148;
+        int per_sm = 0, nsm = 148;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ca_bits_run<RHO, NWX, CPIY>, NWX * 32, smem);
-        cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        return (per_sm > 0 ? per_sm : 1) * nsm;
-    }();
+        grid_local = (per_sm > 0 ? per_sm : 1) * nsm;
+        if (dev >= 0 && dev < kMaxDevices) grids[dev] = grid_local;
+    });
+    int grid = dev >= 0 && dev < kMaxDevices ? grids[dev] : grid_local;
     const Chunk* ch = reinterpret_cast<const Chunk*>(chunks);
     int S = g.side, WP = bits_pitch_words(g.side);
     unsigned* ctl = const_cast<unsigned*>(count);

@@ -271,13 +271,11 @@ template <int KIND, int RHO>
 void launch_fused_t(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t* next, cudaStream_t s) {
     using C = FCfg<RHO>;
     constexpr int NZMAX = 2;
-    // once per process, thread-safe (a function-local static's initialiser)
-    static const bool attr_set = [&] {
+    static std::once_flag once[kMaxDevices];  // once per device (thread-safe)
+    once_per_device(once, current_device(), [] {
         cudaFuncSetAttribute(k_ca_fused<KIND, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    C::smem(C::LMAX * C::LMAX * NZMAX));
-        return true;
-    }();
-    (void)attr_set;
+                             C::smem(C::LMAX * C::LMAX * NZMAX));
+    });
     // patch edge and layers per CTA: as large as possible while the grid still
     // has >= 2 CTAs per SM (small grids trade chunk length for parallelism)
     int P = C::LMAX, NZ = NZMAX;

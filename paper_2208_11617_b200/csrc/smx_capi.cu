@@ -60,19 +60,68 @@ bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 // CA plan runs on. Per host thread, so launches on distinct states from
 // distinct threads never share scratch (the reference's functions are
 // reentrant); calls from one thread are ordered on the stream they pass.
+// A thread's resources are freed by smx_release() or when the thread exits.
 struct DeviceRes {
     cudaStream_t side = nullptr;  // CA plan, concurrent with staging + pack
     cudaEvent_t ev_in = nullptr, ev_plan = nullptr;
     std::map<int64_t, unsigned long long*> prefix;
-    // 0 cov, 1/2 u8, 3/4 bit shadows, 5 CA chunk list, 6 engine control words
-    void* pool[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-    size_t pool_bytes[7] = {0, 0, 0, 0, 0, 0, 0};
+    // 0 cov, 1/2 u8, 3/4 bit shadows, 5 CA chunk list, 6 the engine's control
+    // block (64 B: u32 [0] chunk count, u32 [8] grid barrier), 7 the
+    // first-defect result of smx_verify_cover (its own slot: a verify on one
+    // stream never touches the words of an engine running on another)
+    void* pool[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    size_t pool_bytes[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     std::map<std::pair<const void*, std::pair<int64_t, int64_t>>, CUtensorMap> tmaps;
     smx::DevCounters* counters = nullptr;
     unsigned* sink = nullptr;
 };
 std::mutex g_mu;
 std::map<std::pair<int, std::thread::id>, DeviceRes> g_res;
+
+// frees one DeviceRes on its device (cudaFree synchronises the device)
+void free_res(int dev, DeviceRes& r) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) return;
+    if (cur != dev) cudaSetDevice(dev);
+    for (auto& kv : r.prefix) cudaFree(kv.second);
+    for (int i = 0; i < 8; ++i)
+        if (r.pool[i]) cudaFree(r.pool[i]);
+    if (r.counters) cudaFree(r.counters);
+    if (r.sink) cudaFree(r.sink);
+    if (r.side) cudaStreamDestroy(r.side);
+    if (r.ev_in) cudaEventDestroy(r.ev_in);
+    if (r.ev_plan) cudaEventDestroy(r.ev_plan);
+    r = DeviceRes{};
+    if (cur != dev) cudaSetDevice(cur);
+}
+
+// every device's resources of one host thread; returns how many sets were freed
+int release_thread(std::thread::id tid) {
+    std::vector<std::pair<int, DeviceRes>> mine;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        for (auto it = g_res.begin(); it != g_res.end();) {
+            if (it->first.second == tid) {
+                mine.emplace_back(it->first.first, std::move(it->second));
+                it = g_res.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
+    for (auto& kv : mine) free_res(kv.first, kv.second);
+    return int(mine.size());
+}
+
+// thread-exit hook: a thread that used the ABI frees its scratch when it ends
+// (thread pools no longer accumulate one full set per worker)
+struct ThreadScratchOwner {
+    bool used = false;
+    ~ThreadScratchOwner() {
+        if (used) release_thread(std::this_thread::get_id());
+    }
+};
+thread_local ThreadScratchOwner t_owner;
 
 int cuda_fail(cudaError_t e, const char* what) {
     return fail(SMX_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -86,6 +135,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 int device_res(DeviceRes** out) {
     int dev = 0;
     TRY(cudaGetDevice(&dev));
+    t_owner.used = true;
     std::lock_guard<std::mutex> lk(g_mu);
     *out = &g_res[{dev, std::this_thread::get_id()}];
     return SMX_OK;
@@ -356,13 +406,32 @@ int engine_plan(const smx_grid* g, const smx::Geom& k, int64_t steps, cudaStream
     return SMX_OK;
 }
 
+// One persistent (cooperative, whole-device) engine grid per device at a time:
+// a cooperative launch is sized to fill every SM, so two of them from
+// different host threads / streams must not interleave their CTAs. Each
+// engine launch waits on the previous one's completion event of that device
+// (any thread); pack, unpack and copies of other calls still overlap.
+std::mutex g_engine_mu;
+cudaEvent_t g_engine_done[smx::kMaxDevices] = {};
+
 // join the plan, then ONE persistent launch for all steps
 int engine_run(const smx::Geom& k, uint32_t* A, uint32_t* B, const CUtensorMap* ta, const CUtensorMap* tb,
                int64_t steps, cudaStream_t s, void* pch, unsigned* count) {
     DeviceRes* r;
     if (int rc = device_res(&r)) return rc;
     TRY(cudaStreamWaitEvent(s, r->ev_plan, 0));
+    int dev = 0;
+    TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= smx::kMaxDevices) return fail(SMX_EINVAL, "device ordinal beyond the library's table");
+    std::lock_guard<std::mutex> lk(g_engine_mu);
+    cudaEvent_t& done = g_engine_done[dev];
+    if (!done) {
+        TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    } else {
+        TRY(cudaStreamWaitEvent(s, done, 0));
+    }
     TRY(smx::launch_ca_bits_run(k, ta, tb, A, B, pch, count, int(steps), s));
+    TRY(cudaEventRecord(done, s));
     return SMX_OK;
 }
 
@@ -398,7 +467,12 @@ int ca_runs_step(const smx_grid* g, const smx::Geom& k, int64_t wz0, int64_t wz1
         if (int rc = bits_tmap((const uint32_t*)pb, k.side, k.rho, &tb)) return rc;
         if (int rc = engine_run(k, (uint32_t*)pa, (uint32_t*)pb, ta, tb, 1, s, plan, count)) return rc;
     } else {
+        // a wz sub-range: B is seeded from `next` so the unpack leaves next's
+        // cells outside the range as they were (cells sharing a 32-cell word
+        // with a range tile receive their correctly stepped value: the kernel
+        // stores whole words computed from the full neighbourhood)
         smx::launch_pack_bits(k, cur, (uint32_t*)pa, s);
+        smx::launch_pack_bits(k, next, (uint32_t*)pb, s);
         smx::launch_ca_bits(k, g->kind, int(wz0), int(wz1), ta, (uint32_t*)pb, s);
     }
     smx::launch_unpack_bits(k, (const uint32_t*)pb, next, s);
@@ -941,9 +1015,9 @@ int smx_verify_cover(const uint32_t* coverage, uint64_t ncells, int device_ptr, 
         TRY(cudaMemcpyAsync(p, coverage, ncells * 4, cudaMemcpyHostToDevice, s));
         d = (const uint32_t*)p;
     }
-    void* pctl;
-    if (int rc = pool_get(6, 64, &pctl)) return rc;
-    unsigned long long* first = (unsigned long long*)pctl + 4;  // words 0..3: the CA engine's control
+    void* pfirst;
+    if (int rc = pool_get(7, 8, &pfirst)) return rc;
+    unsigned long long* first = (unsigned long long*)pfirst;
     const unsigned long long init = ncells;
     TRY(cudaMemcpyAsync(first, &init, 8, cudaMemcpyHostToDevice, s));
     if (ncells) smx::launch_first_defect(d, ncells, first, s);
@@ -1102,6 +1176,23 @@ int smx_tiles_unpack(const smx_grid* g, uint8_t* cells, const int32_t* tiles, ui
     smx::launch_tiles_unpack(k, cells, tiles, ntiles, in, (cudaStream_t)stream);
     TRY(cudaGetLastError());
     return SMX_OK;
+}
+
+int smx_release(void) {
+    int dev = 0;
+    TRY(cudaGetDevice(&dev));  // a valid runtime before freeing
+    release_thread(std::this_thread::get_id());
+    return SMX_OK;
+}
+
+uint64_t smx_scratch_bytes(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    uint64_t b = 0;
+    for (auto& kv : g_res) {
+        if (kv.first.second != std::this_thread::get_id()) continue;
+        for (int i = 0; i < 8; ++i) b += kv.second.pool_bytes[i];
+    }
+    return b;
 }
 
 int smx_device_sync(void) {

@@ -3,9 +3,27 @@
 
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include "smx_common.cuh"
 
 namespace smx {
+
+// Kernel attributes (cudaFuncSetAttribute) and occupancy-derived grid sizes
+// belong to ONE device's context: they are set once per (kernel, device), so
+// a process driving several GPUs (smx_ca over `ngpus`, or one host thread per
+// device) configures each device before its first launch.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+template <class Fn>
+inline void once_per_device(std::once_flag (&flags)[kMaxDevices], int dev, Fn&& fn) {
+    if (dev >= 0 && dev < kMaxDevices) std::call_once(flags[dev], fn);
+    else fn();
+}
 
 void launch_outcomes(const Geom& g, smx_outcome* out, unsigned long long count, cudaStream_t s);
 void launch_map_block(const Geom& g, uint32_t* cov, DevCounters* cnt, unsigned* sink, cudaStream_t s);

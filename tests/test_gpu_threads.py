@@ -1,9 +1,12 @@
 """Reentrancy of the C ABI (include/smx_b200.h "Threads"): the reference's
 launch_* functions are pure and may run concurrently on distinct states
-(simulator.hpp:313-326,431-463). Two host threads, each on its own CUDA stream,
-run launch_ca (host buffers, the bit-shadow engine: pack, side-stream plan,
-persistent run, unpack) on different grids at the same time, repeatedly; every
-result must equal the restated oracle's sequential run."""
+(simulator.hpp:313-326,431-463). Two host threads, each on its own CUDA stream
+(passed through launch_ca's `stream`), run launch_ca (host buffers, the
+bit-shadow engine: staging copies, pack, side-stream plan, persistent run,
+unpack) on different grids at the same time, repeatedly; every result must
+equal the restated oracle's sequential run. The library orders the two
+persistent whole-device grids per device; everything else overlaps. Each
+thread's scratch is freed when it exits."""
 import threading
 
 import numpy as np
@@ -32,7 +35,8 @@ def test_concurrent_launch_ca_from_two_threads(cuda, orc):
     def worker(kind, n, rho, seed):
         try:
             torch.cuda.set_device(0)
-            with torch.cuda.stream(torch.cuda.Stream()):
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
                 g = api.make_grid(kind, 3, n, rho)
                 side = g.cell_side()
                 barrier.wait()
@@ -40,7 +44,8 @@ def test_concurrent_launch_ca_from_two_threads(cuda, orc):
                     st = api.make_life_state(3, side, seed)
                     api.launch_ca(g, api.simplex_spec(3, side - 1), st,
                                   api.launch_opts(steps=steps, boundary=api.ca_boundary.dead3d,
-                                                  exec=api.EXEC_BITS, record_coverage=False))
+                                                  exec=api.EXEC_BITS, record_coverage=False),
+                                  stream=stream)
                     if not np.array_equal(st.cells, want[seed]):
                         errors.append((kind, n, rho, seed))
                         return
@@ -53,3 +58,32 @@ def test_concurrent_launch_ca_from_two_threads(cuda, orc):
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+def test_release_and_thread_exit_free_scratch(cuda):
+    """smx_release frees the calling thread's pools; a worker thread's pools
+    are freed when it exits (thread pools must not leak)."""
+    import torch
+
+    g = api.grid_h3d(64)  # side 504: ~80 MB of pools per thread
+    g.rho = 8
+    side = g.cell_side()
+    st = api.make_life_state(3, side, 5)
+    opts = api.launch_opts(steps=1, boundary=api.ca_boundary.dead3d, exec=api.EXEC_BITS, record_coverage=False)
+    api.launch_ca(g, api.simplex_spec(3, side - 1), st, opts)
+    assert api.scratch_bytes() > 0
+    api.release_scratch()
+    assert api.scratch_bytes() == 0
+    free0 = torch.cuda.mem_get_info()[0]
+
+    def worker():
+        s2 = api.make_life_state(3, side, 5)
+        api.launch_ca(g, api.simplex_spec(3, side - 1), s2, opts)
+
+    for _ in range(6):
+        t = threading.Thread(target=worker)
+        t.start()
+        t.join()
+    torch.cuda.synchronize()
+    # six exited workers hold nothing: free memory is back within 64 MiB
+    assert torch.cuda.mem_get_info()[0] > free0 - (64 << 20)

@@ -169,3 +169,37 @@ def test_restated_ca_equals_reference_directly(ref, orc):
         ref.kernel_ca_run(3, side, steps, a)
         orc.ca3d_run(side, steps, b)
         assert (a == b).all()
+
+
+def test_full_size_goldens_small_cases(orc):
+    """tests/golden/ca_full.json (gen_golden_full.py): the cases cheap enough
+    to recompute here — the exact C2 bench tuple (side 252, 100 steps) and the
+    reference's own side-1023 one-step hash."""
+    from conftest import golden
+    cases = golden("ca_full.json")["cases"]
+    for key in ("c2_rho4_100", "side1023_1"):
+        c = cases[key]
+        s = orc.make_life_state(3, c["side"], 42)
+        assert orc.state_hash(3, c["side"], s) == int(c["init_hash"])
+        orc.ca3d_run(c["side"], c["steps"], s)
+        assert orc.state_hash(3, c["side"], s) == int(c["final_hash"]), key
+    assert int(cases["side1023_1"]["final_hash"]) == 13036985295180606544
+
+
+def test_reference_accum_sample(ref):
+    """The bench's reference arm: the reference's own launch_accum sweep over
+    the first block rows of a grid, concurrent replicas."""
+    from oracle.oracle import H2D
+    secs, useful = ref.accum_sample(H2D, 2, 64, 4, 8, 2, 0, 2)
+    assert len(secs) == 2 and all(s > 0 for s in secs)
+    # first 8 block rows of H2D(64) (ex = 32), rho = 4: count their member
+    # cells from the restated map outcomes (strict view: y - 1)
+    from oracle.oracle import Restated
+    out = Restated().map_outcomes(H2D, 2, 64)[: 32 * 8]
+    side, want = 63 * 4, 0
+    for o in out:
+        if o[0]:
+            continue
+        bx, by = o[1] * 4, (o[2] - 1) * 4
+        want += sum(1 for ly in range(4) for lx in range(4) if bx + lx <= by + ly < side)
+    assert useful == want
