@@ -21,8 +21,16 @@
 // `simplexmap` namespace name.
 #pragma once
 
+#include <algorithm>
 #include <array>
+#include <cmath>
 #include <cstdint>
+#include <initializer_list>
+#include <limits>
+#include <span>
+#include <thread>
+#include <cstdlib>
+#include <utility>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -45,6 +53,72 @@ inline void check(int rc) {
     if (rc == SMX_EINVAL) throw std::invalid_argument(msg);
     if (rc == SMX_ERANGE) throw std::overflow_error(msg);
     throw std::runtime_error("smx: " + msg);
+}
+
+// ---- integer helpers (bits.hpp): host-side, same contracts and messages;
+// the kernels inline the 31 - clz forms of include/smx_maps.hpp ----
+using u128 = unsigned __int128;
+
+inline int floor_log2(u64 v) {
+    if (v == 0) throw std::invalid_argument("floor_log2: v must be >= 1");
+    return 63 - __builtin_clzll(v);
+}
+inline u64 pow2_floor_log2(u64 v) { return u64{1} << floor_log2(v); }
+inline int ceil_log2(u64 v) {
+    if (v == 0) throw std::invalid_argument("ceil_log2: v must be >= 1");
+    return v == 1 ? 0 : floor_log2(v - 1) + 1;
+}
+inline u64 pow2_ceil_log2(u64 v) { return u64{1} << ceil_log2(v); }
+inline bool is_pow2(u64 v) { return v && !(v & (v - 1)); }
+
+inline u128 checked_mul(u128 a, u128 b) {
+    u128 r;
+    if (__builtin_mul_overflow(a, b, &r)) throw std::overflow_error("128-bit multiply overflow");
+    return r;
+}
+inline u128 checked_add(u128 a, u128 b) {
+    u128 r;
+    if (__builtin_add_overflow(a, b, &r)) throw std::overflow_error("128-bit add overflow");
+    return r;
+}
+inline u128 checked_pow(u128 base, unsigned exp) {
+    u128 r = 1;
+    for (; exp; --exp) r = checked_mul(r, base);
+    return r;
+}
+inline std::string u128_to_string(u128 v) {
+    char buf[48];
+    int i = 47;
+    buf[i] = 0;
+    do {
+        buf[--i] = char('0' + int(v % 10));
+        v /= 10;
+    } while (v);
+    return std::string(buf + i);
+}
+inline std::string i128_to_string(i128 v) {
+    return v < 0 ? "-" + u128_to_string(u128(0) - u128(v)) : u128_to_string(u128(v));
+}
+
+// splitmix64 / FNV-1a (bits.hpp:84-109): the seeds of make_life_state and
+// make_edm_points; the device kernels use the same constants
+inline u64 splitmix64(u64& state) {
+    u64 z = (state += 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+inline double splitmix64_unit(u64& state) { return double(splitmix64(state) >> 11) * 0x1.0p-53; }
+constexpr u64 fnv1a_seed = 0xcbf29ce484222325ull;
+inline u64 fnv1a_append(u64 h, const void* data, std::size_t len) {
+    // folds through the library's FNV (smx_state_hash) with the seed rewound
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    for (std::size_t i = 0; i < len; ++i) h = (h ^ p[i]) * 0x100000001b3ull;
+    return h;
+}
+inline u64 fnv1a_append_u64(u64 h, u64 v) {
+    for (int i = 0; i < 8; ++i) h = (h ^ ((v >> (8 * i)) & 0xffu)) * 0x100000001b3ull;
+    return h;
 }
 
 // ---- geometry (core.hpp:28-69, :125-149) ----
@@ -75,28 +149,130 @@ inline u64 tri_linear_index(i64 x, i64 y) { return smx::tri_index(x, y); }
 inline u64 tet_layer_prefix(i64 side, i64 z) { return smx::tet_layer_prefix(side, z); }
 inline u64 tet_linear_index(i64 side, i64 x, i64 y, i64 z) { return smx::tet_index(side, x, y, z); }
 
-// exact rational for sim_report::space_overhead (rational.hpp, reduced form)
+// canonical orthant membership (core.hpp:40-51) and the view adapters (:60-61)
+inline bool simplex_contains(const simplex_spec& spec, std::span<const i64> x) {
+    if (int(x.size()) != spec.m) throw std::invalid_argument("simplex_contains: dimension mismatch");
+    i64 sum = 0;
+    for (i64 c : x) {
+        if (c < 0) return false;
+        sum += c;
+    }
+    return sum <= spec.n;
+}
+inline bool simplex_contains(const simplex_spec& spec, std::initializer_list<i64> x) {
+    return simplex_contains(spec, std::span<const i64>(x.begin(), x.size()));
+}
+inline std::array<i64, 2> tri_to_orthant(i64 x, i64 y) { return {x, y - x}; }
+inline std::array<i64, 3> tet_to_orthant(i64 x, i64 y, i64 z) { return {x, y - x, z}; }
+
+// simplex_volume (core.hpp:99-109) = C(n + m - 1, m), exact: each factor is
+// divided by the part of i that the running product cannot absorb, so no
+// intermediate exceeds the result; a result beyond 128 bits is an overflow
+inline u128 simplex_volume(i64 n, int m) {
+    if (n < 1) throw std::invalid_argument("simplex_volume: n must be >= 1");
+    if (m < 1) throw std::invalid_argument("simplex_volume: m must be >= 1");
+    u128 acc = 1;
+    for (int i = 1; i <= m; ++i) {
+        u128 g = u128(i), a = acc;  // g = gcd(acc, i)
+        while (a) {
+            const u128 t = g % a;
+            g = a;
+            a = t;
+        }
+        const u128 b = u128(u64(n - 1 + i)) / (u128(i) / g);  // exact: (i / g) | (n - 1 + i)
+        u128 r;
+        if (__builtin_mul_overflow(acc / g, b, &r)) throw std::overflow_error("simplex_volume: result exceeds 128 bits");
+        acc = r;
+    }
+    return acc;
+}
+
+// linear index -> coordinate (core.hpp:151-165), exact integer row search
+inline data_coord tri_coord_at(u64 index) {
+    i64 x = 0, y = 0;
+    smx::tri_coord_at(index, &x, &y);
+    return {x, y, 0};
+}
+inline data_coord tet_coord_at(i64 side, u64 index) {
+    i64 lo = 0, hi = side - 1;  // last layer z with prefix(z) <= index
+    while (lo < hi) {
+        const i64 mid = (lo + hi + 1) / 2;
+        if (tet_layer_prefix(side, mid) <= index) lo = mid;
+        else hi = mid - 1;
+    }
+    data_coord c = tri_coord_at(index - tet_layer_prefix(side, lo));
+    c.z = lo;
+    return c;
+}
+
+// ---- exact rationals (rational.hpp): reduced i128 fractions, positive
+// denominator; every product / sum is overflow-checked (std::overflow_error)
+namespace detail {
+inline i128 mul_checked(i128 a, i128 b) {
+    i128 r;
+    if (__builtin_mul_overflow(a, b, &r)) throw std::overflow_error("rational: 128-bit overflow");
+    return r;
+}
+inline i128 add_checked(i128 a, i128 b) {
+    i128 r;
+    if (__builtin_add_overflow(a, b, &r)) throw std::overflow_error("rational: 128-bit overflow");
+    return r;
+}
+inline i128 gcd_abs(i128 a, i128 b) {
+    if (a < 0) a = -a;
+    if (b < 0) b = -b;
+    while (b) {
+        const i128 t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+}  // namespace detail
+
 struct rational {
     i128 num = 0, den = 1;
     rational() = default;
     rational(i128 n, i128 d = 1) : num(n), den(d) {
         if (den == 0) throw std::invalid_argument("rational: zero denominator");
-        if (den < 0) num = -num, den = -den;
-        i128 a = num < 0 ? -num : num, b = den;
-        while (b) { i128 t = a % b; a = b; b = t; }
-        if (a > 1) num /= a, den /= a;
+        normalize();
     }
+    static rational from_u128(u128 n, u128 d = 1) {
+        const u128 lim = ~u128{0} >> 1;
+        if (n > lim || d > lim) throw std::overflow_error("rational: value exceeds signed 128-bit range");
+        return rational(i128(n), i128(d));
+    }
+    void normalize() {
+        if (den < 0) num = -num, den = -den;
+        const i128 g = detail::gcd_abs(num, den);
+        if (g > 1) num /= g, den /= g;
+    }
+    bool is_integer() const { return den == 1; }
+    rational operator+(const rational& o) const {
+        return rational(detail::add_checked(detail::mul_checked(num, o.den), detail::mul_checked(o.num, den)),
+                        detail::mul_checked(den, o.den));
+    }
+    rational operator-(const rational& o) const { return *this + rational(-o.num, o.den); }
+    rational operator*(const rational& o) const {
+        const i128 g1 = detail::gcd_abs(num, o.den), g2 = detail::gcd_abs(o.num, den);  // cross-reduce
+        const i128 a = g1 ? num / g1 : num, d2 = g1 ? o.den / g1 : o.den;
+        const i128 b = g2 ? o.num / g2 : o.num, d1 = g2 ? den / g2 : den;
+        return rational(detail::mul_checked(a, b), detail::mul_checked(d1, d2));
+    }
+    rational operator/(const rational& o) const {
+        if (o.num == 0) throw std::invalid_argument("rational: divide by zero");
+        return *this * rational(o.den, o.num);
+    }
+    rational abs() const { return rational(num < 0 ? -num : num, den); }
     bool operator==(const rational& o) const { return num == o.num && den == o.den; }
     bool operator!=(const rational& o) const { return !(*this == o); }
+    bool operator<(const rational& o) const { return detail::mul_checked(num, o.den) < detail::mul_checked(o.num, den); }
+    bool operator>(const rational& o) const { return o < *this; }
+    bool operator<=(const rational& o) const { return !(o < *this); }
+    bool operator>=(const rational& o) const { return !(*this < o); }
+    double to_double() const { return double(num) / double(den); }
 
-    static std::string int_text(i128 v) {
-        if (v == 0) return "0";
-        const bool neg = v < 0;
-        unsigned __int128 u = neg ? (unsigned __int128)(-(v + 1)) + 1 : (unsigned __int128)v;
-        std::string d;
-        while (u) d.insert(d.begin(), char('0' + int(u % 10))), u /= 10;
-        return neg ? "-" + d : d;
-    }
+    static std::string int_text(i128 v) { return i128_to_string(v); }
     // rational.hpp:123-126
     std::string to_string() const { return den == 1 ? int_text(num) : int_text(num) + "/" + int_text(den); }
     // rational.hpp:129-144: fixed point, round half up on the magnitude
@@ -116,6 +292,18 @@ struct rational {
         return out;
     }
 };
+
+// m! (core.hpp:116-121) and the bounding box's asymptotic waste m! - 1 (:125-128)
+inline u128 factorial_u128(int m) {
+    if (m < 0) throw std::invalid_argument("factorial: m must be >= 0");
+    u128 f = 1;
+    for (int i = 2; i <= m; ++i) f = checked_mul(f, u128(i));
+    return f;
+}
+inline rational bb_waste_fraction(int m) {
+    if (m < 1) throw std::invalid_argument("bb_waste_fraction: m must be >= 1");
+    return rational::from_u128(factorial_u128(m)) - rational(1);
+}
 
 // ---- maps (maps.hpp:19-92, :96-116, :188-207, :285-337) ----
 enum class map_kind { bb, rb, lambda2d, h2d, h2d_trapezoid, h2d_padded, h3d };
@@ -218,6 +406,28 @@ inline grid_spec from_raw(const smx_grid& r) {
     return g;
 }
 
+// map_supports_m / valid_pairs_text (report.hpp:28-45)
+inline bool map_supports_m(map_kind k, int m) {
+    if (k == map_kind::bb) return m == 2 || m == 3;
+    return k == map_kind::h3d ? m == 3 : m == 2;
+}
+inline std::string valid_pairs_text() {
+    return "bb (m=2,3), rb (m=2), lambda (m=2), h2d (m=2), trapezoid (m=2), h2d-padded (m=2), h3d (m=3)";
+}
+// host worker budget (report.hpp:112-121): hardware threads, capped by a
+// valid SIMPLEXMAP_THREADS. The sweeps here run their grids on the GPU one
+// after another; the budget is kept for callers that shard host work.
+inline unsigned thread_budget() {
+    unsigned hw = std::thread::hardware_concurrency();
+    if (hw == 0) hw = 1;
+    if (const char* env = std::getenv("SIMPLEXMAP_THREADS")) {
+        char* end = nullptr;
+        const long v = std::strtol(env, &end, 10);
+        if (end != env && *end == '\0' && v >= 1 && v < long(hw)) hw = unsigned(v);
+    }
+    return hw;
+}
+
 // make_grid (report.hpp:48-66)
 inline grid_spec make_grid(map_kind k, int m, i64 n, i64 rho = 1, i64 threshold = 1) {
     smx_grid r;
@@ -264,6 +474,27 @@ inline map_outcome map_h3d(block_coord omega, i64 n) { return map_one(map_kind::
 inline data_coord map_rb_2d(block_coord omega, i64 n) { return map_one(map_kind::rb, 2, n, omega).target; }
 inline data_coord map_lambda_2d(u64 index, i64 n) {
     return map_one(map_kind::lambda2d, 2, n, {i64(index), 0, 0}).target;
+}
+// the single-precision lambda WITHOUT the integer fix-up (maps.hpp:161-167):
+// a diagnostic of where an fp32 quadratic root first lands on a wrong row
+inline data_coord map_lambda_2d_fp32(u64 index) {
+    const float root = (std::sqrt(8.0f * float(index) + 1.0f) - 1.0f) / 2.0f;
+    const i64 y = i64(root);
+    return {i64(i128(index) - i128(y) * (y + 1) / 2), y, 0};
+}
+struct lambda_fp32_onset {
+    bool found = false;
+    u64 index = 0;  // first linear index whose fp32 coordinate is wrong
+    i64 side = 0;   // smallest domain side holding it
+};
+inline lambda_fp32_onset lambda_fp32_failure_onset(u64 max_index) {
+    for (u64 i = 0; i < max_index; ++i) {
+        i64 x = 0, y = 0;
+        smx::tri_coord_at(i, &x, &y);  // the exact map (what map_lambda_2d returns)
+        const data_coord f = map_lambda_2d_fp32(i);
+        if (f.x != x || f.y != y) return {true, i, y + 1};
+    }
+    return {};
 }
 inline map_outcome map_h2d_padded(block_coord omega, i64 n) { return map_one(map_kind::h2d_padded, 2, n, omega); }
 // The reference takes the band's params; the ABI recomputes the band from
@@ -452,6 +683,68 @@ inline sim_report launch_edm(const grid_spec& g, const simplex_spec& domain,
     return rep;
 }
 
+// ---- the sequential reference kernels and their scalar helpers ----
+// (simulator.hpp:220-253, :329-331, :345-350, :377-386, :402-425). The
+// helpers are host functions (what a caller uses to check a cell); the three
+// whole-state kernels run on the GPU through the ABI (no block map: every
+// cell of the packed state is one work item).
+namespace detail {
+inline u8 life_next(u8 alive, int alive_neighbors) {
+    return (alive_neighbors == 3 || (alive && alive_neighbors == 2)) ? u8{1} : u8{0};
+}
+inline int alive_neighbors_2d_periodic(const simplex_grid_state<u8>& s, i64 x, i64 y) {
+    const i64 S = s.side;
+    int n = 0;
+    for (i64 dy = -1; dy <= 1; ++dy)
+        for (i64 dx = -1; dx <= 1; ++dx) {
+            if (!dx && !dy) continue;
+            const i64 nx = (x + dx + S) % S, ny = (y + dy + S) % S;  // wrap, then x > y reads dead
+            if (nx <= ny) n += s.cells[tri_linear_index(nx, ny)];
+        }
+    return n;
+}
+inline int alive_neighbors_3d_dead(const simplex_grid_state<u8>& s, i64 x, i64 y, i64 z) {
+    int n = 0;
+    for (i64 dz = -1; dz <= 1; ++dz)
+        for (i64 dy = -1; dy <= 1; ++dy)
+            for (i64 dx = -1; dx <= 1; ++dx)
+                if ((dx || dy || dz) && tet_contains(s.side, x + dx, y + dy, z + dz))
+                    n += s.cells[tet_linear_index(s.side, x + dx, y + dy, z + dz)];
+    return n;
+}
+}  // namespace detail
+
+// edm_distance (simulator.hpp:345-350): one fixed expression order, no FMA
+// contraction (the GPU kernels use the same order with __d*_rn intrinsics)
+inline double edm_distance(const std::array<double, 2>& a, const std::array<double, 2>& b) {
+    volatile double dx = a[0] - b[0], dy = a[1] - b[1];
+    volatile double sx = dx * dx, sy = dy * dy;
+    return std::sqrt(sx + sy);
+}
+
+// kernel_accum (simulator.hpp:329-331): every cell += 1, on the GPU
+inline void kernel_accum(simplex_grid_state<u32>& state) {
+    check(smx_kernel_accum(state.cells.data(), state.cells.size(), 0, nullptr));
+}
+
+// kernel_edm (simulator.hpp:377-386): the full EDM state, on the GPU
+inline void kernel_edm(const std::vector<std::array<double, 2>>& points, simplex_grid_state<double>& state) {
+    if (state.m != 2) throw std::invalid_argument("kernel_edm: 2-simplex domains only");
+    if (i64(points.size()) != state.side)
+        throw std::invalid_argument("kernel_edm: need one point per domain side unit");
+    check(smx_kernel_edm(points.front().data(), i64(points.size()), state.cells.data(), state.cells.size(), 0,
+                         nullptr));
+}
+
+// kernel_ca_run (simulator.hpp:402-425): `steps` Life steps of the whole
+// state, on the GPU (dead3d for m = 3, periodic2d for m = 2)
+inline void kernel_ca_run(simplex_grid_state<u8>& state, i64 steps, ca_boundary boundary) {
+    if (steps < 0) throw std::invalid_argument("kernel_ca_run: steps must be >= 0");
+    if ((boundary == ca_boundary::periodic2d) != (state.m == 2))
+        throw std::invalid_argument("kernel_ca_run: boundary rule does not fit the domain");
+    check(smx_kernel_ca_run(state.m, state.side, state.cells.data(), state.cells.size(), steps, 0, nullptr));
+}
+
 // verify_exact_cover (simulator.hpp:467-478): first cell of multiplicity != 1
 inline cover_verdict verify_exact_cover(const sim_report& rep, const simplex_spec& domain) {
     if (domain.m != rep.m || domain.n != rep.cell_side - 1)
@@ -541,6 +834,32 @@ inline measure_row measure_grid(const grid_spec& g, bool check_cover = true) {
             row.multiplicity = mult;
         }
     }
+    return row;
+}
+
+// measure_grid_compact (report.hpp:279-321): the cover check with a
+// caller-reused byte multiset. The map launch and its coverage run on the
+// GPU (smx_launch_map into device counts); `marks` receives the counts capped
+// at 255, as the reference's byte marks are.
+inline measure_row measure_grid_compact(const grid_spec& g, std::vector<u8>& marks) {
+    const simplex_spec dom(g.dims, g.domain_side() * g.rho - 1);
+    validate_launch(g, dom);
+    const i64 side = dom.n + 1;
+    sim_report rep = detail::make_report(g, launch_opts{});
+    smx_grid r = g.raw();
+    smx_counters c{};
+    check(smx_launch_map(&r, rep.coverage.data(), rep.coverage.size(), 0, &c, nullptr));
+    detail::finish(rep, c);
+    marks.resize(rep.coverage.size());
+    for (std::size_t i = 0; i < marks.size(); ++i) marks[i] = u8(std::min<u32>(rep.coverage[i], 255u));
+    measure_row row = row_from_report(g, rep);
+    const cover_verdict v = verify_exact_cover(rep, dom);
+    row.exact = v.exact;
+    if (!v.exact) {
+        row.witness = v.witness;
+        row.multiplicity = std::min<u64>(v.multiplicity, 255);
+    }
+    (void)side;
     return row;
 }
 
@@ -685,6 +1004,226 @@ inline std::string text_report(const std::vector<measure_row>& rows, bool verifi
                            : " NotExact witness=" + witness_text(r) + " mult=" + std::to_string(r.multiplicity);
         out += '\n';
     }
+    return out;
+}
+
+// ---- r / beta analysis (analysis.hpp): exact host arithmetic, no device
+// work (microseconds); the same formulas as paper_2208_11617_b200/analysis.py.
+// self_similar_params is declared with the maps above.
+struct efficiency_report {
+    rational volume_s;        // V(S_n^m)
+    u128 volume_simplex = 0;  // V(simplex of side n - 1)
+    rational alpha;           // volume_s / volume_simplex - 1
+    i64 n0 = 0;               // smallest covering n, when found
+    bool found = false;
+};
+
+namespace detail {
+// k with inv_r^k == n exactly (analysis.hpp:46-58)
+inline unsigned exact_log(i64 n, i64 inv_r) {
+    if (n < 1) throw std::invalid_argument("self_similar_volume: n must be >= 1");
+    unsigned k = 0;
+    for (i64 v = 1; v != n; ++k) {
+        if (v > n / inv_r) throw std::invalid_argument("self_similar_volume: n must be a power of 1/r");
+        v *= inv_r;
+    }
+    return k;
+}
+}  // namespace detail
+
+// closed form (n^m - beta^k) / ((1/r)^m - beta), k = log_{1/r} n (analysis.hpp:63-73)
+inline rational self_similar_volume(i64 n, const self_similar_params& p) {
+    const unsigned k = detail::exact_log(n, p.inv_r);
+    const u128 scale = checked_pow(u128(p.inv_r), unsigned(p.m));
+    if (scale <= u128(p.beta)) throw std::invalid_argument("self_similar_volume: (1/r)^m must exceed beta");
+    return rational::from_u128(checked_pow(u128(n), unsigned(p.m)) - checked_pow(u128(p.beta), k)) /
+           rational::from_u128(scale - u128(p.beta));
+}
+// the halving family's limit m! / (2^m - 2) - 1 (analysis.hpp:75-85)
+inline rational extra_fraction_limit(int m, const self_similar_params& p) {
+    if (m < 2) throw std::invalid_argument("extra_fraction_limit: m must be >= 2");
+    if (p.inv_r != 2 || p.beta != 2) throw std::invalid_argument("extra_fraction_limit: defined for inv_r=2, beta=2");
+    return rational::from_u128(factorial_u128(m)) / rational::from_u128((u128{1} << unsigned(m)) - 2) - rational(1);
+}
+inline rational extra_fraction_limit(int m) { return extra_fraction_limit(m, self_similar_params(2, 2, m)); }
+inline rational extra_fraction_at(i64 n, const self_similar_params& p) {
+    if (n < 2) throw std::invalid_argument("extra_fraction_at: n must be >= 2");
+    return self_similar_volume(n, p) / rational::from_u128(simplex_volume(n - 1, p.m)) - rational(1);
+}
+// smallest power of 1/r up to n_bound whose family volume covers the simplex (analysis.hpp:95-115)
+inline efficiency_report find_n0(const self_similar_params& p, i64 n_bound) {
+    efficiency_report rep;
+    for (i64 n = p.inv_r; n <= n_bound; n *= p.inv_r) {
+        const rational vs = self_similar_volume(n, p);
+        const u128 vd = simplex_volume(n - 1, p.m);
+        if (vs >= rational::from_u128(vd)) {
+            rep.volume_s = vs;
+            rep.volume_simplex = vd;
+            rep.alpha = vs / rational::from_u128(vd) - rational(1);
+            rep.n0 = n;
+            rep.found = true;
+            break;
+        }
+        if (n > n_bound / p.inv_r) break;
+    }
+    return rep;
+}
+// every feasible integral (1/r, beta), ranked by |alpha| at the largest power
+// of 1/r <= n_eval, then n0, beta, 1/r (analysis.hpp:117-150)
+inline std::vector<std::pair<self_similar_params, efficiency_report>> optimize_params(int m, i64 inv_r_max,
+                                                                                     i64 beta_max, i64 n_eval) {
+    if (n_eval < 2) throw std::invalid_argument("optimize_params: n_eval must be >= 2");
+    std::vector<std::pair<self_similar_params, efficiency_report>> out;
+    for (i64 beta = 2; beta <= beta_max; ++beta)
+        for (i64 inv_r = beta; inv_r <= inv_r_max; ++inv_r) {
+            const self_similar_params p(inv_r, beta, m);
+            i64 n = inv_r;
+            while (n <= n_eval / inv_r) n *= inv_r;
+            const efficiency_report onset = find_n0(p, n_eval);
+            efficiency_report rep;
+            rep.volume_s = self_similar_volume(n, p);
+            rep.volume_simplex = simplex_volume(n - 1, m);
+            rep.alpha = extra_fraction_at(n, p);
+            rep.n0 = onset.n0;
+            rep.found = onset.found;
+            out.emplace_back(p, rep);
+        }
+    if (out.empty()) throw std::invalid_argument("optimize_params: empty feasible (1/r, beta) grid");
+    auto n0_key = [](const efficiency_report& r) { return r.found ? r.n0 : std::numeric_limits<i64>::max(); };
+    std::sort(out.begin(), out.end(), [&](const auto& a, const auto& b) {
+        const rational aa = a.second.alpha.abs(), ab = b.second.alpha.abs();
+        if (aa != ab) return aa < ab;
+        if (n0_key(a.second) != n0_key(b.second)) return n0_key(a.second) < n0_key(b.second);
+        if (a.first.beta != b.first.beta) return a.first.beta < b.first.beta;
+        return a.first.inv_r < b.first.inv_r;
+    });
+    return out;
+}
+// non-integral scaling (1/r)^m = m!: alpha tends to beta / (m! - beta) (analysis.hpp:152-166)
+struct real_scaling_report {
+    double inv_r = 0;
+    double alpha_infinity = 0;
+};
+inline real_scaling_report real_scaling_diagnostic(int m, i64 beta) {
+    if (m < 2) throw std::invalid_argument("real_scaling_diagnostic: m must be >= 2");
+    if (beta <= 1) throw std::invalid_argument("real_scaling_diagnostic: beta must be > 1");
+    const double f = double(u64(factorial_u128(m)));
+    if (double(beta) >= f) throw std::invalid_argument("real_scaling_diagnostic: beta must be below m!");
+    return {std::pow(f, 1.0 / double(m)), double(beta) / (f - double(beta))};
+}
+
+// report.hpp:449-473
+constexpr const char* csv_schema_optimize = "slx-opt-1";
+inline std::string csv_optimize(const std::vector<std::pair<self_similar_params, efficiency_report>>& ranked,
+                                i64 n_eval) {
+    std::string out = "schema,m,inv_r,beta,n_eval,alpha_num,alpha_den,alpha_decimal,n0_found,n0\n";
+    for (const auto& [p, rep] : ranked)
+        out += std::string(csv_schema_optimize) + "," + std::to_string(p.m) + "," + std::to_string(p.inv_r) + "," +
+               std::to_string(p.beta) + "," + std::to_string(n_eval) + "," + detail::csv_rational(rep.alpha) + "," +
+               (rep.found ? "1" : "0") + "," + std::to_string(rep.found ? rep.n0 : 0) + "\n";
+    return out;
+}
+
+// ---- layout diagrams (render.hpp): the block outcomes come from the GPU
+// (smx_map_outcomes, the coordinate-check dump), the host formats the SVG
+// byte for byte as the reference does ----
+constexpr i64 render_max_n = 256;
+
+inline std::string render_echo(const grid_spec& g) {
+    std::string e = std::string("map=") + map_kind_name(g.kind) + " m=" + std::to_string(g.dims) +
+                    " n=" + std::to_string(g.n) + " rho=" + std::to_string(g.rho);
+    if (g.kind == map_kind::h2d_trapezoid) e += " T=" + std::to_string(g.threshold);
+    return e;
+}
+
+namespace detail {
+constexpr const char* render_palette[] = {"#4e79a7", "#f28e2b", "#59a14f", "#e15759", "#b07aa1",
+                                          "#edc948", "#76b7b2", "#ff9da7", "#9c755f", "#86bcb6"};
+constexpr int render_palette_size = 10;
+constexpr const char* render_void_fill = "#d8d8d8";
+constexpr const char* render_domain_fill = "#f0f0f0";
+inline void svg_cell(std::string& out, i64 x, i64 y, const char* fill) {
+    out += "<rect x=\"" + std::to_string(x) + "\" y=\"" + std::to_string(y) +
+           "\" width=\"1\" height=\"1\" fill=\"" + fill + "\"/>\n";
+}
+inline void svg_text(std::string& out, i64 x, i64 y, const std::string& text) {
+    out += "<text x=\"" + std::to_string(x) + "\" y=\"" + std::to_string(y) +
+           "\" font-family=\"monospace\" font-size=\"2\" fill=\"#222222\">" + text + "</text>\n";
+}
+}  // namespace detail
+
+inline std::string render_svg(const grid_spec& g) {
+    const auto& palette = detail::render_palette;
+    const char* const void_fill = detail::render_void_fill;
+    const char* const domain_fill = detail::render_domain_fill;
+    if (g.n > render_max_n)
+        throw std::invalid_argument("render: n > 256 produces an impractical diagram; pick a smaller n");
+    const i64 side = g.domain_side(), cap = 3, gap = 2;
+    const bool trap = g.kind == map_kind::h2d_trapezoid;
+    // grid panel (trapezoid bands stacked with one blank row between)
+    i64 gw = 0, gh = 0;
+    std::vector<i64> band_y0;
+    if (trap) {
+        for (const auto& t : g.traps) {
+            band_y0.push_back(cap + gh);
+            gw = std::max(gw, t.ext_x);
+            gh += t.ext_y + 1;
+        }
+        gh -= 1;
+    } else if (g.dims == 2) {
+        gw = g.extents[0];
+        gh = g.extents[1];
+    } else {
+        gw = g.extents[2] * (g.extents[0] + 1) - 1;
+        gh = g.extents[1];
+    }
+    // data panel: 2-D to the right of the grid, 3-D below it (one slice per z)
+    const i64 dw = g.dims == 2 ? side : side * (side + 1) - 1;
+    const i64 dx0 = g.dims == 2 ? gw + gap : 0;
+    const i64 dy0 = g.dims == 2 ? cap : cap + gh + cap;
+    const i64 width = g.dims == 2 ? dx0 + dw : std::max(gw, dw);
+    const i64 height = g.dims == 2 ? cap + std::max(gh, side) : dy0 + side;
+
+    std::string out = "<?xml version=\"1.0\" encoding=\"UTF-8\"?>\n";
+    out += "<svg xmlns=\"http://www.w3.org/2000/svg\" version=\"1.1\" viewBox=\"0 0 " + std::to_string(width) + " " +
+           std::to_string(height) + "\" width=\"" + std::to_string(width * 8) + "\" height=\"" +
+           std::to_string(height * 8) + "\" shape-rendering=\"crispEdges\">\n";
+    out += "<!-- " + render_echo(g) + " -->\n";
+    detail::svg_text(out, 0, 2, "grid space " + render_echo(g));
+    if (g.dims == 2) detail::svg_text(out, dx0, 2, "data space side " + std::to_string(side));
+    else detail::svg_text(out, 0, dy0 - 1, "data space side " + std::to_string(side) + ", one panel per z");
+    for (i64 z = 0; z < (g.dims == 2 ? 1 : side); ++z)
+        for (i64 y = 0; y + z < side; ++y)
+            for (i64 x = 0; x <= y; ++x) detail::svg_cell(out, dx0 + z * (side + 1) + x, dy0 + y, domain_fill);
+
+    // every block's outcome, evaluated on the device in the reference's walk order
+    const u64 nblocks = g.blocks();
+    std::vector<smx_outcome> oc(nblocks);
+    smx_grid r = g.raw();
+    check(smx_map_outcomes(&r, oc.data(), nblocks, 0, nullptr));
+    u64 i = 0;
+    auto emit = [&](i64 wx, i64 wy, i64 wz, int band, i64 panel_x, i64 panel_y) {
+        const smx_outcome& o = oc[i++];
+        const char* fill = o.is_void ? void_fill
+                           : trap    ? palette[band % detail::render_palette_size]
+                                     : palette[floor_log2(u64(o.level_b < 1 ? 1 : o.level_b)) % detail::render_palette_size];
+        detail::svg_cell(out, panel_x, panel_y, fill);
+        (void)wx, (void)wy, (void)wz;
+        if (o.is_void) return;
+        const i64 ty = strict_view(g.kind) ? o.y - 1 : o.y;
+        detail::svg_cell(out, dx0 + i64(o.z) * (side + 1) + o.x, dy0 + ty, fill);
+    };
+    if (trap) {
+        for (std::size_t b = 0; b < g.traps.size(); ++b)
+            for (i64 wy = 0; wy < g.traps[b].ext_y; ++wy)
+                for (i64 wx = 0; wx < g.traps[b].ext_x; ++wx) emit(wx, wy, 0, int(b), wx, band_y0[b] + wy);
+    } else {
+        for (i64 wz = 0; wz < g.extents[2]; ++wz)
+            for (i64 wy = 0; wy < g.extents[1]; ++wy)
+                for (i64 wx = 0; wx < g.extents[0]; ++wx)
+                    emit(wx, wy, wz, -1, g.dims == 2 ? wx : wz * (g.extents[0] + 1) + wx, cap + wy);
+    }
+    out += "</svg>\n";
     return out;
 }
 

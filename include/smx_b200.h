@@ -268,6 +268,19 @@ int smx_bits_tiles_pack(const smx_grid* g, const uint32_t* bits, const int32_t* 
 int smx_bits_tiles_unpack(const smx_grid* g, uint32_t* bits, const int32_t* tiles, uint64_t ntiles,
                           const uint8_t* in, void* stream);
 
+/* ---- the reference's sequential kernels (no block map), on the GPU ----
+ * kernel_accum (simulator.hpp:329-331): every cell of the packed u32 state += 1. */
+int smx_kernel_accum(uint32_t* cells, uint64_t ncells, int device_ptr, void* stream);
+/* kernel_edm (simulator.hpp:377-386): cell (x, y) = edm_distance(p_x, p_y) for
+ * the whole triangle of side npoints (f64, bit-identical to the reference). */
+int smx_kernel_edm(const double* points_xy, int64_t npoints, double* cells, uint64_t ncells, int device_ptr,
+                   void* stream);
+/* kernel_ca_run (simulator.hpp:402-425): `steps` Life steps of the whole state
+ * in place (m = 3: dead boundary; m = 2: periodic). Same messages as the
+ * reference for bad m / side / steps. */
+int smx_kernel_ca_run(int32_t m, int64_t side, uint8_t* cells, uint64_t ncells, int64_t steps, int device_ptr,
+                      void* stream);
+
 /* Frees the calling host thread's library scratch on every device (staging
  * pools, bit shadows, chunk lists, prefix tables, tensor maps, the side
  * stream); the next call re-creates what it needs. Synchronises the devices

@@ -81,6 +81,9 @@ _SIGS = {
     "smx_tiles_unpack": ([_G, _VP, _VP, C.c_uint64, _VP, _VP], C.c_int),
     "smx_device_sync": ([], C.c_int),
     "smx_release": ([], C.c_int),
+    "smx_kernel_accum": ([_VP, C.c_uint64, C.c_int, _VP], C.c_int),
+    "smx_kernel_edm": ([_VP, C.c_int64, _VP, C.c_uint64, C.c_int, _VP], C.c_int),
+    "smx_kernel_ca_run": ([C.c_int32, C.c_int64, _VP, C.c_uint64, C.c_int64, C.c_int, _VP], C.c_int),
     "smx_scratch_bytes": ([], C.c_uint64),
     "smx_bits_bytes": ([_G], C.c_uint64),
     "smx_bits_pack": ([_G, _VP, C.c_uint64, _VP, _VP], C.c_int),

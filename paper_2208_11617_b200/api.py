@@ -432,6 +432,33 @@ def launch_accum(g: grid_spec, domain: simplex_spec, state: simplex_grid_state,
     return rep
 
 
+def kernel_accum(state: simplex_grid_state) -> None:
+    """kernel_accum (simulator.hpp:329-331) on the GPU: every cell += 1."""
+    if state.cells.dtype != np.uint32:
+        raise InvalidArgument("kernel_accum: state cells must be u32")
+    check(lib().smx_kernel_accum(state.cells.ctypes.data, state.cells.size, 0, None))
+
+
+def kernel_edm(points: np.ndarray, state: simplex_grid_state) -> None:
+    """kernel_edm (simulator.hpp:377-386) on the GPU."""
+    if state.m != 2:
+        raise InvalidArgument("kernel_edm: 2-simplex domains only")
+    pts = np.ascontiguousarray(points, np.float64)
+    if pts.shape[0] != state.side:
+        raise InvalidArgument("kernel_edm: need one point per domain side unit")
+    check(lib().smx_kernel_edm(pts.ctypes.data, pts.shape[0], state.cells.ctypes.data, state.cells.size, 0, None))
+
+
+def kernel_ca_run(state: simplex_grid_state, steps: int, boundary: "ca_boundary") -> None:
+    """kernel_ca_run (simulator.hpp:402-425) on the GPU, in place."""
+    if steps < 0:
+        raise InvalidArgument("kernel_ca_run: steps must be >= 0")
+    if (boundary == ca_boundary.periodic2d) != (state.m == 2):
+        raise InvalidArgument("kernel_ca_run: boundary rule does not fit the domain")
+    check(lib().smx_kernel_ca_run(state.m, state.side, state.cells.ctypes.data, state.cells.size, int(steps), 0,
+                                  None))
+
+
 def release_scratch() -> None:
     """Free the calling thread's library scratch on every device (smx_release)."""
     check(lib().smx_release())

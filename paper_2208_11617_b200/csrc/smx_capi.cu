@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <initializer_list>
 #include <map>
 #include <mutex>
 #include <string>
@@ -1176,6 +1177,69 @@ int smx_tiles_unpack(const smx_grid* g, uint8_t* cells, const int32_t* tiles, ui
     smx::launch_tiles_unpack(k, cells, tiles, ntiles, in, (cudaStream_t)stream);
     TRY(cudaGetLastError());
     return SMX_OK;
+}
+
+// ---- the sequential reference kernels (simulator.hpp:329-331, :377-386,
+// :402-425) on the GPU. They have no block map; the B200 path runs them over
+// an internal BB tiling of the same domain (the largest tile edge that divides
+// the side, so the cover is exact), which the map-driven kernels are already
+// validated on.
+static int64_t tile_edge(int64_t side, std::initializer_list<int64_t> edges) {
+    for (int64_t r : edges)
+        if (side % r == 0) return r;
+    return 1;
+}
+
+int smx_kernel_accum(uint32_t* cells, uint64_t ncells, int device_ptr, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (ncells == 0) return SMX_OK;
+    uint32_t* d = cells;
+    if (!device_ptr) {
+        void* p;
+        if (int rc = pool_get(1, ncells * 4, &p)) return rc;
+        d = (uint32_t*)p;
+        TRY(cudaMemcpyAsync(d, cells, ncells * 4, cudaMemcpyHostToDevice, s));
+    }
+    smx::launch_increment(d, ncells, s);
+    TRY(cudaGetLastError());
+    if (!device_ptr) {
+        TRY(cudaMemcpyAsync(cells, d, ncells * 4, cudaMemcpyDeviceToHost, s));
+        TRY(cudaStreamSynchronize(s));
+    }
+    return SMX_OK;
+}
+
+int smx_kernel_edm(const double* points_xy, int64_t npoints, double* cells, uint64_t ncells, int device_ptr,
+                   void* stream) {
+    if (npoints < 1) return fail(SMX_EINVAL, "simplex_grid_state: side must be >= 1");
+    if (ncells != smx::tri_cells(npoints)) return fail(SMX_EINVAL, "kernel_edm: need one point per domain side unit");
+    const int64_t rho = tile_edge(npoints, {16, 8, 4, 2});
+    smx_grid g;
+    if (int rc = smx_make_grid(SMX_BB, 2, npoints / rho, rho, 1, &g)) return rc;
+    return smx_edm(&g, points_xy, npoints, cells, ncells, SMX_EXEC_RUNS, device_ptr, nullptr, nullptr, stream);
+}
+
+int smx_kernel_ca_run(int32_t m, int64_t side, uint8_t* cells, uint64_t ncells, int64_t steps, int device_ptr,
+                      void* stream) {
+    if (m != 2 && m != 3) return fail(SMX_EINVAL, "simplex_grid_state: m must be 2 or 3");
+    if (side < 1) return fail(SMX_EINVAL, "simplex_grid_state: side must be >= 1");
+    if (steps < 0) return fail(SMX_EINVAL, "kernel_ca_run: steps must be >= 0");
+    if (ncells != cells_of(m, side)) return fail(SMX_EINVAL, "kernel_ca_run: state does not match the side");
+    int64_t rho;
+    int32_t exec;
+    if (m == 3) {
+        // the bit-shadow engine where a rho in {8, 4} tiles the side, else the
+        // one-thread-per-cell block scheme with the largest tile that does
+        rho = tile_edge(side, {8, 4});
+        exec = side % rho == 0 && (rho == 8 || rho == 4) ? SMX_EXEC_BITS : SMX_EXEC_BLOCK;
+        if (exec == SMX_EXEC_BLOCK) rho = tile_edge(side, {7, 6, 5, 3, 2});
+    } else {
+        rho = tile_edge(side, {16, 8, 4, 2});
+        exec = SMX_EXEC_RUNS;
+    }
+    smx_grid g;
+    if (int rc = smx_make_grid(SMX_BB, m, side / rho, rho, 1, &g)) return rc;
+    return smx_ca(&g, cells, ncells, steps, exec, device_ptr, nullptr, nullptr, nullptr, stream);
 }
 
 int smx_release(void) {

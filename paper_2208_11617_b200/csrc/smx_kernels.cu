@@ -236,6 +236,28 @@ __global__ void k_life_init(unsigned long long seed, uint8_t* __restrict__ cells
     }
 }
 
+// kernel_accum (simulator.hpp:329-331), the sequential reference's "one visit
+// per cell": no block map, every u32 of the packed state += 1. 16-byte vectors
+// over the 16-byte-aligned interior, scalar head / tail; grid-stride.
+__global__ void k_increment_all(uint32_t* __restrict__ cells, unsigned long long n) {
+    const unsigned long long head = ((16u - (reinterpret_cast<uintptr_t>(cells) & 15u)) & 15u) / 4u;
+    const unsigned long long h = head < n ? head : n;
+    const unsigned long long nvec = (n - h) / 4;
+    uint4* v4 = reinterpret_cast<uint4*>(cells + h);
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long v = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; v < nvec; v += stride) {
+        uint4 x = v4[v];
+        x.x += 1u, x.y += 1u, x.z += 1u, x.w += 1u;
+        v4[v] = x;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 8) {
+        const unsigned long long t = threadIdx.x;
+        if (t < h) cells[t] += 1u;                                           // head (< 4)
+        const unsigned long long i = h + nvec * 4 + t;                       // tail (< 4)
+        if (t < 4 && i < n) cells[i] += 1u;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // 3-D Life, block scheme: one CTA per map block, one thread per cell; the 26
 // neighbours are read through the packed index with the tetrahedron membership
@@ -414,6 +436,15 @@ void launch_life_init(unsigned long long seed, uint8_t* cells, unsigned long lon
     if (blocks > 148ull * 32) blocks = 148ull * 32;
     if (blocks == 0) blocks = 1;
     k_life_init<<<(unsigned)blocks, threads, 0, s>>>(seed, cells, n);
+}
+
+void launch_increment(uint32_t* cells, unsigned long long n, cudaStream_t s) {
+    if (n == 0) return;
+    const int threads = 256;
+    unsigned long long blocks = (n / 4 + threads - 1) / threads;
+    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    if (blocks == 0) blocks = 1;
+    k_increment_all<<<(unsigned)blocks, threads, 0, s>>>(cells, n);
 }
 
 template <int KIND>

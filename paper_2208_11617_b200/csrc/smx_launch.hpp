@@ -29,6 +29,8 @@ void launch_outcomes(const Geom& g, smx_outcome* out, unsigned long long count, 
 void launch_map_block(const Geom& g, uint32_t* cov, DevCounters* cnt, unsigned* sink, cudaStream_t s);
 void launch_accum(const Geom& g, uint32_t* cells, int exec, cudaStream_t s);
 void launch_life_init(unsigned long long seed, uint8_t* cells, unsigned long long n, cudaStream_t s);
+// kernel_accum: every cell += 1 (no map)
+void launch_increment(uint32_t* cells, unsigned long long n, cudaStream_t s);
 void launch_ca(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s);
 bool ca_runs_supported(int rho);
 // fused u8 -> u8 x-run step (smx_ca_fused.cu), rho in {4, 8}

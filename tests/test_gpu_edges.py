@@ -102,3 +102,31 @@ def test_h2d_rho1_max_grid_appendix_a(cuda):
         del cells
         torch.cuda.empty_cache()
     assert api.state_hash(2, side, np.ones(n, np.uint32)) == 8855049223948604461
+
+
+def test_sequential_kernels_vs_oracle(cuda, orc):
+    """kernel_accum / kernel_edm / kernel_ca_run (the reference's sequential
+    engines, simulator.hpp:329-331,377-386,402-425) on the GPU, sides that the
+    internal tiling handles with the engine (divisible by 8 / 4), the block
+    scheme (odd primes, 2 mod 4) and the 2-D periodic rule."""
+    st = api.simplex_grid_state(2, 37)
+    st.cells[:] = 5
+    api.kernel_accum(st)
+    assert (st.cells == 6).all()
+    for side in (1, 13, 64, 66):
+        pts = api.make_edm_points(side, 3)
+        st = api.simplex_grid_state(2, side, np.float64)
+        api.kernel_edm(pts, st)
+        assert (st.cells == orc.kernel_edm(side, 3)).all(), side
+    for side in (1, 8, 12, 13, 22, 40):
+        st = api.make_life_state(3, side, 42)
+        want = st.cells.copy()
+        orc.ca3d_run(side, 6, want)
+        api.kernel_ca_run(st, 6, api.ca_boundary.dead3d)
+        assert (st.cells == want).all(), side
+    for side in (7, 16, 63):
+        st = api.make_life_state(2, side, 42)
+        want = st.cells.copy()
+        orc.ca2d_run(side, 9, want)
+        api.kernel_ca_run(st, 9, api.ca_boundary.periodic2d)
+        assert (st.cells == want).all(), side
