@@ -75,6 +75,10 @@ struct DeviceRes {
     std::map<std::pair<const void*, std::pair<int64_t, int64_t>>, CUtensorMap> tmaps;
     smx::DevCounters* counters = nullptr;
     unsigned* sink = nullptr;
+    // pipelined host-buffer calls: the two copy streams and their events
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;
+    cudaEvent_t ev_start = nullptr;
+    std::vector<cudaEvent_t> ev_chunk;
 };
 std::mutex g_mu;
 std::map<std::pair<int, std::thread::id>, DeviceRes> g_res;
@@ -92,6 +96,10 @@ void free_res(int dev, DeviceRes& r) {
     if (r.side) cudaStreamDestroy(r.side);
     if (r.ev_in) cudaEventDestroy(r.ev_in);
     if (r.ev_plan) cudaEventDestroy(r.ev_plan);
+    if (r.copy_in) cudaStreamDestroy(r.copy_in);
+    if (r.copy_out) cudaStreamDestroy(r.copy_out);
+    if (r.ev_start) cudaEventDestroy(r.ev_start);
+    for (cudaEvent_t e : r.ev_chunk) cudaEventDestroy(e);
     r = DeviceRes{};
     if (cur != dev) cudaSetDevice(cur);
 }
@@ -481,6 +489,72 @@ int ca_runs_step(const smx_grid* g, const smx::Geom& k, int64_t wz0, int64_t wz1
     return SMX_OK;
 }
 
+// Host-buffer ACCUM, pipelined: the packed state is cut at tile-row
+// boundaries into ~kPipeBytes chunks; chunk c's H2D copy (copy engine 1),
+// the x-run kernel restricted to the tiles whose data row lies in the chunk
+// (the full map walk; blocks mapping elsewhere drop out in the lane-parallel
+// map), and its D2H copy (copy engine 2) overlap those of the neighbouring
+// chunks, so PCIe runs both directions at once.
+int accum_host_pipelined(const smx_grid* g, const std::vector<smx::Geom>& subs, uint32_t* cells, uint64_t ncells,
+                         int64_t passes, int exec, cudaStream_t s) {
+    constexpr uint64_t kPipeBytes = uint64_t(256) << 20;
+    DeviceRes* r;
+    if (int rc = device_res(&r)) return rc;
+    void* p;
+    if (int rc = pool_get(1, ncells * 4, &p)) return rc;
+    uint32_t* d = (uint32_t*)p;
+    if (!r->copy_in) {
+        TRY(cudaStreamCreateWithFlags(&r->copy_in, cudaStreamNonBlocking));
+        TRY(cudaStreamCreateWithFlags(&r->copy_out, cudaStreamNonBlocking));
+        TRY(cudaEventCreateWithFlags(&r->ev_start, cudaEventDisableTiming));
+    }
+    const int64_t rho = g->rho, S = cell_side_of(g), trows = (S + rho - 1) / rho;
+    auto row_off = [&](int64_t ty) { return smx::tri_cells(std::min(ty * rho, S)); };  // first cell of tile row ty
+    // chunk boundaries (tile rows) so each chunk holds about kPipeBytes
+    std::vector<int64_t> cuts{0};
+    while (cuts.back() < trows) {
+        int64_t lo = cuts.back() + 1, hi = trows;
+        const uint64_t want = row_off(cuts.back()) + kPipeBytes / 4;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) / 2;
+            if (row_off(mid) >= want) hi = mid;
+            else lo = mid + 1;
+        }
+        cuts.push_back(lo);
+    }
+    const size_t nch = cuts.size() - 1;
+    if (r->ev_chunk.size() < 2 * nch) {
+        for (size_t i = r->ev_chunk.size(); i < 2 * nch; ++i) {
+            cudaEvent_t e;
+            TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            r->ev_chunk.push_back(e);
+        }
+    }
+    TRY(cudaEventRecord(r->ev_start, s));  // after the caller's prior work
+    TRY(cudaStreamWaitEvent(r->copy_in, r->ev_start, 0));
+    for (size_t c = 0; c < nch; ++c) {
+        const uint64_t o0 = row_off(cuts[c]), o1 = row_off(cuts[c + 1]);
+        cudaEvent_t in = r->ev_chunk[2 * c], done = r->ev_chunk[2 * c + 1];
+        TRY(cudaMemcpyAsync(d + o0, cells + o0, (o1 - o0) * 4, cudaMemcpyHostToDevice, r->copy_in));
+        TRY(cudaEventRecord(in, r->copy_in));
+        TRY(cudaStreamWaitEvent(s, in, 0));
+        for (int64_t pass = 0; pass < passes; ++pass)
+            for (smx::Geom k : subs) {
+                k.ty0 = int(cuts[c]);
+                k.ty1 = int(cuts[c + 1]);
+                smx::launch_accum(k, d, exec, s);
+            }
+        TRY(cudaGetLastError());
+        TRY(cudaEventRecord(done, s));
+        TRY(cudaStreamWaitEvent(r->copy_out, done, 0));
+        TRY(cudaMemcpyAsync(cells + o0, d + o0, (o1 - o0) * 4, cudaMemcpyDeviceToHost, r->copy_out));
+    }
+    TRY(cudaEventRecord(r->ev_start, r->copy_out));
+    TRY(cudaStreamWaitEvent(s, r->ev_start, 0));  // the caller's stream sees the whole call
+    TRY(cudaStreamSynchronize(s));
+    return SMX_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -703,6 +777,12 @@ int smx_accum(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passe
     if (exec < 0) exec = SMX_EXEC_RUNS;
     if (resolve_exec(exec) < 0) return fail(SMX_EINVAL, "accum: unknown exec scheme");
     cudaStream_t s = (cudaStream_t)stream;
+    // host state, x-run scheme, no coverage, > 1 chunk: the pipelined path
+    if (!device_ptr && !coverage && exec == SMX_EXEC_RUNS && ncells * 4 > (uint64_t(512) << 20)) {
+        if (counters)
+            if (int rc = fill_counters(g, counters, s, nullptr)) return rc;
+        return accum_host_pipelined(g, subs, cells, ncells, passes, exec, s);
+    }
     uint32_t* d = cells;
     uint32_t* dcov = coverage;
     if (!device_ptr) {
@@ -728,6 +808,8 @@ int smx_accum(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passe
     }
     return SMX_OK;
 }
+
+
 
 int smx_accum_range(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passes, int32_t exec,
                     int64_t wy_lo, int64_t wy_hi, smx_counters* counters, void* stream) {

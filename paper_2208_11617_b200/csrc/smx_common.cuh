@@ -21,6 +21,8 @@ struct Geom {
     const unsigned long long* prefix;  // 3-D: tet_layer_prefix(S, z), z = 0..S+1
     trapezoid<int> trap;  // SMX_TRAP: the band this launch covers (one launch per band)
     int wy0;              // first grid row of this launch (row-range shards: wy = wy0 + blockIdx.y)
+    int ty0, ty1;         // x-run 2-D kernels: only tiles whose data tile row is in [ty0, ty1)
+                          // (ty1 == 0: no filter) — one chunk of a pipelined host-buffer call
 };
 
 // strict_view (maps.hpp:35-38): outputs in { x < y }, shifted y - 1 by the sweep

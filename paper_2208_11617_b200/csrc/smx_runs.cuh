@@ -23,7 +23,7 @@ __device__ __forceinline__ void strip_runs(const Geom& g, int x0, int wy, int (*
     outcome<int> o{1, 0, 0, 0, 1, 0};
     if (valid) {
         o = map_block<KIND>(g, wx, wy, 0);
-        valid = !o.is_void;
+        valid = !o.is_void && (g.ty1 == 0 || (o.y >= g.ty0 && o.y < g.ty1));
     }
     const int px = __shfl_up_sync(FULL, o.x, 1);
     const int py = __shfl_up_sync(FULL, o.y, 1);

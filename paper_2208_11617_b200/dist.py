@@ -328,9 +328,10 @@ def bench_sharded(args, api):
     else:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from bench import METRIC, SEED, WORKLOADS, Flusher, timed_steps  # noqa: E402
+    from bench import METRIC, SEED, Flusher, timed_steps  # noqa: E402
 
-    desc, kind, n, rho, nsteps = WORKLOADS["c2"]
+    desc, kind, n, rho, nsteps = ("3-simplex n=256 CA (C2): launch_ca over H3D(64) rho=4, side 252, 100 steps "
+                                  "per call", "h3d", 64, 4, 100)
     g = api.make_grid(api.map_kind[kind], 3, n, rho)
     side = g.cell_side()
     cells = api.tet_cells(side)

@@ -73,3 +73,21 @@ def test_c3_full_size_hash(cuda):
     # Appendix A hash of the one-pass state, computed on the host copy
     host = np.ones(n, np.uint32)
     assert api.state_hash(2, g.cell_side(), host) == 18207742408615288078
+
+
+def test_pipelined_host_accum(cuda):
+    """Host-buffer launch_accum above 512 MB runs pipelined (chunked H2D ||
+    map-filtered x-run kernel || D2H); every cell must still be visited exactly
+    once, for H2D, BB, padded and trapezoid grids, with the reference's
+    counters."""
+    rng = np.random.default_rng(1)
+    for g in (api.make_grid(api.map_kind.h2d, 2, 1024, 16), api.make_grid(api.map_kind.bb, 2, 1023, 16),
+              api.make_grid(api.map_kind.h2d_padded, 2, 1100, 16),
+              api.make_grid(api.map_kind.h2d_trapezoid, 2, 1500, 16, 4)):
+        side = g.cell_side()
+        init = rng.integers(0, 1 << 30, api.tri_cells(side), dtype=np.uint32)
+        st = api.simplex_grid_state(2, side, np.uint32, init.copy())
+        rep = api.launch_accum(g, api.simplex_spec(2, side - 1), st, api.launch_opts(record_coverage=False))
+        assert (st.cells == init + 1).all(), g
+        assert rep.threads_useful == api.tri_cells(side)
+        assert rep.blocks_launched == g.blocks()
