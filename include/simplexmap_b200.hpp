@@ -568,6 +568,11 @@ struct launch_opts {
     bool record_coverage = true;
     u64 block_order_salt = 0;      // accepted; the GPU block scheduler picks the order
     int exec = SMX_EXEC_AUTO;      // B200 extension: SMX_EXEC_BLOCK / SMX_EXEC_RUNS
+    // B200 extension: launch_ca of a 3-simplex over several GPUs
+    // of this process (smx_ca_multi): ngpus shards on devices 0 .. ngpus-1, or
+    // on `devices` when given (an ordinal may repeat)
+    int ngpus = 1;
+    std::vector<int> devices;
 };
 
 struct cover_verdict {
@@ -647,8 +652,19 @@ inline sim_report launch_ca(const grid_spec& g, const simplex_spec& domain, simp
     smx_grid r = g.raw();
     smx_counters c{};
     const bool any = opts.steps > 0;
-    check(smx_ca(&r, state.cells.data(), state.cells.size(), opts.steps, opts.exec, 0, nullptr,
-                 any && rep.coverage_recorded ? rep.coverage.data() : nullptr, any ? &c : nullptr, nullptr));
+    const bool multi = g.dims == 3 && (opts.ngpus > 1 || !opts.devices.empty());
+    if (multi) {
+        // coverage and counters of step 0 from one map launch, then the sharded run
+        if (any)
+            check(smx_launch_map(&r, rep.coverage_recorded ? rep.coverage.data() : nullptr, rep.coverage.size(), 0,
+                                 &c, nullptr));
+        const int nd = opts.devices.empty() ? opts.ngpus : int(opts.devices.size());
+        check(smx_ca_multi(&r, state.cells.data(), state.cells.size(), opts.steps,
+                           opts.devices.empty() ? nullptr : opts.devices.data(), nd, 0, nullptr, nullptr));
+    } else {
+        check(smx_ca(&r, state.cells.data(), state.cells.size(), opts.steps, opts.exec, 0, nullptr,
+                     any && rep.coverage_recorded ? rep.coverage.data() : nullptr, any ? &c : nullptr, nullptr));
+    }
     if (any) detail::finish(rep, c);
     rep.state_hash = state.hash();
     return rep;

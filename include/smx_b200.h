@@ -216,6 +216,20 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
            int device_ptr, uint8_t* scratch, uint32_t* coverage, smx_counters* counters,
            void* stream);
 
+/* launch_ca over `ndev` GPUs of ONE process (the C ABI's
+ * multi-GPU launch_ca; 3-simplex grids, rho in {4, 8}). The grid's wz range is
+ * cut into ndev contiguous shards of whole H levels balanced by useful blocks;
+ * shard i runs on devices[i] (NULL: 0 .. ndev-1; an ordinal may repeat —
+ * shards sharing a device run the same schedule with local copies) with its
+ * own bit-shadow replica and its part of the engine plan, boundary chunks
+ * first; each step's halo bit tiles go to the peers that read them by
+ * peer-to-peer copies (NVLink) while the interior chunks run. `cells`: host
+ * memory (device_ptr = 0) or device memory on devices[0]; `stream` belongs to
+ * devices[0]. counters (nullable) as smx_ca. The per-grid plan and the
+ * replicas are cached per (host thread, grid, device list); smx_release frees them. */
+int smx_ca_multi(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, const int32_t* devices,
+                 int32_t ndev, int device_ptr, smx_counters* counters, void* stream);
+
 /* ---- the x-run CA engine's stages (what smx_ca_step / smx_ca chain) ----
  * A bit shadow holds one bit per cell in pitched rows (row (y, z) at word row
  * z*S + y, smx_bits_words() 32-bit words per row). Device pointers only.
@@ -234,6 +248,22 @@ int smx_bits_unpack(const smx_grid* g, const uint32_t* bits, uint8_t* cells, uin
  * bits_b -> bits_a ... (grid barrier between steps). The result is in bits_a
  * for even `steps`, bits_b for odd. Device pointers (smx_bits_bytes each). */
 int smx_bits_run(const smx_grid* g, uint32_t* bits_a, uint32_t* bits_b, int64_t steps, void* stream);
+
+/* The engine's two stages, exposed for a sharded caller (one rank's part of
+ * launch_ca over blocks with wz in [wz_lo, wz_hi) — SURVEY 8(e)):
+ *   smx_bits_plan:     the map applied once to those blocks -> chunk list
+ *                      (16 B per chunk: int32 cell x0, y0, z0, owned width;
+ *                      rho tile rows per chunk) in `chunks` (capacity
+ *                      smx_bits_plan_capacity(g) entries); *count (device u32)
+ *                      receives the number of chunks. Asynchronous.
+ *   smx_bits_run_list: ONE Life step bits_in -> bits_out over an explicit chunk
+ *                      list (any subset of a plan, *count entries), so a shard
+ *                      can run its boundary chunks first and its interior
+ *                      while the halo travels. Device pointers. */
+uint64_t smx_bits_plan_capacity(const smx_grid* g);
+int smx_bits_plan(const smx_grid* g, int64_t wz_lo, int64_t wz_hi, void* chunks, uint32_t* count, void* stream);
+int smx_bits_run_list(const smx_grid* g, uint32_t* bits_in, uint32_t* bits_out, const void* chunks,
+                      const uint32_t* count, void* stream);
 
 /* simplex_grid_state::hash (simulator.hpp:68-73): FNV-1a-64 over u64 m,
  * u64 side, then the raw cell bytes. Host bytes. */

@@ -348,6 +348,10 @@ class launch_opts:
     record_coverage: bool = True
     block_order_salt: int = 0
     exec: int = EXEC_AUTO
+    # B200 extension: launch_ca of a 3-simplex sharded over GPUs of this
+    # process (smx_ca_multi): ngpus shards on devices 0..ngpus-1 or `devices`
+    ngpus: int = 1
+    devices: tuple = ()
 
 
 @dataclass
@@ -502,9 +506,15 @@ def launch_ca(g: grid_spec, domain: simplex_spec, state: simplex_grid_state,
         raise InvalidArgument("launch_ca: state cells must be u8")
     rep = _make_report(g, opts)
     cnt = _lib.smx_counters()
-    check(lib().smx_ca(C.byref(g.raw), state.cells.ctypes.data, state.cells.size, int(opts.steps),
-                       int(opts.exec), 0, None, _cov_ptr(rep) if opts.steps > 0 else None,
-                       C.byref(cnt) if opts.steps > 0 else None, _raw_stream(stream)))
+    if g.dims == 3 and (opts.ngpus > 1 or opts.devices):
+        if opts.steps > 0:  # step-0 coverage + counters from one map launch
+            ncells = rep.coverage.size if rep.coverage is not None else 0
+            check(lib().smx_launch_map(C.byref(g.raw), _cov_ptr(rep), ncells, 0, C.byref(cnt), None))
+        ca_multi(g, state.cells, int(opts.steps), list(opts.devices) or list(range(opts.ngpus)))
+    else:
+        check(lib().smx_ca(C.byref(g.raw), state.cells.ctypes.data, state.cells.size, int(opts.steps),
+                           int(opts.exec), 0, None, _cov_ptr(rep) if opts.steps > 0 else None,
+                           C.byref(cnt) if opts.steps > 0 else None, _raw_stream(stream)))
     if opts.steps > 0:
         _finish(rep, cnt)
     rep.state_hash = state.hash()
@@ -620,6 +630,19 @@ def ca_device(g: grid_spec, cells, steps: int, exec: int = EXEC_AUTO, scratch=No
                        _ptr(scratch) if scratch is not None else None, None, None, _stream()))
 
 
+def ca_multi(g: grid_spec, cells, steps: int, devices) -> None:
+    """launch_ca over several GPUs of this process (smx_ca_multi): `cells` a
+    host numpy u8 state or a CUDA tensor on devices[0]; `devices` ordinals
+    (may repeat: shards on one device)."""
+    devs = (C.c_int32 * len(devices))(*devices)
+    if isinstance(cells, np.ndarray):
+        check(lib().smx_ca_multi(C.byref(g.raw), cells.ctypes.data, cells.size, int(steps), devs, len(devices), 0,
+                                 None, None))
+    else:
+        check(lib().smx_ca_multi(C.byref(g.raw), _ptr(cells), cells.numel(), int(steps), devs, len(devices), 1,
+                                 None, _stream()))
+
+
 def map_kernel_device(g: grid_spec) -> None:
     check(lib().smx_map_kernel(C.byref(g.raw), _stream()))
 
@@ -676,6 +699,28 @@ def bits_run_device(g: grid_spec, bits_a, bits_b, steps: int) -> None:
     """The engine stage: map once + one persistent launch of `steps` steps
     (result in bits_a for even steps, bits_b for odd)."""
     check(lib().smx_bits_run(C.byref(g.raw), _ptr(bits_a), _ptr(bits_b), steps, _stream()))
+
+
+def bits_plan_capacity(g: grid_spec) -> int:
+    return int(lib().smx_bits_plan_capacity(C.byref(g.raw)))
+
+
+def bits_plan_device(g: grid_spec, wz_lo: int, wz_hi: int):
+    """The engine's plan for the blocks with wz in [wz_lo, wz_hi): returns
+    (chunks, count) device tensors — chunks (capacity, 4) int32 rows
+    {x0, y0, z0, owned width} in cells, count (1,) int32 = chunks used."""
+    import torch
+    cap = max(bits_plan_capacity(g), 1)
+    chunks = torch.empty((cap, 4), dtype=torch.int32, device="cuda")
+    count = torch.zeros(1, dtype=torch.int32, device="cuda")
+    check(lib().smx_bits_plan(C.byref(g.raw), wz_lo, wz_hi, _ptr(chunks), _ptr(count), _stream()))
+    return chunks, count
+
+
+def bits_run_list_device(g: grid_spec, bits_in, bits_out, chunks, count) -> None:
+    """One Life step bits_in -> bits_out over an explicit chunk list."""
+    check(lib().smx_bits_run_list(C.byref(g.raw), _ptr(bits_in), _ptr(bits_out), _ptr(chunks), _ptr(count),
+                                  _stream()))
 
 
 def bits_unpack_device(g: grid_spec, bits, cells) -> None:

@@ -573,7 +573,7 @@ void launch_t(const Geom& g, int wz0, int wz1, const CUtensorMap& tmap, uint32_t
 }
 
 template <int KIND, int RHO>
-void launch_plan_t(const Geom& g, void* chunks, unsigned* count, cudaStream_t s) {
+void launch_plan_t(const Geom& g, int wz0, int wz1, void* chunks, unsigned* count, cudaStream_t s) {
     using C = Cfg<RHO>;
     // Chains stop at patch edges. H3D: 32 x 32 patches (32 divides the n/2
     // extents, so the hinge fold and the slab levels fragment least: H3D(128)
@@ -587,14 +587,14 @@ void launch_plan_t(const Geom& g, void* chunks, unsigned* count, cudaStream_t s)
     static std::once_flag once[kMaxDevices];  // once per device (thread-safe)
     once_per_device(once, current_device(),
                     [&] { cudaFuncSetAttribute(k_ca_plan<KIND, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
-    const dim3 grid((g.ex + P - 1) / P, (g.ey + P - 1) / P, g.ez);
-    k_ca_plan<KIND, RHO><<<grid, PLAN_THREADS, smem, s>>>(g, 0, g.ez, P, NZ,
-                                                                              reinterpret_cast<Chunk*>(chunks), count);
+    if (wz1 <= wz0) return;
+    const dim3 grid((g.ex + P - 1) / P, (g.ey + P - 1) / P, wz1 - wz0);
+    k_ca_plan<KIND, RHO><<<grid, PLAN_THREADS, smem, s>>>(g, wz0, wz1, P, NZ, reinterpret_cast<Chunk*>(chunks), count);
 }
 
 template <int RHO, int NWX, int CPIY>
 cudaError_t launch_run_t(const Geom& g, const CUtensorMap& tA, const CUtensorMap& tB, uint32_t* A, uint32_t* B,
-                         const void* chunks, const unsigned* count, int steps, cudaStream_t s) {
+                         const void* chunks, const unsigned* count, int steps, cudaStream_t s, bool coop = true) {
     using C = Cfg<RHO, CPIY>;
     const int smem = NWX * C::WARP_BYTES;
     // attribute + persistent grid (co-resident CTAs x SMs) once per device
@@ -615,6 +615,8 @@ cudaError_t launch_run_t(const Geom& g, const CUtensorMap& tA, const CUtensorMap
     int S = g.side, WP = bits_pitch_words(g.side);
     unsigned* ctl = const_cast<unsigned*>(count);
     void* args[] = {const_cast<CUtensorMap*>(&tA), const_cast<CUtensorMap*>(&tB), &A, &B, &ch, &ctl, &steps, &S, &WP};
+    if (!coop && steps == 1)  // one step executes no grid barrier: an ordinary launch
+        return cudaLaunchKernel((const void*)k_ca_bits_run<RHO, NWX, CPIY>, dim3(grid), dim3(NWX * 32), args, smem, s);
     return cudaLaunchCooperativeKernel((const void*)k_ca_bits_run<RHO, NWX, CPIY>, dim3(grid), dim3(NWX * 32), args,
                                        smem, s);
 }
@@ -737,14 +739,29 @@ void launch_unpack_bits(const Geom& g, const uint32_t* bits, uint8_t* out, cudaS
 
 unsigned long long ca_plan_capacity(const Geom& g) { return (unsigned long long)g.ex * g.ey * g.ez; }
 
-void launch_ca_plan(const Geom& g, int kind, void* chunks, unsigned* count, cudaStream_t s) {
+void launch_ca_plan_range(const Geom& g, int kind, int wz0, int wz1, void* chunks, unsigned* count, cudaStream_t s) {
     if (kind == SMX_H3D) {
-        if (g.rho == 4) launch_plan_t<SMX_H3D, 4>(g, chunks, count, s);
-        else launch_plan_t<SMX_H3D, 8>(g, chunks, count, s);
+        if (g.rho == 4) launch_plan_t<SMX_H3D, 4>(g, wz0, wz1, chunks, count, s);
+        else launch_plan_t<SMX_H3D, 8>(g, wz0, wz1, chunks, count, s);
     } else {
-        if (g.rho == 4) launch_plan_t<SMX_BB, 4>(g, chunks, count, s);
-        else launch_plan_t<SMX_BB, 8>(g, chunks, count, s);
+        if (g.rho == 4) launch_plan_t<SMX_BB, 4>(g, wz0, wz1, chunks, count, s);
+        else launch_plan_t<SMX_BB, 8>(g, wz0, wz1, chunks, count, s);
     }
+}
+void launch_ca_plan(const Geom& g, int kind, void* chunks, unsigned* count, cudaStream_t s) {
+    launch_ca_plan_range(g, kind, 0, g.ez, chunks, count, s);
+}
+
+// one step over an explicit chunk list (a shard's boundary or interior part):
+// the run kernel with steps = 1, launched as an ordinary grid
+cudaError_t launch_ca_bits_list(const Geom& g, const void* tmIn, uint32_t* in, uint32_t* out, const void* chunks,
+                                const unsigned* count, cudaStream_t s) {
+    const CUtensorMap& t = *reinterpret_cast<const CUtensorMap*>(tmIn);
+    if (g.rho == 4) {
+        if (tet_cells(g.side) <= (32ull << 20)) return launch_run_t<4, 16, 1>(g, t, t, in, out, chunks, count, 1, s, false);
+        return launch_run_t<4, 16, 2>(g, t, t, in, out, chunks, count, 1, s, false);
+    }
+    return launch_run_t<8, 16, 1>(g, t, t, in, out, chunks, count, 1, s, false);
 }
 
 cudaError_t launch_ca_bits_run(const Geom& g, const void* tmA, const void* tmB, uint32_t* A, uint32_t* B,

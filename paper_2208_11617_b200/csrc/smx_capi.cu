@@ -11,7 +11,9 @@
 #include <cstring>
 #include <initializer_list>
 #include <map>
+#include <memory>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <thread>
 #include <utility>
@@ -104,8 +106,11 @@ void free_res(int dev, DeviceRes& r) {
     if (cur != dev) cudaSetDevice(cur);
 }
 
+void release_multi(std::thread::id tid);  // smx_ca_multi's cached shards (below)
+
 // every device's resources of one host thread; returns how many sets were freed
 int release_thread(std::thread::id tid) {
+    release_multi(tid);
     std::vector<std::pair<int, DeviceRes>> mine;
     {
         std::lock_guard<std::mutex> lk(g_mu);
@@ -552,6 +557,396 @@ int accum_host_pipelined(const smx_grid* g, const std::vector<smx::Geom>& subs, 
     TRY(cudaEventRecord(r->ev_start, r->copy_out));
     TRY(cudaStreamWaitEvent(s, r->ev_start, 0));  // the caller's stream sees the whole call
     TRY(cudaStreamSynchronize(s));
+    return SMX_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// launch_ca over several GPUs of ONE process (smx_ca_multi):
+// the grid's wz range is cut into contiguous shards of whole levels balanced by
+// useful blocks; shard s lives on devices[s] with a full bit-shadow replica
+// pair, its part of the engine's plan (the map applied once) split into
+// boundary chunks (holding a tile some peer reads) and interior chunks. Per
+// step: boundary run -> bit-tile pack on the shard's comm stream -> one
+// peer-to-peer copy per receiving peer (NVLink between devices; a plain
+// device copy when two shards share a device) while the interior runs ->
+// the receiver unpacks after its own runs (the runs store whole words).
+// The host-side plan (partition + tile-level halo) is static per grid.
+
+struct HostPlan {
+    std::vector<std::pair<int64_t, int64_t>> wz;    // shard -> [lo, hi)
+    std::vector<std::vector<int32_t>> owned;        // shard -> x, y, z tile triples
+    std::vector<std::vector<std::vector<int32_t>>> send;  // [s][o] tiles s computes that o reads
+    int64_t D = 0;                                  // with-diagonal tile-domain side
+};
+
+int build_host_plan(const smx_grid* g, int G, HostPlan* P) {
+    const int64_t ex = g->extents[0], ey = g->extents[1], ez = g->extents[2];
+    const bool strict = strict_kind_host(g->kind);
+    const int64_t D = strict ? g->n - 1 : g->n;
+    std::vector<uint64_t> useful(size_t(ez), 0);
+    std::vector<int32_t> tiles;  // x, y, z per useful block, wz-major (natural order)
+    std::vector<int64_t> tile_wz;
+    for (int64_t wz = 0; wz < ez; ++wz)
+        for (int64_t wy = 0; wy < ey; ++wy)
+            for (int64_t wx = 0; wx < ex; ++wx) {
+                const smx::outcome<int64_t> o = g->kind == SMX_H3D ? smx::map_h3d<int64_t>(wx, wy, wz, g->n)
+                                                                   : smx::map_bb<int64_t>(wx, wy, wz, g->n, 3);
+                if (o.is_void) continue;
+                ++useful[size_t(wz)];
+                tiles.push_back(int32_t(o.x));
+                tiles.push_back(int32_t(strict ? o.y - 1 : o.y));
+                tiles.push_back(int32_t(o.z));
+                tile_wz.push_back(wz);
+            }
+    // contiguous wz ranges with ~equal useful blocks (dist.partition_wz)
+    std::vector<double> cum(size_t(ez) + 1, 0.0);
+    for (int64_t z = 0; z < ez; ++z) cum[size_t(z) + 1] = cum[size_t(z)] + double(useful[size_t(z)]);
+    std::vector<int64_t> cuts{0};
+    for (int r = 1; r < G; ++r) {
+        const double target = cum.back() * r / G;
+        int64_t k = int64_t(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+        cuts.push_back(std::max(cuts.back(), std::min(k, ez)));
+    }
+    cuts.push_back(ez);
+    P->wz.clear();
+    for (int r = 0; r < G; ++r) P->wz.push_back({cuts[size_t(r)], cuts[size_t(r) + 1]});
+    const size_t ntiles = tile_wz.size();
+    std::vector<int16_t> owner(size_t(D * D * D), int16_t(-1));
+    std::vector<int16_t> own_of(ntiles);
+    P->owned.assign(size_t(G), {});
+    for (size_t i = 0; i < ntiles; ++i) {
+        int r = 0;
+        while (tile_wz[i] >= P->wz[size_t(r)].second) ++r;
+        own_of[i] = int16_t(r);
+        const int64_t x = tiles[3 * i], y = tiles[3 * i + 1], z = tiles[3 * i + 2];
+        owner[size_t((z * D + y) * D + x)] = int16_t(r);
+        P->owned[size_t(r)].insert(P->owned[size_t(r)].end(), {int32_t(x), int32_t(y), int32_t(z)});
+    }
+    // tile-level 26-neighbourhood: t is sent to every other owner of a neighbour
+    auto keys = std::vector<std::vector<std::vector<int64_t>>>(static_cast<size_t>(G),
+                                                               std::vector<std::vector<int64_t>>(static_cast<size_t>(G)));
+    for (size_t i = 0; i < ntiles; ++i) {
+        const int64_t x = tiles[3 * i], y = tiles[3 * i + 1], z = tiles[3 * i + 2];
+        const int s = own_of[i];
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int64_t nx = x + dx, ny = y + dy, nz = z + dz;
+                    if ((!dx && !dy && !dz) || !smx::tet_contains<int64_t>(D, nx, ny, nz)) continue;
+                    const int o = owner[size_t((nz * D + ny) * D + nx)];
+                    if (o >= 0 && o != s) keys[size_t(s)][size_t(o)].push_back((z * D + y) * D + x);
+                }
+    }
+    P->send.assign(size_t(G), std::vector<std::vector<int32_t>>(size_t(G)));
+    for (int s2 = 0; s2 < G; ++s2)
+        for (int o = 0; o < G; ++o) {
+            auto& k = keys[size_t(s2)][size_t(o)];
+            std::sort(k.begin(), k.end());
+            k.erase(std::unique(k.begin(), k.end()), k.end());
+            for (int64_t key : k)
+                P->send[size_t(s2)][size_t(o)].insert(P->send[size_t(s2)][size_t(o)].end(),
+                                                      {int32_t(key % D), int32_t(key / D % D), int32_t(key / (D * D))});
+        }
+    P->D = D;
+    return SMX_OK;
+}
+
+struct PeerCopy {
+    int peer;
+    uint64_t src_off, dst_off, bytes;
+};
+
+struct Shard {
+    int dev = 0;
+    smx::Geom k{};
+    cudaStream_t cs = nullptr, ms = nullptr;          // compute, comm
+    cudaEvent_t ev_b = nullptr, ev_sent = nullptr, ev_done = nullptr;
+    uint32_t *A = nullptr, *B = nullptr;              // bit-shadow replicas
+    const CUtensorMap *tA = nullptr, *tB = nullptr;
+    void *bnd = nullptr, *inn = nullptr;              // chunk lists
+    uint32_t* cnt = nullptr;                          // [0] boundary, [1] interior chunk counts
+    uint64_t nb = 0, ni = 0;
+    int32_t *send_t = nullptr, *recv_t = nullptr, *own_t = nullptr;
+    uint64_t nsend = 0, nrecv = 0, nown = 0;
+    uint8_t *send_b = nullptr, *recv_b = nullptr, *own_b = nullptr, *u8 = nullptr;
+    std::vector<PeerCopy> copies;
+    std::vector<int> senders;                         // shards that copy into this one
+    std::vector<uint8_t*> gather_in;                  // shard 0 only: one buffer per other shard
+};
+
+struct MultiRes {
+    std::vector<Shard> shards;
+    ~MultiRes() { destroy(); }
+    void destroy() {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        for (auto& sh : shards) {
+            cudaSetDevice(sh.dev);
+            cudaDeviceSynchronize();
+            for (void* p : std::initializer_list<void*>{sh.A, sh.B, sh.bnd, sh.inn, sh.cnt, sh.send_t, sh.recv_t,
+                                                        sh.own_t, sh.send_b, sh.recv_b, sh.own_b, sh.u8})
+                if (p) cudaFree(p);
+            for (uint8_t* p : sh.gather_in)
+                if (p) cudaFree(p);
+            for (cudaEvent_t e : {sh.ev_b, sh.ev_sent, sh.ev_done})
+                if (e) cudaEventDestroy(e);
+            if (sh.cs) cudaStreamDestroy(sh.cs);
+            if (sh.ms) cudaStreamDestroy(sh.ms);
+        }
+        shards.clear();
+        cudaSetDevice(cur);
+    }
+};
+
+struct MultiKey {
+    std::thread::id tid;
+    int32_t kind;
+    int64_t n, rho;
+    std::vector<int> devs;
+    bool operator<(const MultiKey& o) const {
+        return std::tie(tid, kind, n, rho, devs) < std::tie(o.tid, o.kind, o.n, o.rho, o.devs);
+    }
+};
+std::mutex g_multi_mu;
+std::map<MultiKey, std::unique_ptr<MultiRes>> g_multi;
+
+void release_multi(std::thread::id tid) {
+    std::vector<std::unique_ptr<MultiRes>> mine;
+    {
+        std::lock_guard<std::mutex> lk(g_multi_mu);
+        for (auto it = g_multi.begin(); it != g_multi.end();) {
+            if (it->first.tid == tid) {
+                mine.push_back(std::move(it->second));
+                it = g_multi.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
+    mine.clear();  // destructors free on each shard's device
+}
+
+template <class T>
+int dev_upload(const std::vector<T>& h, T** d) {
+    TRY(cudaMalloc(d, std::max<size_t>(h.size(), 1) * sizeof(T)));
+    if (!h.empty()) TRY(cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return SMX_OK;
+}
+
+// builds every shard: streams, replicas, the plan split, halo lists and copies
+int multi_setup(const smx_grid* g, const std::vector<int>& devs, MultiRes* M) {
+    const int G = int(devs.size());
+    HostPlan P;
+    if (int rc = build_host_plan(g, G, &P)) return rc;
+    M->shards.assign(size_t(G), Shard{});
+    const uint64_t tb = smx::bits_tile_bytes(int(g->rho));
+    for (int s = 0; s < G; ++s) {
+        Shard& sh = M->shards[size_t(s)];
+        sh.dev = devs[size_t(s)];
+        TRY(cudaSetDevice(sh.dev));
+        if (int rc = make_geom(g, &sh.k, true)) return rc;
+        TRY(cudaStreamCreateWithFlags(&sh.cs, cudaStreamNonBlocking));
+        TRY(cudaStreamCreateWithFlags(&sh.ms, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&sh.ev_b, &sh.ev_sent, &sh.ev_done}) TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        const size_t bb = bits_bytes(sh.k.side);
+        TRY(cudaMalloc(&sh.A, bb + 256));
+        TRY(cudaMalloc(&sh.B, bb + 256));
+        TRY(cudaMalloc(&sh.u8, smx::tet_cells(sh.k.side) + 256));
+        if (int rc = bits_tmap(sh.A, sh.k.side, sh.k.rho, &sh.tA)) return rc;
+        if (int rc = bits_tmap(sh.B, sh.k.side, sh.k.rho, &sh.tB)) return rc;
+        // the shard's plan, split on the host by the tiles its peers read
+        void* all = nullptr;
+        uint32_t* cnt = nullptr;
+        TRY(cudaMalloc(&all, std::max<uint64_t>(smx::ca_plan_capacity(sh.k), 1) * 16));
+        TRY(cudaMalloc(&cnt, 8));
+        TRY(cudaMemset(cnt, 0, 8));
+        smx::launch_ca_plan_range(sh.k, g->kind, int(P.wz[size_t(s)].first), int(P.wz[size_t(s)].second), all, cnt,
+                                  sh.cs);
+        TRY(cudaGetLastError());
+        uint32_t n = 0;
+        TRY(cudaMemcpyAsync(&n, cnt, 4, cudaMemcpyDeviceToHost, sh.cs));
+        TRY(cudaStreamSynchronize(sh.cs));
+        std::vector<int32_t> ch(size_t(n) * 4);
+        if (n) TRY(cudaMemcpy(ch.data(), all, size_t(n) * 16, cudaMemcpyDeviceToHost));
+        TRY(cudaFree(all));
+        sh.cnt = cnt;
+        const int64_t D = P.D, rho = g->rho;
+        std::vector<uint8_t> mark(size_t(D * D * D), 0);
+        std::vector<int32_t> send_all;
+        for (int o = 0; o < G; ++o) {
+            const auto& t = P.send[size_t(s)][size_t(o)];
+            for (size_t i = 0; i < t.size(); i += 3) mark[size_t((int64_t(t[i + 2]) * D + t[i + 1]) * D + t[i])] = 1;
+        }
+        std::vector<int32_t> bnd, inn;
+        for (uint32_t c = 0; c < n; ++c) {
+            const int32_t* q = &ch[size_t(c) * 4];
+            const int64_t tx0 = q[0] / rho, tx1 = (q[0] + q[3] + rho - 1) / rho, ty = q[1] / rho, tz = q[2] / rho;
+            bool hit = false;
+            for (int64_t tx = tx0; tx < tx1 && tx < D && !hit; ++tx) hit = mark[size_t((tz * D + ty) * D + tx)] != 0;
+            (hit ? bnd : inn).insert((hit ? bnd : inn).end(), q, q + 4);
+        }
+        sh.nb = bnd.size() / 4;
+        sh.ni = inn.size() / 4;
+        if (int rc = dev_upload(bnd, (int32_t**)&sh.bnd)) return rc;
+        if (int rc = dev_upload(inn, (int32_t**)&sh.inn)) return rc;
+        const uint32_t counts[2] = {uint32_t(sh.nb), uint32_t(sh.ni)};
+        TRY(cudaMemcpy(sh.cnt, counts, 8, cudaMemcpyHostToDevice));
+        // send list: every peer's tiles in peer order, one pack launch per step
+        for (int o = 0; o < G; ++o) {
+            const auto& t = P.send[size_t(s)][size_t(o)];
+            send_all.insert(send_all.end(), t.begin(), t.end());
+        }
+        sh.nsend = send_all.size() / 3;
+        if (int rc = dev_upload(send_all, &sh.send_t)) return rc;
+        TRY(cudaMalloc(&sh.send_b, std::max<uint64_t>(sh.nsend * tb, 1)));
+        std::vector<int32_t> recv_all;
+        for (int q = 0; q < G; ++q) {
+            const auto& t = P.send[size_t(q)][size_t(s)];
+            recv_all.insert(recv_all.end(), t.begin(), t.end());
+            if (!t.empty()) sh.senders.push_back(q);
+        }
+        sh.nrecv = recv_all.size() / 3;
+        if (int rc = dev_upload(recv_all, &sh.recv_t)) return rc;
+        TRY(cudaMalloc(&sh.recv_b, std::max<uint64_t>(sh.nrecv * tb, 1)));
+        sh.nown = P.owned[size_t(s)].size() / 3;
+        if (int rc = dev_upload(P.owned[size_t(s)], &sh.own_t)) return rc;
+        TRY(cudaMalloc(&sh.own_b, std::max<uint64_t>(sh.nown * tb, 1)));
+    }
+    // peer copies: s's slice for o lands at o's offset for sender s
+    for (int s = 0; s < G; ++s) {
+        uint64_t src = 0;
+        for (int o = 0; o < G; ++o) {
+            const uint64_t k = P.send[size_t(s)][size_t(o)].size() / 3;
+            if (!k) continue;
+            uint64_t dst = 0;
+            for (int q = 0; q < s; ++q) dst += P.send[size_t(q)][size_t(o)].size() / 3;
+            M->shards[size_t(s)].copies.push_back({o, src * tb, dst * tb, k * tb});
+            src += k;
+        }
+    }
+    // peer access between distinct devices (NVLink P2P); same-device shards copy locally
+    for (int s = 0; s < G; ++s)
+        for (int o = 0; o < G; ++o) {
+            const int a = devs[size_t(s)], b = devs[size_t(o)];
+            if (a == b) continue;
+            int can = 0;
+            TRY(cudaDeviceCanAccessPeer(&can, a, b));
+            if (can) {
+                TRY(cudaSetDevice(a));
+                const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+                cudaGetLastError();
+            }
+        }
+    Shard& s0 = M->shards[0];
+    TRY(cudaSetDevice(s0.dev));
+    s0.gather_in.assign(size_t(G), nullptr);
+    for (int s = 1; s < G; ++s) TRY(cudaMalloc(&s0.gather_in[size_t(s)], std::max<uint64_t>(M->shards[size_t(s)].nown * tb, 1)));
+    return SMX_OK;
+}
+
+// one sharded step, A -> B on every shard
+int multi_step(MultiRes* M, bool even) {
+    const int G = int(M->shards.size());
+    for (auto& sh : M->shards) {
+        TRY(cudaSetDevice(sh.dev));
+        uint32_t* in = even ? sh.A : sh.B;
+        uint32_t* out = even ? sh.B : sh.A;
+        const CUtensorMap* tin = even ? sh.tA : sh.tB;
+        if (sh.nb) TRY(smx::launch_ca_bits_list(sh.k, tin, in, out, sh.bnd, sh.cnt, sh.cs));
+        TRY(cudaEventRecord(sh.ev_b, sh.cs));
+        TRY(cudaStreamWaitEvent(sh.ms, sh.ev_b, 0));
+        if (sh.nsend) smx::launch_bits_tiles_pack(sh.k, out, sh.send_t, sh.nsend, sh.send_b, sh.ms);
+        if (sh.ni) TRY(smx::launch_ca_bits_list(sh.k, tin, in, out, sh.inn, sh.cnt + 1, sh.cs));
+    }
+    for (auto& sh : M->shards) {
+        TRY(cudaSetDevice(sh.dev));
+        for (const PeerCopy& c : sh.copies) {
+            Shard& o = M->shards[size_t(c.peer)];
+            TRY(cudaStreamWaitEvent(sh.ms, o.ev_done, 0));  // o has unpacked the previous step's halo
+            TRY(cudaMemcpyPeerAsync(o.recv_b + c.dst_off, o.dev, sh.send_b + c.src_off, sh.dev, c.bytes, sh.ms));
+        }
+        TRY(cudaEventRecord(sh.ev_sent, sh.ms));
+    }
+    for (auto& sh : M->shards) {
+        TRY(cudaSetDevice(sh.dev));
+        uint32_t* out = even ? sh.B : sh.A;
+        for (int q : sh.senders) TRY(cudaStreamWaitEvent(sh.cs, M->shards[size_t(q)].ev_sent, 0));
+        if (sh.nrecv) smx::launch_bits_tiles_unpack(sh.k, out, sh.recv_t, sh.nrecv, sh.recv_b, sh.cs);
+        TRY(cudaGetLastError());
+        TRY(cudaEventRecord(sh.ev_done, sh.cs));
+    }
+    (void)G;
+    return SMX_OK;
+}
+
+int ca_multi(const smx_grid* g, const std::vector<int>& devs, uint8_t* cells, uint64_t ncells, int64_t steps,
+             int device_ptr, smx_counters* counters, cudaStream_t s) {
+    int caller_dev = 0;
+    TRY(cudaGetDevice(&caller_dev));
+    MultiRes* M = nullptr;
+    {
+        const MultiKey key{std::this_thread::get_id(), g->kind, g->n, g->rho, devs};
+        std::lock_guard<std::mutex> lk(g_multi_mu);
+        auto& slot = g_multi[key];
+        if (!slot) slot.reset(new MultiRes());
+        M = slot.get();
+    }
+    if (M->shards.empty()) {
+        const int rc = multi_setup(g, devs, M);
+        if (rc) {
+            M->destroy();
+            cudaSetDevice(caller_dev);
+            return rc;
+        }
+    }
+    const int G = int(devs.size());
+    Shard& s0 = M->shards[0];
+    TRY(cudaSetDevice(s0.dev));
+    if (counters && steps > 0)
+        if (int rc = fill_counters(g, counters, s, nullptr)) return rc;
+    // the state onto shard 0's device, then to every replica
+    TRY(cudaEventRecord(s0.ev_done, s));
+    TRY(cudaStreamWaitEvent(s0.cs, s0.ev_done, 0));
+    TRY(cudaMemcpyAsync(s0.u8, cells, ncells, device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s0.cs));
+    TRY(cudaEventRecord(s0.ev_b, s0.cs));
+    for (auto& sh : M->shards) {
+        TRY(cudaSetDevice(sh.dev));
+        TRY(cudaStreamWaitEvent(sh.cs, s0.ev_b, 0));
+        if (&sh != &s0) TRY(cudaMemcpyPeerAsync(sh.u8, sh.dev, s0.u8, s0.dev, ncells, sh.cs));
+        smx::launch_pack_bits(sh.k, sh.u8, sh.A, sh.cs);
+        TRY(cudaGetLastError());
+        TRY(cudaEventRecord(sh.ev_done, sh.cs));
+    }
+    for (int64_t st = 0; st < steps; ++st)
+        if (int rc = multi_step(M, (st & 1) == 0)) return rc;
+    // gather: every other shard's owned bit tiles into shard 0's final shadow
+    const bool odd = (steps & 1) != 0;
+    for (int q = 1; q < G; ++q) {
+        Shard& sh = M->shards[size_t(q)];
+        TRY(cudaSetDevice(sh.dev));
+        if (sh.nown) {
+            smx::launch_bits_tiles_pack(sh.k, odd ? sh.B : sh.A, sh.own_t, sh.nown, sh.own_b, sh.cs);
+            TRY(cudaMemcpyPeerAsync(s0.gather_in[size_t(q)], s0.dev, sh.own_b, sh.dev,
+                                    sh.nown * smx::bits_tile_bytes(int(g->rho)), sh.cs));
+        }
+        TRY(cudaEventRecord(sh.ev_sent, sh.cs));
+    }
+    TRY(cudaSetDevice(s0.dev));
+    uint32_t* fin = odd ? s0.B : s0.A;
+    for (int q = 1; q < G; ++q) {
+        Shard& sh = M->shards[size_t(q)];
+        TRY(cudaStreamWaitEvent(s0.cs, sh.ev_sent, 0));
+        if (sh.nown) smx::launch_bits_tiles_unpack(s0.k, fin, sh.own_t, sh.nown, s0.gather_in[size_t(q)], s0.cs);
+    }
+    smx::launch_unpack_bits(s0.k, fin, s0.u8, s0.cs);
+    TRY(cudaGetLastError());
+    TRY(cudaMemcpyAsync(cells, s0.u8, ncells, device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s0.cs));
+    TRY(cudaEventRecord(s0.ev_done, s0.cs));
+    TRY(cudaStreamWaitEvent(s, s0.ev_done, 0));  // the caller's stream sees the whole call
+    if (!device_ptr) TRY(cudaStreamSynchronize(s));
+    TRY(cudaSetDevice(caller_dev));
     return SMX_OK;
 }
 
@@ -1087,6 +1482,40 @@ int smx_bits_run(const smx_grid* g, uint32_t* bits_a, uint32_t* bits_b, int64_t 
     return bits_engine(g, k, bits_a, bits_b, ta, tb, steps, (cudaStream_t)stream);
 }
 
+uint64_t smx_bits_plan_capacity(const smx_grid* g) {
+    smx::Geom k;
+    if (!g || make_geom(g, &k, false)) return 0;
+    return smx::ca_plan_capacity(k);
+}
+
+int smx_bits_plan(const smx_grid* g, int64_t wz_lo, int64_t wz_hi, void* chunks, uint32_t* count, void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    int32_t ex = SMX_EXEC_BITS;
+    if (int rc = ca_validate(g, smx::tet_cells(k.side), &ex)) return rc;
+    if (wz_lo < 0 || wz_hi > g->extents[2] || wz_lo > wz_hi) return fail(SMX_EINVAL, "bits_plan: wz range outside the grid");
+    if (!chunks || !count) return fail(SMX_EINVAL, "null output");
+    cudaStream_t s = (cudaStream_t)stream;
+    TRY(cudaMemsetAsync(count, 0, 4, s));
+    smx::launch_ca_plan_range(k, g->kind, int(wz_lo), int(wz_hi), chunks, count, s);
+    TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
+int smx_bits_run_list(const smx_grid* g, uint32_t* bits_in, uint32_t* bits_out, const void* chunks,
+                      const uint32_t* count, void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    int32_t ex = SMX_EXEC_BITS;
+    if (int rc = ca_validate(g, smx::tet_cells(k.side), &ex)) return rc;
+    if (bits_in == bits_out) return fail(SMX_EINVAL, "bits_run_list: the two shadows must not alias");
+    if (!chunks || !count) return fail(SMX_EINVAL, "null chunk list");
+    const CUtensorMap* tm;
+    if (int rc = bits_tmap(bits_in, k.side, k.rho, &tm)) return rc;
+    TRY(smx::launch_ca_bits_list(k, tm, bits_in, bits_out, chunks, count, (cudaStream_t)stream));
+    return SMX_OK;
+}
+
 int smx_verify_cover(const uint32_t* coverage, uint64_t ncells, int device_ptr, uint64_t* first_bad,
                      uint32_t* multiplicity, void* stream) {
     if (!first_bad) return fail(SMX_EINVAL, "null output");
@@ -1322,6 +1751,29 @@ int smx_kernel_ca_run(int32_t m, int64_t side, uint8_t* cells, uint64_t ncells, 
     smx_grid g;
     if (int rc = smx_make_grid(SMX_BB, m, side / rho, rho, 1, &g)) return rc;
     return smx_ca(&g, cells, ncells, steps, exec, device_ptr, nullptr, nullptr, nullptr, stream);
+}
+
+int smx_ca_multi(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, const int32_t* devices,
+                 int32_t ndev, int device_ptr, smx_counters* counters, void* stream) {
+    smx::Geom k;
+    if (int rc = make_geom(g, &k, true)) return rc;
+    int32_t ex = SMX_EXEC_BITS;
+    if (int rc = ca_validate(g, ncells, &ex)) return rc;
+    if (g->dims != 3) return fail(SMX_EINVAL, "launch_ca: the multi-GPU engine shards 3-simplex grids");
+    if (steps < 0) return fail(SMX_EINVAL, "launch_ca: steps must be >= 0");
+    if (steps > INT32_MAX) return fail(SMX_ERANGE, "launch_ca: steps must fit int32");
+    if (ndev < 1) return fail(SMX_EINVAL, "launch_ca: ngpus must be >= 1");
+    int count = 0;
+    TRY(cudaGetDeviceCount(&count));
+    std::vector<int> devs;
+    for (int i = 0; i < ndev; ++i) {
+        const int d = devices ? devices[i] : i;
+        if (d < 0 || d >= count) return fail(SMX_EINVAL, "launch_ca: device ordinal " + std::to_string(d) + " not present");
+        devs.push_back(d);
+    }
+    if (ndev > int(g->extents[2])) return fail(SMX_EINVAL, "launch_ca: more shards than grid layers (wz)");
+    if (ndev > 32767) return fail(SMX_EINVAL, "launch_ca: too many shards");
+    return ca_multi(g, devs, cells, ncells, steps, device_ptr, counters, (cudaStream_t)stream);
 }
 
 int smx_release(void) {

@@ -49,6 +49,10 @@ void launch_ca_bits(const Geom& g, int kind, int wz0, int wz1, const void* tmap,
 // cooperative launch runs `steps` bit-sliced steps A -> B -> A ...
 unsigned long long ca_plan_capacity(const Geom& g);
 void launch_ca_plan(const Geom& g, int kind, void* chunks, unsigned* count, cudaStream_t s);
+void launch_ca_plan_range(const Geom& g, int kind, int wz0, int wz1, void* chunks, unsigned* count, cudaStream_t s);
+// one step A -> B over an explicit chunk list (ordinary launch, no grid barrier)
+cudaError_t launch_ca_bits_list(const Geom& g, const void* tmIn, uint32_t* in, uint32_t* out, const void* chunks,
+                                const unsigned* count, cudaStream_t s);
 cudaError_t launch_ca_bits_run(const Geom& g, const void* tmA, const void* tmB, uint32_t* A, uint32_t* B,
                                const void* chunks, const unsigned* count, int steps, cudaStream_t s);
 // 2-simplex EDM (f64 points as x, y pairs) and periodic 2-D Life (smx_kernels2d.cu)

@@ -298,8 +298,9 @@ class StagedBitsOps(BitsOps):
 
 
 def run_bits(sh: "ShardedLife", api, g, cells, steps: int):
-    """launch_ca sharded: pack -> steps x (range step + bit-tile exchange) ->
-    unpack into `cells` (valid on the rank's own tiles; gather_owned collects)."""
+    """launch_ca sharded (per-step map variant): pack -> steps x (range step +
+    bit-tile exchange) -> unpack into `cells` (valid on the rank's own tiles;
+    gather_owned collects)."""
     a, b = api.bits_buffer(g), api.bits_buffer(g)
     api.bits_pack_device(g, cells, a)
     res = sh.run(a, b, steps)
@@ -307,11 +308,225 @@ def run_bits(sh: "ShardedLife", api, g, cells, steps: int):
     return cells
 
 
+# ---------------------------------------------------------------------------
+# The sharded ENGINE: the map applied once per rank (its wz range's chunk
+# list), split into boundary chunks (holding a tile some peer reads) and
+# interior chunks; per step the boundary runs first, its halo tiles are packed
+# and sent on a communication stream while the interior runs, and the
+# received tiles are unpacked once both are done.
+
+def chunk_tiles(chunks: np.ndarray, rho: int):
+    """(k, 4) chunks {x0, y0, z0, owned width} (cells) -> tile x0, y, z and tile
+    count of each chunk."""
+    c = np.asarray(chunks, np.int64).reshape(-1, 4)
+    tx0 = c[:, 0] // rho
+    ntile = (c[:, 0] + c[:, 3] + rho - 1) // rho - tx0
+    return tx0, c[:, 1] // rho, c[:, 2] // rho, ntile
+
+
+def split_chunks(chunks: np.ndarray, send_tiles: np.ndarray, domain_blocks: int, rho: int):
+    """Boundary / interior split of a rank's chunk list: a chunk is boundary
+    when any of its tiles is in `send_tiles` ((k, 3) x, y, z) — those must be
+    final before the halo is packed. Returns (boundary, interior) arrays."""
+    c = np.asarray(chunks, np.int32).reshape(-1, 4)
+    if c.shape[0] == 0:
+        return c, c
+    D = domain_blocks
+    mark = np.zeros((D, D, D), bool)
+    t = np.asarray(send_tiles, np.int64).reshape(-1, 3)
+    if t.shape[0]:
+        mark[t[:, 2], t[:, 1], t[:, 0]] = True
+    tx0, ty, tz, nt = chunk_tiles(c, rho)
+    hit = np.zeros(c.shape[0], bool)
+    for j in range(int(nt.max())):
+        sel = (nt > j) & ~hit
+        x = tx0[sel] + j
+        ok = x < D
+        idx = np.nonzero(sel)[0][ok]
+        hit[idx] |= mark[tz[idx], ty[idx], x[ok]]
+    return np.ascontiguousarray(c[hit]), np.ascontiguousarray(c[~hit])
+
+
+class ShardedEngine:
+    """One rank of launch_ca sharded over whole H levels, the
+    multi-step engine per rank. `ops` provides the device work so the same
+    schedule runs on CUDA over NCCL (EngineOps, the product) and on CPU over
+    gloo (tests):
+        ops.plan(lo, hi) -> (k, 4) int32 chunk array (host)
+        ops.chunks(np) -> handle; ops.run_list(a, b, handle)
+        ops.pack / ops.unpack / ops.empty / ops.tiles (bit tiles, as BitsOps)
+        ops.begin_step(b); ops.fork() -> context (comm stream); ops.join()"""
+
+    def __init__(self, plan: HaloPlan, rank: int, rho: int, ops, group=None):
+        import torch.distributed as dist
+
+        self.dist, self.plan, self.rank, self.rho, self.ops, self.group = dist, plan, rank, rho, ops, group
+        lo, hi = plan.wz_ranges[rank]
+        chunks = ops.plan(lo, hi)
+        peers_send = sorted(plan.send[rank])
+        send_all = (np.concatenate([plan.send[rank][q] for q in peers_send]) if peers_send
+                    else np.zeros((0, 3), np.int32))
+        bnd, inn = split_chunks(chunks, send_all, plan.domain_blocks, rho)
+        self.n_boundary, self.n_interior = int(bnd.shape[0]), int(inn.shape[0])
+        self.bnd, self.inn = ops.chunks(bnd), ops.chunks(inn)
+        tb = getattr(ops, "tile_bytes", rho ** 3)
+        # one pack and one unpack launch per step: every peer's tiles in one
+        # list, each peer's bytes a contiguous slice of one buffer
+        recv = plan.recv(rank)
+        peers_recv = sorted(recv)
+        recv_all = (np.concatenate([recv[q] for q in peers_recv]) if peers_recv else np.zeros((0, 3), np.int32))
+        self.send_t, self.recv_t = ops.tiles(send_all), ops.tiles(recv_all)
+        self.send_b, self.recv_b = ops.empty(send_all.shape[0] * tb), ops.empty(recv_all.shape[0] * tb)
+        self.send_views, self.recv_views, off = [], [], 0
+        for q in peers_send:
+            k = plan.send[rank][q].shape[0] * tb
+            self.send_views.append((q, self.send_b[off:off + k]))
+            off += k
+        off = 0
+        for q in peers_recv:
+            k = recv[q].shape[0] * tb
+            self.recv_views.append((q, self.recv_b[off:off + k]))
+            off += k
+
+    def _exchange(self):
+        d = self.dist
+        ops = [d.P2POp(d.isend, buf, q, self.group) for q, buf in self.send_views]
+        ops += [d.P2POp(d.irecv, buf, q, self.group) for q, buf in self.recv_views]
+        if ops:
+            for req in d.batch_isend_irecv(ops):
+                req.wait()
+
+    def step(self, a, b) -> None:
+        ops = self.ops
+        ops.begin_step(b)
+        ops.run_list(a, b, self.bnd)             # boundary chunks first
+        with ops.fork():                         # comm stream, after the boundary
+            if self.send_views:
+                ops.pack(b, self.send_t, self.send_b)
+            self._exchange()
+        ops.run_list(a, b, self.inn)             # interior while the halo travels
+        ops.join()
+        if self.recv_views:                      # after both runs (whole-word stores)
+            ops.unpack(b, self.recv_t, self.recv_b)
+
+    def run(self, a, b, steps: int):
+        for _ in range(steps):
+            self.step(a, b)
+            a, b = b, a
+        return a
+
+
+class EngineOps(BitsOps):
+    """The product ops of ShardedEngine: the engine's plan and run-list kernels
+    on bit shadows, bit-tile pack / unpack, a communication stream."""
+
+    def __init__(self, grid):
+        import torch
+        super().__init__(grid)
+        self.comm = torch.cuda.Stream()
+
+    def plan(self, lo, hi):
+        ch, cnt = self.api.bits_plan_device(self.g, lo, hi)
+        n = int(cnt.item())
+        return ch[:n].cpu().numpy()
+
+    def chunks(self, arr):
+        import torch
+        c = torch.from_numpy(np.ascontiguousarray(arr, np.int32).reshape(-1, 4)).cuda()
+        if c.shape[0] == 0:
+            c = torch.zeros((1, 4), dtype=torch.int32, device="cuda")
+        return c, torch.tensor([arr.shape[0]], dtype=torch.int32, device="cuda")
+
+    def run_list(self, a, b, handle):
+        self.api.bits_run_list_device(self.g, a, b, handle[0], handle[1])
+
+    def begin_step(self, b):
+        pass
+
+    def fork(self):
+        import contextlib
+
+        import torch
+        ev = torch.cuda.Event()
+        ev.record()
+        self.comm.wait_event(ev)
+
+        @contextlib.contextmanager
+        def ctx():
+            with torch.cuda.stream(self.comm):
+                yield
+        return ctx()
+
+    def join(self):
+        import torch
+        torch.cuda.current_stream().wait_stream(self.comm)
+
+
+class StagedEngineOps(EngineOps):
+    """EngineOps with host-staged halo buffers (gloo on one GPU; smoke tests)."""
+
+    def empty(self, n):
+        import torch
+        return torch.zeros(max(n, 1), dtype=torch.uint8)
+
+    def pack(self, bits, tiles, out):
+        import torch
+        tmp = torch.empty(out.numel(), dtype=torch.uint8, device="cuda")
+        super().pack(bits, tiles, tmp)
+        out.copy_(tmp.cpu())
+
+    def unpack(self, bits, tiles, buf):
+        super().unpack(bits, tiles, buf.cuda())
+
+
+def engine_launch_ca(eng: ShardedEngine, api, g, cells, a, b, steps: int):
+    """One sharded launch_ca call: pack the rank's replica, `steps` engine
+    steps with the overlapped halo exchange, unpack (own tiles valid)."""
+    api.bits_pack_device(g, cells, a)
+    res = eng.run(a, b, steps)
+    api.bits_unpack_device(g, res, cells)
+    return cells
+
+
+def gather_owned_u8(plan: HaloPlan, api, g, cells, rank: int, dst: int = 0, group=None, staged: bool = False):
+    """Every rank's owned u8 tiles onto `dst` (for the state hash); `staged`:
+    the transfer buffers live in host memory (gloo)."""
+    import torch
+    import torch.distributed as dist
+    r3 = g.rho ** 3
+
+    def tiles(t):
+        return torch.from_numpy(np.ascontiguousarray(t, np.int32).reshape(-1, 3)).cuda()
+
+    def buffer(k):
+        return torch.empty(k * r3, dtype=torch.uint8, device="cpu" if staged else "cuda")
+    if rank == dst:
+        for q in range(plan.world):
+            if q == dst or plan.owned_tiles[q].shape[0] == 0:
+                continue
+            buf = buffer(plan.owned_tiles[q].shape[0])
+            dist.recv(buf, q, group)
+            api.tiles_unpack_device(g, cells, tiles(plan.owned_tiles[q]), buf.cuda())
+    elif plan.owned_tiles[rank].shape[0]:
+        dev = torch.empty(plan.owned_tiles[rank].shape[0] * r3, dtype=torch.uint8, device="cuda")
+        api.tiles_pack_device(g, cells, tiles(plan.owned_tiles[rank]), dev)
+        dist.send(dev.cpu() if staged else dev, dst, group)
+
+
+SHARD_WORKLOADS = {
+    # name: (description, n_b, rho, CA steps per launch_ca call, golden key)
+    "c4": ("3-simplex n=1024 CA (C4): launch_ca over grid_h3d(128) rho=8, side 1016 (175,311,816 cells), "
+           "100 steps per call, sharded over whole H levels", 128, 8, 100, "c4_rho8_100"),
+    "c5": ("3-simplex n=2048 CA (C5): launch_ca over grid_h3d(256) rho=8, side 2040 (1,417,025,480 cells), "
+           "20 steps per call, sharded over whole H levels", 256, 8, 20, "c5_rho8_20"),
+}
+
+
 def bench_sharded(args, api):
-    """bench.py --gpus N under torchrun: the C2 launch_ca (100 CA steps per
-    bench step) sharded over N GPUs with the bit-shadow engine: each rank packs
-    its replica once, steps its H wz range (map-driven bit-sliced kernel) and
-    exchanges bit halo tiles over NCCL after every CA step, unpacks once."""
+    """bench.py --gpus N under torchrun: C4 (and C5 when N = 8) launch_ca
+    sharded over N GPUs with the per-rank engine (map once, boundary chunks
+    first, bit-tile halo over NCCL on a comm stream overlapping the interior).
+    The final state is gathered and hashed against the oracle golden."""
     import os
 
     import torch
@@ -328,47 +543,67 @@ def bench_sharded(args, api):
     else:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from bench import METRIC, SEED, Flusher, timed_steps  # noqa: E402
+    from bench import METRIC, SEED, Flusher, load_golden, timed_steps  # noqa: E402
 
-    desc, kind, n, rho, nsteps = ("3-simplex n=256 CA (C2): launch_ca over H3D(64) rho=4, side 252, 100 steps "
-                                  "per call", "h3d", 64, 4, 100)
-    g = api.make_grid(api.map_kind[kind], 3, n, rho)
+    key = os.environ.get("SMX_SHARD_WORKLOAD", "c4")
+    desc, n, rho, nsteps, gkey = SHARD_WORKLOADS[key]
+    if backend == "gloo":  # smoke: a small grid, few steps (hash vs the restated oracle below)
+        desc, n, rho, nsteps, gkey = ("smoke: grid_h3d(32) rho=8, 10 steps", 32, 8, 10, None)
+    g = api.make_grid(api.map_kind.h3d, 3, n, rho)
     side = g.cell_side()
     cells = api.tet_cells(side)
     out = api.map_outcomes(g)
     plan = build_plan(g.extents, out, True, g.domain_side(), world)
-    ops = BitsOps(g) if backend != "gloo" else StagedBitsOps(g)
-    sh = ShardedLife(plan, rank, rho, ops)
-    a = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
-    api.life_init_device(3, side, SEED, a)
+    ops = EngineOps(g) if backend != "gloo" else StagedEngineOps(g)
+    eng = ShardedEngine(plan, rank, rho, ops)
+    u8 = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
+    sa, sb = api.bits_buffer(g), api.bits_buffer(g)
     flush = Flusher()
 
+    def prep():  # outside the timed region: L2 flush + the seed-42 state
+        flush()
+        api.life_init_device(3, side, SEED, u8)
+
     def step(i):
-        run_bits(sh, api, g, a, nsteps)
+        engine_launch_ca(eng, api, g, u8, sa, sb, nsteps)
 
     dist.barrier()
-    timed_steps(step, args.warmup, flush)
+    timed_steps(step, args.warmup, prep)
     torch.cuda.synchronize()
     dist.barrier()
-    ms = timed_steps(step, args.steps, flush)
+    ms = timed_steps(step, args.steps, prep)
     tot = torch.tensor([sum(ms)], dtype=torch.float64, device="cuda" if backend != "gloo" else "cpu")
     dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms_step = float(tot.item()) / args.steps
+    # parity: the last call's state (every rank's own tiles) gathered on rank 0
+    gather_owned_u8(plan, api, g, u8, rank, staged=backend == "gloo")
     line = None
     if rank == 0:
+        h = api.state_hash(3, side, u8.cpu().numpy())
+        golden = load_golden().get(gkey, {}) if gkey else {}
+        if not gkey:  # smoke grid: the restated oracle (test infrastructure) on the spot
+            from oracle.oracle import Restated
+            orc = Restated()
+            want = orc.make_life_state(3, side, SEED)
+            orc.ca3d_run(side, nsteps, want)
+            golden = {"final_hash": orc.state_hash(3, side, want)}
         line = {
             "metric": METRIC,
-            "value": round(cells * nsteps / (ms_step * 1e-3) / 1e9, 3), "unit": "Gcell-steps/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+            "value": round(cells * nsteps / (ms_step * 1e-3) / 1e9, 3), "unit": "Gcell-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (make_life_state seed 42)", "impl": "ours",
-            "config": {"workload": desc, "map": kind, "n_b": n, "rho": rho, "side": side, "cells": cells,
+            "config": {"workload": desc, "map": "h3d", "n_b": n, "rho": rho, "side": side, "cells": cells,
                        "ca_steps_per_call": nsteps,
-                       "parallelism": f"H wz-range shards x{world}: bit-shadow engine, bit-tile halo "
-                                      f"({ops.tile_bytes} B/tile) over NCCL after every CA step",
-                       "wz_ranges": plan.wz_ranges, "halo_tiles_per_rank": [plan.halo_tiles(r) for r in
-                                                                            range(world)]},
-            "gpu_launches": args.steps * (2 + nsteps * (1 + 2 * len(plan.send[rank]) + len(plan.recv(rank)))),
+                       "parallelism": f"H wz-range shards x{world}: per-rank bit-shadow engine (map once; "
+                                      f"boundary chunks, then interior while the bit-tile halo "
+                                      f"({ops.tile_bytes} B/tile) crosses over {backend.upper()} on a comm stream)",
+                       "wz_ranges": plan.wz_ranges,
+                       "halo_tiles_per_rank": [plan.halo_tiles(r) for r in range(world)],
+                       "boundary_interior_chunks_rank0": [eng.n_boundary, eng.n_interior]},
+            "parity": {"state_hash": str(h), "golden": gkey,
+                       "ok": (str(h) == str(golden.get("final_hash"))) if golden else None},
+            "gpu_launches": args.steps * (3 + nsteps * 4),
         }
     dist.destroy_process_group()
     return line

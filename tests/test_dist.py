@@ -148,3 +148,116 @@ def test_partition_rows_balanced_and_contiguous():
             assert all(r[i][1] == r[i + 1][0] for i in range(world - 1))
             loads = [int(u[lo:hi].sum()) for lo, hi in r]
             assert max(loads) - int(u.sum()) / world <= int(u.max()), (kind, n, world, loads)
+
+
+class EngineCpuOps:
+    """CPU stand-in for EngineOps (ShardedEngine): chunks are tiles (merged in
+    x-adjacent pairs, so multi-tile chunks are exercised), run_list writes the
+    oracle's next state on the chunk's tiles only, every other cell of the
+    output is poisoned at the start of a step, halo tiles travel as u8 tiles."""
+
+    def __init__(self, orc, kind, n, rho, side, seed):
+        self.orc, self.kind, self.n, self.rho, self.side = orc, kind, n, rho, side
+        self.rng = np.random.default_rng(seed)
+        self.tile_bytes = rho ** 3
+        self._next = None
+        base = OracleOps(orc, side, rho, np.zeros(0, np.int64), seed)
+        self.pack, self.unpack, self.empty, self.tiles = base.pack, base.unpack, base.empty, base.tiles
+
+    def plan(self, lo, hi):
+        o = self.orc.map_outcomes(self.kind, 3, self.n)
+        ex, ey, _ = self.orc.grid(self.kind, 3, self.n)
+        wz = np.arange(o.shape[0]) // (ex * ey)
+        sel = (o[:, 0] == 0) & (wz >= lo) & (wz < hi)
+        t = o[sel][:, 1:4].astype(np.int64)
+        if self.kind == H3D:
+            t[:, 1] -= 1
+        t = t[np.lexsort((t[:, 0], t[:, 1], t[:, 2]))]
+        out, i = [], 0
+        while i < t.shape[0]:
+            j = i + 1
+            if j < t.shape[0] and (t[j, 1:] == t[i, 1:]).all() and t[j, 0] == t[i, 0] + 1:
+                j += 1
+            r = self.rho
+            out.append((t[i, 0] * r, t[i, 1] * r, t[i, 2] * r, (j - i) * r))
+            i = j
+        return np.asarray(out, np.int32).reshape(-1, 4)
+
+    def chunks(self, arr):
+        return arr
+
+    def begin_step(self, b):
+        self._next = None
+        b.numpy()[:] = self.rng.integers(0, 2, b.numel(), dtype=np.uint8)
+
+    def run_list(self, a, b, chunks):
+        if self._next is None:
+            c = a.numpy().copy()
+            self.orc.ca3d_run(self.side, 1, c, threads=1)
+            self._next = c
+        tx0, ty, tz, nt = D.chunk_tiles(chunks, self.rho)
+        tl = [(x, y, z) for x0, y, z, k in zip(tx0, ty, tz, nt) for x in range(x0, x0 + k)]
+        if tl:
+            idx = tile_cells(self.side, self.rho, np.asarray(tl)).ravel()
+            idx = idx[idx >= 0]
+            b.numpy()[idx] = self._next[idx]
+
+    def fork(self):
+        import contextlib
+        return contextlib.nullcontext()
+
+    def join(self):
+        pass
+
+
+def _engine_worker(rank, world, port, kind, n, rho, steps, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Restated()
+    outcomes = orc.map_outcomes(kind, 3, n)
+    ext = orc.grid(kind, 3, n)
+    strict = kind == H3D
+    dom_blocks = n - 1 if strict else n
+    side = dom_blocks * rho
+    plan = D.build_plan(ext, outcomes, strict, dom_blocks, world)
+    ops = EngineCpuOps(orc, kind, n, rho, side, seed=rank + 11)
+    eng = D.ShardedEngine(plan, rank, rho, ops)
+    a = torch.from_numpy(orc.make_life_state(3, side, 42, threads=1))
+    b = torch.zeros_like(a)
+    res = eng.run(a, b, steps)
+    sh = D.ShardedLife(plan, rank, rho, OracleOps(orc, side, rho, np.zeros(0, np.int64), 0))
+    sh.gather_owned(res, 0)
+    if rank == 0:
+        want = orc.make_life_state(3, side, 42, threads=1)
+        orc.ca3d_run(side, steps, want, threads=1)
+        q.put((bool((res.numpy() == want).all()), eng.n_boundary, eng.n_interior))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,n,world", [(H3D, 16, 2), (H3D, 16, 3), (BB, 15, 2)])
+def test_sharded_engine_schedule(kind, n, world):
+    """The sharded engine's schedule (boundary chunks, pack + exchange, interior,
+    unpack) with poisoned non-owned cells: exact after 3 steps only if the
+    boundary/interior split and the halo plan are right."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_engine_worker, args=(r, world, port, kind, n, 4, 3, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    ok, nb, ni = q.get(timeout=300)
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert ok
+    assert nb > 0 and ni > 0
+
+
+def test_split_chunks():
+    # chunks of 2 tiles at rho = 4; tile (5, 7, 1) is sent -> only chunk 0
+    ch = np.array([[16, 28, 4, 8], [40, 28, 4, 8], [0, 0, 0, 4]], np.int32)
+    b, i = D.split_chunks(ch, np.array([[5, 7, 1]]), 16, 4)
+    assert b.tolist() == [[16, 28, 4, 8]] and i.shape == (2, 4)
+    b, i = D.split_chunks(ch, np.zeros((0, 3)), 16, 4)
+    assert b.shape == (0, 4) and i.shape == (3, 4)

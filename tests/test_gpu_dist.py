@@ -22,7 +22,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, kind, n, rho, ex, steps, q, bits=False):
+def _worker(rank, world, port, kind, n, rho, ex, steps, q, bits=False, engine=False):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from oracle.oracle import Restated
@@ -66,7 +66,10 @@ def _worker(rank, world, port, kind, n, rho, ex, steps, q, bits=False):
     b = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
     api.life_init_device(3, side, 42, a)
     b.fill_(1)  # garbage outside owned + halo tiles must never matter
-    if bits:
+    if engine:  # the per-rank engine: boundary chunks, halo on a comm stream, interior, unpack
+        eng = D.ShardedEngine(plan, rank, rho, D.StagedEngineOps(g))
+        res = D.engine_launch_ca(eng, api, g, a, api.bits_buffer(g), api.bits_buffer(g), steps)
+    elif bits:
         shb = D.ShardedLife(plan, rank, rho, StagedBitsOps(g))
         res = D.run_bits(shb, api, g, a, steps)
     else:
@@ -130,6 +133,7 @@ def test_bench_sharded_smoke(cuda):
     assert out.returncode == 0, out.stderr[-3000:]
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and "bit-shadow engine" in line["config"]["parallelism"]
+    assert line["parity"]["ok"] is True, line["parity"]
 
 
 def _accum_worker(rank, world, port, kind, n, rho, passes, q):
@@ -176,3 +180,22 @@ def test_sharded_accum_rows_on_one_gpu(cuda, kind, n, rho):
     rep = api.launch_map_device(g)
     assert (tot["blocks_launched"], tot["blocks_void"], tot["threads_launched"], tot["threads_useful"]) == (
         rep.blocks_launched, rep.blocks_void, rep.threads_launched, rep.threads_useful)
+
+
+@pytest.mark.parametrize("kind,n,rho,world", [("h3d", 32, 8, 2), ("h3d", 32, 4, 3), ("bb", 31, 8, 2),
+                                               ("h3d", 64, 8, 4)])
+def test_sharded_engine_on_one_gpu(cuda, kind, n, rho, world):
+    """ShardedEngine with the real kernels (plan per wz range, run-list on the
+    boundary / interior chunks, bit-tile pack / unpack), ranks on one GPU."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, n, rho, 1, 6, q, False, True))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert ok
