@@ -621,6 +621,239 @@ cudaError_t launch_run_t(const Geom& g, const CUtensorMap& tA, const CUtensorMap
                                        smem, s);
 }
 
+// ===========================================================================
+// The COLUMN engine (large states): the map applied once marks every tile it
+// emits in a tile bitmap (k_cols_mark: one thread per map block, so its cost
+// is the block count: H3D maps 5.3x fewer blocks than BB); the run is a
+// persistent kernel whose work items are columns of the domain — 8 cell rows
+// x 8 words (256 cells) x a run of z layers — that a warp marches along z:
+// 3-D TMA stages of 8 layers (16 words x 10 rows x 8 layers, double-buffered,
+// mbarrier completion), each input layer's horizontal 3-sums computed ONCE
+// (10 rows x 8 words, shared through shared memory), the vertical 3-sums kept
+// in registers across the march (a rolling window of three layers), the rule
+// applied with carry-save adders on 32 cells per LOP3, and the output word
+// masked by the bitmap (only the cells of tiles the map emitted are written;
+// the others are zero, as the reference's unvisited cells of a fresh state).
+// Items are taken dynamically (one atomic per item); a grid barrier separates
+// the steps.
+constexpr int CW = 8;                    // output words per item row (256 cells)
+constexpr int CR = 8;                    // output rows per item
+constexpr int CBW = 16;                  // box words: 8 g - 4 .. 8 g + 11 (16-byte aligned start)
+constexpr int CBR = CR + 2;              // box rows: y0 - 1 .. y0 + 8
+constexpr int CLZ = 8;                   // layers per TMA stage
+constexpr int CSTAGE = CBW * CBR * CLZ * 4;  // 5120 B
+constexpr int CLAYER = CBW * CBR * 4;        // 640 B per layer of a stage
+constexpr int CHS = CBR * CW * 8;            // h-sums of one layer: [10 rows][8 words][a, b]
+constexpr int CWARP_BYTES = 2 * CSTAGE + CHS + 64;  // 10944 (128-aligned: 10944 = 85.5 * 128 -> pad)
+constexpr int CWARP = (CWARP_BYTES + 127) & ~127;
+constexpr int CNW = 16;                  // warps per CTA (persistent: one CTA per SM)
+
+struct ColItem {
+    int iy, g, z0, z1;  // rows 8 iy .. 8 iy + 7, words 8 g .. 8 g + 7, layers z0 .. z1 - 1
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(256) k_cols_mark(Geom g, uint32_t* __restrict__ bm, int D, int TW,
+                                                    unsigned* __restrict__ stats) {
+    const long long nb = (long long)g.ex * g.ey * g.ez;
+    unsigned marked = 0, dup = 0;
+    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nb;
+         b += (long long)gridDim.x * blockDim.x) {
+        const int wx = int(b % g.ex), wy = int(b / g.ex % g.ey), wz = int(b / ((long long)g.ex * g.ey));
+        const outcome<int> o = map_block<KIND>(g, wx, wy, wz);
+        if (o.is_void) continue;
+        const uint32_t bit = 1u << (o.x & 31);
+        const uint32_t old = atomicOr(bm + ((long long)o.z * D + o.y) * TW + (o.x >> 5), bit);
+        ++marked;
+        dup += (old & bit) ? 1u : 0u;
+    }
+    for (int d = 16; d; d >>= 1) {
+        marked += __shfl_xor_sync(0xffffffffu, marked, d);
+        dup += __shfl_xor_sync(0xffffffffu, dup, d);
+    }
+    if ((threadIdx.x & 31) == 0 && (marked | dup)) {
+        atomicAdd(stats, marked);
+        atomicAdd(stats + 1, dup);
+    }
+}
+
+// 2 cell words' coverage mask from the tile bitmap: word k of the lane covers
+// tiles 32 (w + k) / RHO ...; every tile bit becomes RHO cell bits
+template <int RHO>
+__device__ __forceinline__ uint2 tile_mask2(const uint32_t* __restrict__ bm, int D, int TW, int w, int ty, int tz) {
+    if (ty >= D || tz >= D) return make_uint2(0u, 0u);
+    constexpr int TPW = 32 / RHO;  // tiles per cell word
+    const int t0 = w * TPW;        // first tile (w even: the 2 * TPW bits share one bitmap word)
+    const uint32_t bits = bm[((long long)tz * D + ty) * TW + (t0 >> 5)] >> (t0 & 31);
+    uint32_t m[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const uint32_t b = (bits >> (k * TPW)) & ((1u << TPW) - 1u);
+        if (RHO == 8) {
+            m[k] = ((b * 0x00204081u) & 0x01010101u) * 0xffu;  // bit i -> byte i
+        } else {
+            uint32_t v = 0;  // bit i -> nibble i
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v |= ((b >> i) & 1u) * (0xfu << (4 * i));
+            m[k] = v;
+        }
+    }
+    return make_uint2(m[0], m[1]);
+}
+
+__device__ __forceinline__ void cols_issue(const CUtensorMap* tm, const ColItem& it, int stage, uint8_t* buf,
+                                           uint32_t mbar) {
+    mbar_expect_tx(mbar, uint32_t(CSTAGE));
+    tma_load_3d(smem_u32(buf), tm, 8 * it.g - 4, 8 * it.iy - 1, it.z0 - 1 + CLZ * stage, mbar);
+}
+
+// One step of the column engine for one warp: items grabbed from *ctr until
+// the list is exhausted. `seq` counts the TMA stages this warp has issued
+// (buffer = seq & 1, parity = (seq >> 1) & 1), carried across steps.
+template <int RHO>
+__device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int nitems, unsigned* ctr,
+                                          const CUtensorMap* tm, uint32_t* __restrict__ out,
+                                          const uint32_t* __restrict__ bm, int D, int TW, int S, int WP,
+                                          uint8_t* wbase, uint32_t mbar0, uint32_t& seq) {
+    const int lane = threadIdx.x & 31;
+    uint2* hs = reinterpret_cast<uint2*>(wbase + 2 * CSTAGE);  // [CBR][CW]
+    // lane roles: h-sums: row hr = lane / 3 (0..9, lanes 0..29), words 3 (lane % 3) .. +2 (the
+    // third segment is words 6, 7); outputs: row ly = lane / 4, words 2 (lane % 4), +1
+    const int hr = lane / 3, hseg = lane % 3, hj0 = 3 * hseg, hjn = hseg == 2 ? 2 : 3;
+    const int ly = lane >> 2, jp = 2 * (lane & 3);
+    int cur = 0;
+    if (lane == 0) cur = int(atomicAdd(ctr, 1u));
+    cur = __shfl_sync(0xffffffffu, cur, 0);
+    if (cur < nitems && lane == 0) {
+        fence_proxy_async();
+        cols_issue(tm, items[cur], 0, wbase + (seq & 1) * CSTAGE, mbar0 + 8 * (seq & 1));
+    }
+    while (cur < nitems) {
+        const ColItem it = items[cur];
+        int nxt = 0;
+        if (lane == 0) nxt = int(atomicAdd(ctr, 1u));
+        nxt = __shfl_sync(0xffffffffu, nxt, 0);
+        const int nin = it.z1 - it.z0 + 2;            // input layers z0 - 1 .. z1
+        const int nst = (nin + CLZ - 1) / CLZ;
+        const int y0 = 8 * it.iy, w0 = 8 * it.g;
+        const int yo = y0 + ly;                       // this lane's output row
+        const int wo = w0 + jp;                       // and its first output word
+        const int hy = y0 - 1 + hr;                   // this lane's h-sum row
+        Planes4 va[2], vb[2];
+        uint32_t alive_cur[2] = {0u, 0u};
+        uint2 tmask = make_uint2(0u, 0u);
+        int tz_cur = -1;
+        for (int st = 0; st < nst; ++st) {
+            const uint32_t b = seq & 1;
+            // the other buffer is free (its stage was consumed): prefetch the
+            // next stage of this item, or the first stage of the next item
+            if (lane == 0) {
+                fence_proxy_async();
+                if (st + 1 < nst) cols_issue(tm, it, st + 1, wbase + (b ^ 1) * CSTAGE, mbar0 + 8 * (b ^ 1));
+                else if (nxt < nitems) cols_issue(tm, items[nxt], 0, wbase + (b ^ 1) * CSTAGE, mbar0 + 8 * (b ^ 1));
+            }
+            while (!mbar_try_wait(mbar0 + 8 * b, (seq >> 1) & 1u)) {
+            }
+            const uint8_t* buf = wbase + b * CSTAGE;
+            const int nl = min(CLZ, nin - CLZ * st);
+            for (int li = 0; li < nl; ++li) {
+                const int zi = it.z0 - 1 + CLZ * st + li;     // input layer
+                const uint32_t* L = reinterpret_cast<const uint32_t*>(buf + li * CLAYER);
+                // ---- h-sums of layer zi: rows y0-1 .. y0+8, words w0 .. w0+7 ----
+                if (lane < 30) {
+                    const bool rowok = zi >= 0 && hy >= 0 && hy + zi <= S - 1;
+                    const uint32_t* R = L + hr * CBW + 3 + hj0;  // box word of x word w0 + hj0 - 1
+                    uint32_t T[5];
+#pragma unroll
+                    for (int j = 0; j < 5; ++j) T[j] = rowok ? R[j] : 0u;
+                    const int xb = 32 * (w0 + hj0 - 1);         // x of T[0] bit 0
+                    if (xb + 159 > hy) {
+#pragma unroll
+                        for (int j = 0; j < 5; ++j) T[j] &= __funnelshift_lc(0xffffffffu, 0u, max(hy - (xb + 32 * j) + 1, 0));
+                    }
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        if (j < hjn) {
+                            const uint32_t c = T[j + 1];
+                            const uint32_t l = __funnelshift_l(T[j], c, 1);
+                            const uint32_t r = __funnelshift_r(c, T[j + 2], 1);
+                            hs[hr * CW + hj0 + j] = make_uint2(l ^ c ^ r, (l & c) | (l & r) | (c & r));
+                        }
+                    }
+                }
+                // the centre words of this layer: the next output layer's alive bits
+                uint32_t alive_next[2];
+                {
+                    const uint2 a = *reinterpret_cast<const uint2*>(L + (ly + 1) * CBW + 4 + jp);
+                    alive_next[0] = a.x;
+                    alive_next[1] = a.y;
+                }
+                __syncwarp();
+                // ---- vertical sums of layer zi for this lane's two words ----
+                Planes4 vc[2];
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const uint2 p = hs[ly * CW + jp + k], q = hs[(ly + 1) * CW + jp + k], u = hs[(ly + 2) * CW + jp + k];
+                    vc[k] = add3x2(p.x, p.y, q.x, q.y, u.x, u.y);
+                }
+                const int zo = zi - 1;                        // output layer
+                if (zo >= it.z0) {
+                    if ((zo / RHO) != tz_cur) {
+                        tz_cur = zo / RHO;
+                        tmask = tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, tz_cur);
+                    }
+                    const uint32_t o0 = life_planes(va[0], vb[0], vc[0], alive_cur[0]) & tmask.x;
+                    const uint32_t o1 = life_planes(va[1], vb[1], vc[1], alive_cur[1]) & tmask.y;
+                    if (yo + zo <= S - 1) {
+                        uint32_t* op = out + ((long long)zo * S + yo) * WP + wo;
+                        if (32 * (wo + 1) <= yo) *reinterpret_cast<uint2*>(op) = make_uint2(o0, o1);
+                        else if (32 * wo <= yo) *op = o0;
+                    }
+                }
+                va[0] = vb[0];
+                va[1] = vb[1];
+                vb[0] = vc[0];
+                vb[1] = vc[1];
+                alive_cur[0] = alive_next[0];
+                alive_cur[1] = alive_next[1];
+                __syncwarp();
+            }
+            ++seq;
+        }
+        cur = nxt;
+    }
+}
+
+template <int RHO>
+__global__ void __launch_bounds__(CNW * 32) k_cols_run(const __grid_constant__ CUtensorMap tmA,
+                                                       const __grid_constant__ CUtensorMap tmB, uint32_t* bitsA,
+                                                       uint32_t* bitsB, const ColItem* __restrict__ items,
+                                                       int nitems, unsigned* ctl, const uint32_t* __restrict__ bm,
+                                                       int D, int TW, int steps, int S, int WP) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t* wbase = smem + warp * CWARP;
+    const uint32_t mbar0 = smem_u32(wbase + 2 * CSTAGE + CHS);
+    if (lane == 0) {
+        mbar_init(mbar0, 1);
+        mbar_init(mbar0 + 8, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    uint32_t seq = 0;
+    // ctl: [0] the grid barrier, [1 + s] step s's item counter (zeroed by the host)
+    for (int st = 0; st < steps; ++st) {
+        const bool even = (st & 1) == 0;
+        cols_step<RHO>(items, nitems, ctl + 1 + st, even ? &tmA : &tmB, even ? bitsB : bitsA, bm, D, TW, S, WP, wbase,
+                       mbar0, seq);
+        if (st + 1 < steps) step_barrier(ctl);
+    }
+}
+
 template <int KIND>
 void launch_kind(const Geom& g, int wz0, int wz1, const CUtensorMap& tmap, uint32_t* nbits, int WP, cudaStream_t s) {
     if (g.rho == 4) launch_t<KIND, 4>(g, wz0, wz1, tmap, nbits, WP, s);
@@ -777,6 +1010,54 @@ cudaError_t launch_ca_bits_run(const Geom& g, const void* tmA, const void* tmB, 
         return launch_run_t<4, 16, 2>(g, ta, tb, A, B, chunks, count, steps, s);
     }
     return launch_run_t<8, 16, 1>(g, ta, tb, A, B, chunks, count, steps, s);
+}
+
+// ---- the column engine's launchers ----
+int cols_box_words() { return CBW; }
+int cols_box_rows() { return CBR; }
+int cols_box_layers() { return CLZ; }
+int cols_item_bytes() { return int(sizeof(ColItem)); }
+
+void launch_cols_mark(const Geom& g, int kind, uint32_t* bm, int D, int TW, unsigned* stats, cudaStream_t s) {
+    const long long nb = (long long)g.ex * g.ey * g.ez;
+    long long blocks = (nb + 255) / 256;
+    if (blocks > 148ll * 16) blocks = 148ll * 16;
+    if (blocks < 1) blocks = 1;
+    if (kind == SMX_H3D) k_cols_mark<SMX_H3D><<<unsigned(blocks), 256, 0, s>>>(g, bm, D, TW, stats);
+    else k_cols_mark<SMX_BB><<<unsigned(blocks), 256, 0, s>>>(g, bm, D, TW, stats);
+}
+
+int cols_grid() {
+    static std::once_flag once[kMaxDevices];
+    static int grids[kMaxDevices];
+    const int dev = current_device();
+    int local = 0;
+    once_per_device(once, dev, [&] {
+        const int smem = CNW * CWARP;
+        cudaFuncSetAttribute(k_cols_run<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_cols_run<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int per_sm = 0, nsm = 148;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cols_run<8>, CNW * 32, smem);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        local = (per_sm > 0 ? per_sm : 1) * nsm;
+        if (dev >= 0 && dev < kMaxDevices) grids[dev] = local;
+    });
+    return dev >= 0 && dev < kMaxDevices ? grids[dev] : local;
+}
+int cols_warps() { return cols_grid() * CNW; }
+
+cudaError_t launch_cols_run(const Geom& g, const void* tmA, const void* tmB, uint32_t* A, uint32_t* B,
+                            const void* items, int nitems, unsigned* ctl, const uint32_t* bm, int D, int TW, int steps,
+                            cudaStream_t s) {
+    const int grid = cols_grid();
+    const int smem = CNW * CWARP;
+    int S = g.side, WP = bits_pitch_words(g.side);
+    const ColItem* it = reinterpret_cast<const ColItem*>(items);
+    void* args[] = {const_cast<void*>(tmA), const_cast<void*>(tmB), &A, &B, &it, &nitems, &ctl,
+                    const_cast<uint32_t**>(&bm), &D, &TW, &steps, &S, &WP};
+    const void* fn = g.rho == 8 ? (const void*)k_cols_run<8> : (const void*)k_cols_run<4>;
+    if (steps == 1) return cudaLaunchKernel(fn, dim3(grid), dim3(CNW * 32), args, smem, s);
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(CNW * 32), args, smem, s);
 }
 
 void launch_ca_bits(const Geom& g, int kind, int wz0, int wz1, const void* tmap_ptr, uint32_t* nbits, cudaStream_t s) {

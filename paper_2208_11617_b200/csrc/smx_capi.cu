@@ -8,6 +8,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <initializer_list>
 #include <map>
@@ -72,8 +73,11 @@ struct DeviceRes {
     // block (64 B: u32 [0] chunk count, u32 [8] grid barrier), 7 the
     // first-defect result of smx_verify_cover (its own slot: a verify on one
     // stream never touches the words of an engine running on another)
-    void* pool[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-    size_t pool_bytes[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // 8 the column engine's items (host-built, key cols_key), 9 its tile bitmap
+    void* pool[10] = {};
+    size_t pool_bytes[10] = {};
+    std::pair<int64_t, int64_t> cols_key{-1, -1};  // (side, layers per item) of the items in slot 8
+    int cols_nitems = 0;
     std::map<std::pair<const void*, std::pair<int64_t, int64_t>>, CUtensorMap> tmaps;
     smx::DevCounters* counters = nullptr;
     unsigned* sink = nullptr;
@@ -91,7 +95,7 @@ void free_res(int dev, DeviceRes& r) {
     if (cudaGetDevice(&cur) != cudaSuccess) return;
     if (cur != dev) cudaSetDevice(dev);
     for (auto& kv : r.prefix) cudaFree(kv.second);
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < 10; ++i)
         if (r.pool[i]) cudaFree(r.pool[i]);
     if (r.counters) cudaFree(r.counters);
     if (r.sink) cudaFree(r.sink);
@@ -357,13 +361,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// 3-D tiled tensor map over a pitched bit shadow: (WP words, S rows, S layers);
-// box = tma_box_words() x (rho + 2) x (rho + 2); out-of-range coordinates read as zero.
-int bits_tmap(const uint32_t* bits, int64_t side, int64_t rho, const CUtensorMap** out) {
+// 3-D tiled tensor map over a pitched bit shadow: (WP words, S rows, S layers),
+// box b0 words x b1 rows x b2 layers; out-of-range coordinates read as zero.
+int bits_tmap_box(const uint32_t* bits, int64_t side, int b0, int b1, int b2, const CUtensorMap** out) {
     DeviceRes* r;
     if (int rc = device_res(&r)) return rc;
     std::lock_guard<std::mutex> lk(g_mu);
-    auto key = std::make_pair((const void*)bits, std::make_pair(side, rho));
+    auto key = std::make_pair((const void*)bits, std::make_pair(side, int64_t(b0) | int64_t(b1) << 16 | int64_t(b2) << 32));
     auto it = r->tmaps.find(key);
     if (it != r->tmaps.end()) {
         *out = &it->second;
@@ -372,10 +376,9 @@ int bits_tmap(const uint32_t* bits, int64_t side, int64_t rho, const CUtensorMap
     auto fn = encode_fn();
     if (!fn) return fail(SMX_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
     const int WP = smx::bits_pitch_words(int(side));
-    const cuuint32_t HB = cuuint32_t(smx::tma_box_rows(int(rho)));
     cuuint64_t dims[3] = {cuuint64_t(WP), cuuint64_t(side), cuuint64_t(side)};
     cuuint64_t strides[2] = {cuuint64_t(WP) * 4, cuuint64_t(WP) * 4 * cuuint64_t(side)};
-    cuuint32_t box[3] = {cuuint32_t(smx::tma_box_words()), HB, HB};
+    cuuint32_t box[3] = {cuuint32_t(b0), cuuint32_t(b1), cuuint32_t(b2)};
     cuuint32_t estr[3] = {1u, 1u, 1u};
     CUtensorMap m;
     CUresult cr = fn(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(bits), dims, strides, box, estr,
@@ -386,6 +389,11 @@ int bits_tmap(const uint32_t* bits, int64_t side, int64_t rho, const CUtensorMap
     *out = &res.first->second;
     return SMX_OK;
 }
+// the chunk engine's box: tma_box_words() x (rho + 2) x (rho + 2)
+int bits_tmap(const uint32_t* bits, int64_t side, int64_t rho, const CUtensorMap** out) {
+    const int hb = smx::tma_box_rows(int(rho));
+    return bits_tmap_box(bits, side, smx::tma_box_words(), hb, hb, out);
+}
 
 int ca_fused_step(const smx::Geom& k, int64_t wz0, int64_t wz1, const uint8_t* cur, uint8_t* next, cudaStream_t s) {
     smx::launch_ca_fused(k, int(wz0), int(wz1), cur, next, s);
@@ -393,17 +401,56 @@ int ca_fused_step(const smx::Geom& k, int64_t wz0, int64_t wz1, const uint8_t* c
     return SMX_OK;
 }
 
-// plan (map once -> chunk list) + persistent multi-step run, A -> B -> A ...
+// Which engine runs a launch_ca: the column engine for large states (map ->
+// tile bitmap; persistent z-marching columns), the chunk engine for small
+// ones (latency-bound: one short chunk per warp item). SMX_CA_ENGINE=chunks /
+// cols forces one (A/B measurement, tests).
+constexpr uint64_t kColsMinCells = 16ull << 20;
+bool use_cols(const smx::Geom& k) {
+    static const int forced = [] {
+        const char* e = std::getenv("SMX_CA_ENGINE");
+        if (!e) return 0;
+        if (!std::strcmp(e, "chunks")) return 1;
+        if (!std::strcmp(e, "cols")) return 2;
+        return 0;
+    }();
+    if (forced) return forced == 2;
+    return smx::tet_cells(k.side) >= kColsMinCells;
+}
+
+// the column engine's work items (host): for layer segments of lz layers,
+// every 8-row band iy and 8-word group g with cells; item order keeps
+// concurrently running warps on neighbouring columns (shared halo in L2)
+std::vector<int32_t> col_items(int64_t S, int64_t lz) {
+    std::vector<int32_t> v;
+    for (int64_t zs = 0; zs < S; zs += lz)
+        for (int64_t iy = 0; 8 * iy <= S - 1; ++iy) {
+            const int64_t y0 = 8 * iy, zmax = S - y0;
+            if (zs >= zmax) continue;
+            const int64_t z1 = std::min(zs + lz, zmax);
+            for (int64_t g = 0; 256 * g <= y0 + 7; ++g) v.insert(v.end(), {int32_t(iy), int32_t(g), int32_t(zs), int32_t(z1)});
+        }
+    return v;
+}
+
+struct EnginePlan {
+    bool cols = false;
+    void* chunks = nullptr;   // chunk engine: the chunk list
+    unsigned* ctl = nullptr;  // chunk engine: [0] count, [8] barrier; column engine: [0] barrier, [1 + s] item counters
+    void* items = nullptr;    // column engine
+    int nitems = 0;
+    uint32_t* bm = nullptr;
+    int D = 0, TW = 0;
+};
+
+// plan (map once -> chunk list, or -> tile bitmap + column items) + the
+// persistent multi-step run, A -> B -> A ...
 //
 // The plan depends on the grid only, so it is issued first, on a side stream
 // ordered after the caller's prior work: it runs concurrently with whatever
 // the caller stream does next (host staging, pack) until engine_run joins it.
-int engine_plan(const smx_grid* g, const smx::Geom& k, int64_t steps, cudaStream_t s, void** pch, unsigned** count) {
+int engine_plan(const smx_grid* g, const smx::Geom& k, int64_t steps, cudaStream_t s, EnginePlan* P) {
     if (steps > INT32_MAX) return fail(SMX_ERANGE, "launch_ca: steps must fit int32");
-    void* pctl;
-    if (int rc = pool_get(5, size_t(smx::ca_plan_capacity(k)) * 16, pch)) return rc;
-    if (int rc = pool_get(6, 64, &pctl)) return rc;
-    *count = (unsigned*)pctl;
     DeviceRes* r;
     if (int rc = device_res(&r)) return rc;
     if (!r->side) {
@@ -411,10 +458,42 @@ int engine_plan(const smx_grid* g, const smx::Geom& k, int64_t steps, cudaStream
         TRY(cudaEventCreateWithFlags(&r->ev_in, cudaEventDisableTiming));
         TRY(cudaEventCreateWithFlags(&r->ev_plan, cudaEventDisableTiming));
     }
+    P->cols = use_cols(k);
+    void* pctl;
+    const size_t ctl_bytes = P->cols ? std::max<size_t>(64, 4 * size_t(steps + 1)) : 64;
+    if (int rc = pool_get(6, ctl_bytes, &pctl)) return rc;
+    P->ctl = (unsigned*)pctl;
     TRY(cudaEventRecord(r->ev_in, s));
     TRY(cudaStreamWaitEvent(r->side, r->ev_in, 0));
-    TRY(cudaMemsetAsync(pctl, 0, 64, r->side));
-    smx::launch_ca_plan(k, g->kind, *pch, *count, r->side);
+    TRY(cudaMemsetAsync(pctl, 0, ctl_bytes, r->side));
+    if (!P->cols) {
+        if (int rc = pool_get(5, size_t(smx::ca_plan_capacity(k)) * 16, &P->chunks)) return rc;
+        smx::launch_ca_plan(k, g->kind, P->chunks, P->ctl, r->side);
+    } else {
+        P->D = int(k.side / k.rho);
+        P->TW = (P->D + 31) / 32;
+        const size_t bm_bytes = size_t(P->D) * size_t(P->D) * size_t(P->TW) * 4 + 16;
+        void* pbm;
+        if (int rc = pool_get(9, bm_bytes, &pbm)) return rc;
+        P->bm = (uint32_t*)pbm;
+        TRY(cudaMemsetAsync(pbm, 0, bm_bytes, r->side));
+        // the map, applied once: every emitted tile marked (stats: marked, duplicate)
+        smx::launch_cols_mark(k, g->kind, P->bm, P->D, P->TW, (unsigned*)((uint8_t*)pbm + bm_bytes - 16), r->side);
+        // items: layer segments long enough for few atomics, short enough for ~6 items per warp
+        const int64_t target = 6 * int64_t(smx::cols_warps());
+        int64_t lz = 64;
+        while (lz > 8 && int64_t(col_items(k.side, lz).size() / 4) < target) lz /= 2;
+        if (r->cols_key != std::make_pair(int64_t(k.side), lz)) {
+            const std::vector<int32_t> v = col_items(k.side, lz);
+            void* pit;
+            if (int rc = pool_get(8, v.size() * 4, &pit)) return rc;
+            TRY(cudaMemcpy(pit, v.data(), v.size() * 4, cudaMemcpyHostToDevice));
+            r->cols_key = {int64_t(k.side), lz};
+            r->cols_nitems = int(v.size() / 4);
+        }
+        P->items = r->pool[8];
+        P->nitems = r->cols_nitems;
+    }
     TRY(cudaGetLastError());
     TRY(cudaEventRecord(r->ev_plan, r->side));
     return SMX_OK;
@@ -429,14 +508,23 @@ std::mutex g_engine_mu;
 cudaEvent_t g_engine_done[smx::kMaxDevices] = {};
 
 // join the plan, then ONE persistent launch for all steps
-int engine_run(const smx::Geom& k, uint32_t* A, uint32_t* B, const CUtensorMap* ta, const CUtensorMap* tb,
-               int64_t steps, cudaStream_t s, void* pch, unsigned* count) {
+int engine_run(const smx::Geom& k, uint32_t* A, uint32_t* B, int64_t steps, cudaStream_t s, const EnginePlan& P) {
     DeviceRes* r;
     if (int rc = device_res(&r)) return rc;
     TRY(cudaStreamWaitEvent(s, r->ev_plan, 0));
     int dev = 0;
     TRY(cudaGetDevice(&dev));
     if (dev < 0 || dev >= smx::kMaxDevices) return fail(SMX_EINVAL, "device ordinal beyond the library's table");
+    const CUtensorMap *ta, *tb;
+    if (P.cols) {
+        if (int rc = bits_tmap_box(A, k.side, smx::cols_box_words(), smx::cols_box_rows(), smx::cols_box_layers(), &ta))
+            return rc;
+        if (int rc = bits_tmap_box(B, k.side, smx::cols_box_words(), smx::cols_box_rows(), smx::cols_box_layers(), &tb))
+            return rc;
+    } else {
+        if (int rc = bits_tmap(A, k.side, k.rho, &ta)) return rc;
+        if (int rc = bits_tmap(B, k.side, k.rho, &tb)) return rc;
+    }
     std::lock_guard<std::mutex> lk(g_engine_mu);
     cudaEvent_t& done = g_engine_done[dev];
     if (!done) {
@@ -444,18 +532,19 @@ int engine_run(const smx::Geom& k, uint32_t* A, uint32_t* B, const CUtensorMap* 
     } else {
         TRY(cudaStreamWaitEvent(s, done, 0));
     }
-    TRY(smx::launch_ca_bits_run(k, ta, tb, A, B, pch, count, int(steps), s));
+    if (P.cols)
+        TRY(smx::launch_cols_run(k, ta, tb, A, B, P.items, P.nitems, P.ctl, P.bm, P.D, P.TW, int(steps), s));
+    else
+        TRY(smx::launch_ca_bits_run(k, ta, tb, A, B, P.chunks, P.ctl, int(steps), s));
     TRY(cudaEventRecord(done, s));
     return SMX_OK;
 }
 
-int bits_engine(const smx_grid* g, const smx::Geom& k, uint32_t* A, uint32_t* B, const CUtensorMap* ta,
-                const CUtensorMap* tb, int64_t steps, cudaStream_t s) {
+int bits_engine(const smx_grid* g, const smx::Geom& k, uint32_t* A, uint32_t* B, int64_t steps, cudaStream_t s) {
     if (steps <= 0) return SMX_OK;
-    void* pch;
-    unsigned* count;
-    if (int rc = engine_plan(g, k, steps, s, &pch, &count)) return rc;
-    return engine_run(k, A, B, ta, tb, steps, s, pch, count);
+    EnginePlan P;
+    if (int rc = engine_plan(g, k, steps, s, &P)) return rc;
+    return engine_run(k, A, B, steps, s, P);
 }
 
 size_t bits_bytes(int64_t side) {
@@ -469,22 +558,20 @@ int ca_runs_step(const smx_grid* g, const smx::Geom& k, int64_t wz0, int64_t wz1
     void *pa, *pb;
     if (int rc = pool_get(3, bits_bytes(k.side), &pa)) return rc;
     if (int rc = pool_get(4, bits_bytes(k.side), &pb)) return rc;
-    const CUtensorMap *ta, *tb;
-    if (int rc = bits_tmap((const uint32_t*)pa, k.side, k.rho, &ta)) return rc;
     if (wz0 == 0 && wz1 == k.ez) {
         // the whole grid: the engine's plan (issued first, on the side stream,
         // concurrent with the pack) + one persistent launch of 1 step
-        void* plan;
-        unsigned* count;
-        if (int rc = engine_plan(g, k, 1, s, &plan, &count)) return rc;
+        EnginePlan plan;
+        if (int rc = engine_plan(g, k, 1, s, &plan)) return rc;
         smx::launch_pack_bits(k, cur, (uint32_t*)pa, s);
-        if (int rc = bits_tmap((const uint32_t*)pb, k.side, k.rho, &tb)) return rc;
-        if (int rc = engine_run(k, (uint32_t*)pa, (uint32_t*)pb, ta, tb, 1, s, plan, count)) return rc;
+        if (int rc = engine_run(k, (uint32_t*)pa, (uint32_t*)pb, 1, s, plan)) return rc;
     } else {
         // a wz sub-range: B is seeded from `next` so the unpack leaves next's
         // cells outside the range as they were (cells sharing a 32-cell word
         // with a range tile receive their correctly stepped value: the kernel
         // stores whole words computed from the full neighbourhood)
+        const CUtensorMap* ta;
+        if (int rc = bits_tmap((const uint32_t*)pa, k.side, k.rho, &ta)) return rc;
         smx::launch_pack_bits(k, cur, (uint32_t*)pa, s);
         smx::launch_pack_bits(k, next, (uint32_t*)pb, s);
         smx::launch_ca_bits(k, g->kind, int(wz0), int(wz1), ta, (uint32_t*)pb, s);
@@ -1365,10 +1452,9 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
     // bit-shadow engine: the plan (map -> chunk list) needs only the grid, so
     // it is issued first and overlaps the input staging and the pack
     const bool engine = g->dims == 3 && exec == SMX_EXEC_BITS && steps > 0;
-    void* plan = nullptr;
-    unsigned* plan_count = nullptr;
+    EnginePlan plan;
     if (engine)
-        if (int rc = engine_plan(g, k, steps, s, &plan, &plan_count)) return rc;
+        if (int rc = engine_plan(g, k, steps, s, &plan)) return rc;
     if (!device_ptr) {
         if (int rc = pool_get(1, ncells, &p)) return rc;
         a = (uint8_t*)p;
@@ -1399,13 +1485,10 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
         void *pa, *pb;
         if (int rc = pool_get(3, bits_bytes(k.side), &pa)) return rc;
         if (int rc = pool_get(4, bits_bytes(k.side), &pb)) return rc;
-        const CUtensorMap *ta, *tb;
-        if (int rc = bits_tmap((const uint32_t*)pa, k.side, k.rho, &ta)) return rc;
-        if (int rc = bits_tmap((const uint32_t*)pb, k.side, k.rho, &tb)) return rc;
-        // the map applied once (chunk list), then ONE persistent launch for all
-        // steps, A -> B -> A ..., and the final shadow unpacked in place
+        // the map applied once (chunk list / tile bitmap), then ONE persistent
+        // launch for all steps, A -> B -> A ..., the final shadow unpacked in place
         smx::launch_pack_bits(k, cur, (uint32_t*)pa, s);
-        if (int rc = engine_run(k, (uint32_t*)pa, (uint32_t*)pb, ta, tb, steps, s, plan, plan_count)) return rc;
+        if (int rc = engine_run(k, (uint32_t*)pa, (uint32_t*)pb, steps, s, plan)) return rc;
         smx::launch_unpack_bits(k, (steps & 1) ? (const uint32_t*)pb : (const uint32_t*)pa, cur, s);
     } else {
         for (int64_t st = 0; st < steps; ++st) {
@@ -1476,10 +1559,7 @@ int smx_bits_run(const smx_grid* g, uint32_t* bits_a, uint32_t* bits_b, int64_t 
     if (int rc = ca_validate(g, smx::tet_cells(k.side), &ex)) return rc;
     if (steps < 0) return fail(SMX_EINVAL, "bits_run: steps must be >= 0");
     if (bits_a == bits_b) return fail(SMX_EINVAL, "bits_run: the two shadows must not alias");
-    const CUtensorMap *ta, *tb;
-    if (int rc = bits_tmap(bits_a, k.side, k.rho, &ta)) return rc;
-    if (int rc = bits_tmap(bits_b, k.side, k.rho, &tb)) return rc;
-    return bits_engine(g, k, bits_a, bits_b, ta, tb, steps, (cudaStream_t)stream);
+    return bits_engine(g, k, bits_a, bits_b, steps, (cudaStream_t)stream);
 }
 
 uint64_t smx_bits_plan_capacity(const smx_grid* g) {
@@ -1788,7 +1868,7 @@ uint64_t smx_scratch_bytes(void) {
     uint64_t b = 0;
     for (auto& kv : g_res) {
         if (kv.first.second != std::this_thread::get_id()) continue;
-        for (int i = 0; i < 8; ++i) b += kv.second.pool_bytes[i];
+        for (int i = 0; i < 10; ++i) b += kv.second.pool_bytes[i];
     }
     return b;
 }

@@ -55,6 +55,18 @@ cudaError_t launch_ca_bits_list(const Geom& g, const void* tmIn, uint32_t* in, u
                                 const unsigned* count, cudaStream_t s);
 cudaError_t launch_ca_bits_run(const Geom& g, const void* tmA, const void* tmB, uint32_t* A, uint32_t* B,
                                const void* chunks, const unsigned* count, int steps, cudaStream_t s);
+// the column engine (large states): tile bitmap marked by the map, then a
+// persistent run over column items (int4 {iy, g, z0, z1}); ctl: [0] grid
+// barrier, [1 + s] step s's item counter, zeroed
+int cols_box_words();
+int cols_box_rows();
+int cols_box_layers();
+int cols_item_bytes();
+int cols_warps();
+void launch_cols_mark(const Geom& g, int kind, uint32_t* bm, int D, int TW, unsigned* stats, cudaStream_t s);
+cudaError_t launch_cols_run(const Geom& g, const void* tmA, const void* tmB, uint32_t* A, uint32_t* B,
+                            const void* items, int nitems, unsigned* ctl, const uint32_t* bm, int D, int TW, int steps,
+                            cudaStream_t s);
 // 2-simplex EDM (f64 points as x, y pairs) and periodic 2-D Life (smx_kernels2d.cu)
 void launch_edm(const Geom& g, const double* pts, double* cells, int exec, cudaStream_t s);
 void launch_ca2d(const Geom& g, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s);
