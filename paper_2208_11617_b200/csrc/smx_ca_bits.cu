@@ -710,17 +710,26 @@ __device__ __forceinline__ void cols_issue(const CUtensorMap* tm, const ColItem&
 // One step of the column engine for one warp: items grabbed from *ctr until
 // the list is exhausted. `seq` counts the TMA stages this warp has issued
 // (buffer = seq & 1, parity = (seq >> 1) & 1), carried across steps.
+//
+// Per input layer (box rows y0-1 .. y0+8, box words w0-4 .. w0+11):
+//   h-sums: 20 lanes, lane (row hr = lane >> 1, half hc = lane & 1) loads the
+//     aligned 16-byte chunk of x words w0 + 4 hc .. +3 and ONE edge word (w0-1
+//     or w0+8); the word across the middle comes from its partner lane by one
+//     shuffle; 4 horizontal 3-sums as two bit-planes -> shared memory
+//   vertical 3-sums: lane (ly = lane >> 2, words jp = 2 (lane & 3), +1), three
+//     16-byte loads, kept in registers for three layers
+//   rule + masked 8-byte store for the output layer one behind.
 template <int RHO>
 __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int nitems, unsigned* ctr,
                                           const CUtensorMap* tm, uint32_t* __restrict__ out,
                                           const uint32_t* __restrict__ bm, int D, int TW, int S, int WP,
                                           uint8_t* wbase, uint32_t mbar0, uint32_t& seq) {
     const int lane = threadIdx.x & 31;
-    uint2* hs = reinterpret_cast<uint2*>(wbase + 2 * CSTAGE);  // [CBR][CW]
-    // lane roles: h-sums: row hr = lane / 3 (0..9, lanes 0..29), words 3 (lane % 3) .. +2 (the
-    // third segment is words 6, 7); outputs: row ly = lane / 4, words 2 (lane % 4), +1
-    const int hr = lane / 3, hseg = lane % 3, hj0 = 3 * hseg, hjn = hseg == 2 ? 2 : 3;
-    const int ly = lane >> 2, jp = 2 * (lane & 3);
+    uint2* hs = reinterpret_cast<uint2*>(wbase + 2 * CSTAGE);  // [CBR][CW] (a, b) planes
+    const int hr = lane >> 1, hc = lane & 1;                   // h-sum role (lanes 0..19)
+    const bool hlane = lane < 2 * CBR;
+    const int ly = lane >> 2, jp = 2 * (lane & 3);             // output role
+    const long long zstride = (long long)S * WP;
     int cur = 0;
     if (lane == 0) cur = int(atomicAdd(ctr, 1u));
     cur = __shfl_sync(0xffffffffu, cur, 0);
@@ -733,12 +742,27 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
         int nxt = 0;
         if (lane == 0) nxt = int(atomicAdd(ctr, 1u));
         nxt = __shfl_sync(0xffffffffu, nxt, 0);
-        const int nin = it.z1 - it.z0 + 2;            // input layers z0 - 1 .. z1
+        const int nin = it.z1 - it.z0 + 2;  // input layers z0 - 1 .. z1
         const int nst = (nin + CLZ - 1) / CLZ;
         const int y0 = 8 * it.iy, w0 = 8 * it.g;
-        const int yo = y0 + ly;                       // this lane's output row
-        const int wo = w0 + jp;                       // and its first output word
-        const int hy = y0 - 1 + hr;                   // this lane's h-sum row
+        // h-sum role, per item: the row's layer limit and the x <= y masks of
+        // the 4 main words and the edge word (all zero for rows y < 0)
+        const int hy = y0 - 1 + hr;
+        const unsigned hzlim = unsigned(S - 1 - hy);  // input row is a cell row iff 0 <= zi <= S-1-hy
+        uint32_t M[4], Me;
+        {
+            const int xm = 32 * (w0 + 4 * hc), xe = hc ? 32 * (w0 + 8) : 32 * (w0 - 1);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) M[j] = __funnelshift_lc(0xffffffffu, 0u, max(hy - (xm + 32 * j) + 1, 0));
+            Me = __funnelshift_lc(0xffffffffu, 0u, max(hy - xe + 1, 0));
+        }
+        const int hoff = hr * CBW + 4 + 4 * hc;  // box word of the main chunk
+        const int eoff = hr * CBW + (hc ? 12 : 3);
+        // output role, per item
+        const int yo = y0 + ly, wo = w0 + jp;
+        const int ozlim = S - 1 - yo;  // output layer zo holds row yo iff zo <= S-1-yo
+        const int smode = 32 * (wo + 1) <= yo ? 2 : (32 * wo <= yo ? 1 : 0);
+        uint32_t* optr = out + ((long long)it.z0 * S + yo) * WP + wo;
         Planes4 va[2], vb[2];
         uint32_t alive_cur[2] = {0u, 0u};
         uint2 tmask = make_uint2(0u, 0u);
@@ -754,69 +778,79 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
             }
             while (!mbar_try_wait(mbar0 + 8 * b, (seq >> 1) & 1u)) {
             }
-            const uint8_t* buf = wbase + b * CSTAGE;
+            const uint32_t* buf = reinterpret_cast<const uint32_t*>(wbase + b * CSTAGE);
             const int nl = min(CLZ, nin - CLZ * st);
-            for (int li = 0; li < nl; ++li) {
-                const int zi = it.z0 - 1 + CLZ * st + li;     // input layer
-                const uint32_t* L = reinterpret_cast<const uint32_t*>(buf + li * CLAYER);
-                // ---- h-sums of layer zi: rows y0-1 .. y0+8, words w0 .. w0+7 ----
-                if (lane < 30) {
-                    const bool rowok = zi >= 0 && hy >= 0 && hy + zi <= S - 1;
-                    const uint32_t* R = L + hr * CBW + 3 + hj0;  // box word of x word w0 + hj0 - 1
-                    uint32_t T[5];
+            const int zbase = it.z0 - 1 + CLZ * st;
 #pragma unroll
-                    for (int j = 0; j < 5; ++j) T[j] = rowok ? R[j] : 0u;
-                    const int xb = 32 * (w0 + hj0 - 1);         // x of T[0] bit 0
-                    if (xb + 159 > hy) {
-#pragma unroll
-                        for (int j = 0; j < 5; ++j) T[j] &= __funnelshift_lc(0xffffffffu, 0u, max(hy - (xb + 32 * j) + 1, 0));
+            for (int li = 0; li < CLZ; ++li) {
+                if (li < nl) {
+                    const int zi = zbase + li;  // input layer
+                    const uint32_t* L = buf + li * (CLAYER / 4);
+                    // ---- h-sums ----
+                    uint4 m = make_uint4(0u, 0u, 0u, 0u);
+                    uint32_t e = 0u;
+                    if (hlane) {
+                        m = *reinterpret_cast<const uint4*>(L + hoff);
+                        e = L[eoff];
+                        const uint32_t rv = unsigned(zi) <= hzlim ? 0xffffffffu : 0u;
+                        m.x &= M[0] & rv;
+                        m.y &= M[1] & rv;
+                        m.z &= M[2] & rv;
+                        m.w &= M[3] & rv;
+                        e &= Me & rv;
                     }
+                    const uint32_t give = hc ? m.x : m.w;  // the partner's missing neighbour word
+                    const uint32_t got = __shfl_xor_sync(0xffffffffu, give, 1);
+                    if (hlane) {
+                        const uint32_t lw = hc ? got : e, rw = hc ? e : got;
+                        const uint32_t W[6] = {lw, m.x, m.y, m.z, m.w, rw};
+                        uint32_t ha[4], hb[4];
 #pragma unroll
-                    for (int j = 0; j < 3; ++j) {
-                        if (j < hjn) {
-                            const uint32_t c = T[j + 1];
-                            const uint32_t l = __funnelshift_l(T[j], c, 1);
-                            const uint32_t r = __funnelshift_r(c, T[j + 2], 1);
-                            hs[hr * CW + hj0 + j] = make_uint2(l ^ c ^ r, (l & c) | (l & r) | (c & r));
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t c = W[j + 1];
+                            const uint32_t l = __funnelshift_l(W[j], c, 1);
+                            const uint32_t r = __funnelshift_r(c, W[j + 2], 1);
+                            ha[j] = l ^ c ^ r;
+                            hb[j] = (l & c) | (l & r) | (c & r);
                         }
+                        uint4* dst = reinterpret_cast<uint4*>(hs + hr * CW + 4 * hc);
+                        dst[0] = make_uint4(ha[0], hb[0], ha[1], hb[1]);
+                        dst[1] = make_uint4(ha[2], hb[2], ha[3], hb[3]);
                     }
-                }
-                // the centre words of this layer: the next output layer's alive bits
-                uint32_t alive_next[2];
-                {
-                    const uint2 a = *reinterpret_cast<const uint2*>(L + (ly + 1) * CBW + 4 + jp);
-                    alive_next[0] = a.x;
-                    alive_next[1] = a.y;
-                }
-                __syncwarp();
-                // ---- vertical sums of layer zi for this lane's two words ----
-                Planes4 vc[2];
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    const uint2 p = hs[ly * CW + jp + k], q = hs[(ly + 1) * CW + jp + k], u = hs[(ly + 2) * CW + jp + k];
-                    vc[k] = add3x2(p.x, p.y, q.x, q.y, u.x, u.y);
-                }
-                const int zo = zi - 1;                        // output layer
-                if (zo >= it.z0) {
-                    if ((zo / RHO) != tz_cur) {
-                        tz_cur = zo / RHO;
-                        tmask = tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, tz_cur);
+                    // the centre words of this layer: the next output layer's alive bits
+                    const uint2 an = *reinterpret_cast<const uint2*>(L + (ly + 1) * CBW + 4 + jp);
+                    __syncwarp();
+                    // ---- vertical sums of layer zi for this lane's two words ----
+                    Planes4 vc[2];
+                    {
+                        const uint4 p = *reinterpret_cast<const uint4*>(hs + ly * CW + jp);
+                        const uint4 q = *reinterpret_cast<const uint4*>(hs + (ly + 1) * CW + jp);
+                        const uint4 u = *reinterpret_cast<const uint4*>(hs + (ly + 2) * CW + jp);
+                        vc[0] = add3x2(p.x, p.y, q.x, q.y, u.x, u.y);
+                        vc[1] = add3x2(p.z, p.w, q.z, q.w, u.z, u.w);
                     }
-                    const uint32_t o0 = life_planes(va[0], vb[0], vc[0], alive_cur[0]) & tmask.x;
-                    const uint32_t o1 = life_planes(va[1], vb[1], vc[1], alive_cur[1]) & tmask.y;
-                    if (yo + zo <= S - 1) {
-                        uint32_t* op = out + ((long long)zo * S + yo) * WP + wo;
-                        if (32 * (wo + 1) <= yo) *reinterpret_cast<uint2*>(op) = make_uint2(o0, o1);
-                        else if (32 * wo <= yo) *op = o0;
+                    const int zo = zi - 1;  // output layer
+                    if (zo >= it.z0) {
+                        if (zo / RHO != tz_cur) {
+                            tz_cur = zo / RHO;
+                            tmask = tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, tz_cur);
+                        }
+                        const uint32_t o0 = life_planes(va[0], vb[0], vc[0], alive_cur[0]) & tmask.x;
+                        const uint32_t o1 = life_planes(va[1], vb[1], vc[1], alive_cur[1]) & tmask.y;
+                        if (zo <= ozlim) {
+                            if (smode == 2) *reinterpret_cast<uint2*>(optr) = make_uint2(o0, o1);
+                            else if (smode == 1) *optr = o0;
+                        }
+                        optr += zstride;
                     }
+                    va[0] = vb[0];
+                    va[1] = vb[1];
+                    vb[0] = vc[0];
+                    vb[1] = vc[1];
+                    alive_cur[0] = an.x;
+                    alive_cur[1] = an.y;
+                    __syncwarp();
                 }
-                va[0] = vb[0];
-                va[1] = vb[1];
-                vb[0] = vc[0];
-                vb[1] = vc[1];
-                alive_cur[0] = alive_next[0];
-                alive_cur[1] = alive_next[1];
-                __syncwarp();
             }
             ++seq;
         }
