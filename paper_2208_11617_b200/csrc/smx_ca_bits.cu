@@ -643,7 +643,7 @@ constexpr int CBR = CR + 2;              // box rows: y0 - 1 .. y0 + 8
 constexpr int CLZ = 8;                   // layers per TMA stage
 constexpr int CSTAGE = CBW * CBR * CLZ * 4;  // 5120 B
 constexpr int CLAYER = CBW * CBR * 4;        // 640 B per layer of a stage
-constexpr int CHS = CBR * CW * 8;            // h-sums of one layer: [10 rows][8 words][a, b]
+constexpr int CHS = 2 * CBR * CW * 8;        // h-sums of two layers: [parity][10 rows][8 words][a, b]
 constexpr int CWARP_BYTES = 2 * CSTAGE + CHS + 64;  // 10944 (128-aligned: 10944 = 85.5 * 128 -> pad)
 constexpr int CWARP = (CWARP_BYTES + 127) & ~127;
 constexpr int CNW = 16;                  // warps per CTA (persistent: one CTA per SM)
@@ -724,11 +724,12 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
                                           const CUtensorMap* tm, uint32_t* __restrict__ out,
                                           const uint32_t* __restrict__ bm, int D, int TW, int S, int WP,
                                           uint8_t* wbase, uint32_t mbar0, uint32_t& seq) {
+    static_assert(CLZ == 8 && (RHO == 8 || RHO == 4), "stage = 8 layers; tiles of 8 or 4 layers");
     const int lane = threadIdx.x & 31;
-    uint2* hs = reinterpret_cast<uint2*>(wbase + 2 * CSTAGE);  // [CBR][CW] (a, b) planes
-    const int hr = lane >> 1, hc = lane & 1;                   // h-sum role (lanes 0..19)
+    uint2* hsb = reinterpret_cast<uint2*>(wbase + 2 * CSTAGE);  // 2 x [CBR][CW] (a, b), by layer parity
+    const int hr = min(lane >> 1, CBR - 1), hc = lane & 1;      // h-sum role (lanes 0..19; 20..31 mirror row 9)
     const bool hlane = lane < 2 * CBR;
-    const int ly = lane >> 2, jp = 2 * (lane & 3);             // output role
+    const int ly = lane >> 2, jp = 2 * (lane & 3);              // output role
     const long long zstride = (long long)S * WP;
     int cur = 0;
     if (lane == 0) cur = int(atomicAdd(ctr, 1u));
@@ -742,31 +743,34 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
         int nxt = 0;
         if (lane == 0) nxt = int(atomicAdd(ctr, 1u));
         nxt = __shfl_sync(0xffffffffu, nxt, 0);
-        const int nin = it.z1 - it.z0 + 2;  // input layers z0 - 1 .. z1
-        const int nst = (nin + CLZ - 1) / CLZ;
+        // input layers z0 - 1 .. z1 in whole stages (z0 is a multiple of 8;
+        // the layers past z1 of the last stage are computed, never stored)
+        const int nst = (it.z1 - it.z0 + 2 + CLZ - 1) / CLZ;
         const int y0 = 8 * it.iy, w0 = 8 * it.g;
         // h-sum role, per item: the row's layer limit and the x <= y masks of
-        // the 4 main words and the edge word (all zero for rows y < 0)
+        // the 4 main words and the edge word
         const int hy = y0 - 1 + hr;
         const unsigned hzlim = unsigned(S - 1 - hy);  // input row is a cell row iff 0 <= zi <= S-1-hy
-        uint32_t M[4], Me;
+        uint32_t M0, M1, M2, M3, Me;
         {
             const int xm = 32 * (w0 + 4 * hc), xe = hc ? 32 * (w0 + 8) : 32 * (w0 - 1);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) M[j] = __funnelshift_lc(0xffffffffu, 0u, max(hy - (xm + 32 * j) + 1, 0));
+            M0 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm + 1, 0));
+            M1 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm - 31, 0));
+            M2 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm - 63, 0));
+            M3 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm - 95, 0));
             Me = __funnelshift_lc(0xffffffffu, 0u, max(hy - xe + 1, 0));
         }
         const int hoff = hr * CBW + 4 + 4 * hc;  // box word of the main chunk
         const int eoff = hr * CBW + (hc ? 12 : 3);
+        uint2* hsw = hsb + hr * CW + 4 * hc;      // this lane's h-sum slots (parity 0)
         // output role, per item
         const int yo = y0 + ly, wo = w0 + jp;
-        const int ozlim = S - 1 - yo;  // output layer zo holds row yo iff zo <= S-1-yo
+        const int ozlim = min(S - 1 - yo, it.z1 - 1);  // stored layers: z0 <= zo <= ozlim
         const int smode = 32 * (wo + 1) <= yo ? 2 : (32 * wo <= yo ? 1 : 0);
-        uint32_t* optr = out + ((long long)it.z0 * S + yo) * WP + wo;
-        Planes4 va[2], vb[2];
-        uint32_t alive_cur[2] = {0u, 0u};
-        uint2 tmask = make_uint2(0u, 0u);
-        int tz_cur = -1;
+        uint32_t* optr = out + ((long long)(it.z0 - 2) * S + yo) * WP + wo;  // output layer of input layer z0 - 1
+        Sat3 va[2], vb[2];
+        uint32_t alive_cur0 = 0u, alive_cur1 = 0u;
+        uint2 mprev = make_uint2(0u, 0u);
         for (int st = 0; st < nst; ++st) {
             const uint32_t b = seq & 1;
             // the other buffer is free (its stage was consumed): prefetch the
@@ -776,82 +780,73 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
                 if (st + 1 < nst) cols_issue(tm, it, st + 1, wbase + (b ^ 1) * CSTAGE, mbar0 + 8 * (b ^ 1));
                 else if (nxt < nitems) cols_issue(tm, items[nxt], 0, wbase + (b ^ 1) * CSTAGE, mbar0 + 8 * (b ^ 1));
             }
+            // output layers of this stage: z0 - 2 + 8 st + li; their tile masks
+            const int zt = it.z0 + CLZ * st;  // layer of li = 2 (a multiple of 8)
+            const uint2 m0 = tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, zt / RHO);
+            const uint2 m1 = RHO == 4 ? tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, zt / RHO + 1) : m0;
             while (!mbar_try_wait(mbar0 + 8 * b, (seq >> 1) & 1u)) {
             }
             const uint32_t* buf = reinterpret_cast<const uint32_t*>(wbase + b * CSTAGE);
-            const int nl = min(CLZ, nin - CLZ * st);
             const int zbase = it.z0 - 1 + CLZ * st;
 #pragma unroll
             for (int li = 0; li < CLZ; ++li) {
-                if (li < nl) {
-                    const int zi = zbase + li;  // input layer
-                    const uint32_t* L = buf + li * (CLAYER / 4);
-                    // ---- h-sums ----
-                    uint4 m = make_uint4(0u, 0u, 0u, 0u);
-                    uint32_t e = 0u;
+                const int zi = zbase + li;  // input layer
+                const uint32_t* L = buf + li * (CLAYER / 4);
+                uint2* hs = hsb + (li & 1) * (CBR * CW);
+                // ---- h-sums ----
+                uint4 m = *reinterpret_cast<const uint4*>(L + hoff);
+                uint32_t e = L[eoff];
+                const uint32_t rv = 0u - uint32_t(unsigned(zi) <= hzlim);  // all ones iff a cell row
+                m.x &= M0 & rv;  // one 3-input AND each
+                m.y &= M1 & rv;
+                m.z &= M2 & rv;
+                m.w &= M3 & rv;
+                e &= Me & rv;
+                const uint32_t got = __shfl_xor_sync(0xffffffffu, hc ? m.x : m.w, 1);  // partner's word
+                {
+                    const uint32_t W0 = hc ? got : e, W5 = hc ? e : got;
+                    const uint32_t l0 = __funnelshift_l(W0, m.x, 1), r0 = __funnelshift_r(m.x, m.y, 1);
+                    const uint32_t l1 = __funnelshift_l(m.x, m.y, 1), r1 = __funnelshift_r(m.y, m.z, 1);
+                    const uint32_t l2 = __funnelshift_l(m.y, m.z, 1), r2 = __funnelshift_r(m.z, m.w, 1);
+                    const uint32_t l3 = __funnelshift_l(m.z, m.w, 1), r3 = __funnelshift_r(m.w, W5, 1);
                     if (hlane) {
-                        m = *reinterpret_cast<const uint4*>(L + hoff);
-                        e = L[eoff];
-                        const uint32_t rv = unsigned(zi) <= hzlim ? 0xffffffffu : 0u;
-                        m.x &= M[0] & rv;
-                        m.y &= M[1] & rv;
-                        m.z &= M[2] & rv;
-                        m.w &= M[3] & rv;
-                        e &= Me & rv;
+                        uint4* dst = reinterpret_cast<uint4*>(hsw + (li & 1) * (CBR * CW));
+                        dst[0] = make_uint4(l0 ^ m.x ^ r0, (l0 & m.x) | (l0 & r0) | (m.x & r0), l1 ^ m.y ^ r1,
+                                            (l1 & m.y) | (l1 & r1) | (m.y & r1));
+                        dst[1] = make_uint4(l2 ^ m.z ^ r2, (l2 & m.z) | (l2 & r2) | (m.z & r2), l3 ^ m.w ^ r3,
+                                            (l3 & m.w) | (l3 & r3) | (m.w & r3));
                     }
-                    const uint32_t give = hc ? m.x : m.w;  // the partner's missing neighbour word
-                    const uint32_t got = __shfl_xor_sync(0xffffffffu, give, 1);
-                    if (hlane) {
-                        const uint32_t lw = hc ? got : e, rw = hc ? e : got;
-                        const uint32_t W[6] = {lw, m.x, m.y, m.z, m.w, rw};
-                        uint32_t ha[4], hb[4];
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const uint32_t c = W[j + 1];
-                            const uint32_t l = __funnelshift_l(W[j], c, 1);
-                            const uint32_t r = __funnelshift_r(c, W[j + 2], 1);
-                            ha[j] = l ^ c ^ r;
-                            hb[j] = (l & c) | (l & r) | (c & r);
-                        }
-                        uint4* dst = reinterpret_cast<uint4*>(hs + hr * CW + 4 * hc);
-                        dst[0] = make_uint4(ha[0], hb[0], ha[1], hb[1]);
-                        dst[1] = make_uint4(ha[2], hb[2], ha[3], hb[3]);
-                    }
-                    // the centre words of this layer: the next output layer's alive bits
-                    const uint2 an = *reinterpret_cast<const uint2*>(L + (ly + 1) * CBW + 4 + jp);
-                    __syncwarp();
-                    // ---- vertical sums of layer zi for this lane's two words ----
-                    Planes4 vc[2];
-                    {
-                        const uint4 p = *reinterpret_cast<const uint4*>(hs + ly * CW + jp);
-                        const uint4 q = *reinterpret_cast<const uint4*>(hs + (ly + 1) * CW + jp);
-                        const uint4 u = *reinterpret_cast<const uint4*>(hs + (ly + 2) * CW + jp);
-                        vc[0] = add3x2(p.x, p.y, q.x, q.y, u.x, u.y);
-                        vc[1] = add3x2(p.z, p.w, q.z, q.w, u.z, u.w);
-                    }
-                    const int zo = zi - 1;  // output layer
-                    if (zo >= it.z0) {
-                        if (zo / RHO != tz_cur) {
-                            tz_cur = zo / RHO;
-                            tmask = tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, tz_cur);
-                        }
-                        const uint32_t o0 = life_planes(va[0], vb[0], vc[0], alive_cur[0]) & tmask.x;
-                        const uint32_t o1 = life_planes(va[1], vb[1], vc[1], alive_cur[1]) & tmask.y;
-                        if (zo <= ozlim) {
-                            if (smode == 2) *reinterpret_cast<uint2*>(optr) = make_uint2(o0, o1);
-                            else if (smode == 1) *optr = o0;
-                        }
-                        optr += zstride;
-                    }
-                    va[0] = vb[0];
-                    va[1] = vb[1];
-                    vb[0] = vc[0];
-                    vb[1] = vc[1];
-                    alive_cur[0] = an.x;
-                    alive_cur[1] = an.y;
-                    __syncwarp();
                 }
+                // the centre words of this layer: the next output layer's alive bits
+                const uint2 an = *reinterpret_cast<const uint2*>(L + (ly + 1) * CBW + 4 + jp);
+                __syncwarp();
+                // ---- vertical sums of layer zi for this lane's two words ----
+                Sat3 vc[2];
+                {
+                    const uint4 p = *reinterpret_cast<const uint4*>(hs + ly * CW + jp);
+                    const uint4 q = *reinterpret_cast<const uint4*>(hs + (ly + 1) * CW + jp);
+                    const uint4 u = *reinterpret_cast<const uint4*>(hs + (ly + 2) * CW + jp);
+                    vc[0] = sat3(add3x2(p.x, p.y, q.x, q.y, u.x, u.y));
+                    vc[1] = sat3(add3x2(p.z, p.w, q.z, q.w, u.z, u.w));
+                }
+                // ---- rule for output layer zo = zi - 1 (stored when z0 <= zo <= ozlim) ----
+                const uint2 tmk = li < 2 ? mprev : (RHO == 4 && li >= 6 ? m1 : m0);
+                const uint32_t o0 = life_sat(va[0], vb[0], vc[0], alive_cur0) & tmk.x;
+                const uint32_t o1 = life_sat(va[1], vb[1], vc[1], alive_cur1) & tmk.y;
+                const int zo = zi - 1;
+                if (zo >= it.z0 && zo <= ozlim) {
+                    if (smode == 2) *reinterpret_cast<uint2*>(optr) = make_uint2(o0, o1);
+                    else if (smode == 1) *optr = o0;
+                }
+                optr += zstride;
+                va[0] = vb[0];
+                va[1] = vb[1];
+                vb[0] = vc[0];
+                vb[1] = vc[1];
+                alive_cur0 = an.x;
+                alive_cur1 = an.y;
             }
+            mprev = RHO == 4 ? m1 : m0;
             ++seq;
         }
         cur = nxt;

@@ -81,6 +81,26 @@ __device__ __forceinline__ uint32_t life_planes(const Planes4& a, const Planes4&
     return (eq3 | (eq4 & alive)) & ~(r3 | r4);
 }
 
+// The column engine's rule on SATURATED vertical sums: a 9-cell sum v <= 9 is
+// kept as its low three bit-planes plus a flag for v >= 5 (computed once per
+// layer, used by three output layers). S = va + vb + vc is 3 or 4 only if no
+// term is >= 5, so the 27-sum needs three carry-save planes, one carry chain
+// of two bits and a kill flag (k3 | c3: S >= 8; any big term: S >= 5).
+struct Sat3 {
+    uint32_t b0, b1, b2, big;
+};
+__device__ __forceinline__ Sat3 sat3(const Planes4& v) { return Sat3{v.b0, v.b1, v.b2, v.b3 | (v.b2 & (v.b1 | v.b0))}; }
+__device__ __forceinline__ uint32_t life_sat(const Sat3& a, const Sat3& b, const Sat3& c, uint32_t alive) {
+    const uint32_t s0 = a.b0 ^ b.b0 ^ c.b0, k1 = (a.b0 & b.b0) | (a.b0 & c.b0) | (b.b0 & c.b0);
+    const uint32_t s1 = a.b1 ^ b.b1 ^ c.b1, k2 = (a.b1 & b.b1) | (a.b1 & c.b1) | (b.b1 & c.b1);
+    const uint32_t s2 = a.b2 ^ b.b2 ^ c.b2, k3 = (a.b2 & b.b2) | (a.b2 & c.b2) | (b.b2 & c.b2);
+    const uint32_t t1 = s1 ^ k1, c2 = s1 & k1;
+    const uint32_t t2 = s2 ^ k2 ^ c2, c3 = (s2 & k2) | (s2 & c2) | (k2 & c2);
+    const uint32_t kill = k3 | c3 | a.big | b.big | c.big;
+    const uint32_t eq3 = s0 & t1 & ~t2, eq4 = ~s0 & ~t1 & t2;  // S == 3, S == 4 (when not killed)
+    return (eq3 | (eq4 & alive)) & ~kill;
+}
+
 // ---- map-driven chunking ----
 
 // Phases 1-2 of both engines; every thread of the CTA must call it. The CTA
