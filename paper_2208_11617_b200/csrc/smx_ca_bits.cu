@@ -35,6 +35,7 @@
 // chunk. Bits for x > y of a row (not cells) are never trusted: every reader
 // masks them.
 #include <cooperative_groups.h>
+#include <type_traits>
 #include <cuda.h>
 
 #include "smx_ca_common.cuh"
@@ -719,6 +720,14 @@ __device__ __forceinline__ void cols_issue(const CUtensorMap* tm, const ColItem&
 //   vertical 3-sums: lane (ly = lane >> 2, words jp = 2 (lane & 3), +1), three
 //     16-byte loads, kept in registers for three layers
 //   rule + masked 8-byte store for the output layer one behind.
+// x << 1 | prev >> 31 and x >> 1 | next << 31 on the FMA pipe (IMAD / IMAD.HI):
+// the rule's carry-save logic saturates the ALU pipe (LOP3, rt 2 cycles per
+// SMSP), so the word shifts of the horizontal sums run beside it
+__device__ __forceinline__ uint32_t shl1_fma(uint32_t prev, uint32_t x) { return x * 2u + __umulhi(prev, 2u); }
+__device__ __forceinline__ uint32_t shr1_fma(uint32_t x, uint32_t next) {
+    return __umulhi(x, 0x80000000u) + next * 0x80000000u;
+}
+
 template <int RHO>
 __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int nitems, unsigned* ctr,
                                           const CUtensorMap* tm, uint32_t* __restrict__ out,
@@ -743,10 +752,16 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
         int nxt = 0;
         if (lane == 0) nxt = int(atomicAdd(ctr, 1u));
         nxt = __shfl_sync(0xffffffffu, nxt, 0);
-        // input layers z0 - 1 .. z1 in whole stages (z0 is a multiple of 8;
-        // the layers past z1 of the last stage are computed, never stored)
-        const int nst = (it.z1 - it.z0 + 2 + CLZ - 1) / CLZ;
+        // input layers z0 - 1 .. z1 (z0 is a multiple of 8): full stages of 8
+        // layers, then a tail stage of the rest
+        const int nin = it.z1 - it.z0 + 2;
+        const int nfull = nin / CLZ, tail = nin % CLZ;
+        const int nst = nfull + (tail ? 1 : 0);
         const int y0 = 8 * it.iy, w0 = 8 * it.g;
+        // interior items (warp-uniform): no cell of the box lies past the
+        // diagonal (x > y) or above the tetrahedron's face (y + z > S - 1), every
+        // output word is a full word of cells: no masking anywhere
+        const bool interior = y0 >= 32 * (w0 + 9) && y0 + 8 + it.z1 <= S - 1;
         // h-sum role, per item: the row's layer limit and the x <= y masks of
         // the 4 main words and the edge word
         const int hy = y0 - 1 + hr;
@@ -771,6 +786,66 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
         Sat3 va[2], vb[2];
         uint32_t alive_cur0 = 0u, alive_cur1 = 0u;
         uint2 mprev = make_uint2(0u, 0u);
+
+        // one input layer: h-sums -> vertical sums -> the rule for the layer behind
+        auto layer = [&](auto fast, const uint32_t* L, int li, int zi, const uint2& m0, const uint2& m1) {
+            constexpr bool FAST = decltype(fast)::value;
+            uint2* hs = hsb + (li & 1) * (CBR * CW);
+            uint4 m = *reinterpret_cast<const uint4*>(L + hoff);
+            uint32_t e = L[eoff];
+            if (!FAST) {
+                const uint32_t rv = 0u - uint32_t(unsigned(zi) <= hzlim);  // all ones iff a cell row
+                m.x &= M0 & rv;
+                m.y &= M1 & rv;
+                m.z &= M2 & rv;
+                m.w &= M3 & rv;
+                e &= Me & rv;
+            }
+            const uint32_t got = __shfl_xor_sync(0xffffffffu, hc ? m.x : m.w, 1);  // partner's word
+            {
+                const uint32_t W0 = hc ? got : e, W5 = hc ? e : got;
+                const uint32_t l0 = shl1_fma(W0, m.x), r0 = shr1_fma(m.x, m.y);
+                const uint32_t l1 = shl1_fma(m.x, m.y), r1 = shr1_fma(m.y, m.z);
+                const uint32_t l2 = shl1_fma(m.y, m.z), r2 = shr1_fma(m.z, m.w);
+                const uint32_t l3 = shl1_fma(m.z, m.w), r3 = shr1_fma(m.w, W5);
+                if (hlane) {
+                    uint4* dst = reinterpret_cast<uint4*>(hsw + (li & 1) * (CBR * CW));
+                    dst[0] = make_uint4(l0 ^ m.x ^ r0, (l0 & m.x) | (l0 & r0) | (m.x & r0), l1 ^ m.y ^ r1,
+                                        (l1 & m.y) | (l1 & r1) | (m.y & r1));
+                    dst[1] = make_uint4(l2 ^ m.z ^ r2, (l2 & m.z) | (l2 & r2) | (m.z & r2), l3 ^ m.w ^ r3,
+                                        (l3 & m.w) | (l3 & r3) | (m.w & r3));
+                }
+            }
+            const uint2 an = *reinterpret_cast<const uint2*>(L + (ly + 1) * CBW + 4 + jp);
+            __syncwarp();
+            Sat3 vc[2];
+            {
+                const uint4 p = *reinterpret_cast<const uint4*>(hs + ly * CW + jp);
+                const uint4 q = *reinterpret_cast<const uint4*>(hs + (ly + 1) * CW + jp);
+                const uint4 u = *reinterpret_cast<const uint4*>(hs + (ly + 2) * CW + jp);
+                vc[0] = sat3(add3x2(p.x, p.y, q.x, q.y, u.x, u.y));
+                vc[1] = sat3(add3x2(p.z, p.w, q.z, q.w, u.z, u.w));
+            }
+            // the rule for output layer zo = zi - 1 (stored when z0 <= zo <= ozlim)
+            const uint2 tmk = li < 2 ? mprev : (RHO == 4 && li >= 6 ? m1 : m0);
+            const uint32_t o0 = life_sat(va[0], vb[0], vc[0], alive_cur0) & tmk.x;
+            const uint32_t o1 = life_sat(va[1], vb[1], vc[1], alive_cur1) & tmk.y;
+            const int zo = zi - 1;
+            if (FAST) {
+                if (zo >= it.z0 && zo < it.z1) *reinterpret_cast<uint2*>(optr) = make_uint2(o0, o1);
+            } else if (zo >= it.z0 && zo <= ozlim) {
+                if (smode == 2) *reinterpret_cast<uint2*>(optr) = make_uint2(o0, o1);
+                else if (smode == 1) *optr = o0;
+            }
+            optr += zstride;
+            va[0] = vb[0];
+            va[1] = vb[1];
+            vb[0] = vc[0];
+            vb[1] = vc[1];
+            alive_cur0 = an.x;
+            alive_cur1 = an.y;
+        };
+
         for (int st = 0; st < nst; ++st) {
             const uint32_t b = seq & 1;
             // the other buffer is free (its stage was consumed): prefetch the
@@ -788,63 +863,20 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
             }
             const uint32_t* buf = reinterpret_cast<const uint32_t*>(wbase + b * CSTAGE);
             const int zbase = it.z0 - 1 + CLZ * st;
+            if (st < nfull) {
+                if (interior) {
 #pragma unroll
-            for (int li = 0; li < CLZ; ++li) {
-                const int zi = zbase + li;  // input layer
-                const uint32_t* L = buf + li * (CLAYER / 4);
-                uint2* hs = hsb + (li & 1) * (CBR * CW);
-                // ---- h-sums ----
-                uint4 m = *reinterpret_cast<const uint4*>(L + hoff);
-                uint32_t e = L[eoff];
-                const uint32_t rv = 0u - uint32_t(unsigned(zi) <= hzlim);  // all ones iff a cell row
-                m.x &= M0 & rv;  // one 3-input AND each
-                m.y &= M1 & rv;
-                m.z &= M2 & rv;
-                m.w &= M3 & rv;
-                e &= Me & rv;
-                const uint32_t got = __shfl_xor_sync(0xffffffffu, hc ? m.x : m.w, 1);  // partner's word
-                {
-                    const uint32_t W0 = hc ? got : e, W5 = hc ? e : got;
-                    const uint32_t l0 = __funnelshift_l(W0, m.x, 1), r0 = __funnelshift_r(m.x, m.y, 1);
-                    const uint32_t l1 = __funnelshift_l(m.x, m.y, 1), r1 = __funnelshift_r(m.y, m.z, 1);
-                    const uint32_t l2 = __funnelshift_l(m.y, m.z, 1), r2 = __funnelshift_r(m.z, m.w, 1);
-                    const uint32_t l3 = __funnelshift_l(m.z, m.w, 1), r3 = __funnelshift_r(m.w, W5, 1);
-                    if (hlane) {
-                        uint4* dst = reinterpret_cast<uint4*>(hsw + (li & 1) * (CBR * CW));
-                        dst[0] = make_uint4(l0 ^ m.x ^ r0, (l0 & m.x) | (l0 & r0) | (m.x & r0), l1 ^ m.y ^ r1,
-                                            (l1 & m.y) | (l1 & r1) | (m.y & r1));
-                        dst[1] = make_uint4(l2 ^ m.z ^ r2, (l2 & m.z) | (l2 & r2) | (m.z & r2), l3 ^ m.w ^ r3,
-                                            (l3 & m.w) | (l3 & r3) | (m.w & r3));
-                    }
+                    for (int li = 0; li < CLZ; ++li)
+                        layer(std::true_type{}, buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
+                } else {
+#pragma unroll
+                    for (int li = 0; li < CLZ; ++li)
+                        layer(std::false_type{}, buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
                 }
-                // the centre words of this layer: the next output layer's alive bits
-                const uint2 an = *reinterpret_cast<const uint2*>(L + (ly + 1) * CBW + 4 + jp);
-                __syncwarp();
-                // ---- vertical sums of layer zi for this lane's two words ----
-                Sat3 vc[2];
-                {
-                    const uint4 p = *reinterpret_cast<const uint4*>(hs + ly * CW + jp);
-                    const uint4 q = *reinterpret_cast<const uint4*>(hs + (ly + 1) * CW + jp);
-                    const uint4 u = *reinterpret_cast<const uint4*>(hs + (ly + 2) * CW + jp);
-                    vc[0] = sat3(add3x2(p.x, p.y, q.x, q.y, u.x, u.y));
-                    vc[1] = sat3(add3x2(p.z, p.w, q.z, q.w, u.z, u.w));
-                }
-                // ---- rule for output layer zo = zi - 1 (stored when z0 <= zo <= ozlim) ----
-                const uint2 tmk = li < 2 ? mprev : (RHO == 4 && li >= 6 ? m1 : m0);
-                const uint32_t o0 = life_sat(va[0], vb[0], vc[0], alive_cur0) & tmk.x;
-                const uint32_t o1 = life_sat(va[1], vb[1], vc[1], alive_cur1) & tmk.y;
-                const int zo = zi - 1;
-                if (zo >= it.z0 && zo <= ozlim) {
-                    if (smode == 2) *reinterpret_cast<uint2*>(optr) = make_uint2(o0, o1);
-                    else if (smode == 1) *optr = o0;
-                }
-                optr += zstride;
-                va[0] = vb[0];
-                va[1] = vb[1];
-                vb[0] = vc[0];
-                vb[1] = vc[1];
-                alive_cur0 = an.x;
-                alive_cur1 = an.y;
+            } else {
+#pragma unroll 1
+                for (int li = 0; li < tail; ++li)
+                    layer(std::false_type{}, buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
             }
             mprev = RHO == 4 ? m1 : m0;
             ++seq;
