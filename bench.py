@@ -537,7 +537,8 @@ def extra_configs(api, sampler, peak, args, energy):
         each final state hashed against the oracle golden), the dominant
         kernel's roofline, and single u8 -> u8 steps."""
         r = {"grid": f"h3d({n}) vs bb({n - 1}), rho={rho}", "ca_steps_per_call": ca_steps,
-             "l2": "flushed before every call"}
+             "l2": "flushed before every call",
+             "engine_kind": api.ca_engine(api.make_grid(api.map_kind.h3d, 3, n, rho))}
         h = engine_case(api, "h3d", n, rho, ca_steps, K if ca_steps * n <= 12800 else 3, 1, flush, key, golden)
         cells = h["cells"]
         r["cells"] = cells

@@ -248,6 +248,11 @@ int smx_bits_unpack(const smx_grid* g, const uint32_t* bits, uint8_t* cells, uin
  * bits_b -> bits_a ... (grid barrier between steps). The result is in bits_a
  * for even `steps`, bits_b for odd. Device pointers (smx_bits_bytes each). */
 int smx_bits_run(const smx_grid* g, uint32_t* bits_a, uint32_t* bits_b, int64_t steps, void* stream);
+/* Which engine smx_ca / smx_bits_run use for a 3-simplex grid: 0 = the chunk
+ * engine (the map -> chains of x-adjacent tiles; small states), 1 = the
+ * column engine (the map -> a tile bitmap; persistent z-marching columns of
+ * 8 rows x 256 cells; large states); -1 for other grids. */
+int smx_ca_engine(const smx_grid* g);
 
 /* The engine's two stages, exposed for a sharded caller (one rank's part of
  * launch_ca over blocks with wz in [wz_lo, wz_hi) — SURVEY 8(e)):

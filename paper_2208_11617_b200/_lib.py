@@ -81,6 +81,7 @@ _SIGS = {
     "smx_tiles_unpack": ([_G, _VP, _VP, C.c_uint64, _VP, _VP], C.c_int),
     "smx_device_sync": ([], C.c_int),
     "smx_release": ([], C.c_int),
+    "smx_ca_engine": ([_G], C.c_int),
     "smx_ca_multi": ([_G, _VP, C.c_uint64, C.c_int64, _VP, C.c_int32, C.c_int, _VP, _VP], C.c_int),
     "smx_bits_plan_capacity": ([_G], C.c_uint64),
     "smx_bits_plan": ([_G, C.c_int64, C.c_int64, _VP, _VP, _VP], C.c_int),

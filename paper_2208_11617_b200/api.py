@@ -701,6 +701,11 @@ def bits_run_device(g: grid_spec, bits_a, bits_b, steps: int) -> None:
     check(lib().smx_bits_run(C.byref(g.raw), _ptr(bits_a), _ptr(bits_b), steps, _stream()))
 
 
+def ca_engine(g: grid_spec) -> str:
+    """The multi-step CA engine smx_ca uses for this grid: "chunk" or "column"."""
+    return {0: "chunk", 1: "column"}.get(int(lib().smx_ca_engine(C.byref(g.raw))), "none")
+
+
 def bits_plan_capacity(g: grid_spec) -> int:
     return int(lib().smx_bits_plan_capacity(C.byref(g.raw)))
 

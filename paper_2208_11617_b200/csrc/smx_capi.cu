@@ -403,9 +403,12 @@ int ca_fused_step(const smx::Geom& k, int64_t wz0, int64_t wz1, const uint8_t* c
 
 // Which engine runs a launch_ca: the column engine for large states (map ->
 // tile bitmap; persistent z-marching columns), the chunk engine for small
-// ones (latency-bound: one short chunk per warp item). SMX_CA_ENGINE=chunks /
-// cols forces one (A/B measurement, tests).
-constexpr uint64_t kColsMinCells = 16ull << 20;
+// ones (latency-bound: one short chunk per warp item). Crossover measured on
+// B200 (tools/engine_ab.py, profiles/r2/engine_ab.txt): side 504-508 (21-22 M
+// cells) chunks 10.5 / 15.1 us per step vs columns 15.9 / 17.2; side 1016-1020
+// (175-177 M) columns 47.5 / 58.3 vs chunks 52.3 / 90.6; side 2040 columns 217
+// vs 384. SMX_CA_ENGINE=chunks / cols forces one (A/B measurement, tests).
+constexpr uint64_t kColsMinCells = 96ull << 20;
 bool use_cols(const smx::Geom& k) {
     static const int forced = [] {
         const char* e = std::getenv("SMX_CA_ENGINE");
@@ -1550,6 +1553,12 @@ int smx_bits_unpack(const smx_grid* g, const uint32_t* bits, uint8_t* cells, uin
     smx::launch_unpack_bits(k, bits, cells, (cudaStream_t)stream);
     TRY(cudaGetLastError());
     return SMX_OK;
+}
+
+int smx_ca_engine(const smx_grid* g) {
+    smx::Geom k;
+    if (!g || g->dims != 3 || make_geom(g, &k, false)) return -1;
+    return use_cols(k) ? 1 : 0;
 }
 
 int smx_bits_run(const smx_grid* g, uint32_t* bits_a, uint32_t* bits_b, int64_t steps, void* stream) {
