@@ -602,12 +602,14 @@ def accum_device(g: grid_spec, cells, passes: int = 1, exec: int = EXEC_RUNS) ->
 
 
 def accum_range_device(g: grid_spec, cells, passes: int, wy_lo: int, wy_hi: int,
-                       exec: int = EXEC_RUNS) -> dict:
+                       exec: int = EXEC_RUNS, counters: bool = True) -> dict | None:
     """ACCUM over grid rows [wy_lo, wy_hi) only (a multi-GPU shard, SURVEY 8(e));
-    returns that range's launch counters."""
+    returns that range's launch counters (counters=False: none, no sync)."""
     cnt = _lib.smx_counters()
     check(lib().smx_accum_range(C.byref(g.raw), _ptr(cells), cells.numel(), passes, exec, wy_lo, wy_hi,
-                                C.byref(cnt), _stream()))
+                                C.byref(cnt) if counters else None, _stream()))
+    if not counters:
+        return None
     return {"blocks_launched": int(cnt.blocks_launched), "blocks_void": int(cnt.blocks_void),
             "threads_launched": int(cnt.threads_launched), "threads_useful": int(cnt.threads_useful)}
 

@@ -132,8 +132,10 @@ def test_bench_sharded_smoke(cuda):
                          timeout=900)
     assert out.returncode == 0, out.stderr[-3000:]
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
-    assert line["n_gpus"] == 2 and line["value"] > 0 and "bit-shadow engine" in line["config"]["parallelism"]
-    assert line["parity"]["ok"] is True, line["parity"]
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["parity"]["all_cells_equal_passes_once"]
+    ca = line["ca_sharded"]["C4"]
+    assert "bit-shadow engine" in ca["parallelism"] and ca["value"] > 0
+    assert ca["parity"]["ok"] is True, ca["parity"]
 
 
 def _accum_worker(rank, world, port, kind, n, rho, passes, q):
