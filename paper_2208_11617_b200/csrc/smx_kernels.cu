@@ -5,6 +5,9 @@
 // Reference semantics: detail::sweep (simulator.hpp:177-218) — map -> Void ->
 // strict y-1 -> rho^m cells -> membership -> packed index -> body.
 #include "smx_common.cuh"
+#include <algorithm>
+#include <cstdlib>
+
 #include "smx_launch.hpp"
 #include "smx_runs.cuh"
 
@@ -239,16 +242,24 @@ __global__ void k_life_init(unsigned long long seed, uint8_t* __restrict__ cells
 // kernel_accum (simulator.hpp:329-331), the sequential reference's "one visit
 // per cell": no block map, every u32 of the packed state += 1. 16-byte vectors
 // over the 16-byte-aligned interior, scalar head / tail; grid-stride.
-__global__ void k_increment_all(uint32_t* __restrict__ cells, unsigned long long n) {
+__global__ void __launch_bounds__(256) k_increment_all(uint32_t* __restrict__ cells, unsigned long long n) {
     const unsigned long long head = ((16u - (reinterpret_cast<uintptr_t>(cells) & 15u)) & 15u) / 4u;
     const unsigned long long h = head < n ? head : n;
     const unsigned long long nvec = (n - h) / 4;
     uint4* v4 = reinterpret_cast<uint4*>(cells + h);
+    // 4 vectors per thread in flight (loads before stores)
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long v = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; v < nvec; v += stride) {
-        uint4 x = v4[v];
-        x.x += 1u, x.y += 1u, x.z += 1u, x.w += 1u;
-        v4[v] = x;
+    for (unsigned long long v = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; v < nvec; v += 4 * stride) {
+        uint4 x[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (v + k * stride < nvec) x[k] = v4[v + k * stride];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (v + k * stride < nvec) {
+                x[k].x += 1u, x[k].y += 1u, x[k].z += 1u, x[k].w += 1u;
+                v4[v + k * stride] = x[k];
+            }
     }
     if (blockIdx.x == 0 && threadIdx.x < 8) {
         const unsigned long long t = threadIdx.x;
@@ -424,6 +435,9 @@ static void launch_accum_k(const Geom& g, uint32_t* cells, int exec, cudaStream_
     // 32 blocks per CTA strip, 2 rows x 4 vectors in flight per lane, 4 CTAs
     // per SM (<= 64 registers): C3 at 0.85 of the HBM peak
     // (profiles/r1/accum_sweep.txt; 3 CTAs: 0.78, 5 CTAs: spills, 0.60)
+    // (a warp-persistent variant — each warp maps and streams its own strips,
+    // no CTA barrier — measured slower on B200: C3 3.28 vs 3.04 ms, BB 3.86 vs
+    // 3.03 ms; tools/accum_ceiling.py)
     launch_runs_t<KIND, 32, 2, 4>(g, cells, s);
 }
 void launch_accum(const Geom& g, uint32_t* cells, int exec, cudaStream_t s) {
@@ -441,8 +455,8 @@ void launch_life_init(unsigned long long seed, uint8_t* cells, unsigned long lon
 void launch_increment(uint32_t* cells, unsigned long long n, cudaStream_t s) {
     if (n == 0) return;
     const int threads = 256;
-    unsigned long long blocks = (n / 4 + threads - 1) / threads;
-    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    unsigned long long blocks = (n / 16 + threads - 1) / threads;
+    if (blocks > 148ull * 8) blocks = 148ull * 8;
     if (blocks == 0) blocks = 1;
     k_increment_all<<<(unsigned)blocks, threads, 0, s>>>(cells, n);
 }

@@ -16,6 +16,8 @@ def t(fn, n=10):
 s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 res = {}
 res['accum_runs_ms'] = t(lambda: api.accum_device(g, a, 1, api.EXEC_RUNS))
+gb = api.make_grid(api.map_kind.bb, 2, 4095, 16)
+res['accum_runs_bb_ms'] = t(lambda: api.accum_device(gb, a, 1, api.EXEC_RUNS))
 res['kernel_accum_ms'] = t(lambda: _lib.check(L.smx_kernel_accum(C.c_void_p(a.data_ptr()), cells, 1, s)))
 b = torch.empty_like(a)
 res['torch_copy_ms'] = t(lambda: b.copy_(a))
