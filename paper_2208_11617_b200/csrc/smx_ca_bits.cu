@@ -650,12 +650,8 @@ constexpr int CWARP = (CWARP_BYTES + 127) & ~127;
 constexpr int CNW = 16;                  // warps per CTA (persistent: one CTA per SM; 18 with the 96-register cap: 234 vs 217 us per C5 step)
 
 struct ColItem {
-    // rows 8 iy .. 8 iy + 7, layers z0 .. z1 - 1; words 8 g .. 8 g + 7 (g >= 0),
-    // or a half item of words 4 h .. 4 h + 3 with g = -h - 1 (a band's last,
-    // partly filled group: 4 words computed instead of 8)
-    int iy, g, z0, z1;
+    int iy, g, z0, z1;  // rows 8 iy .. 8 iy + 7, words 8 g .. 8 g + 7, layers z0 .. z1 - 1
 };
-__device__ __forceinline__ int item_w0(const ColItem& it) { return it.g >= 0 ? 8 * it.g : 4 * (-it.g - 1); }
 
 template <int KIND>
 __global__ void __launch_bounds__(256) k_cols_mark(Geom g, uint32_t* __restrict__ bm, int D, int TW,
@@ -709,7 +705,7 @@ __device__ __forceinline__ uint2 tile_mask2(const uint32_t* __restrict__ bm, int
 __device__ __forceinline__ void cols_issue(const CUtensorMap* tm, const ColItem& it, int stage, uint8_t* buf,
                                            uint32_t mbar) {
     mbar_expect_tx(mbar, uint32_t(CSTAGE));
-    tma_load_3d(smem_u32(buf), tm, item_w0(it) - 4, 8 * it.iy - 1, it.z0 - 1 + CLZ * stage, mbar);
+    tma_load_3d(smem_u32(buf), tm, 8 * it.g - 4, 8 * it.iy - 1, it.z0 - 1 + CLZ * stage, mbar);
 }
 
 // One step of the column engine for one warp: items grabbed from *ctr until
@@ -732,187 +728,18 @@ __device__ __forceinline__ uint32_t shr1_fma(uint32_t x, uint32_t next) {
     return __umulhi(x, 0x80000000u) + next * 0x80000000u;
 }
 
-// One column item (CWT = 8 words, or 4 for a band's last partly filled
-// group). The warp's TMA stage sequence `seq` continues across items; the last
-// stage prefetches the next item's first stage (`nxt`).
-template <int RHO, int CWT>
-__device__ __forceinline__ void cols_item(const ColItem& it, const ColItem* __restrict__ items, int nxt, int nitems,
-                                          const CUtensorMap* tm, uint32_t* __restrict__ out,
-                                          const uint32_t* __restrict__ bm, int D, int TW, int S, int WP,
-                                          uint8_t* wbase, uint32_t mbar0, uint32_t& seq) {
-    static_assert(CLZ == 8 && (RHO == 8 || RHO == 4), "stage = 8 layers; tiles of 8 or 4 layers");
-    static_assert(CWT == 8 || CWT == 4, "items are 8 or 4 words wide");
-    constexpr int NWL = CWT / 4;  // output words per lane
-    const int lane = threadIdx.x & 31;
-    uint2* hsb = reinterpret_cast<uint2*>(wbase + 2 * CSTAGE);  // 2 x [CBR][CWT] (a, b), by layer parity
-    // h-sum role (lanes 0..19; 20..31 mirror row 9): row hr; CWT = 8: the half
-    // hc of the 8 words (4 h-sums), the neighbour across the middle from the
-    // partner lane; CWT = 4: 2 h-sums (words 2 hc, 2 hc + 1) from the same chunk
-    const int hr = min(lane >> 1, CBR - 1), hc = lane & 1;
-    const bool hlane = lane < 2 * CBR;
-    const int ly = lane >> 2, jp = NWL * (lane & 3);  // output role
-    const long long zstride = (long long)S * WP;
-    const int nin = it.z1 - it.z0 + 2;  // input layers z0 - 1 .. z1 (z0 is a multiple of 8)
-    const int nfull = nin / CLZ, tail = nin % CLZ;
-    const int nst = nfull + (tail ? 1 : 0);
-    const int y0 = 8 * it.iy, w0 = item_w0(it);
-    // interior items (warp-uniform): no cell of the box lies past the diagonal
-    // or above the tetrahedron's face; every output word is a full word of cells
-    const bool interior = y0 >= 32 * (w0 + CWT + 1) && y0 + 8 + it.z1 <= S - 1;
-    const int hy = y0 - 1 + hr;
-    const unsigned hzlim = unsigned(S - 1 - hy);  // input row is a cell row iff 0 <= zi <= S-1-hy
-    // x <= y masks: the chunk's 4 words (x words w0 + 4 hc .. for CWT 8, w0 .. for CWT 4) and the edge word
-    uint32_t M0, M1, M2, M3, Me;
-    {
-        const int xm = 32 * (w0 + (CWT == 8 ? 4 * hc : 0));
-        const int xe = CWT == 8 ? (hc ? 32 * (w0 + 8) : 32 * (w0 - 1)) : (hc ? 32 * (w0 + 4) : 32 * (w0 - 1));
-        M0 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm + 1, 0));
-        M1 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm - 31, 0));
-        M2 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm - 63, 0));
-        M3 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm - 95, 0));
-        Me = __funnelshift_lc(0xffffffffu, 0u, max(hy - xe + 1, 0));
-    }
-    const int hoff = hr * CBW + 4 + (CWT == 8 ? 4 * hc : 0);  // box word of the chunk
-    const int eoff = hr * CBW + (CWT == 8 ? (hc ? 12 : 3) : (hc ? 8 : 3));
-    uint2* hsw = hsb + hr * CWT + (CWT == 8 ? 4 * hc : 2 * hc);  // this lane's h-sum slots (parity 0)
-    // output role
-    const int yo = y0 + ly, wo = w0 + jp;
-    const int ozlim = min(S - 1 - yo, it.z1 - 1);  // stored layers: z0 <= zo <= ozlim
-    const int smode = NWL == 2 && 32 * (wo + 1) <= yo ? 2 : (32 * wo <= yo ? 1 : 0);
-    uint32_t* optr = out + ((long long)(it.z0 - 2) * S + yo) * WP + wo;  // output layer of input layer z0 - 1
-    Sat3 va[NWL], vb[NWL];
-    uint32_t alive_cur[NWL];
-#pragma unroll
-    for (int k = 0; k < NWL; ++k) alive_cur[k] = 0u;
-    uint2 mprev = make_uint2(0u, 0u);
-
-    // one input layer: h-sums -> vertical sums -> the rule for the layer behind
-    auto layer = [&](auto fast, const uint32_t* L, int li, int zi, const uint2& m0, const uint2& m1) {
-        constexpr bool FAST = decltype(fast)::value;
-        uint2* hs = hsb + (li & 1) * (CBR * CWT);
-        uint4 m = *reinterpret_cast<const uint4*>(L + hoff);
-        uint32_t e = L[eoff];
-        if (!FAST) {
-            const uint32_t rv = 0u - uint32_t(unsigned(zi) <= hzlim);  // all ones iff a cell row
-            m.x &= M0 & rv;
-            m.y &= M1 & rv;
-            m.z &= M2 & rv;
-            m.w &= M3 & rv;
-            e &= Me & rv;
-        }
-        if (CWT == 8) {
-            const uint32_t got = __shfl_xor_sync(0xffffffffu, hc ? m.x : m.w, 1);  // partner's word
-            const uint32_t W0 = hc ? got : e, W5 = hc ? e : got;
-            const uint32_t l0 = shl1_fma(W0, m.x), r0 = shr1_fma(m.x, m.y);
-            const uint32_t l1 = shl1_fma(m.x, m.y), r1 = shr1_fma(m.y, m.z);
-            const uint32_t l2 = shl1_fma(m.y, m.z), r2 = shr1_fma(m.z, m.w);
-            const uint32_t l3 = shl1_fma(m.z, m.w), r3 = shr1_fma(m.w, W5);
-            if (hlane) {
-                uint4* dst = reinterpret_cast<uint4*>(hsw + (li & 1) * (CBR * CWT));
-                dst[0] = make_uint4(l0 ^ m.x ^ r0, (l0 & m.x) | (l0 & r0) | (m.x & r0), l1 ^ m.y ^ r1,
-                                    (l1 & m.y) | (l1 & r1) | (m.y & r1));
-                dst[1] = make_uint4(l2 ^ m.z ^ r2, (l2 & m.z) | (l2 & r2) | (m.z & r2), l3 ^ m.w ^ r3,
-                                    (l3 & m.w) | (l3 & r3) | (m.w & r3));
-            }
-        } else {
-            // words (A, B) = (w0, w0+1) with neighbours (edge, w0+2), or
-            // (w0+2, w0+3) with neighbours (w0+1, edge)
-            const uint32_t P = hc ? m.y : e, A = hc ? m.z : m.x, B = hc ? m.w : m.y, Q = hc ? e : m.z;
-            const uint32_t l0 = shl1_fma(P, A), r0 = shr1_fma(A, B);
-            const uint32_t l1 = shl1_fma(A, B), r1 = shr1_fma(B, Q);
-            if (hlane) {
-                uint4* dst = reinterpret_cast<uint4*>(hsw + (li & 1) * (CBR * CWT));
-                dst[0] = make_uint4(l0 ^ A ^ r0, (l0 & A) | (l0 & r0) | (A & r0), l1 ^ B ^ r1,
-                                    (l1 & B) | (l1 & r1) | (B & r1));
-            }
-        }
-        uint32_t an[NWL];
-        if (NWL == 2) {
-            const uint2 a2 = *reinterpret_cast<const uint2*>(L + (ly + 1) * CBW + 4 + jp);
-            an[0] = a2.x;
-            an[NWL - 1] = a2.y;
-        } else {
-            an[0] = L[(ly + 1) * CBW + 4 + jp];
-        }
-        __syncwarp();
-        Sat3 vc[NWL];
-        if (NWL == 2) {
-            const uint4 p = *reinterpret_cast<const uint4*>(hs + ly * CWT + jp);
-            const uint4 q = *reinterpret_cast<const uint4*>(hs + (ly + 1) * CWT + jp);
-            const uint4 u = *reinterpret_cast<const uint4*>(hs + (ly + 2) * CWT + jp);
-            vc[0] = sat3(add3x2(p.x, p.y, q.x, q.y, u.x, u.y));
-            vc[NWL - 1] = sat3(add3x2(p.z, p.w, q.z, q.w, u.z, u.w));
-        } else {
-            const uint2 p = hs[ly * CWT + jp], q = hs[(ly + 1) * CWT + jp], u = hs[(ly + 2) * CWT + jp];
-            vc[0] = sat3(add3x2(p.x, p.y, q.x, q.y, u.x, u.y));
-        }
-        // the rule for output layer zo = zi - 1 (stored when z0 <= zo <= ozlim)
-        const uint2 tmk = li < 2 ? mprev : (RHO == 4 && li >= 6 ? m1 : m0);
-        uint32_t o[NWL];
-        o[0] = life_sat(va[0], vb[0], vc[0], alive_cur[0]) & tmk.x;
-        if (NWL == 2) o[NWL - 1] = life_sat(va[NWL - 1], vb[NWL - 1], vc[NWL - 1], alive_cur[NWL - 1]) & tmk.y;
-        const int zo = zi - 1;
-        if (FAST) {
-            if (zo >= it.z0 && zo < it.z1) {
-                if (NWL == 2) *reinterpret_cast<uint2*>(optr) = make_uint2(o[0], o[NWL - 1]);
-                else *optr = o[0];
-            }
-        } else if (zo >= it.z0 && zo <= ozlim) {
-            if (smode == 2) *reinterpret_cast<uint2*>(optr) = make_uint2(o[0], o[NWL - 1]);
-            else if (smode == 1) *optr = o[0];
-        }
-        optr += zstride;
-#pragma unroll
-        for (int k = 0; k < NWL; ++k) {
-            va[k] = vb[k];
-            vb[k] = vc[k];
-            alive_cur[k] = an[k];
-        }
-    };
-
-    for (int st = 0; st < nst; ++st) {
-        const uint32_t b = seq & 1;
-        // the other buffer is free (its stage was consumed): prefetch the
-        // next stage of this item, or the first stage of the next item
-        if (lane == 0) {
-            fence_proxy_async();
-            if (st + 1 < nst) cols_issue(tm, it, st + 1, wbase + (b ^ 1) * CSTAGE, mbar0 + 8 * (b ^ 1));
-            else if (nxt < nitems) cols_issue(tm, items[nxt], 0, wbase + (b ^ 1) * CSTAGE, mbar0 + 8 * (b ^ 1));
-        }
-        // output layers of this stage: z0 - 2 + 8 st + li; their tile masks
-        const int zt = it.z0 + CLZ * st;  // layer of li = 2 (a multiple of 8)
-        const uint2 m0 = tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, zt / RHO);
-        const uint2 m1 = RHO == 4 ? tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, zt / RHO + 1) : m0;
-        while (!mbar_try_wait(mbar0 + 8 * b, (seq >> 1) & 1u)) {
-        }
-        const uint32_t* buf = reinterpret_cast<const uint32_t*>(wbase + b * CSTAGE);
-        const int zbase = it.z0 - 1 + CLZ * st;
-        if (st < nfull) {
-            if (interior) {
-#pragma unroll
-                for (int li = 0; li < CLZ; ++li) layer(std::true_type{}, buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
-            } else {
-#pragma unroll
-                for (int li = 0; li < CLZ; ++li) layer(std::false_type{}, buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
-            }
-        } else {
-#pragma unroll 1
-            for (int li = 0; li < tail; ++li) layer(std::false_type{}, buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
-        }
-        mprev = RHO == 4 ? m1 : m0;
-        ++seq;
-    }
-}
-
-// One step of the column engine for one warp: items grabbed from *ctr until
-// the list is exhausted. `seq` counts the TMA stages this warp has issued
-// (buffer = seq & 1, parity = (seq >> 1) & 1), carried across steps.
 template <int RHO>
 __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int nitems, unsigned* ctr,
                                           const CUtensorMap* tm, uint32_t* __restrict__ out,
                                           const uint32_t* __restrict__ bm, int D, int TW, int S, int WP,
                                           uint8_t* wbase, uint32_t mbar0, uint32_t& seq) {
+    static_assert(CLZ == 8 && (RHO == 8 || RHO == 4), "stage = 8 layers; tiles of 8 or 4 layers");
     const int lane = threadIdx.x & 31;
+    uint2* hsb = reinterpret_cast<uint2*>(wbase + 2 * CSTAGE);  // 2 x [CBR][CW] (a, b), by layer parity
+    const int hr = min(lane >> 1, CBR - 1), hc = lane & 1;      // h-sum role (lanes 0..19; 20..31 mirror row 9)
+    const bool hlane = lane < 2 * CBR;
+    const int ly = lane >> 2, jp = 2 * (lane & 3);              // output role
+    const long long zstride = (long long)S * WP;
     int cur = 0;
     if (lane == 0) cur = int(atomicAdd(ctr, 1u));
     cur = __shfl_sync(0xffffffffu, cur, 0);
@@ -925,8 +752,135 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
         int nxt = 0;
         if (lane == 0) nxt = int(atomicAdd(ctr, 1u));
         nxt = __shfl_sync(0xffffffffu, nxt, 0);
-        if (it.g >= 0) cols_item<RHO, 8>(it, items, nxt, nitems, tm, out, bm, D, TW, S, WP, wbase, mbar0, seq);
-        else cols_item<RHO, 4>(it, items, nxt, nitems, tm, out, bm, D, TW, S, WP, wbase, mbar0, seq);
+        // input layers z0 - 1 .. z1 (z0 is a multiple of 8): full stages of 8
+        // layers, then a tail stage of the rest
+        const int nin = it.z1 - it.z0 + 2;
+        const int nfull = nin / CLZ, tail = nin % CLZ;
+        const int nst = nfull + (tail ? 1 : 0);
+        const int y0 = 8 * it.iy, w0 = 8 * it.g;
+        // interior items (warp-uniform): no cell of the box lies past the
+        // diagonal (x > y) or above the tetrahedron's face (y + z > S - 1), every
+        // output word is a full word of cells: no masking anywhere
+        const bool interior = y0 >= 32 * (w0 + 9) && y0 + 8 + it.z1 <= S - 1;
+        // h-sum role, per item: the row's layer limit and the x <= y masks of
+        // the 4 main words and the edge word
+        const int hy = y0 - 1 + hr;
+        const unsigned hzlim = unsigned(S - 1 - hy);  // input row is a cell row iff 0 <= zi <= S-1-hy
+        uint32_t M0, M1, M2, M3, Me;
+        {
+            const int xm = 32 * (w0 + 4 * hc), xe = hc ? 32 * (w0 + 8) : 32 * (w0 - 1);
+            M0 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm + 1, 0));
+            M1 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm - 31, 0));
+            M2 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm - 63, 0));
+            M3 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm - 95, 0));
+            Me = __funnelshift_lc(0xffffffffu, 0u, max(hy - xe + 1, 0));
+        }
+        const int hoff = hr * CBW + 4 + 4 * hc;  // box word of the main chunk
+        const int eoff = hr * CBW + (hc ? 12 : 3);
+        uint2* hsw = hsb + hr * CW + 4 * hc;      // this lane's h-sum slots (parity 0)
+        // output role, per item
+        const int yo = y0 + ly, wo = w0 + jp;
+        const int ozlim = min(S - 1 - yo, it.z1 - 1);  // stored layers: z0 <= zo <= ozlim
+        const int smode = 32 * (wo + 1) <= yo ? 2 : (32 * wo <= yo ? 1 : 0);
+        uint32_t* optr = out + ((long long)(it.z0 - 2) * S + yo) * WP + wo;  // output layer of input layer z0 - 1
+        Sat3 va[2], vb[2];
+        uint32_t alive_cur0 = 0u, alive_cur1 = 0u;
+        uint2 mprev = make_uint2(0u, 0u);
+
+        // one input layer: h-sums -> vertical sums -> the rule for the layer behind
+        auto layer = [&](auto fast, const uint32_t* L, int li, int zi, const uint2& m0, const uint2& m1) {
+            constexpr bool FAST = decltype(fast)::value;
+            uint2* hs = hsb + (li & 1) * (CBR * CW);
+            uint4 m = *reinterpret_cast<const uint4*>(L + hoff);
+            uint32_t e = L[eoff];
+            if (!FAST) {
+                const uint32_t rv = 0u - uint32_t(unsigned(zi) <= hzlim);  // all ones iff a cell row
+                m.x &= M0 & rv;
+                m.y &= M1 & rv;
+                m.z &= M2 & rv;
+                m.w &= M3 & rv;
+                e &= Me & rv;
+            }
+            const uint32_t got = __shfl_xor_sync(0xffffffffu, hc ? m.x : m.w, 1);  // partner's word
+            {
+                const uint32_t W0 = hc ? got : e, W5 = hc ? e : got;
+                const uint32_t l0 = shl1_fma(W0, m.x), r0 = shr1_fma(m.x, m.y);
+                const uint32_t l1 = shl1_fma(m.x, m.y), r1 = shr1_fma(m.y, m.z);
+                const uint32_t l2 = shl1_fma(m.y, m.z), r2 = shr1_fma(m.z, m.w);
+                const uint32_t l3 = shl1_fma(m.z, m.w), r3 = shr1_fma(m.w, W5);
+                if (hlane) {
+                    uint4* dst = reinterpret_cast<uint4*>(hsw + (li & 1) * (CBR * CW));
+                    dst[0] = make_uint4(l0 ^ m.x ^ r0, (l0 & m.x) | (l0 & r0) | (m.x & r0), l1 ^ m.y ^ r1,
+                                        (l1 & m.y) | (l1 & r1) | (m.y & r1));
+                    dst[1] = make_uint4(l2 ^ m.z ^ r2, (l2 & m.z) | (l2 & r2) | (m.z & r2), l3 ^ m.w ^ r3,
+                                        (l3 & m.w) | (l3 & r3) | (m.w & r3));
+                }
+            }
+            const uint2 an = *reinterpret_cast<const uint2*>(L + (ly + 1) * CBW + 4 + jp);
+            __syncwarp();
+            Sat3 vc[2];
+            {
+                const uint4 p = *reinterpret_cast<const uint4*>(hs + ly * CW + jp);
+                const uint4 q = *reinterpret_cast<const uint4*>(hs + (ly + 1) * CW + jp);
+                const uint4 u = *reinterpret_cast<const uint4*>(hs + (ly + 2) * CW + jp);
+                vc[0] = sat3(add3x2(p.x, p.y, q.x, q.y, u.x, u.y));
+                vc[1] = sat3(add3x2(p.z, p.w, q.z, q.w, u.z, u.w));
+            }
+            // the rule for output layer zo = zi - 1 (stored when z0 <= zo <= ozlim)
+            const uint2 tmk = li < 2 ? mprev : (RHO == 4 && li >= 6 ? m1 : m0);
+            const uint32_t o0 = life_sat(va[0], vb[0], vc[0], alive_cur0) & tmk.x;
+            const uint32_t o1 = life_sat(va[1], vb[1], vc[1], alive_cur1) & tmk.y;
+            const int zo = zi - 1;
+            if (FAST) {
+                if (zo >= it.z0 && zo < it.z1) *reinterpret_cast<uint2*>(optr) = make_uint2(o0, o1);
+            } else if (zo >= it.z0 && zo <= ozlim) {
+                if (smode == 2) *reinterpret_cast<uint2*>(optr) = make_uint2(o0, o1);
+                else if (smode == 1) *optr = o0;
+            }
+            optr += zstride;
+            va[0] = vb[0];
+            va[1] = vb[1];
+            vb[0] = vc[0];
+            vb[1] = vc[1];
+            alive_cur0 = an.x;
+            alive_cur1 = an.y;
+        };
+
+        for (int st = 0; st < nst; ++st) {
+            const uint32_t b = seq & 1;
+            // the other buffer is free (its stage was consumed): prefetch the
+            // next stage of this item, or the first stage of the next item
+            if (lane == 0) {
+                fence_proxy_async();
+                if (st + 1 < nst) cols_issue(tm, it, st + 1, wbase + (b ^ 1) * CSTAGE, mbar0 + 8 * (b ^ 1));
+                else if (nxt < nitems) cols_issue(tm, items[nxt], 0, wbase + (b ^ 1) * CSTAGE, mbar0 + 8 * (b ^ 1));
+            }
+            // output layers of this stage: z0 - 2 + 8 st + li; their tile masks
+            const int zt = it.z0 + CLZ * st;  // layer of li = 2 (a multiple of 8)
+            const uint2 m0 = tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, zt / RHO);
+            const uint2 m1 = RHO == 4 ? tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, zt / RHO + 1) : m0;
+            while (!mbar_try_wait(mbar0 + 8 * b, (seq >> 1) & 1u)) {
+            }
+            const uint32_t* buf = reinterpret_cast<const uint32_t*>(wbase + b * CSTAGE);
+            const int zbase = it.z0 - 1 + CLZ * st;
+            if (st < nfull) {
+                if (interior) {
+#pragma unroll
+                    for (int li = 0; li < CLZ; ++li)
+                        layer(std::true_type{}, buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
+                } else {
+#pragma unroll
+                    for (int li = 0; li < CLZ; ++li)
+                        layer(std::false_type{}, buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
+                }
+            } else {
+#pragma unroll 1
+                for (int li = 0; li < tail; ++li)
+                    layer(std::false_type{}, buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
+            }
+            mprev = RHO == 4 ? m1 : m0;
+            ++seq;
+        }
         cur = nxt;
     }
 }

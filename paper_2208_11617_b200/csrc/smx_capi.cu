@@ -422,10 +422,8 @@ bool use_cols(const smx::Geom& k) {
 }
 
 // the column engine's work items (host): for layer segments of lz layers,
-// every 8-row band iy and 8-word group g with cells (a band's last group is a
-// 4-word half item, g = -h - 1, when at most 4 of its words hold cells); item
-// order keeps concurrently running warps on neighbouring columns (shared halo
-// in L2)
+// every 8-row band iy and 8-word group g with cells; item order keeps
+// concurrently running warps on neighbouring columns (shared halo in L2)
 std::vector<int32_t> col_items(int64_t S, int64_t lz) {
     std::vector<int32_t> v;
     for (int64_t zs = 0; zs < S; zs += lz)
@@ -433,11 +431,7 @@ std::vector<int32_t> col_items(int64_t S, int64_t lz) {
             const int64_t y0 = 8 * iy, zmax = S - y0;
             if (zs >= zmax) continue;
             const int64_t z1 = std::min(zs + lz, zmax);
-            const int64_t words = std::min<int64_t>(y0 + 7, S - 1) / 32 + 1;  // words with cells in the band
-            const int64_t full = words / 8, rest = words % 8;
-            for (int64_t g = 0; g < full; ++g) v.insert(v.end(), {int32_t(iy), int32_t(g), int32_t(zs), int32_t(z1)});
-            if (rest > 4) v.insert(v.end(), {int32_t(iy), int32_t(full), int32_t(zs), int32_t(z1)});
-            else if (rest > 0) v.insert(v.end(), {int32_t(iy), int32_t(-2 * full - 1), int32_t(zs), int32_t(z1)});
+            for (int64_t g = 0; 256 * g <= y0 + 7; ++g) v.insert(v.end(), {int32_t(iy), int32_t(g), int32_t(zs), int32_t(z1)});
         }
     return v;
 }
