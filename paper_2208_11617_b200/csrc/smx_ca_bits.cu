@@ -863,19 +863,16 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
             }
             const uint32_t* buf = reinterpret_cast<const uint32_t*>(wbase + b * CSTAGE);
             const int zbase = it.z0 - 1 + CLZ * st;
-            if (st < nfull) {
-                if (interior) {
+            if (st < nfull && interior) {
 #pragma unroll
-                    for (int li = 0; li < CLZ; ++li)
-                        layer(std::true_type{}, buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
-                } else {
-#pragma unroll
-                    for (int li = 0; li < CLZ; ++li)
-                        layer(std::false_type{}, buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
-                }
+                for (int li = 0; li < CLZ; ++li)
+                    layer(std::true_type{}, buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
             } else {
+                // boundary items and tail stages: one rolled copy of the layer
+                // (the instruction cache holds the whole kernel)
+                const int nl = st < nfull ? CLZ : tail;
 #pragma unroll 1
-                for (int li = 0; li < tail; ++li)
+                for (int li = 0; li < nl; ++li)
                     layer(std::false_type{}, buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
             }
             mprev = RHO == 4 ? m1 : m0;
