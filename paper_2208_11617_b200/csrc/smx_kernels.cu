@@ -170,14 +170,35 @@ __device__ __forceinline__ void accum_rows(uint32_t* __restrict__ cells, const u
     }
 }
 
-template <int KIND, int KX, int RR, int NV>
+template <int KIND, int KX, int RR, int NV, int KS = 1>
 __global__ void __launch_bounds__(ACC_THREADS, 4) k_accum_runs(Geom g, uint32_t* __restrict__ cells) {
-    __shared__ int s_run[KX][3];
-    __shared__ int s_nruns;
+    // KS strips of KX blocks per CTA, mapped concurrently by warps 0 .. KS-1
+    __shared__ int s_run[KS * KX][3];
+    __shared__ int s_nrun[KS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp == 0) strip_runs<KIND, KX>(g, blockIdx.x * KX, g.wy0 + blockIdx.y, s_run, &s_nruns);
+    if (warp < KS)
+        strip_runs<KIND, KX>(g, (blockIdx.x * KS + warp) * KX, g.wy0 + blockIdx.y, s_run + warp * KX, &s_nrun[warp]);
     __syncthreads();
-    const int nruns = s_nruns;
+    // compact the strips' run tables (KS <= 4: a warp-0 pass)
+    int nruns = s_nrun[0];
+    if (KS > 1) {
+        __shared__ int s_total;
+        if (warp == 0) {
+            int off = s_nrun[0];
+            for (int k = 1; k < KS; ++k) {
+                const int n = s_nrun[k];  // <= KX = 32: one lane per run, uniform syncs
+                int a = 0, b = 0, c = 0;
+                if (lane < n) a = s_run[k * KX + lane][0], b = s_run[k * KX + lane][1], c = s_run[k * KX + lane][2];
+                __syncwarp();
+                if (lane < n) s_run[off + lane][0] = a, s_run[off + lane][1] = b, s_run[off + lane][2] = c;
+                __syncwarp();
+                off += n;
+            }
+            if (lane == 0) s_total = off;
+        }
+        __syncthreads();
+        nruns = s_total;
+    }
     const int rho = g.rho, S = g.side;
     const int rows = nruns * rho;
     constexpr int NW = ACC_THREADS / 32;
@@ -421,9 +442,9 @@ void launch_map_block(const Geom& g, uint32_t* cov, DevCounters* cnt, unsigned* 
     SMX_DISPATCH_KIND(g.kind, launch_map_block_k, g, 0, g.ez, cov, cnt, sink, s);
 }
 
-template <int KIND, int KX, int RR, int NV>
+template <int KIND, int KX, int RR, int NV, int KS = 1>
 static void launch_runs_t(const Geom& g, uint32_t* cells, cudaStream_t s) {
-    k_accum_runs<KIND, KX, RR, NV><<<dim3((g.ex + KX - 1) / KX, g.ey, 1), ACC_THREADS, 0, s>>>(g, cells);
+    k_accum_runs<KIND, KX, RR, NV, KS><<<dim3((g.ex + KX * KS - 1) / (KX * KS), g.ey, 1), ACC_THREADS, 0, s>>>(g, cells);
 }
 
 template <int KIND>
@@ -438,7 +459,13 @@ static void launch_accum_k(const Geom& g, uint32_t* cells, int exec, cudaStream_
     // (a warp-persistent variant — each warp maps and streams its own strips,
     // no CTA barrier — measured slower on B200: C3 3.28 vs 3.04 ms, BB 3.86 vs
     // 3.03 ms; tools/accum_ceiling.py)
-    launch_runs_t<KIND, 32, 2, 4>(g, cells, s);
+    // two 32-block strips per CTA (mapped concurrently by warps 0 and 1), one
+    // row per warp at a time with 4 x 16-byte vectors per lane: consecutive
+    // warps stream consecutive cell rows. Measured at C3 (tools/accum_ceiling.py,
+    // profiles/r2/accum_shapes.txt; GB/s H / BB): 1 strip, 2 rows x 4 vectors
+    // 5645 / 5686; 2 strips, 2 x 4: 6102 / 6261; 2 strips, 1 x 8: 6267 / 6503;
+    // 2 strips, 1 x 4: 6338 / 6596; 4 strips, 1 x 4: 6254 / 6444.
+    launch_runs_t<KIND, 32, 1, 4, 2>(g, cells, s);
 }
 void launch_accum(const Geom& g, uint32_t* cells, int exec, cudaStream_t s) {
     SMX_DISPATCH_KIND(g.kind, launch_accum_k, g, cells, exec, s);
