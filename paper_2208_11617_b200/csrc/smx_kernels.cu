@@ -175,30 +175,10 @@ __global__ void __launch_bounds__(ACC_THREADS, 4) k_accum_runs(Geom g, uint32_t*
     // KS strips of KX blocks per CTA, mapped concurrently by warps 0 .. KS-1
     __shared__ int s_run[KS * KX][3];
     __shared__ int s_nrun[KS];
+    __shared__ int s_total;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp < KS)
-        strip_runs<KIND, KX>(g, (blockIdx.x * KS + warp) * KX, g.wy0 + blockIdx.y, s_run + warp * KX, &s_nrun[warp]);
-    __syncthreads();
-    // compact the strips' run tables (KS <= 4: a warp-0 pass)
-    int nruns = s_nrun[0];
-    if (KS > 1) {
-        __shared__ int s_total;
-        if (warp == 0) {
-            int off = s_nrun[0];
-            for (int k = 1; k < KS; ++k) {
-                const int n = s_nrun[k];  // <= KX = 32: one lane per run, uniform syncs
-                int a = 0, b = 0, c = 0;
-                if (lane < n) a = s_run[k * KX + lane][0], b = s_run[k * KX + lane][1], c = s_run[k * KX + lane][2];
-                __syncwarp();
-                if (lane < n) s_run[off + lane][0] = a, s_run[off + lane][1] = b, s_run[off + lane][2] = c;
-                __syncwarp();
-                off += n;
-            }
-            if (lane == 0) s_total = off;
-        }
-        __syncthreads();
-        nruns = s_total;
-    }
+    strips_runs<KIND, KX, KS>(g, blockIdx.x, g.wy0 + blockIdx.y, s_run, s_nrun, &s_total);
+    const int nruns = s_total;
     const int rho = g.rho, S = g.side;
     const int rows = nruns * rho;
     constexpr int NW = ACC_THREADS / 32;

@@ -71,6 +71,9 @@ __global__ void k_edm_block(Geom g, const double2* __restrict__ pts, double* __r
         }
 }
 
+// (two strips per CTA with paired 16-byte stores measured slower here: 591 vs
+// 633 Gcells/s at C1; the write-only stream prefers one strip and lane-strided
+// 8-byte stores)
 template <int KIND>
 __global__ void __launch_bounds__(T2_THREADS) k_edm_runs(Geom g, const double2* __restrict__ pts,
                                                          double* __restrict__ cells) {

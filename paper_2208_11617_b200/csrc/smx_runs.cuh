@@ -48,6 +48,33 @@ __device__ __forceinline__ void strip_runs(const Geom& g, int x0, int wy, int (*
     if (lane == 0) *s_nruns = __popc(heads);
 }
 
+// KS strips of KX blocks (x0 = (xs * KS + k) * KX, k < KS) of grid row wy,
+// mapped concurrently by warps 0 .. KS-1, their run tables compacted into
+// s_run[0 .. *s_total). Every thread of the CTA must call it (it ends with a
+// __syncthreads). s_run holds KS * KX entries.
+template <int KIND, int KX, int KS>
+__device__ __forceinline__ void strips_runs(const Geom& g, int xs, int wy, int (*s_run)[3], int* s_nrun,
+                                            int* s_total) {
+    static_assert(KX <= 32, "one warp maps a strip");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp < KS) strip_runs<KIND, KX>(g, (xs * KS + warp) * KX, wy, s_run + warp * KX, &s_nrun[warp]);
+    __syncthreads();
+    if (warp == 0) {
+        int off = s_nrun[0];
+        for (int k = 1; k < KS; ++k) {
+            const int n = s_nrun[k];  // <= KX <= 32: one lane per run, uniform syncs
+            int a = 0, b = 0, c = 0;
+            if (lane < n) a = s_run[k * KX + lane][0], b = s_run[k * KX + lane][1], c = s_run[k * KX + lane][2];
+            __syncwarp();
+            if (lane < n) s_run[off + lane][0] = a, s_run[off + lane][1] = b, s_run[off + lane][2] = c;
+            __syncwarp();
+            off += n;
+        }
+        if (lane == 0) *s_total = off;
+    }
+    __syncthreads();
+}
+
 // Row r of a strip's runs (rho rows per run) -> the with-diagonal cell row cy
 // and its cell span [xlo, xhi) clipped to x <= y; false when empty.
 __device__ __forceinline__ bool run_row(const int (*s_run)[3], int rr, int rho, int S, int* cy, int* xlo,
