@@ -4,6 +4,8 @@
     python tools/prof_case.py accum h2d 4096 16 [runs|block] [iters]
     python tools/prof_case.py map h3d 256 1
     python tools/prof_case.py ca2d h2d 4096 16 [runs|block] [iters]
+    python tools/prof_case.py multi h3d 32 8 bits [iters]        (smx_ca_multi, 3 shards on one GPU)
+    SMX_CA_ENGINE=cols python tools/prof_case.py engine h3d 32 8 bits 2   (the column engine)
 """
 import os
 import statistics
@@ -21,7 +23,7 @@ def main():
     what, kind, n, rho = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4])
     ex = {"runs": api.EXEC_RUNS, "block": api.EXEC_BLOCK, "bits": api.EXEC_BITS}[sys.argv[5] if len(sys.argv) > 5 else "runs"]
     iters = int(sys.argv[6]) if len(sys.argv) > 6 else 5
-    m = 2 if what in ("accum", "ca2d") or (what == "map" and kind == "h2d") else 3
+    m = 2 if what in ("accum", "ca2d", "kaccum") or (what == "map" and kind == "h2d") else 3
     if what == "map" and kind == "bb" and len(sys.argv) > 7:
         m = int(sys.argv[7])
     g = api.make_grid(api.map_kind[kind], m, n, rho)
@@ -51,6 +53,16 @@ def main():
         bufs = [a, b]
         fn = lambda i: api.ca_step_device(g, bufs[i % 2], bufs[(i + 1) % 2], ex)  # noqa: E731
         cells_done = cells
+    elif what == "multi":  # smx_ca_multi, three shards on this device, 3 steps per call
+        cells = api.tet_cells(side)
+        a = torch.empty(cells + 256, dtype=torch.uint8, device="cuda")[:cells]
+        api.life_init_device(3, side, 42, a)
+        fn = lambda i: api.ca_multi(g, a, 3, [0, 0, 0])  # noqa: E731
+        cells_done = cells * 3
+    elif what == "kaccum":  # kernel_accum (no map) on a host state
+        st = api.simplex_grid_state(2, side)
+        fn = lambda i: api.kernel_accum(st)  # noqa: E731
+        cells_done = api.tri_cells(side)
     elif what == "accum":
         cells = api.tri_cells(side)
         a = torch.zeros(cells, dtype=torch.int32, device="cuda")
