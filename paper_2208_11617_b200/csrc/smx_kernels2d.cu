@@ -16,6 +16,8 @@
 // x-adjacent tiles into runs; EDM streams whole cell rows of the runs with
 // lane-consecutive 8-byte stores, Life cuts them into 32-cell bit-sliced items).
 #include "smx_common.cuh"
+#include <cstdlib>
+
 #include "smx_launch.hpp"
 #include "smx_ca_common.cuh"
 #include "smx_runs.cuh"
@@ -74,7 +76,7 @@ __global__ void k_edm_block(Geom g, const double2* __restrict__ pts, double* __r
 // (two strips per CTA with paired 16-byte stores measured slower here: 591 vs
 // 633 Gcells/s at C1; the write-only stream prefers one strip and lane-strided
 // 8-byte stores)
-template <int KIND>
+template <int KIND, int EDM_ILP>
 __global__ void __launch_bounds__(T2_THREADS) k_edm_runs(Geom g, const double2* __restrict__ pts,
                                                          double* __restrict__ cells) {
     __shared__ int s_run[T2_KX][3];
@@ -88,7 +90,21 @@ __global__ void __launch_bounds__(T2_THREADS) k_edm_runs(Geom g, const double2* 
         if (!run_row(s_run, rr, g.rho, g.side, &cy, &xlo, &xhi)) continue;
         const double2 py = pts[cy];
         double* row = cells + tri_idx(0, cy);
-        for (int x = xlo + lane; x < xhi; x += 32) row[x] = edm_dist(__ldg(pts + x), py);
+        if (EDM_ILP > 1) {
+            // EDM_ILP cells per lane in flight: the point loads of all of them
+            // issue before the first distance
+            int x = xlo + lane;
+            for (; x + 32 * (EDM_ILP - 1) < xhi; x += 32 * EDM_ILP) {
+                double2 p[EDM_ILP];
+#pragma unroll
+                for (int k = 0; k < EDM_ILP; ++k) p[k] = __ldg(pts + x + 32 * k);
+#pragma unroll
+                for (int k = 0; k < EDM_ILP; ++k) row[x + 32 * k] = edm_dist(p[k], py);
+            }
+            for (; x < xhi; x += 32) row[x] = edm_dist(__ldg(pts + x), py);
+        } else {
+            for (int x = xlo + lane; x < xhi; x += 32) row[x] = edm_dist(__ldg(pts + x), py);
+        }
     }
 }
 
@@ -297,7 +313,8 @@ template <int KIND>
 void launch_edm_k(const Geom& g, const double* pts, double* cells, int exec, cudaStream_t s) {
     const double2* p = reinterpret_cast<const double2*>(pts);
     if (exec == SMX_EXEC_BLOCK) k_edm_block<KIND><<<dim3(g.ex, g.ey, 1), block2(g), 0, s>>>(g, p, cells);
-    else k_edm_runs<KIND><<<dim3((g.ex + T2_KX - 1) / T2_KX, g.ey, 1), T2_THREADS, 0, s>>>(g, p, cells);
+    else  // 4 cells per lane in flight (measured at C1, profiles/r2/edm_ilp.txt: 611 / 634 / 658 Gcells/s for 1 / 2 / 4)
+        k_edm_runs<KIND, 4><<<dim3((g.ex + T2_KX - 1) / T2_KX, g.ey, 1), T2_THREADS, 0, s>>>(g, p, cells);
 }
 
 template <int KIND>
