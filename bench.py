@@ -603,6 +603,12 @@ def extra_configs(api, sampler, peak, args, energy):
                              "parity": c5r4["check"]}
     del c5r4
     torch.cuda.empty_cache()
+    c5r16 = engine_case(api, "h3d", 128, 16, 20, 3, 1, flush, "c5_rho16_20", golden)
+    out["C5_rho16_engine"] = {"grid": "h3d(128) rho=16", "side": c5r16["side"], "cells": c5r16["cells"],
+                              "h_gcell_steps_s": round(gcells(c5r16["cells"] * 20, statistics.mean(c5r16["ms"])), 2),
+                              "parity": c5r16["check"], "engine_kind": "column"}
+    del c5r16
+    torch.cuda.empty_cache()
     out["map_kernel_3d"] = map_pair(3, 256)
     out.update(next_rows(api, flush, peak, K))
     out["cpu_reference"] = cpu_reference_rows()

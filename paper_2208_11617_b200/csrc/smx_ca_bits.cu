@@ -690,7 +690,9 @@ __device__ __forceinline__ uint2 tile_mask2(const uint32_t* __restrict__ bm, int
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
         const uint32_t b = (bits >> (k * TPW)) & ((1u << TPW) - 1u);
-        if (RHO == 8) {
+        if (RHO == 16) {
+            m[k] = ((b & 1u) ? 0x0000ffffu : 0u) | ((b & 2u) ? 0xffff0000u : 0u);  // bit i -> half i
+        } else if (RHO == 8) {
             m[k] = ((b * 0x00204081u) & 0x01010101u) * 0xffu;  // bit i -> byte i
         } else {
             uint32_t v = 0;  // bit i -> nibble i
@@ -733,7 +735,10 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
                                           const CUtensorMap* tm, uint32_t* __restrict__ out,
                                           const uint32_t* __restrict__ bm, int D, int TW, int S, int WP,
                                           uint8_t* wbase, uint32_t mbar0, uint32_t& seq) {
-    static_assert(CLZ == 8 && (RHO == 8 || RHO == 4), "stage = 8 layers; tiles of 8 or 4 layers");
+    static_assert(CLZ == 8 && (RHO == 16 || RHO == 8 || RHO == 4), "stage = 8 layers; tiles of 16, 8 or 4 layers");
+    // the tile index of output layer z0 - 2 + 8 st + li: for RHO = 8 and 16 it
+    // changes only between li = 1 and 2 (z0 and the stage start are multiples
+    // of 8), for RHO = 4 also between li = 5 and 6
     const int lane = threadIdx.x & 31;
     uint2* hsb = reinterpret_cast<uint2*>(wbase + 2 * CSTAGE);  // 2 x [CBR][CW] (a, b), by layer parity
     const int hr = min(lane >> 1, CBR - 1), hc = lane & 1;      // h-sum role (lanes 0..19; 20..31 mirror row 9)
@@ -971,6 +976,7 @@ __global__ void k_bits_tiles_unpack(uint32_t* __restrict__ bits, int S, int WP, 
 }
 
 bool ca_runs_supported(int rho) { return rho == 4 || rho == 8; }
+bool cols_supported(int rho) { return rho == 4 || rho == 8 || rho == 16; }
 
 unsigned long long bits_tile_bytes(int rho) { return rho == 8 ? 64ull : 8ull; }
 
@@ -1092,6 +1098,7 @@ int cols_grid() {
     int local = 0;
     once_per_device(once, dev, [&] {
         const int smem = CNW * CWARP;
+        cudaFuncSetAttribute(k_cols_run<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(k_cols_run<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(k_cols_run<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 0, nsm = 148;
@@ -1113,7 +1120,8 @@ cudaError_t launch_cols_run(const Geom& g, const void* tmA, const void* tmB, uin
     const ColItem* it = reinterpret_cast<const ColItem*>(items);
     void* args[] = {const_cast<void*>(tmA), const_cast<void*>(tmB), &A, &B, &it, &nitems, &ctl,
                     const_cast<uint32_t**>(&bm), &D, &TW, &steps, &S, &WP};
-    const void* fn = g.rho == 8 ? (const void*)k_cols_run<8> : (const void*)k_cols_run<4>;
+    const void* fn = g.rho == 16 ? (const void*)k_cols_run<16>
+                     : g.rho == 8 ? (const void*)k_cols_run<8> : (const void*)k_cols_run<4>;
     if (steps == 1) return cudaLaunchKernel(fn, dim3(grid), dim3(CNW * 32), args, smem, s);
     return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(CNW * 32), args, smem, s);
 }

@@ -409,7 +409,7 @@ int ca_fused_step(const smx::Geom& k, int64_t wz0, int64_t wz1, const uint8_t* c
 // (175-177 M) columns 47.5 / 58.3 vs chunks 52.3 / 90.6; side 2040 columns 217
 // vs 384. SMX_CA_ENGINE=chunks / cols forces one (A/B measurement, tests).
 constexpr uint64_t kColsMinCells = 96ull << 20;
-bool use_cols(const smx::Geom& k) {
+int cols_forced() {
     static const int forced = [] {
         const char* e = std::getenv("SMX_CA_ENGINE");
         if (!e) return 0;
@@ -417,9 +417,15 @@ bool use_cols(const smx::Geom& k) {
         if (!std::strcmp(e, "cols")) return 2;
         return 0;
     }();
-    if (forced) return forced == 2;
-    return smx::tet_cells(k.side) >= kColsMinCells;
+    return forced;
 }
+bool use_cols_side(int64_t side, int64_t rho) {
+    if (rho == 16) return cols_forced() != 1 && smx::cols_supported(16) &&
+                          (cols_forced() == 2 || smx::tet_cells(side) >= kColsMinCells);  // no chunk engine at 16
+    if (cols_forced()) return cols_forced() == 2;
+    return smx::tet_cells(side) >= kColsMinCells;
+}
+bool use_cols(const smx::Geom& k) { return use_cols_side(k.side, k.rho); }
 
 // the column engine's work items (host): for layer segments of lz layers,
 // every 8-row band iy and 8-word group g with cells; item order keeps
@@ -1380,11 +1386,15 @@ static int ca_validate(const smx_grid* g, uint64_t ncells, int32_t* exec) {
     }
     if (g->kind != SMX_BB && g->kind != SMX_H3D)
         return fail(SMX_EINVAL, "launch_ca: 3-simplex grids are bb or h3d");
-    if (*exec < 0) *exec = smx::ca_runs_supported(int(g->rho)) ? SMX_EXEC_BITS : SMX_EXEC_BLOCK;
+    // rho = 16 runs the bit-shadow path only through the column engine (large states)
+    const bool cols16 = g->rho == 16 && use_cols_side(cell_side_of(g), 16);
+    if (*exec < 0) *exec = smx::ca_runs_supported(int(g->rho)) || cols16 ? SMX_EXEC_BITS : SMX_EXEC_BLOCK;
     if (*exec != SMX_EXEC_BLOCK && *exec != SMX_EXEC_RUNS && *exec != SMX_EXEC_BITS)
         return fail(SMX_EINVAL, "ca: unknown exec scheme");
+    if (*exec == SMX_EXEC_BITS && cols16) return SMX_OK;
     if (*exec != SMX_EXEC_BLOCK && !smx::ca_runs_supported(int(g->rho)))
-        return fail(SMX_EINVAL, "ca: the x-run schemes support rho in {4, 8}; use SMX_EXEC_BLOCK");
+        return fail(SMX_EINVAL, "ca: the x-run schemes support rho in {4, 8} (16: the bit-shadow column engine "
+                                "for states >= 96 M cells); use SMX_EXEC_BLOCK");
     return SMX_OK;
 }
 
@@ -1427,6 +1437,8 @@ int smx_ca_step_range(const smx_grid* g, const uint8_t* cur, uint8_t* next, uint
     if (wz_lo < 0 || wz_hi > g->extents[2] || wz_lo > wz_hi)
         return fail(SMX_EINVAL, "ca_step_range: wz range outside the grid");
     if (cur == next) return fail(SMX_EINVAL, "ca_step_range: cur and next must not alias");
+    if (exec == SMX_EXEC_BITS && !smx::ca_runs_supported(int(g->rho)))
+        return fail(SMX_EINVAL, "ca_step_range: the bit-shadow range step supports rho in {4, 8}");
     if (int rc = check_align16(cur, next)) return rc;
     if (auto_exec && exec == SMX_EXEC_BITS && prefer_fused(g, ncells)) exec = SMX_EXEC_RUNS;
     if (exec == SMX_EXEC_BITS) return ca_runs_step(g, k, wz_lo, wz_hi, cur, next, (cudaStream_t)stream);
@@ -1522,7 +1534,7 @@ uint64_t smx_bits_bytes(const smx_grid* g) {
 int smx_bits_pack(const smx_grid* g, const uint8_t* cells, uint64_t ncells, uint32_t* bits, void* stream) {
     smx::Geom k;
     if (int rc = make_geom(g, &k, true)) return rc;
-    int32_t ex = SMX_EXEC_RUNS;
+    int32_t ex = SMX_EXEC_BITS;
     if (int rc = ca_validate(g, ncells, &ex)) return rc;
     smx::launch_pack_bits(k, cells, bits, (cudaStream_t)stream);
     TRY(cudaGetLastError());
@@ -1548,7 +1560,7 @@ int smx_bits_step(const smx_grid* g, const uint32_t* bits_in, uint32_t* bits_out
 int smx_bits_unpack(const smx_grid* g, const uint32_t* bits, uint8_t* cells, uint64_t ncells, void* stream) {
     smx::Geom k;
     if (int rc = make_geom(g, &k, true)) return rc;
-    int32_t ex = SMX_EXEC_RUNS;
+    int32_t ex = SMX_EXEC_BITS;
     if (int rc = ca_validate(g, ncells, &ex)) return rc;
     smx::launch_unpack_bits(k, bits, cells, (cudaStream_t)stream);
     TRY(cudaGetLastError());
@@ -1582,6 +1594,7 @@ int smx_bits_plan(const smx_grid* g, int64_t wz_lo, int64_t wz_hi, void* chunks,
     if (int rc = make_geom(g, &k, true)) return rc;
     int32_t ex = SMX_EXEC_BITS;
     if (int rc = ca_validate(g, smx::tet_cells(k.side), &ex)) return rc;
+    if (!smx::ca_runs_supported(int(g->rho))) return fail(SMX_EINVAL, "bits_plan: the chunk engine supports rho in {4, 8}");
     if (wz_lo < 0 || wz_hi > g->extents[2] || wz_lo > wz_hi) return fail(SMX_EINVAL, "bits_plan: wz range outside the grid");
     if (!chunks || !count) return fail(SMX_EINVAL, "null output");
     cudaStream_t s = (cudaStream_t)stream;
@@ -1597,6 +1610,7 @@ int smx_bits_run_list(const smx_grid* g, uint32_t* bits_in, uint32_t* bits_out, 
     if (int rc = make_geom(g, &k, true)) return rc;
     int32_t ex = SMX_EXEC_BITS;
     if (int rc = ca_validate(g, smx::tet_cells(k.side), &ex)) return rc;
+    if (!smx::ca_runs_supported(int(g->rho))) return fail(SMX_EINVAL, "bits_plan: the chunk engine supports rho in {4, 8}");
     if (bits_in == bits_out) return fail(SMX_EINVAL, "bits_run_list: the two shadows must not alias");
     if (!chunks || !count) return fail(SMX_EINVAL, "null chunk list");
     const CUtensorMap* tm;
@@ -1849,6 +1863,7 @@ int smx_ca_multi(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t ste
     int32_t ex = SMX_EXEC_BITS;
     if (int rc = ca_validate(g, ncells, &ex)) return rc;
     if (g->dims != 3) return fail(SMX_EINVAL, "launch_ca: the multi-GPU engine shards 3-simplex grids");
+    if (!smx::ca_runs_supported(int(g->rho))) return fail(SMX_EINVAL, "launch_ca: the multi-GPU engine supports rho in {4, 8}");
     if (steps < 0) return fail(SMX_EINVAL, "launch_ca: steps must be >= 0");
     if (steps > INT32_MAX) return fail(SMX_ERANGE, "launch_ca: steps must fit int32");
     if (ndev < 1) return fail(SMX_EINVAL, "launch_ca: ngpus must be >= 1");

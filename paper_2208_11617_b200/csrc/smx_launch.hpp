@@ -32,7 +32,8 @@ void launch_life_init(unsigned long long seed, uint8_t* cells, unsigned long lon
 // kernel_accum: every cell += 1 (no map)
 void launch_increment(uint32_t* cells, unsigned long long n, cudaStream_t s);
 void launch_ca(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s);
-bool ca_runs_supported(int rho);
+bool ca_runs_supported(int rho);  // the chunk engine, fused and range steps: rho in {4, 8}
+bool cols_supported(int rho);     // the column engine: rho in {4, 8, 16}
 // fused u8 -> u8 x-run step (smx_ca_fused.cu), rho in {4, 8}
 void launch_ca_fused(const Geom& g, int wz0, int wz1, const uint8_t* cur, uint8_t* next, cudaStream_t s);
 // bit-shadow engine (smx_ca_bits.cu)

@@ -34,15 +34,23 @@ CASES = [
     ("c5_rho8_2", 2040, 2, "C5: grid_h3d(256) / grid_bb(255,3), rho=8, 2 steps"),
     ("c5_rho8_20", 2040, 20, "C5: 20 steps (the bench's engine call)"),
     ("c5_rho4_20", 2044, 20, "C5 at rho=4: grid_h3d(512), 20 steps"),
+    ("c5_rho16_20", 2032, 20, "C5 at rho=16: grid_h3d(128) / grid_bb(127,3), 20 steps"),
     ("side1023_1", 1023, 1, "SURVEY Appendix A: H3D(1024) rho=1 / BB(1023), one step"),
 ]
 APPENDIX_A_1023 = 13036985295180606544
 
 
 def main() -> None:
+    """`python gen_golden_full.py [label ...]`: (re)compute only those cases,
+    keeping the others already in ca_full.json."""
     o = Restated()
     out = {"note": __doc__.strip().splitlines()[0], "seed": SEED, "cases": {}}
+    only = set(sys.argv[1:])
+    if only and os.path.exists(OUT):
+        out = json.load(open(OUT))
     for label, side, steps, note in CASES:
+        if only and label not in only and label != "side1023_1":
+            continue
         t0 = time.time()
         s = o.make_life_state(3, side, SEED)
         init_hash = o.state_hash(3, side, s)
