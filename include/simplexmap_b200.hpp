@@ -1,24 +1,22 @@
-// simplexmap_b200.hpp — C++ drop-in for the hot path of the reference
-// `simplexmap` API (arXiv 2208.11617 reference, /root/reference/proj/include/
-// simplexmap/{core,maps,simulator,report}.hpp), backed by the sm_100a kernels
-// through the C ABI in smx_b200.h (link libsmx_b200.so).
+// simplexmap_b200.hpp — C++ drop-in for the reference `simplexmap` API
+// (arXiv 2208.11617 reference, /root/reference/proj/include/simplexmap/
+// {bits,core,rational,maps,simulator,report,analysis,render}.hpp), backed by the
+// sm_100a kernels through the C ABI in smx_b200.h (link libsmx_b200.so).
 //
-// Same names, argument meaning and exceptions as the reference for the
-// functions on the path: grid_bb / grid_h2d / grid_h3d / make_grid,
-// map_bb / map_h2d / map_h3d, simplex_grid_state<T> (+hash), launch_map,
-// launch_accum, launch_ca (dead3d), make_life_state, verify_exact_cover; and
-// the general-n / comparison 2-D maps: grid_rb,
-// grid_lambda, grid_h2d_padded, grid_trapezoids, decompose_trapezoids,
-// map_rb_2d, map_lambda_2d, map_h2d_padded, map_h2d_trapezoid; the EDM and
-// 2-D periodic Life kernels (make_edm_points, launch_edm, launch_ca m=2); and
-// the report layer (report.hpp: measure_grid, verify_sweep, analyze_sweep,
-// parse_n_range, csv_measure / csv_analyze / csv_simulate, text_report).
-// Out of scope (not declared here): the r/beta analysis (Python:
-// paper_2208_11617_b200.analysis), rendering.
+// Same names, argument meaning and exceptions as the reference for its whole
+// public surface: the integer helpers and exact rationals; every map and grid
+// (BB, H2D, H3D, padded, trapezoid bands, RB, lambda + its fp32 diagnostic);
+// simplex_grid_state<T> (+hash); launch_map / launch_accum / launch_ca /
+// launch_edm and verify_exact_cover on the GPU; the sequential kernel_accum /
+// kernel_edm / kernel_ca_run (on the GPU too) and their scalar helpers; the
+// report layer (measure_grid[_compact], sweeps, CSV emitters, text_report);
+// the r/beta analysis (exact host arithmetic); render_svg (block outcomes from
+// the GPU). include/simplexmap/*.hpp forward here, so `-I<repo>/include`
+// replaces the reference's include path (the reference's own test suites
+// compile unmodified against it: tests/cpp/Makefile).
 //
-// Switching from the reference: include this header instead of
-// <simplexmap/simulator.hpp> and define SMX_B200_AS_SIMPLEXMAP to get the
-// `simplexmap` namespace name.
+// Direct use: include this header and define SMX_B200_AS_SIMPLEXMAP to get the
+// `simplexmap` namespace name (the forwarding headers do that).
 #pragma once
 
 #include <algorithm>
