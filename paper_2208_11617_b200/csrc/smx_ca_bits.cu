@@ -887,6 +887,43 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
     }
 }
 
+// The chunk engine's canonical plan: from the tile bitmap the map marked
+// (k_cols_mark), every tile row (ty, tz) of the domain is cut into chunks of
+// at most LMAX x-adjacent marked tiles — the same chunk list for every exact
+// map, so H and BB run identical steps and differ only in the mapping work.
+// One thread per tile row; chunks appended to one global list.
+template <int RHO>
+__global__ void __launch_bounds__(256) k_chunkify(const uint32_t* __restrict__ bm, int D, int TW,
+                                                  Chunk* __restrict__ out, unsigned* __restrict__ count) {
+    constexpr int LMAX = PlanCfg<RHO>::LMAX;
+    const long long nrows = (long long)D * D;
+    for (long long rr = blockIdx.x * (long long)blockDim.x + threadIdx.x; rr < nrows;
+         rr += (long long)gridDim.x * blockDim.x) {
+        const int tz = int(rr / D), ty = int(rr % D);
+        if (ty + tz > D - 1) continue;  // no cells in this tile row
+        const uint32_t* row = bm + rr * TW;
+        Chunk buf[4];
+        int nb = 0;
+        auto flush = [&]() {
+            if (!nb) return;
+            const unsigned base = atomicAdd(count, unsigned(nb));
+            for (int i = 0; i < nb; ++i) out[base + i] = buf[i];
+            nb = 0;
+        };
+        int start = -1;  // first tile of the current run of marked tiles
+        for (int tx = 0; tx <= ty + 1; ++tx) {  // tiles x <= y hold cells; tx = ty + 1 closes the run
+            const bool on = tx <= ty && ((row[tx >> 5] >> (tx & 31)) & 1u);
+            if (on && start < 0) start = tx;
+            if ((!on || tx - start == LMAX) && start >= 0) {
+                buf[nb++] = Chunk{start * RHO, ty * RHO, tz * RHO, (tx - start) * RHO};
+                if (nb == 4) flush();
+                start = on ? tx : -1;
+            }
+        }
+        flush();
+    }
+}
+
 template <int RHO>
 __global__ void __launch_bounds__(CNW * 32) k_cols_run(const __grid_constant__ CUtensorMap tmA,
                                                        const __grid_constant__ CUtensorMap tmB, uint32_t* bitsA,
@@ -1074,6 +1111,15 @@ cudaError_t launch_ca_bits_run(const Geom& g, const void* tmA, const void* tmB, 
         return launch_run_t<4, 16, 2>(g, ta, tb, A, B, chunks, count, steps, s);
     }
     return launch_run_t<8, 16, 1>(g, ta, tb, A, B, chunks, count, steps, s);
+}
+
+void launch_chunkify(int rho, const uint32_t* bm, int D, int TW, void* chunks, unsigned* count, cudaStream_t s) {
+    const long long nrows = (long long)D * D;
+    long long blocks = (nrows + 255) / 256;
+    if (blocks > 148ll * 8) blocks = 148ll * 8;
+    if (blocks < 1) blocks = 1;
+    if (rho == 8) k_chunkify<8><<<unsigned(blocks), 256, 0, s>>>(bm, D, TW, reinterpret_cast<Chunk*>(chunks), count);
+    else k_chunkify<4><<<unsigned(blocks), 256, 0, s>>>(bm, D, TW, reinterpret_cast<Chunk*>(chunks), count);
 }
 
 // ---- the column engine's launchers ----

@@ -475,9 +475,25 @@ int engine_plan(const smx_grid* g, const smx::Geom& k, int64_t steps, cudaStream
     TRY(cudaEventRecord(r->ev_in, s));
     TRY(cudaStreamWaitEvent(r->side, r->ev_in, 0));
     TRY(cudaMemsetAsync(pctl, 0, ctl_bytes, r->side));
-    if (!P->cols) {
+    // SMX_CHUNK_PLAN=adjacency: the chunk engine's round-1 plan (chains of
+    // x-adjacent tiles found through the map's block adjacency, k_ca_plan)
+    static const bool adjacency_plan = [] {
+        const char* e = std::getenv("SMX_CHUNK_PLAN");
+        return e && !std::strcmp(e, "adjacency");
+    }();
+    if (!P->cols && adjacency_plan) {
         if (int rc = pool_get(5, size_t(smx::ca_plan_capacity(k)) * 16, &P->chunks)) return rc;
         smx::launch_ca_plan(k, g->kind, P->chunks, P->ctl, r->side);
+    } else if (!P->cols) {
+        // the map marks its tiles; every tile row is cut into chunks (canonical)
+        const int D = int(k.side / k.rho), TW = (D + 31) / 32;
+        const size_t bm_bytes = size_t(D) * size_t(D) * size_t(TW) * 4 + 16;
+        void* pbm;
+        if (int rc = pool_get(9, bm_bytes, &pbm)) return rc;
+        if (int rc = pool_get(5, size_t(smx::ca_plan_capacity(k)) * 16, &P->chunks)) return rc;
+        TRY(cudaMemsetAsync(pbm, 0, bm_bytes, r->side));
+        smx::launch_cols_mark(k, g->kind, (uint32_t*)pbm, D, TW, (unsigned*)((uint8_t*)pbm + bm_bytes - 16), r->side);
+        smx::launch_chunkify(int(k.rho), (const uint32_t*)pbm, D, TW, P->chunks, P->ctl, r->side);
     } else {
         P->D = int(k.side / k.rho);
         P->TW = (P->D + 31) / 32;
