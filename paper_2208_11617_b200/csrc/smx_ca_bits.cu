@@ -891,37 +891,61 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
 // (k_cols_mark), every tile row (ty, tz) of the domain is cut into chunks of
 // at most LMAX x-adjacent marked tiles — the same chunk list for every exact
 // map, so H and BB run identical steps and differ only in the mapping work.
-// One thread per tile row; chunks appended to one global list.
-template <int RHO>
-__global__ void __launch_bounds__(256) k_chunkify(const uint32_t* __restrict__ bm, int D, int TW,
-                                                  Chunk* __restrict__ out, unsigned* __restrict__ count) {
+// Three passes keep the list in domain order (tz, ty, tx), so the chunks the
+// persistent kernel runs concurrently are spatial neighbours: per tile row the
+// chunk count, one exclusive scan (a single CTA), then the chunks at their offsets.
+template <int RHO, bool WRITE>
+__device__ __forceinline__ unsigned row_chunks(const uint32_t* __restrict__ row, int ty, int tz, Chunk* out) {
     constexpr int LMAX = PlanCfg<RHO>::LMAX;
+    unsigned n = 0;
+    int start = -1;  // first tile of the current run of marked tiles
+    for (int tx = 0; tx <= ty + 1; ++tx) {  // tiles x <= y hold cells; tx = ty + 1 closes the run
+        const bool on = tx <= ty && ((row[tx >> 5] >> (tx & 31)) & 1u);
+        if (on && start < 0) start = tx;
+        if ((!on || tx - start == LMAX) && start >= 0) {
+            if (WRITE) out[n] = Chunk{start * RHO, ty * RHO, tz * RHO, (tx - start) * RHO};
+            ++n;
+            start = on ? tx : -1;
+        }
+    }
+    return n;
+}
+
+template <int RHO, bool WRITE>
+__global__ void __launch_bounds__(256) k_chunk_rows(const uint32_t* __restrict__ bm, int D, int TW,
+                                                    unsigned* __restrict__ cnt, Chunk* __restrict__ out) {
     const long long nrows = (long long)D * D;
     for (long long rr = blockIdx.x * (long long)blockDim.x + threadIdx.x; rr < nrows;
          rr += (long long)gridDim.x * blockDim.x) {
         const int tz = int(rr / D), ty = int(rr % D);
-        if (ty + tz > D - 1) continue;  // no cells in this tile row
-        const uint32_t* row = bm + rr * TW;
-        Chunk buf[4];
-        int nb = 0;
-        auto flush = [&]() {
-            if (!nb) return;
-            const unsigned base = atomicAdd(count, unsigned(nb));
-            for (int i = 0; i < nb; ++i) out[base + i] = buf[i];
-            nb = 0;
-        };
-        int start = -1;  // first tile of the current run of marked tiles
-        for (int tx = 0; tx <= ty + 1; ++tx) {  // tiles x <= y hold cells; tx = ty + 1 closes the run
-            const bool on = tx <= ty && ((row[tx >> 5] >> (tx & 31)) & 1u);
-            if (on && start < 0) start = tx;
-            if ((!on || tx - start == LMAX) && start >= 0) {
-                buf[nb++] = Chunk{start * RHO, ty * RHO, tz * RHO, (tx - start) * RHO};
-                if (nb == 4) flush();
-                start = on ? tx : -1;
-            }
-        }
-        flush();
+        const bool cells = ty + tz <= D - 1;  // the tile row holds cells
+        if (!WRITE) cnt[rr] = cells ? row_chunks<RHO, false>(bm + rr * TW, ty, tz, nullptr) : 0u;
+        else if (cells) row_chunks<RHO, true>(bm + rr * TW, ty, tz, out + cnt[rr]);
     }
+}
+
+// in-place exclusive scan of n counts by one CTA of 1024 threads; *total = the sum
+__global__ void __launch_bounds__(1024) k_scan_counts(unsigned* __restrict__ c, long long n, unsigned* __restrict__ total) {
+    __shared__ unsigned s_part[1024];
+    const int t = threadIdx.x;
+    const long long per = (n + 1023) / 1024, lo = t * per, hi = min(n, lo + per);
+    unsigned sum = 0;
+    for (long long i = lo; i < hi; ++i) sum += c[i];
+    s_part[t] = sum;
+    __syncthreads();
+    for (int d = 1; d < 1024; d <<= 1) {  // inclusive Hillis-Steele over the partials
+        const unsigned v = t >= d ? s_part[t - d] : 0u;
+        __syncthreads();
+        s_part[t] += v;
+        __syncthreads();
+    }
+    unsigned run = t ? s_part[t - 1] : 0u;
+    for (long long i = lo; i < hi; ++i) {
+        const unsigned v = c[i];
+        c[i] = run;
+        run += v;
+    }
+    if (t == 1023) *total = s_part[1023];
 }
 
 template <int RHO>
@@ -1113,13 +1137,18 @@ cudaError_t launch_ca_bits_run(const Geom& g, const void* tmA, const void* tmB, 
     return launch_run_t<8, 16, 1>(g, ta, tb, A, B, chunks, count, steps, s);
 }
 
-void launch_chunkify(int rho, const uint32_t* bm, int D, int TW, void* chunks, unsigned* count, cudaStream_t s) {
+void launch_chunkify(int rho, const uint32_t* bm, int D, int TW, unsigned* rowcnt, void* chunks, unsigned* count,
+                     cudaStream_t s) {
     const long long nrows = (long long)D * D;
     long long blocks = (nrows + 255) / 256;
     if (blocks > 148ll * 8) blocks = 148ll * 8;
     if (blocks < 1) blocks = 1;
-    if (rho == 8) k_chunkify<8><<<unsigned(blocks), 256, 0, s>>>(bm, D, TW, reinterpret_cast<Chunk*>(chunks), count);
-    else k_chunkify<4><<<unsigned(blocks), 256, 0, s>>>(bm, D, TW, reinterpret_cast<Chunk*>(chunks), count);
+    Chunk* out = reinterpret_cast<Chunk*>(chunks);
+    if (rho == 8) k_chunk_rows<8, false><<<unsigned(blocks), 256, 0, s>>>(bm, D, TW, rowcnt, out);
+    else k_chunk_rows<4, false><<<unsigned(blocks), 256, 0, s>>>(bm, D, TW, rowcnt, out);
+    k_scan_counts<<<1, 1024, 0, s>>>(rowcnt, nrows, count);
+    if (rho == 8) k_chunk_rows<8, true><<<unsigned(blocks), 256, 0, s>>>(bm, D, TW, rowcnt, out);
+    else k_chunk_rows<4, true><<<unsigned(blocks), 256, 0, s>>>(bm, D, TW, rowcnt, out);
 }
 
 // ---- the column engine's launchers ----

@@ -73,9 +73,10 @@ struct DeviceRes {
     // block (64 B: u32 [0] chunk count, u32 [8] grid barrier), 7 the
     // first-defect result of smx_verify_cover (its own slot: a verify on one
     // stream never touches the words of an engine running on another)
-    // 8 the column engine's items (host-built, key cols_key), 9 its tile bitmap
-    void* pool[10] = {};
-    size_t pool_bytes[10] = {};
+    // 8 the column engine's items (host-built, key cols_key), 9 the tile
+    // bitmap (both engines), 10 the chunk plan's per-row counts
+    void* pool[11] = {};
+    size_t pool_bytes[11] = {};
     std::pair<int64_t, int64_t> cols_key{-1, -1};  // (side, layers per item) of the items in slot 8
     int cols_nitems = 0;
     std::map<std::pair<const void*, std::pair<int64_t, int64_t>>, CUtensorMap> tmaps;
@@ -95,7 +96,7 @@ void free_res(int dev, DeviceRes& r) {
     if (cudaGetDevice(&cur) != cudaSuccess) return;
     if (cur != dev) cudaSetDevice(dev);
     for (auto& kv : r.prefix) cudaFree(kv.second);
-    for (int i = 0; i < 10; ++i)
+    for (int i = 0; i < 11; ++i)
         if (r.pool[i]) cudaFree(r.pool[i]);
     if (r.counters) cudaFree(r.counters);
     if (r.sink) cudaFree(r.sink);
@@ -493,7 +494,9 @@ int engine_plan(const smx_grid* g, const smx::Geom& k, int64_t steps, cudaStream
         if (int rc = pool_get(5, size_t(smx::ca_plan_capacity(k)) * 16, &P->chunks)) return rc;
         TRY(cudaMemsetAsync(pbm, 0, bm_bytes, r->side));
         smx::launch_cols_mark(k, g->kind, (uint32_t*)pbm, D, TW, (unsigned*)((uint8_t*)pbm + bm_bytes - 16), r->side);
-        smx::launch_chunkify(int(k.rho), (const uint32_t*)pbm, D, TW, P->chunks, P->ctl, r->side);
+        void* prc;
+        if (int rc = pool_get(10, size_t(D) * size_t(D) * 4, &prc)) return rc;
+        smx::launch_chunkify(int(k.rho), (const uint32_t*)pbm, D, TW, (unsigned*)prc, P->chunks, P->ctl, r->side);
     } else {
         P->D = int(k.side / k.rho);
         P->TW = (P->D + 31) / 32;
@@ -1908,7 +1911,7 @@ uint64_t smx_scratch_bytes(void) {
     uint64_t b = 0;
     for (auto& kv : g_res) {
         if (kv.first.second != std::this_thread::get_id()) continue;
-        for (int i = 0; i < 10; ++i) b += kv.second.pool_bytes[i];
+        for (int i = 0; i < 11; ++i) b += kv.second.pool_bytes[i];
     }
     return b;
 }

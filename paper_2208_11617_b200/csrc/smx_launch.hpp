@@ -66,7 +66,9 @@ int cols_item_bytes();
 int cols_warps();
 void launch_cols_mark(const Geom& g, int kind, uint32_t* bm, int D, int TW, unsigned* stats, cudaStream_t s);
 // the chunk engine's canonical plan from the tile bitmap (rho in {4, 8})
-void launch_chunkify(int rho, const uint32_t* bm, int D, int TW, void* chunks, unsigned* count, cudaStream_t s);
+// rowcnt: D * D u32 scratch; *count receives the chunk total
+void launch_chunkify(int rho, const uint32_t* bm, int D, int TW, unsigned* rowcnt, void* chunks, unsigned* count,
+                     cudaStream_t s);
 cudaError_t launch_cols_run(const Geom& g, const void* tmA, const void* tmB, uint32_t* A, uint32_t* B,
                             const void* items, int nitems, unsigned* ctl, const uint32_t* bm, int D, int TW, int steps,
                             cudaStream_t s);
