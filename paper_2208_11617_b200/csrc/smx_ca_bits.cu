@@ -655,12 +655,13 @@ struct ColItem {
 
 template <int KIND>
 __global__ void __launch_bounds__(256) k_cols_mark(Geom g, uint32_t* __restrict__ bm, int D, int TW,
-                                                    unsigned* __restrict__ stats) {
-    const long long nb = (long long)g.ex * g.ey * g.ez;
+                                                    unsigned* __restrict__ stats, int wz0, int wz1) {
+    // blocks with wz in [wz0, wz1) (a shard's whole levels; the full grid: 0, ez)
+    const long long plane = (long long)g.ex * g.ey, nb = plane * (wz1 - wz0);
     unsigned marked = 0, dup = 0;
     for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nb;
          b += (long long)gridDim.x * blockDim.x) {
-        const int wx = int(b % g.ex), wy = int(b / g.ex % g.ey), wz = int(b / ((long long)g.ex * g.ey));
+        const int wx = int(b % g.ex), wy = int(b / g.ex % g.ey), wz = wz0 + int(b / plane);
         const outcome<int> o = map_block<KIND>(g, wx, wy, wz);
         if (o.is_void) continue;
         const uint32_t bit = 1u << (o.x & 31);
@@ -1157,13 +1158,16 @@ int cols_box_rows() { return CBR; }
 int cols_box_layers() { return CLZ; }
 int cols_item_bytes() { return int(sizeof(ColItem)); }
 
-void launch_cols_mark(const Geom& g, int kind, uint32_t* bm, int D, int TW, unsigned* stats, cudaStream_t s) {
-    const long long nb = (long long)g.ex * g.ey * g.ez;
+void launch_cols_mark(const Geom& g, int kind, uint32_t* bm, int D, int TW, unsigned* stats, cudaStream_t s,
+                      int wz0, int wz1) {
+    if (wz1 < 0) wz1 = g.ez;
+    if (wz1 <= wz0) return;
+    const long long nb = (long long)g.ex * g.ey * (wz1 - wz0);
     long long blocks = (nb + 255) / 256;
     if (blocks > 148ll * 16) blocks = 148ll * 16;
     if (blocks < 1) blocks = 1;
-    if (kind == SMX_H3D) k_cols_mark<SMX_H3D><<<unsigned(blocks), 256, 0, s>>>(g, bm, D, TW, stats);
-    else k_cols_mark<SMX_BB><<<unsigned(blocks), 256, 0, s>>>(g, bm, D, TW, stats);
+    if (kind == SMX_H3D) k_cols_mark<SMX_H3D><<<unsigned(blocks), 256, 0, s>>>(g, bm, D, TW, stats, wz0, wz1);
+    else k_cols_mark<SMX_BB><<<unsigned(blocks), 256, 0, s>>>(g, bm, D, TW, stats, wz0, wz1);
 }
 
 int cols_grid() {

@@ -443,6 +443,24 @@ std::vector<int32_t> col_items(int64_t S, int64_t lz) {
     return v;
 }
 
+// the chunk engine's canonical plan of the blocks with wz in [wz0, wz1) on
+// stream s: the map marks their tiles, the marked tile rows are cut into
+// chunks in domain order; *count (device) = the chunk total
+int canonical_plan(const smx_grid* g, const smx::Geom& k, int64_t wz0, int64_t wz1, void* chunks, unsigned* count,
+                   cudaStream_t s) {
+    const int D = int(k.side / k.rho), TW = (D + 31) / 32;
+    const size_t bm_bytes = size_t(D) * size_t(D) * size_t(TW) * 4 + 16;
+    void *pbm, *prc;
+    if (int rc = pool_get(9, bm_bytes, &pbm)) return rc;
+    if (int rc = pool_get(10, size_t(D) * size_t(D) * 4, &prc)) return rc;
+    TRY(cudaMemsetAsync(pbm, 0, bm_bytes, s));
+    smx::launch_cols_mark(k, g->kind, (uint32_t*)pbm, D, TW, (unsigned*)((uint8_t*)pbm + bm_bytes - 16), s, int(wz0),
+                          int(wz1));
+    smx::launch_chunkify(int(k.rho), (const uint32_t*)pbm, D, TW, (unsigned*)prc, chunks, count, s);
+    TRY(cudaGetLastError());
+    return SMX_OK;
+}
+
 struct EnginePlan {
     bool cols = false;
     void* chunks = nullptr;   // chunk engine: the chunk list
@@ -487,16 +505,8 @@ int engine_plan(const smx_grid* g, const smx::Geom& k, int64_t steps, cudaStream
         smx::launch_ca_plan(k, g->kind, P->chunks, P->ctl, r->side);
     } else if (!P->cols) {
         // the map marks its tiles; every tile row is cut into chunks (canonical)
-        const int D = int(k.side / k.rho), TW = (D + 31) / 32;
-        const size_t bm_bytes = size_t(D) * size_t(D) * size_t(TW) * 4 + 16;
-        void* pbm;
-        if (int rc = pool_get(9, bm_bytes, &pbm)) return rc;
         if (int rc = pool_get(5, size_t(smx::ca_plan_capacity(k)) * 16, &P->chunks)) return rc;
-        TRY(cudaMemsetAsync(pbm, 0, bm_bytes, r->side));
-        smx::launch_cols_mark(k, g->kind, (uint32_t*)pbm, D, TW, (unsigned*)((uint8_t*)pbm + bm_bytes - 16), r->side);
-        void* prc;
-        if (int rc = pool_get(10, size_t(D) * size_t(D) * 4, &prc)) return rc;
-        smx::launch_chunkify(int(k.rho), (const uint32_t*)pbm, D, TW, (unsigned*)prc, P->chunks, P->ctl, r->side);
+        if (int rc = canonical_plan(g, k, 0, k.ez, P->chunks, P->ctl, r->side)) return rc;
     } else {
         P->D = int(k.side / k.rho);
         P->TW = (P->D + 31) / 32;
@@ -876,9 +886,7 @@ int multi_setup(const smx_grid* g, const std::vector<int>& devs, MultiRes* M) {
         TRY(cudaMalloc(&all, std::max<uint64_t>(smx::ca_plan_capacity(sh.k), 1) * 16));
         TRY(cudaMalloc(&cnt, 8));
         TRY(cudaMemset(cnt, 0, 8));
-        smx::launch_ca_plan_range(sh.k, g->kind, int(P.wz[size_t(s)].first), int(P.wz[size_t(s)].second), all, cnt,
-                                  sh.cs);
-        TRY(cudaGetLastError());
+        if (int rc = canonical_plan(g, sh.k, P.wz[size_t(s)].first, P.wz[size_t(s)].second, all, cnt, sh.cs)) return rc;
         uint32_t n = 0;
         TRY(cudaMemcpyAsync(&n, cnt, 4, cudaMemcpyDeviceToHost, sh.cs));
         TRY(cudaStreamSynchronize(sh.cs));
@@ -1618,9 +1626,7 @@ int smx_bits_plan(const smx_grid* g, int64_t wz_lo, int64_t wz_hi, void* chunks,
     if (!chunks || !count) return fail(SMX_EINVAL, "null output");
     cudaStream_t s = (cudaStream_t)stream;
     TRY(cudaMemsetAsync(count, 0, 4, s));
-    smx::launch_ca_plan_range(k, g->kind, int(wz_lo), int(wz_hi), chunks, count, s);
-    TRY(cudaGetLastError());
-    return SMX_OK;
+    return canonical_plan(g, k, wz_lo, wz_hi, chunks, count, s);
 }
 
 int smx_bits_run_list(const smx_grid* g, uint32_t* bits_in, uint32_t* bits_out, const void* chunks,

@@ -64,7 +64,9 @@ int cols_box_rows();
 int cols_box_layers();
 int cols_item_bytes();
 int cols_warps();
-void launch_cols_mark(const Geom& g, int kind, uint32_t* bm, int D, int TW, unsigned* stats, cudaStream_t s);
+// the map over blocks with wz in [wz0, wz1) (default: the whole grid) -> tile bitmap
+void launch_cols_mark(const Geom& g, int kind, uint32_t* bm, int D, int TW, unsigned* stats, cudaStream_t s,
+                      int wz0 = 0, int wz1 = -1);
 // the chunk engine's canonical plan from the tile bitmap (rho in {4, 8})
 // rowcnt: D * D u32 scratch; *count receives the chunk total
 void launch_chunkify(int rho, const uint32_t* bm, int D, int TW, unsigned* rowcnt, void* chunks, unsigned* count,
