@@ -802,10 +802,14 @@ struct Shard {
 
 struct MultiRes {
     std::vector<Shard> shards;
+    cudaGraphExec_t pair = nullptr;  // two sharded steps (A -> B -> A) as one multi-device graph
+    bool pair_failed = false;        // capture unsupported here: the steps are issued one by one
     ~MultiRes() { destroy(); }
     void destroy() {
         int cur = 0;
         cudaGetDevice(&cur);
+        if (pair) cudaGraphExecDestroy(pair);
+        pair = nullptr;
         for (auto& sh : shards) {
             cudaSetDevice(sh.dev);
             cudaDeviceSynchronize();
@@ -1004,6 +1008,65 @@ int multi_step(MultiRes* M, bool even) {
     return SMX_OK;
 }
 
+// capture two sharded steps (A -> B, B -> A) into one multi-device graph,
+// once per MultiRes; on any capture error the steps run uncaptured
+int multi_pair_graph(MultiRes* M) {
+    if (M->pair) return SMX_OK;
+    if (M->pair_failed) return SMX_ECUDA;
+    Shard& s0 = M->shards[0];
+    auto bail = [&](cudaError_t e) {
+        cudaGraph_t dead = nullptr;
+        cudaSetDevice(s0.dev);
+        cudaStreamEndCapture(s0.cs, &dead);
+        if (dead) cudaGraphDestroy(dead);
+        cudaGetLastError();
+        M->pair_failed = true;
+        return cuda_fail(e, "capturing the sharded step pair");
+    };
+    cudaError_t e = cudaSetDevice(s0.dev);
+    if (e == cudaSuccess) e = cudaStreamBeginCapture(s0.cs, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return bail(e);
+    // fork: every stream of every shard joins the capture; the cross-step
+    // event (ev_done: a receiver unpacked its halo) is re-recorded inside it
+    if ((e = cudaEventRecord(s0.ev_b, s0.cs)) != cudaSuccess) return bail(e);
+    for (auto& sh : M->shards) {
+        cudaSetDevice(sh.dev);
+        if (&sh != &s0 && (e = cudaStreamWaitEvent(sh.cs, s0.ev_b, 0)) != cudaSuccess) return bail(e);
+        if ((e = cudaStreamWaitEvent(sh.ms, s0.ev_b, 0)) != cudaSuccess) return bail(e);
+        if ((e = cudaEventRecord(sh.ev_done, sh.cs)) != cudaSuccess) return bail(e);
+    }
+    if (multi_step(M, true) != SMX_OK || multi_step(M, false) != SMX_OK) return bail(cudaErrorStreamCaptureInvalidated);
+    // join: every stream back into the origin
+    for (auto& sh : M->shards) {
+        cudaSetDevice(sh.dev);
+        if ((e = cudaEventRecord(sh.ev_sent, sh.ms)) != cudaSuccess) return bail(e);
+        cudaSetDevice(s0.dev);
+        if ((e = cudaStreamWaitEvent(s0.cs, sh.ev_sent, 0)) != cudaSuccess) return bail(e);
+        if (&sh != &s0) {
+            cudaSetDevice(sh.dev);
+            if ((e = cudaEventRecord(sh.ev_done, sh.cs)) != cudaSuccess) return bail(e);
+            cudaSetDevice(s0.dev);
+            if ((e = cudaStreamWaitEvent(s0.cs, sh.ev_done, 0)) != cudaSuccess) return bail(e);
+        }
+    }
+    cudaSetDevice(s0.dev);
+    cudaGraph_t graph = nullptr;
+    if ((e = cudaStreamEndCapture(s0.cs, &graph)) != cudaSuccess) {
+        cudaGetLastError();
+        M->pair_failed = true;
+        return cuda_fail(e, "capturing the sharded step pair");
+    }
+    e = cudaGraphInstantiate(&M->pair, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        M->pair = nullptr;
+        M->pair_failed = true;
+        return cuda_fail(e, "instantiating the sharded step pair");
+    }
+    return SMX_OK;
+}
+
 int ca_multi(const smx_grid* g, const std::vector<int>& devs, uint8_t* cells, uint64_t ncells, int64_t steps,
              int device_ptr, smx_counters* counters, cudaStream_t s) {
     int caller_dev = 0;
@@ -1042,7 +1105,29 @@ int ca_multi(const smx_grid* g, const std::vector<int>& devs, uint8_t* cells, ui
         TRY(cudaGetLastError());
         TRY(cudaEventRecord(sh.ev_done, sh.cs));
     }
-    for (int64_t st = 0; st < steps; ++st)
+    // the steps: pairs of steps through one captured multi-device graph (one
+    // launch instead of ~(5 + peers) API calls per shard and step), an odd
+    // last step issued directly
+    int64_t st = 0;
+    if (!M->pair && !M->pair_failed && steps >= 4) {
+        // the first pair runs uncaptured: every kernel's per-device attributes
+        // are set before any capture begins
+        for (; st < 2; ++st)
+            if (int rc = multi_step(M, (st & 1) == 0)) return rc;
+    }
+    if (steps - st >= 2 && (M->pair || st > 0) && multi_pair_graph(M) == SMX_OK) {
+        TRY(cudaSetDevice(s0.dev));
+        for (auto& sh : M->shards) TRY(cudaStreamWaitEvent(s0.cs, sh.ev_done, 0));  // every replica packed
+        for (; st + 2 <= steps; st += 2) TRY(cudaGraphLaunch(M->pair, s0.cs));
+        TRY(cudaEventRecord(s0.ev_b, s0.cs));
+        for (auto& sh : M->shards) {  // everything after waits for the graphs
+            TRY(cudaSetDevice(sh.dev));
+            TRY(cudaStreamWaitEvent(sh.cs, s0.ev_b, 0));
+            TRY(cudaStreamWaitEvent(sh.ms, s0.ev_b, 0));
+            TRY(cudaEventRecord(sh.ev_done, sh.cs));
+        }
+    }
+    for (; st < steps; ++st)
         if (int rc = multi_step(M, (st & 1) == 0)) return rc;
     // gather: every other shard's owned bit tiles into shard 0's final shadow
     const bool odd = (steps & 1) != 0;
