@@ -1008,11 +1008,31 @@ int multi_step(MultiRes* M, bool even) {
     return SMX_OK;
 }
 
+int multi_pair_capture(MultiRes* M);
+
+// events last recorded inside a capture cannot be waited on eagerly: record
+// every shard's events again at the tails of their streams
+void multi_rearm_events(MultiRes* M) {
+    for (auto& sh : M->shards) {
+        cudaSetDevice(sh.dev);
+        cudaEventRecord(sh.ev_b, sh.cs);
+        cudaEventRecord(sh.ev_done, sh.cs);
+        cudaEventRecord(sh.ev_sent, sh.ms);
+    }
+    cudaSetDevice(M->shards[0].dev);
+}
+
 // capture two sharded steps (A -> B, B -> A) into one multi-device graph,
 // once per MultiRes; on any capture error the steps run uncaptured
 int multi_pair_graph(MultiRes* M) {
     if (M->pair) return SMX_OK;
     if (M->pair_failed) return SMX_ECUDA;
+    const int rc = multi_pair_capture(M);
+    multi_rearm_events(M);
+    return rc;
+}
+
+int multi_pair_capture(MultiRes* M) {
     Shard& s0 = M->shards[0];
     auto bail = [&](cudaError_t e) {
         cudaGraph_t dead = nullptr;
