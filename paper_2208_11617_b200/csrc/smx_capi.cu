@@ -992,7 +992,9 @@ int multi_step(MultiRes* M, bool even) {
         for (const PeerCopy& c : sh.copies) {
             Shard& o = M->shards[size_t(c.peer)];
             TRY(cudaStreamWaitEvent(sh.ms, o.ev_done, 0));  // o has unpacked the previous step's halo
-            TRY(cudaMemcpyPeerAsync(o.recv_b + c.dst_off, o.dev, sh.send_b + c.src_off, sh.dev, c.bytes, sh.ms));
+            // unified addressing: NVLink P2P between peer-enabled devices, a device copy within one
+            // (cudaMemcpyDefault, unlike cudaMemcpyPeerAsync, is capturable into the step-pair graph)
+            TRY(cudaMemcpyAsync(o.recv_b + c.dst_off, sh.send_b + c.src_off, c.bytes, cudaMemcpyDefault, sh.ms));
         }
         TRY(cudaEventRecord(sh.ev_sent, sh.ms));
     }
@@ -1026,9 +1028,13 @@ void multi_rearm_events(MultiRes* M) {
 // once per MultiRes; on any capture error the steps run uncaptured
 int multi_pair_graph(MultiRes* M) {
     if (M->pair) return SMX_OK;
-    if (M->pair_failed) return SMX_ECUDA;
+    static const bool no_graph = std::getenv("SMX_MULTI_NOGRAPH") != nullptr;  // A/B: steps issued one by one
+    if (M->pair_failed || no_graph) return SMX_ECUDA;
     const int rc = multi_pair_capture(M);
     multi_rearm_events(M);
+    if (std::getenv("SMX_DEBUG_MULTI"))
+        std::fprintf(stderr, "smx_ca_multi: step-pair graph %s (%zu shards)%s%s\n", rc ? "NOT captured" : "captured",
+                     M->shards.size(), rc ? ": " : "", rc ? g_err.c_str() : "");
     return rc;
 }
 
