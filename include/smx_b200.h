@@ -247,6 +247,9 @@ int smx_bits_unpack(const smx_grid* g, const uint32_t* bits, uint8_t* cells, uin
  * persistent cooperative launch runs `steps` bit-sliced Life steps bits_a ->
  * bits_b -> bits_a ... (grid barrier between steps). The result is in bits_a
  * for even `steps`, bits_b for odd. Device pointers (smx_bits_bytes each). */
+/* Both shadows must hold zero in every non-cell bit (rows y > S-1-z, words and
+ * bits past x = y): allocate them zeroed (smx_bits_pack keeps it: it writes
+ * the cell words with zero bits past the diagonal; the engines keep it). */
 int smx_bits_run(const smx_grid* g, uint32_t* bits_a, uint32_t* bits_b, int64_t steps, void* stream);
 /* Which engine smx_ca / smx_bits_run use for a 3-simplex grid: 0 = the chunk
  * engine (the map -> chains of x-adjacent tiles; small states), 1 = the

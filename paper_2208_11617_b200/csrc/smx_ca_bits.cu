@@ -764,23 +764,10 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
         const int nfull = nin / CLZ, tail = nin % CLZ;
         const int nst = nfull + (tail ? 1 : 0);
         const int y0 = 8 * it.iy, w0 = 8 * it.g;
-        // interior items (warp-uniform): no cell of the box lies past the
-        // diagonal (x > y) or above the tetrahedron's face (y + z > S - 1), every
-        // output word is a full word of cells: no masking anywhere
-        const bool interior = y0 >= 32 * (w0 + 9) && y0 + 8 + it.z1 <= S - 1;
-        // h-sum role, per item: the row's layer limit and the x <= y masks of
-        // the 4 main words and the edge word
-        const int hy = y0 - 1 + hr;
-        const unsigned hzlim = unsigned(S - 1 - hy);  // input row is a cell row iff 0 <= zi <= S-1-hy
-        uint32_t M0, M1, M2, M3, Me;
-        {
-            const int xm = 32 * (w0 + 4 * hc), xe = hc ? 32 * (w0 + 8) : 32 * (w0 - 1);
-            M0 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm + 1, 0));
-            M1 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm - 31, 0));
-            M2 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm - 63, 0));
-            M3 = __funnelshift_lc(0xffffffffu, 0u, max(hy - xm - 95, 0));
-            Me = __funnelshift_lc(0xffffffffu, 0u, max(hy - xe + 1, 0));
-        }
+        // no input masking: every non-cell bit of the shadow is zero (rows above
+        // the tetrahedron's face, words and bits past x = y: the pack writes
+        // them zero, these stores mask them, the pools start zeroed) and the
+        // box's out-of-range coordinates are TMA zero-fill
         const int hoff = hr * CBW + 4 + 4 * hc;  // box word of the main chunk
         const int eoff = hr * CBW + (hc ? 12 : 3);
         uint2* hsw = hsb + hr * CW + 4 * hc;      // this lane's h-sum slots (parity 0)
@@ -788,25 +775,19 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
         const int yo = y0 + ly, wo = w0 + jp;
         const int ozlim = min(S - 1 - yo, it.z1 - 1);  // stored layers: z0 <= zo <= ozlim
         const int smode = 32 * (wo + 1) <= yo ? 2 : (32 * wo <= yo ? 1 : 0);
+        // x <= y within this lane's two output words (keeps the zero invariant)
+        const uint32_t xm0 = __funnelshift_lc(0xffffffffu, 0u, max(yo - 32 * wo + 1, 0));
+        const uint32_t xm1 = __funnelshift_lc(0xffffffffu, 0u, max(yo - 32 * wo - 31, 0));
         uint32_t* optr = out + ((long long)(it.z0 - 2) * S + yo) * WP + wo;  // output layer of input layer z0 - 1
         Sat3 va[2], vb[2];
         uint32_t alive_cur0 = 0u, alive_cur1 = 0u;
         uint2 mprev = make_uint2(0u, 0u);
 
         // one input layer: h-sums -> vertical sums -> the rule for the layer behind
-        auto layer = [&](auto fast, const uint32_t* L, int li, int zi, const uint2& m0, const uint2& m1) {
-            constexpr bool FAST = decltype(fast)::value;
+        auto layer = [&](const uint32_t* L, int li, int zi, const uint2& m0, const uint2& m1) {
             uint2* hs = hsb + (li & 1) * (CBR * CW);
-            uint4 m = *reinterpret_cast<const uint4*>(L + hoff);
-            uint32_t e = L[eoff];
-            if (!FAST) {
-                const uint32_t rv = 0u - uint32_t(unsigned(zi) <= hzlim);  // all ones iff a cell row
-                m.x &= M0 & rv;
-                m.y &= M1 & rv;
-                m.z &= M2 & rv;
-                m.w &= M3 & rv;
-                e &= Me & rv;
-            }
+            const uint4 m = *reinterpret_cast<const uint4*>(L + hoff);
+            const uint32_t e = L[eoff];
             const uint32_t got = __shfl_xor_sync(0xffffffffu, hc ? m.x : m.w, 1);  // partner's word
             {
                 const uint32_t W0 = hc ? got : e, W5 = hc ? e : got;
@@ -837,9 +818,7 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
             const uint32_t o0 = life_sat(va[0], vb[0], vc[0], alive_cur0) & tmk.x;
             const uint32_t o1 = life_sat(va[1], vb[1], vc[1], alive_cur1) & tmk.y;
             const int zo = zi - 1;
-            if (FAST) {
-                if (zo >= it.z0 && zo < it.z1) *reinterpret_cast<uint2*>(optr) = make_uint2(o0, o1);
-            } else if (zo >= it.z0 && zo <= ozlim) {
+            if (zo >= it.z0 && zo <= ozlim) {
                 if (smode == 2) *reinterpret_cast<uint2*>(optr) = make_uint2(o0, o1);
                 else if (smode == 1) *optr = o0;
             }
@@ -863,23 +842,20 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
             }
             // output layers of this stage: z0 - 2 + 8 st + li; their tile masks
             const int zt = it.z0 + CLZ * st;  // layer of li = 2 (a multiple of 8)
-            const uint2 m0 = tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, zt / RHO);
-            const uint2 m1 = RHO == 4 ? tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, zt / RHO + 1) : m0;
+            uint2 m0 = tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, zt / RHO);
+            uint2 m1 = RHO == 4 ? tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, zt / RHO + 1) : m0;
+            m0.x &= xm0, m0.y &= xm1, m1.x &= xm0, m1.y &= xm1;
             while (!mbar_try_wait(mbar0 + 8 * b, (seq >> 1) & 1u)) {
             }
             const uint32_t* buf = reinterpret_cast<const uint32_t*>(wbase + b * CSTAGE);
             const int zbase = it.z0 - 1 + CLZ * st;
-            if (st < nfull && interior) {
+            if (st < nfull) {
 #pragma unroll
-                for (int li = 0; li < CLZ; ++li)
-                    layer(std::true_type{}, buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
+                for (int li = 0; li < CLZ; ++li) layer(buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
             } else {
-                // boundary items and tail stages: one rolled copy of the layer
-                // (the instruction cache holds the whole kernel)
-                const int nl = st < nfull ? CLZ : tail;
+                // the tail stage: one rolled copy of the layer
 #pragma unroll 1
-                for (int li = 0; li < nl; ++li)
-                    layer(std::false_type{}, buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
+                for (int li = 0; li < tail; ++li) layer(buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
             }
             mprev = RHO == 4 ? m1 : m0;
             ++seq;

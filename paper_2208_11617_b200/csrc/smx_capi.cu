@@ -78,6 +78,11 @@ struct DeviceRes {
     void* pool[11] = {};
     size_t pool_bytes[11] = {};
     std::pair<int64_t, int64_t> cols_key{-1, -1};  // (side, layers per item) of the items in slot 8
+    // the bit-shadow pools (slots 3, 4) keep every non-cell bit zero (the
+    // column engine reads them unmasked): zeroed when (re)allocated or when
+    // the side — the pitched layout — changes
+    const void* shadow_ptr[2] = {nullptr, nullptr};
+    int64_t shadow_side[2] = {-1, -1};
     int cols_nitems = 0;
     std::map<std::pair<const void*, std::pair<int64_t, int64_t>>, CUtensorMap> tmaps;
     smx::DevCounters* counters = nullptr;
@@ -198,6 +203,9 @@ int pool_get(int slot, size_t bytes, void** out) {
     *out = r->pool[slot];
     return SMX_OK;
 }
+
+// a bit-shadow pool slot (3 or 4) for side S whose non-cell bits are zero
+int shadow_get(int slot, int64_t side, void** out, cudaStream_t s);
 
 int counters_buf(smx::DevCounters** out) {
     DeviceRes* r;
@@ -589,13 +597,27 @@ size_t bits_bytes(int64_t side) {
     return size_t(smx::bits_rows(int(side))) * size_t(smx::bits_pitch_words(int(side))) * 4;
 }
 
+int shadow_get(int slot, int64_t side, void** out, cudaStream_t s) {
+    const size_t bytes = bits_bytes(side);
+    if (int rc = pool_get(slot, bytes, out)) return rc;
+    DeviceRes* r;
+    if (int rc = device_res(&r)) return rc;
+    const int i = slot - 3;
+    if (r->shadow_ptr[i] != *out || r->shadow_side[i] != side) {
+        TRY(cudaMemsetAsync(*out, 0, bytes, s));
+        r->shadow_ptr[i] = *out;
+        r->shadow_side[i] = side;
+    }
+    return SMX_OK;
+}
+
 // One x-run step u8 -> u8: pack cur into pooled bit shadow A, k_ca_bits A -> B,
 // unpack B into next.
 int ca_runs_step(const smx_grid* g, const smx::Geom& k, int64_t wz0, int64_t wz1, const uint8_t* cur, uint8_t* next,
                  cudaStream_t s) {
     void *pa, *pb;
-    if (int rc = pool_get(3, bits_bytes(k.side), &pa)) return rc;
-    if (int rc = pool_get(4, bits_bytes(k.side), &pb)) return rc;
+    if (int rc = shadow_get(3, k.side, &pa, s)) return rc;
+    if (int rc = shadow_get(4, k.side, &pb, s)) return rc;
     if (wz0 == 0 && wz1 == k.ez) {
         // the whole grid: the engine's plan (issued first, on the side stream,
         // concurrent with the pack) + one persistent launch of 1 step
@@ -1636,8 +1658,8 @@ int smx_ca(const smx_grid* g, uint8_t* cells, uint64_t ncells, int64_t steps, in
     } else if (engine) {
         // bit-shadow engine: pack once, steps x (bits -> bits), unpack once
         void *pa, *pb;
-        if (int rc = pool_get(3, bits_bytes(k.side), &pa)) return rc;
-        if (int rc = pool_get(4, bits_bytes(k.side), &pb)) return rc;
+        if (int rc = shadow_get(3, k.side, &pa, s)) return rc;
+        if (int rc = shadow_get(4, k.side, &pb, s)) return rc;
         // the map applied once (chunk list / tile bitmap), then ONE persistent
         // launch for all steps, A -> B -> A ..., the final shadow unpacked in place
         smx::launch_pack_bits(k, cur, (uint32_t*)pa, s);
