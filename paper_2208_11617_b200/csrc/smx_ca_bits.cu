@@ -647,7 +647,7 @@ constexpr int CLAYER = CBW * CBR * 4;        // 640 B per layer of a stage
 constexpr int CHS = 2 * CBR * CW * 8;        // h-sums of two layers: [parity][10 rows][8 words][a, b]
 constexpr int CWARP_BYTES = 2 * CSTAGE + CHS + 64;  // 10944 (128-aligned: 10944 = 85.5 * 128 -> pad)
 constexpr int CWARP = (CWARP_BYTES + 127) & ~127;
-constexpr int CNW = 16;                  // warps per CTA (persistent: one CTA per SM; 18 with the 96-register cap: 234 vs 217 us per C5 step)
+constexpr int CNW = 16;                  // warps per CTA (persistent: one CTA per SM; 18 measured no faster: 219 vs 218 us per C5 step)
 
 struct ColItem {
     int iy, g, z0, z1;  // rows 8 iy .. 8 iy + 7, words 8 g .. 8 g + 7, layers z0 .. z1 - 1
