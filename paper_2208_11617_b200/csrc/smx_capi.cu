@@ -525,12 +525,14 @@ int engine_plan(const smx_grid* g, const smx::Geom& k, int64_t steps, cudaStream
         TRY(cudaMemsetAsync(pbm, 0, bm_bytes, r->side));
         // the map, applied once: every emitted tile marked (stats: marked, duplicate)
         smx::launch_cols_mark(k, g->kind, P->bm, P->D, P->TW, (unsigned*)((uint8_t*)pbm + bm_bytes - 16), r->side);
-        // items: layer segments long enough for few atomics, short enough for ~6 items per warp
-        const int64_t target = 6 * int64_t(smx::cols_warps());
-        int64_t lz = 64;
-        while (lz > 8 && int64_t(col_items(k.side, lz).size() / 4) < target) lz /= 2;
-        if (r->cols_key != std::make_pair(int64_t(k.side), lz)) {
-            const std::vector<int32_t> v = col_items(k.side, lz);
+        // items: layer segments long enough for few atomics, short enough for
+        // ~6 items per warp; built and uploaded once per side (host work off
+        // the per-call path)
+        if (r->cols_key.first != int64_t(k.side)) {
+            const int64_t target = 6 * int64_t(smx::cols_warps());
+            int64_t lz = 64;
+            std::vector<int32_t> v = col_items(k.side, lz);
+            while (lz > 8 && int64_t(v.size() / 4) < target) v = col_items(k.side, lz /= 2);
             void* pit;
             if (int rc = pool_get(8, v.size() * 4, &pit)) return rc;
             TRY(cudaMemcpy(pit, v.data(), v.size() * 4, cudaMemcpyHostToDevice));
