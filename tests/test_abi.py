@@ -152,3 +152,15 @@ def test_accum_range_contract_checked_before_device_work():
     for g in (api.grid_h3d(8), api.grid_trapezoids(9, 1)):
         rc = L.smx_accum_range(C.byref(g.raw), None, 0, 1, api.EXEC_RUNS, 0, 1, None, None)
         assert rc == 1 and b"row ranges" in L.smx_last_error()
+
+
+def test_engine_choice_and_rho16_rules_host_side():
+    """smx_ca_engine (host-side decision, no device work): the column engine
+    for states >= 96 M cells, the chunk engine below; none for 2-D grids."""
+    big = api.make_grid(api.map_kind.h3d, 3, 256, 8)     # C5: 1.42 G cells
+    c4 = api.make_grid(api.map_kind.h3d, 3, 128, 8)      # C4: 175 M
+    c2 = api.make_grid(api.map_kind.h3d, 3, 64, 4)       # C2: 2.7 M
+    assert api.ca_engine(big) == "column" and api.ca_engine(c4) == "column"
+    assert api.ca_engine(c2) == "chunk"
+    assert api.ca_engine(api.make_grid(api.map_kind.h3d, 3, 128, 16)) == "column"
+    assert api.ca_engine(api.grid_h2d(64)) == "none"
