@@ -368,9 +368,9 @@ __device__ __forceinline__ void run_items(const Chunk* __restrict__ s_chunk, int
                 const uint2 p = reinterpret_cast<const uint2*>(H + 8 * r0)[w];
                 const uint2 q = reinterpret_cast<const uint2*>(H + 8 * (r0 + 1))[w];
                 const uint2 u = reinterpret_cast<const uint2*>(H + 8 * (r0 + 2))[w];
-                return add3x2(p.x, p.y, q.x, q.y, u.x, u.y);
+                return vsum3(p.x, p.y, q.x, q.y, u.x, u.y);
             };
-            Planes4 va = vsum(lz0), vb = vsum(lz0 + 1);
+            V3 va = vsum(lz0), vb = vsum(lz0 + 1);
             const int y = ch.y0 + ly;
             const int w0 = ch.x0 >> 5;
             const int xw = 32 * (w0 + w);  // x of this lane's word
@@ -384,9 +384,9 @@ __device__ __forceinline__ void run_items(const Chunk* __restrict__ s_chunk, int
                                    ((w0 - 1) & 3) + 1 + w;
 #pragma unroll 2
             for (int lz = lz0; lz < lz0 + LZN; ++lz) {
-                const Planes4 vc = vsum(lz + 2);
+                const V3 vc = vsum(lz + 2);
                 const uint32_t alive = arow[lz * HL * BOXW];
-                const uint32_t O = life_planes(va, vb, vc, alive);
+                const uint32_t O = life_v3(va, vb, vc, alive, 0xffffffffu);
                 va = vb;
                 vb = vc;
                 if (ch.z0 + lz < zmax) *optr = O;
@@ -779,7 +779,7 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
         const uint32_t xm0 = __funnelshift_lc(0xffffffffu, 0u, max(yo - 32 * wo + 1, 0));
         const uint32_t xm1 = __funnelshift_lc(0xffffffffu, 0u, max(yo - 32 * wo - 31, 0));
         uint32_t* optr = out + ((long long)(it.z0 - 2) * S + yo) * WP + wo;  // output layer of input layer z0 - 1
-        Sat3 va[2], vb[2];
+        V3 va[2], vb[2];
         uint32_t alive_cur0 = 0u, alive_cur1 = 0u;
         uint2 mprev = make_uint2(0u, 0u);
 
@@ -805,18 +805,18 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
             }
             const uint2 an = *reinterpret_cast<const uint2*>(L + (ly + 1) * CBW + 4 + jp);
             __syncwarp();
-            Sat3 vc[2];
+            V3 vc[2];
             {
                 const uint4 p = *reinterpret_cast<const uint4*>(hs + ly * CW + jp);
                 const uint4 q = *reinterpret_cast<const uint4*>(hs + (ly + 1) * CW + jp);
                 const uint4 u = *reinterpret_cast<const uint4*>(hs + (ly + 2) * CW + jp);
-                vc[0] = sat3(add3x2(p.x, p.y, q.x, q.y, u.x, u.y));
-                vc[1] = sat3(add3x2(p.z, p.w, q.z, q.w, u.z, u.w));
+                vc[0] = vsum3(p.x, p.y, q.x, q.y, u.x, u.y);
+                vc[1] = vsum3(p.z, p.w, q.z, q.w, u.z, u.w);
             }
             // the rule for output layer zo = zi - 1 (stored when z0 <= zo <= ozlim)
             const uint2 tmk = li < 2 ? mprev : (RHO == 4 && li >= 6 ? m1 : m0);
-            const uint32_t o0 = life_sat(va[0], vb[0], vc[0], alive_cur0) & tmk.x;
-            const uint32_t o1 = life_sat(va[1], vb[1], vc[1], alive_cur1) & tmk.y;
+            const uint32_t o0 = life_v3(va[0], vb[0], vc[0], alive_cur0, tmk.x);
+            const uint32_t o1 = life_v3(va[1], vb[1], vc[1], alive_cur1, tmk.y);
             const int zo = zi - 1;
             if (zo >= it.z0 && zo <= ozlim) {
                 if (smode == 2) *reinterpret_cast<uint2*>(optr) = make_uint2(o0, o1);

@@ -81,24 +81,55 @@ __device__ __forceinline__ uint32_t life_planes(const Planes4& a, const Planes4&
     return (eq3 | (eq4 & alive)) & ~(r3 | r4);
 }
 
-// The column engine's rule on SATURATED vertical sums: a 9-cell sum v <= 9 is
-// kept as its low three bit-planes plus a flag for v >= 5 (computed once per
-// layer, used by three output layers). S = va + vb + vc is 3 or 4 only if no
-// term is >= 5, so the 27-sum needs three carry-save planes, one carry chain
-// of two bits and a kill flag (k3 | c3: S >= 8; any big term: S >= 5).
-struct Sat3 {
-    uint32_t b0, b1, b2, big;
+// ---- the engines' rule as an explicit LOP3 network ----
+//
+// One LOP3 (any 3-input boolean function) per line; the immediates are the
+// function applied to (0xF0, 0xCC, 0xAA). ptxas keeps asm lop3 as written, so
+// the ALU-pipe count per output word is the count below: 6 for the vertical
+// sum (once per layer, used by three output layers) + 14 for the rule incl.
+// the output mask, against 10 + 17 for the add3x2 / four-plane form.
+template <unsigned LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+    return d;
+}
+
+// A 9-cell (3 rows x 3 columns) sum v <= 9 as three bit-planes, SATURATED:
+// exact for v <= 7, and 6 or 7 for v = 8, 9. The rule only asks whether the
+// 27-sum is 3 or 4, which a term >= 5 already rules out, so three planes carry
+// everything it needs.
+struct V3 {
+    uint32_t b0, b1, b2;
 };
-__device__ __forceinline__ Sat3 sat3(const Planes4& v) { return Sat3{v.b0, v.b1, v.b2, v.b3 | (v.b2 & (v.b1 | v.b0))}; }
-__device__ __forceinline__ uint32_t life_sat(const Sat3& a, const Sat3& b, const Sat3& c, uint32_t alive) {
-    const uint32_t s0 = a.b0 ^ b.b0 ^ c.b0, k1 = (a.b0 & b.b0) | (a.b0 & c.b0) | (b.b0 & c.b0);
-    const uint32_t s1 = a.b1 ^ b.b1 ^ c.b1, k2 = (a.b1 & b.b1) | (a.b1 & c.b1) | (b.b1 & c.b1);
-    const uint32_t s2 = a.b2 ^ b.b2 ^ c.b2, k3 = (a.b2 & b.b2) | (a.b2 & c.b2) | (b.b2 & c.b2);
-    const uint32_t t1 = s1 ^ k1, c2 = s1 & k1;
-    const uint32_t t2 = s2 ^ k2 ^ c2, c3 = (s2 & k2) | (s2 & c2) | (k2 & c2);
-    const uint32_t kill = k3 | c3 | a.big | b.big | c.big;
-    const uint32_t eq3 = s0 & t1 & ~t2, eq4 = ~s0 & ~t1 & t2;  // S == 3, S == 4 (when not killed)
-    return (eq3 | (eq4 & alive)) & ~kill;
+// p, q, u: three horizontal 3-sums (bit-planes x0, x1 of values <= 3)
+__device__ __forceinline__ V3 vsum3(uint32_t p0, uint32_t p1, uint32_t q0, uint32_t q1, uint32_t u0, uint32_t u1) {
+    const uint32_t s0 = lop3<0x96>(p0, q0, u0);  // weight 1
+    const uint32_t k1 = lop3<0xe8>(p0, q0, u0);  // carry, weight 2
+    const uint32_t t = lop3<0x96>(p1, q1, u1);   // weight 2
+    const uint32_t m = lop3<0xe8>(p1, q1, u1);   // weight 4
+    // v = s0 + 2 (t + k1) + 4 m: b1 = t ^ k1, b2 = m ^ (t & k1); when v >= 8
+    // (m & t & k1) both are forced to 1 instead
+    return V3{s0, lop3<0xbc>(t, k1, m), lop3<0xf8>(m, t, k1)};
+}
+// next = (S == 3) | (alive & S == 4) for S = a + b + c (the 27-sum including
+// the cell), masked: with s0, k1 / s1, k2 the carry-save sums of planes 0 / 1,
+// S = s0 + 2 (s1 + k1) + 4 (k2 + a2 + b2 + c2). S == 3 needs s0 = 1, exactly
+// one of s1, k1 and no weight-4 term; S == 4 needs s0 = 0 and either s1 = k1 = 1
+// and no weight-4 term, or s1 = k1 = 0 and exactly one.
+__device__ __forceinline__ uint32_t life_v3(const V3& a, const V3& b, const V3& c, uint32_t alive, uint32_t mask) {
+    const uint32_t s0 = lop3<0x96>(a.b0, b.b0, c.b0), k1 = lop3<0xe8>(a.b0, b.b0, c.b0);
+    const uint32_t s1 = lop3<0x96>(a.b1, b.b1, c.b1), k2 = lop3<0xe8>(a.b1, b.b1, c.b1);
+    const uint32_t o2 = lop3<0xfe>(a.b2, b.b2, c.b2);  // any of a2, b2, c2
+    const uint32_t e2 = lop3<0x16>(a.b2, b.b2, c.b2);  // exactly one
+    const uint32_t w0 = lop3<0x03>(o2, k2, 0u);        // no weight-4 term
+    const uint32_t w1 = lop3<0x3a>(k2, o2, e2);        // exactly one weight-4 term
+    const uint32_t g = lop3<0x68>(s0, s1, k1);         // s0 ? s1 ^ k1 : s1 & k1
+    const uint32_t sl = lop3<0xfc>(s0, alive, 0u);     // s0 | alive
+    const uint32_t t3 = lop3<0x80>(g, w0, sl);         // S == 3, or alive & S == 4 (s1 = k1 = 1)
+    const uint32_t z = lop3<0x01>(s0, s1, k1);         // s0 = s1 = k1 = 0
+    const uint32_t t4 = lop3<0x80>(z, w1, alive);      // alive & S == 4 (s1 = k1 = 0)
+    return lop3<0xa8>(t3, t4, mask);
 }
 
 // ---- map-driven chunking ----
