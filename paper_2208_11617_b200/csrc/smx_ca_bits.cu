@@ -681,12 +681,17 @@ __global__ void __launch_bounds__(256) k_cols_mark(Geom g, uint32_t* __restrict_
 
 // 2 cell words' coverage mask from the tile bitmap: word k of the lane covers
 // tiles 32 (w + k) / RHO ...; every tile bit becomes RHO cell bits
+// a lane's bitmap word for tile row (ty, tz) (its two output words' tiles
+// start at bit t0 & 31, t0 = w * 32 / RHO; w even: the 2 * 32 / RHO bits share
+// one word); 0 past the domain. Loaded a stage ahead of its use (tile_mask2).
+__device__ __forceinline__ uint32_t tile_word(const uint32_t* __restrict__ bm, int D, int TW, int t0, int ty, int tz) {
+    if (ty >= D || tz >= D) return 0u;
+    return __ldg(bm + ((long long)tz * D + ty) * TW + (t0 >> 5));
+}
 template <int RHO>
-__device__ __forceinline__ uint2 tile_mask2(const uint32_t* __restrict__ bm, int D, int TW, int w, int ty, int tz) {
-    if (ty >= D || tz >= D) return make_uint2(0u, 0u);
+__device__ __forceinline__ uint2 tile_mask2(uint32_t word, int t0) {
     constexpr int TPW = 32 / RHO;  // tiles per cell word
-    const int t0 = w * TPW;        // first tile (w even: the 2 * TPW bits share one bitmap word)
-    const uint32_t bits = bm[((long long)tz * D + ty) * TW + (t0 >> 5)] >> (t0 & 31);
+    const uint32_t bits = word >> (t0 & 31);
     uint32_t m[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
@@ -743,21 +748,43 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
     const int lane = threadIdx.x & 31;
     uint2* hsb = reinterpret_cast<uint2*>(wbase + 2 * CSTAGE);  // 2 x [CBR][CW] (a, b), by layer parity
     const int hr = min(lane >> 1, CBR - 1), hc = lane & 1;      // h-sum role (lanes 0..19; 20..31 mirror row 9)
-    const bool hlane = lane < 2 * CBR;
     const int ly = lane >> 2, jp = 2 * (lane & 3);              // output role
     const long long zstride = (long long)S * WP;
+    // item indices come from one atomic per item, grabbed an item ahead by
+    // lane 0, which also loads the item and issues its first stage; the other
+    // lanes get it by shuffle only when they need it (the atomic's and the
+    // load's latency overlap the current item). The bitmap words of a stage's
+    // tile masks are loaded a stage ahead.
     int cur = 0;
-    if (lane == 0) cur = int(atomicAdd(ctr, 1u));
+    ColItem it{0, 0, 0, 0};
+    if (lane == 0) {
+        cur = int(atomicAdd(ctr, 1u));
+        if (cur < nitems) {
+            it = items[cur];
+            fence_proxy_async();
+            cols_issue(tm, it, 0, wbase + (seq & 1) * CSTAGE, mbar0 + 8 * (seq & 1));
+        }
+    }
     cur = __shfl_sync(0xffffffffu, cur, 0);
-    if (cur < nitems && lane == 0) {
-        fence_proxy_async();
-        cols_issue(tm, items[cur], 0, wbase + (seq & 1) * CSTAGE, mbar0 + 8 * (seq & 1));
+    it.iy = __shfl_sync(0xffffffffu, it.iy, 0);
+    it.g = __shfl_sync(0xffffffffu, it.g, 0);
+    it.z0 = __shfl_sync(0xffffffffu, it.z0, 0);
+    it.z1 = __shfl_sync(0xffffffffu, it.z1, 0);
+    constexpr int TPW = 32 / RHO;
+    // the first stage's bitmap words (layer z0 of tile row (y / RHO, z0 / RHO))
+    uint32_t bw0 = 0u, bw1 = 0u;
+    if (cur < nitems) {
+        const int yo = 8 * it.iy + ly, t0 = (8 * it.g + jp) * TPW;
+        bw0 = tile_word(bm, D, TW, t0, yo / RHO, it.z0 / RHO);
+        if (RHO == 4) bw1 = tile_word(bm, D, TW, t0, yo / RHO, it.z0 / RHO + 1);
     }
     while (cur < nitems) {
-        const ColItem it = items[cur];
         int nxt = 0;
-        if (lane == 0) nxt = int(atomicAdd(ctr, 1u));
-        nxt = __shfl_sync(0xffffffffu, nxt, 0);
+        ColItem itn{0, 0, 0, 0};
+        if (lane == 0) {
+            nxt = int(atomicAdd(ctr, 1u));
+            if (nxt < nitems) itn = items[nxt];
+        }
         // input layers z0 - 1 .. z1 (z0 is a multiple of 8): full stages of 8
         // layers, then a tail stage of the rest
         const int nin = it.z1 - it.z0 + 2;
@@ -783,36 +810,37 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
         uint32_t alive_cur0 = 0u, alive_cur1 = 0u;
         uint2 mprev = make_uint2(0u, 0u);
 
-        // one input layer: h-sums -> vertical sums -> the rule for the layer behind
-        auto layer = [&](const uint32_t* L, int li, int zi, const uint2& m0, const uint2& m1) {
-            uint2* hs = hsb + (li & 1) * (CBR * CW);
+        // h-sums of input layer li (all 32 lanes store: lanes 20..31 repeat
+        // row 9's values, which keeps the code branch-free)
+        auto hsum = [&](const uint32_t* L, int li) {
             const uint4 m = *reinterpret_cast<const uint4*>(L + hoff);
             const uint32_t e = L[eoff];
             const uint32_t got = __shfl_xor_sync(0xffffffffu, hc ? m.x : m.w, 1);  // partner's word
-            {
-                const uint32_t W0 = hc ? got : e, W5 = hc ? e : got;
-                const uint32_t l0 = shl1_fma(W0, m.x), r0 = shr1_fma(m.x, m.y);
-                const uint32_t l1 = shl1_fma(m.x, m.y), r1 = shr1_fma(m.y, m.z);
-                const uint32_t l2 = shl1_fma(m.y, m.z), r2 = shr1_fma(m.z, m.w);
-                const uint32_t l3 = shl1_fma(m.z, m.w), r3 = shr1_fma(m.w, W5);
-                if (hlane) {
-                    uint4* dst = reinterpret_cast<uint4*>(hsw + (li & 1) * (CBR * CW));
-                    dst[0] = make_uint4(l0 ^ m.x ^ r0, (l0 & m.x) | (l0 & r0) | (m.x & r0), l1 ^ m.y ^ r1,
-                                        (l1 & m.y) | (l1 & r1) | (m.y & r1));
-                    dst[1] = make_uint4(l2 ^ m.z ^ r2, (l2 & m.z) | (l2 & r2) | (m.z & r2), l3 ^ m.w ^ r3,
-                                        (l3 & m.w) | (l3 & r3) | (m.w & r3));
-                }
-            }
-            const uint2 an = *reinterpret_cast<const uint2*>(L + (ly + 1) * CBW + 4 + jp);
-            __syncwarp();
+            const uint32_t W0 = hc ? got : e, W5 = hc ? e : got;
+            const uint32_t l0 = shl1_fma(W0, m.x), r0 = shr1_fma(m.x, m.y);
+            const uint32_t l1 = shl1_fma(m.x, m.y), r1 = shr1_fma(m.y, m.z);
+            const uint32_t l2 = shl1_fma(m.y, m.z), r2 = shr1_fma(m.z, m.w);
+            const uint32_t l3 = shl1_fma(m.z, m.w), r3 = shr1_fma(m.w, W5);
+            uint4* dst = reinterpret_cast<uint4*>(hsw + (li & 1) * (CBR * CW));
+            dst[0] = make_uint4(lop3<0x96>(l0, m.x, r0), lop3<0xe8>(l0, m.x, r0), lop3<0x96>(l1, m.y, r1),
+                                lop3<0xe8>(l1, m.y, r1));
+            dst[1] = make_uint4(lop3<0x96>(l2, m.z, r2), lop3<0xe8>(l2, m.z, r2), lop3<0x96>(l3, m.w, r3),
+                                lop3<0xe8>(l3, m.w, r3));
+        };
+        // input layer li of a stage of n: its h-sums are in shared memory; the
+        // next layer's h-sums are computed while its vertical sums and the rule
+        // for the layer behind run (independent work for the scheduler)
+        auto layer = [&](const uint32_t* buf, int li, int n, int zi, const uint2& m0, const uint2& m1) {
+            __syncwarp();  // h-sums of layer li visible; layer li - 1's reads done
+            const uint2* hs = hsb + (li & 1) * (CBR * CW);
+            const uint4 p = *reinterpret_cast<const uint4*>(hs + ly * CW + jp);
+            const uint4 q = *reinterpret_cast<const uint4*>(hs + (ly + 1) * CW + jp);
+            const uint4 u = *reinterpret_cast<const uint4*>(hs + (ly + 2) * CW + jp);
+            const uint2 an = *reinterpret_cast<const uint2*>(buf + li * (CLAYER / 4) + (ly + 1) * CBW + 4 + jp);
+            if (li + 1 < n) hsum(buf + (li + 1) * (CLAYER / 4), li + 1);
             V3 vc[2];
-            {
-                const uint4 p = *reinterpret_cast<const uint4*>(hs + ly * CW + jp);
-                const uint4 q = *reinterpret_cast<const uint4*>(hs + (ly + 1) * CW + jp);
-                const uint4 u = *reinterpret_cast<const uint4*>(hs + (ly + 2) * CW + jp);
-                vc[0] = vsum3(p.x, p.y, q.x, q.y, u.x, u.y);
-                vc[1] = vsum3(p.z, p.w, q.z, q.w, u.z, u.w);
-            }
+            vc[0] = vsum3(p.x, p.y, q.x, q.y, u.x, u.y);
+            vc[1] = vsum3(p.z, p.w, q.z, q.w, u.z, u.w);
             // the rule for output layer zo = zi - 1 (stored when z0 <= zo <= ozlim)
             const uint2 tmk = li < 2 ? mprev : (RHO == 4 && li >= 6 ? m1 : m0);
             const uint32_t o0 = life_v3(va[0], vb[0], vc[0], alive_cur0, tmk.x);
@@ -831,6 +859,7 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
             alive_cur1 = an.y;
         };
 
+        const int t0 = wo * TPW;
         for (int st = 0; st < nst; ++st) {
             const uint32_t b = seq & 1;
             // the other buffer is free (its stage was consumed): prefetch the
@@ -838,29 +867,49 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
             if (lane == 0) {
                 fence_proxy_async();
                 if (st + 1 < nst) cols_issue(tm, it, st + 1, wbase + (b ^ 1) * CSTAGE, mbar0 + 8 * (b ^ 1));
-                else if (nxt < nitems) cols_issue(tm, items[nxt], 0, wbase + (b ^ 1) * CSTAGE, mbar0 + 8 * (b ^ 1));
+                else if (nxt < nitems) cols_issue(tm, itn, 0, wbase + (b ^ 1) * CSTAGE, mbar0 + 8 * (b ^ 1));
             }
             // output layers of this stage: z0 - 2 + 8 st + li; their tile masks
-            const int zt = it.z0 + CLZ * st;  // layer of li = 2 (a multiple of 8)
-            uint2 m0 = tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, zt / RHO);
-            uint2 m1 = RHO == 4 ? tile_mask2<RHO>(bm, D, TW, wo, yo / RHO, zt / RHO + 1) : m0;
+            // (from the words loaded a stage ago), and the next stage's words
+            uint2 m0 = tile_mask2<RHO>(bw0, t0);
+            uint2 m1 = RHO == 4 ? tile_mask2<RHO>(bw1, t0) : m0;
             m0.x &= xm0, m0.y &= xm1, m1.x &= xm0, m1.y &= xm1;
+            if (st + 1 < nst) {
+                const int zt = it.z0 + CLZ * (st + 1);
+                bw0 = tile_word(bm, D, TW, t0, yo / RHO, zt / RHO);
+                if (RHO == 4) bw1 = tile_word(bm, D, TW, t0, yo / RHO, zt / RHO + 1);
+            } else {
+                // the next item: broadcast (lane 0 loaded it an item ago)
+                nxt = __shfl_sync(0xffffffffu, nxt, 0);
+                itn.iy = __shfl_sync(0xffffffffu, itn.iy, 0);
+                itn.g = __shfl_sync(0xffffffffu, itn.g, 0);
+                itn.z0 = __shfl_sync(0xffffffffu, itn.z0, 0);
+                itn.z1 = __shfl_sync(0xffffffffu, itn.z1, 0);
+                if (nxt < nitems) {
+                    const int nyo = 8 * itn.iy + ly, nt0 = (8 * itn.g + jp) * TPW;
+                    bw0 = tile_word(bm, D, TW, nt0, nyo / RHO, itn.z0 / RHO);
+                    if (RHO == 4) bw1 = tile_word(bm, D, TW, nt0, nyo / RHO, itn.z0 / RHO + 1);
+                }
+            }
             while (!mbar_try_wait(mbar0 + 8 * b, (seq >> 1) & 1u)) {
             }
             const uint32_t* buf = reinterpret_cast<const uint32_t*>(wbase + b * CSTAGE);
             const int zbase = it.z0 - 1 + CLZ * st;
+            __syncwarp();  // the previous stage's last h-sum reads are done
+            hsum(buf, 0);
             if (st < nfull) {
 #pragma unroll
-                for (int li = 0; li < CLZ; ++li) layer(buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
+                for (int li = 0; li < CLZ; ++li) layer(buf, li, CLZ, zbase + li, m0, m1);
             } else {
                 // the tail stage: one rolled copy of the layer
 #pragma unroll 1
-                for (int li = 0; li < tail; ++li) layer(buf + li * (CLAYER / 4), li, zbase + li, m0, m1);
+                for (int li = 0; li < tail; ++li) layer(buf, li, tail, zbase + li, m0, m1);
             }
             mprev = RHO == 4 ? m1 : m0;
             ++seq;
         }
         cur = nxt;
+        it = itn;
     }
 }
 
