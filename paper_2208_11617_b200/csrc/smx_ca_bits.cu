@@ -645,9 +645,8 @@ constexpr int CLZ = 8;                   // layers per TMA stage
 constexpr int CSTAGE = CBW * CBR * CLZ * 4;  // 5120 B
 constexpr int CLAYER = CBW * CBR * 4;        // 640 B per layer of a stage
 constexpr int CHS = 2 * CBR * CW * 8;        // h-sums of two layers: [parity][10 rows][8 words][a, b]
-constexpr int CWARP_BYTES = 2 * CSTAGE + CHS + 64;  // 10944 (128-aligned: 10944 = 85.5 * 128 -> pad)
-constexpr int CWARP = (CWARP_BYTES + 127) & ~127;
-constexpr int CNW = 16;                  // warps per CTA (persistent: one CTA per SM; 18 measured no faster: 219 vs 218 us per C5 step)
+constexpr int CWARP = 2 * CSTAGE + CHS;  // 11520 B per warp (90 x 128); the mbarriers follow all warps' regions
+constexpr int CNW = 16;                  // warps per CTA (persistent: one CTA per SM; 20 measured slower: 202 vs 195 us per C5 step)
 
 struct ColItem {
     int iy, g, z0, z1;  // rows 8 iy .. 8 iy + 7, words 8 g .. 8 g + 7, layers z0 .. z1 - 1
@@ -983,7 +982,7 @@ __global__ void __launch_bounds__(CNW * 32) k_cols_run(const __grid_constant__ C
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint8_t* wbase = smem + warp * CWARP;
-    const uint32_t mbar0 = smem_u32(wbase + 2 * CSTAGE + CHS);
+    const uint32_t mbar0 = smem_u32(smem + CNW * CWARP + 16 * warp);
     if (lane == 0) {
         mbar_init(mbar0, 1);
         mbar_init(mbar0 + 8, 1);
@@ -1201,7 +1200,7 @@ int cols_grid() {
     const int dev = current_device();
     int local = 0;
     once_per_device(once, dev, [&] {
-        const int smem = CNW * CWARP;
+        const int smem = CNW * (CWARP + 16);
         cudaFuncSetAttribute(k_cols_run<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(k_cols_run<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(k_cols_run<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1219,7 +1218,7 @@ cudaError_t launch_cols_run(const Geom& g, const void* tmA, const void* tmB, uin
                             const void* items, int nitems, unsigned* ctl, const uint32_t* bm, int D, int TW, int steps,
                             cudaStream_t s) {
     const int grid = cols_grid();
-    const int smem = CNW * CWARP;
+    const int smem = CNW * (CWARP + 16);
     int S = g.side, WP = bits_pitch_words(g.side);
     const ColItem* it = reinterpret_cast<const ColItem*>(items);
     void* args[] = {const_cast<void*>(tmA), const_cast<void*>(tmB), &A, &B, &it, &nitems, &ctl,

@@ -372,6 +372,20 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 3-D tiled tensor map over a pitched bit shadow: (WP words, S rows, S layers),
 // box b0 words x b1 rows x b2 layers; out-of-range coordinates read as zero.
+// L2 sector promotion of the bit-shadow boxes (SMX_TMA_PROMO=none|64|128|256
+// for experiments; default 128)
+CUtensorMapL2promotion tma_promotion() {
+    static const CUtensorMapL2promotion p = [] {
+        const char* e = std::getenv("SMX_TMA_PROMO");
+        if (!e) return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+        const std::string v(e);
+        if (v == "none") return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+        if (v == "64") return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+        if (v == "256") return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+        return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    }();
+    return p;
+}
 int bits_tmap_box(const uint32_t* bits, int64_t side, int b0, int b1, int b2, const CUtensorMap** out) {
     DeviceRes* r;
     if (int rc = device_res(&r)) return rc;
@@ -391,7 +405,7 @@ int bits_tmap_box(const uint32_t* bits, int64_t side, int b0, int b1, int b2, co
     cuuint32_t estr[3] = {1u, 1u, 1u};
     CUtensorMap m;
     CUresult cr = fn(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(bits), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, tma_promotion(),
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return fail(SMX_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(cr)));
     auto res = r->tmaps.emplace(key, m);
@@ -525,14 +539,21 @@ int engine_plan(const smx_grid* g, const smx::Geom& k, int64_t steps, cudaStream
         TRY(cudaMemsetAsync(pbm, 0, bm_bytes, r->side));
         // the map, applied once: every emitted tile marked (stats: marked, duplicate)
         smx::launch_cols_mark(k, g->kind, P->bm, P->D, P->TW, (unsigned*)((uint8_t*)pbm + bm_bytes - 16), r->side);
-        // items: layer segments long enough for few atomics, short enough for
-        // ~6 items per warp; built and uploaded once per side (host work off
-        // the per-call path)
+        // items: layer segments long enough for few atomics and little
+        // warm-up, short enough for ~6 items per warp where the side allows;
+        // built and uploaded once per side (host work off the per-call path)
         if (r->cols_key.first != int64_t(k.side)) {
             const int64_t target = 6 * int64_t(smx::cols_warps());
             int64_t lz = 64;
             std::vector<int32_t> v = col_items(k.side, lz);
-            while (lz > 8 && int64_t(v.size() / 4) < target) v = col_items(k.side, lz /= 2);
+            if (const char* e = std::getenv("SMX_COLS_LZ")) {  // experiments: a fixed item length
+                lz = std::max<int64_t>(8, std::atoll(e) / 8 * 8);
+                v = col_items(k.side, lz);
+            } else {
+                // not below 32 layers: an item pays two warm-up layers and a
+                // partial tail stage (C4: lz 8 -> 32 is 43.4 -> 38.0 us per step)
+                while (lz > 32 && int64_t(v.size() / 4) < target) v = col_items(k.side, lz /= 2);
+            }
             void* pit;
             if (int rc = pool_get(8, v.size() * 4, &pit)) return rc;
             TRY(cudaMemcpy(pit, v.data(), v.size() * 4, cudaMemcpyHostToDevice));
