@@ -829,7 +829,7 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
         // input layer li of a stage of n: its h-sums are in shared memory; the
         // next layer's h-sums are computed while its vertical sums and the rule
         // for the layer behind run (independent work for the scheduler)
-        auto layer = [&](const uint32_t* buf, int li, int n, int zi, const uint2& m0, const uint2& m1) {
+        auto layer = [&](const uint32_t* buf, int li, int n, int zi, const uint2& m0, const uint2& m1, bool first) {
             __syncwarp();  // h-sums of layer li visible; layer li - 1's reads done
             const uint2* hs = hsb + (li & 1) * (CBR * CW);
             const uint4 p = *reinterpret_cast<const uint4*>(hs + ly * CW + jp);
@@ -840,14 +840,17 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
             V3 vc[2];
             vc[0] = vsum3(p.x, p.y, q.x, q.y, u.x, u.y);
             vc[1] = vsum3(p.z, p.w, q.z, q.w, u.z, u.w);
-            // the rule for output layer zo = zi - 1 (stored when z0 <= zo <= ozlim)
-            const uint2 tmk = li < 2 ? mprev : (RHO == 4 && li >= 6 ? m1 : m0);
-            const uint32_t o0 = life_v3(va[0], vb[0], vc[0], alive_cur0, tmk.x);
-            const uint32_t o1 = life_v3(va[1], vb[1], vc[1], alive_cur1, tmk.y);
-            const int zo = zi - 1;
-            if (zo >= it.z0 && zo <= ozlim) {
-                if (smode == 2) *reinterpret_cast<uint2*>(optr) = make_uint2(o0, o1);
-                else if (smode == 1) *optr = o0;
+            // the rule for output layer zo = zi - 1 (stored when z0 <= zo <= ozlim;
+            // skipped for the item's two warm-up layers, zo = z0 - 2, z0 - 1)
+            if (li >= 2 || !first) {
+                const uint2 tmk = li < 2 ? mprev : (RHO == 4 && li >= 6 ? m1 : m0);
+                const uint32_t o0 = life_v3(va[0], vb[0], vc[0], alive_cur0, tmk.x);
+                const uint32_t o1 = life_v3(va[1], vb[1], vc[1], alive_cur1, tmk.y);
+                const int zo = zi - 1;
+                if (zo >= it.z0 && zo <= ozlim) {
+                    if (smode == 2) *reinterpret_cast<uint2*>(optr) = make_uint2(o0, o1);
+                    else if (smode == 1) *optr = o0;
+                }
             }
             optr += zstride;
             va[0] = vb[0];
@@ -896,13 +899,18 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
             const int zbase = it.z0 - 1 + CLZ * st;
             __syncwarp();  // the previous stage's last h-sum reads are done
             hsum(buf, 0);
+            const bool first = st == 0;
             if (st < nfull) {
 #pragma unroll
-                for (int li = 0; li < CLZ; ++li) layer(buf, li, CLZ, zbase + li, m0, m1);
+                for (int li = 0; li < CLZ; ++li) layer(buf, li, CLZ, zbase + li, m0, m1, first);
+            } else if (tail == 2) {
+                // the usual tail (items of a multiple of 8 layers read 2 more)
+                layer(buf, 0, 2, zbase, m0, m1, first);
+                layer(buf, 1, 2, zbase + 1, m0, m1, first);
             } else {
-                // the tail stage: one rolled copy of the layer
+                // other tails (segments cut by the tetrahedron's face): one rolled copy
 #pragma unroll 1
-                for (int li = 0; li < tail; ++li) layer(buf, li, tail, zbase + li, m0, m1);
+                for (int li = 0; li < tail; ++li) layer(buf, li, tail, zbase + li, m0, m1, first);
             }
             mprev = RHO == 4 ? m1 : m0;
             ++seq;
