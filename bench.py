@@ -585,6 +585,11 @@ def extra_configs(api, sampler, peak, args, energy):
                        "h_vs_bb": round(bms / hms, 3), "h_ms_per_call": round(hms, 4),
                        "h_u8_basis_gb_s": round(gbs, 1), "h_roofline_frac": round(gbs / peak, 4),
                        "run_kernel_ms_per_step": round(kms, 5), "run_kernel_roofline_frac": round(kgbs / peak, 4),
+                       # the bytes the bit engine must move (bit shadow read + written once per step)
+                       # against HBM: it is instruction bound (ncu: ALU pipe / issue), not HBM bound
+                       "run_kernel_bits_basis_frac": round(2.0 * cells / 8 / (kms * 1e-3) / 1e9 / peak, 4),
+                       "run_kernel_bound": "instruction issue (LOP3 on the ALU pipe + shared-memory latency; "
+                                           "DESIGN.md section 6)",
                        "note": "pack + plan + ONE persistent launch of ca_steps steps + unpack per call; "
                                "2 B/cell/step u8 basis"}
         for name, ex in (("single_auto", api.EXEC_AUTO), ("single_fused", api.EXEC_RUNS),
