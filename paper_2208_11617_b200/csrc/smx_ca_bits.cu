@@ -34,6 +34,7 @@
 // every cell of every tile the map emits; each tile is processed by exactly one
 // chunk. Bits for x > y of a row (not cells) are never trusted: every reader
 // masks them.
+#include <cstdlib>
 #include <cooperative_groups.h>
 #include <type_traits>
 #include <cuda.h>
@@ -920,6 +921,224 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
     }
 }
 
+// ---- the 12-row column shape ----
+// Items of 12 output rows x 8 words: the 14 box rows give 28 of the 32 lanes
+// an h-sum role (the 8-row shape: 20), and each lane owns ONE word of three
+// consecutive output rows (rows oc .. oc + 2, oc = 3 (lane >> 3), word
+// lane & 7): five h-sum rows loaded (two shared between its three vertical
+// sums), three independent rule chains per lane. The double-buffered 14-row
+// stages take 16128 B per warp: 14 warps per SM.
+constexpr int C2R = 12;                        // output rows per item
+constexpr int C2BR = C2R + 2;                  // box rows: y0 - 1 .. y0 + 12
+constexpr int C2STAGE = CBW * C2BR * CLZ * 4;  // 7168 B
+constexpr int C2LAYER = CBW * C2BR * 4;        // 896 B per layer of a stage
+constexpr int C2HS = 2 * C2BR * CW * 8;        // h-sums of two layers: [parity][14 rows][8 words][a, b]
+constexpr int C2WARP = 2 * C2STAGE + C2HS;     // 16128 B per warp (126 x 128)
+constexpr int C2NW = 14;                       // warps per CTA (227 KB of shared memory)
+
+// a lane's one cell word's coverage mask from its bitmap word (tiles t0 ..)
+template <int RHO>
+__device__ __forceinline__ uint32_t tile_mask1(uint32_t word, int t0) {
+    constexpr int TPW = 32 / RHO;
+    const uint32_t b = (word >> (t0 & 31)) & ((1u << TPW) - 1u);
+    if (RHO == 16) return ((b & 1u) ? 0x0000ffffu : 0u) | ((b & 2u) ? 0xffff0000u : 0u);
+    if (RHO == 8) return ((b * 0x00204081u) & 0x01010101u) * 0xffu;  // bit i -> byte i
+    uint32_t v = 0;                                                   // bit i -> nibble i
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v |= ((b >> i) & 1u) * (0xfu << (4 * i));
+    return v;
+}
+
+__device__ __forceinline__ void cols_issue12(const CUtensorMap* tm, const ColItem& it, int stage, uint8_t* buf,
+                                             uint32_t mbar) {
+    mbar_expect_tx(mbar, uint32_t(C2STAGE));
+    tma_load_3d(smem_u32(buf), tm, 8 * it.g - 4, C2R * it.iy - 1, it.z0 - 1 + CLZ * stage, mbar);
+}
+
+// One step of the 12-row column engine for one warp (the structure of
+// cols_step: items from *ctr, TMA stages of 8 layers double-buffered, h-sums
+// once per input layer, rolling vertical sums, masked stores).
+template <int RHO>
+__device__ __forceinline__ void cols_step12(const ColItem* __restrict__ items, int nitems, unsigned* ctr,
+                                            const CUtensorMap* tm, uint32_t* __restrict__ out,
+                                            const uint32_t* __restrict__ bm, int D, int TW, int S, int WP,
+                                            uint8_t* wbase, uint32_t mbar0, uint32_t& seq) {
+    static_assert(CLZ == 8 && (RHO == 16 || RHO == 8 || RHO == 4), "stage = 8 layers; tiles of 16, 8 or 4 layers");
+    const int lane = threadIdx.x & 31;
+    uint2* hsb = reinterpret_cast<uint2*>(wbase + 2 * C2STAGE);  // 2 x [C2BR][CW] (a, b), by layer parity
+    const int hr = min(lane >> 1, C2BR - 1), hc = lane & 1;      // h-sum role (lanes 0..27; 28..31 mirror row 13)
+    const int oc = 3 * (lane >> 3), ow = lane & 7;               // output role: item rows oc .. oc + 2, word ow
+    const long long zstride = (long long)S * WP;
+    constexpr int TPW = 32 / RHO;
+    int cur = 0;
+    ColItem it{0, 0, 0, 0};
+    if (lane == 0) {
+        cur = int(atomicAdd(ctr, 1u));
+        if (cur < nitems) {
+            it = items[cur];
+            fence_proxy_async();
+            cols_issue12(tm, it, 0, wbase + (seq & 1) * C2STAGE, mbar0 + 8 * (seq & 1));
+        }
+    }
+    cur = __shfl_sync(0xffffffffu, cur, 0);
+    it.iy = __shfl_sync(0xffffffffu, it.iy, 0);
+    it.g = __shfl_sync(0xffffffffu, it.g, 0);
+    it.z0 = __shfl_sync(0xffffffffu, it.z0, 0);
+    it.z1 = __shfl_sync(0xffffffffu, it.z1, 0);
+    // bitmap words of a stage's tile layer(s) for the lane's two tile rows
+    // (rows oc .. oc + 2 span at most two), loaded a stage ahead
+    uint32_t bwa0 = 0u, bwb0 = 0u, bwa1 = 0u, bwb1 = 0u;
+    auto load_bw = [&](const ColItem& c, int z) {
+        const int ya = C2R * c.iy + oc, t0 = (8 * c.g + ow) * TPW;
+        const int ta = ya / RHO, tb = (ya + 2) / RHO;
+        bwa0 = tile_word(bm, D, TW, t0, ta, z / RHO);
+        bwb0 = tile_word(bm, D, TW, t0, tb, z / RHO);
+        if (RHO == 4) {
+            bwa1 = tile_word(bm, D, TW, t0, ta, z / RHO + 1);
+            bwb1 = tile_word(bm, D, TW, t0, tb, z / RHO + 1);
+        }
+    };
+    if (cur < nitems) load_bw(it, it.z0);
+    while (cur < nitems) {
+        int nxt = 0;
+        ColItem itn{0, 0, 0, 0};
+        if (lane == 0) {
+            nxt = int(atomicAdd(ctr, 1u));
+            if (nxt < nitems) itn = items[nxt];
+        }
+        const int nin = it.z1 - it.z0 + 2;
+        const int nfull = nin / CLZ, tail = nin % CLZ;
+        const int nst = nfull + (tail ? 1 : 0);
+        const int y0 = C2R * it.iy, w0 = 8 * it.g;
+        const int hoff = hr * CBW + 4 + 4 * hc;  // box word of the main chunk
+        const int eoff = hr * CBW + (hc ? 12 : 3);
+        uint2* hsw = hsb + hr * CW + 4 * hc;
+        // output role, per item: rows yo + k, word wo
+        const int yo = y0 + oc, wo = w0 + ow;
+        const bool sel1 = (yo + 1) / RHO != yo / RHO;  // row 1's tile row is row 2's
+        unsigned zn[3];
+        uint32_t xm[3];
+        uint32_t* optr[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            // stored layers z0 <= zo < z0 + zn[k] (none when the word holds no cell of the row)
+            zn[k] = 32 * wo <= yo + k ? unsigned(max(min(S - 1 - (yo + k), it.z1 - 1) - it.z0 + 1, 0)) : 0u;
+            xm[k] = __funnelshift_lc(0xffffffffu, 0u, max(yo + k - 32 * wo + 1, 0));  // x <= y
+            optr[k] = out + ((long long)(it.z0 - 2) * S + yo + k) * WP + wo;  // output layer of input layer z0 - 1
+        }
+        V3 va[3], vb[3];
+        uint32_t alive[3] = {0u, 0u, 0u}, mprev[3] = {0u, 0u, 0u};
+
+        auto hsum = [&](const uint32_t* L, int li) {
+            const uint4 m = *reinterpret_cast<const uint4*>(L + hoff);
+            const uint32_t e = L[eoff];
+            const uint32_t got = __shfl_xor_sync(0xffffffffu, hc ? m.x : m.w, 1);  // partner's word
+            const uint32_t W0 = hc ? got : e, W5 = hc ? e : got;
+            const uint32_t l0 = shl1_fma(W0, m.x), r0 = shr1_fma(m.x, m.y);
+            const uint32_t l1 = shl1_fma(m.x, m.y), r1 = shr1_fma(m.y, m.z);
+            const uint32_t l2 = shl1_fma(m.y, m.z), r2 = shr1_fma(m.z, m.w);
+            const uint32_t l3 = shl1_fma(m.z, m.w), r3 = shr1_fma(m.w, W5);
+            uint4* dst = reinterpret_cast<uint4*>(hsw + (li & 1) * (C2BR * CW));
+            dst[0] = make_uint4(lop3<0x96>(l0, m.x, r0), lop3<0xe8>(l0, m.x, r0), lop3<0x96>(l1, m.y, r1),
+                                lop3<0xe8>(l1, m.y, r1));
+            dst[1] = make_uint4(lop3<0x96>(l2, m.z, r2), lop3<0xe8>(l2, m.z, r2), lop3<0x96>(l3, m.w, r3),
+                                lop3<0xe8>(l3, m.w, r3));
+        };
+        auto layer = [&](const uint32_t* buf, int li, int n, int zi, const uint32_t (&m0)[3], const uint32_t (&m1)[3],
+                         bool first) {
+            __syncwarp();  // h-sums of layer li visible; layer li - 1's reads done
+            const uint2* hs = hsb + (li & 1) * (C2BR * CW) + oc * CW + ow;
+            const uint2 h0 = hs[0], h1 = hs[CW], h2 = hs[2 * CW], h3 = hs[3 * CW], h4 = hs[4 * CW];
+            const uint32_t* ce = buf + li * (C2LAYER / 4) + (oc + 1) * CBW + 4 + ow;
+            const uint32_t an0 = ce[0], an1 = ce[CBW], an2 = ce[2 * CBW];
+            if (li + 1 < n) hsum(buf + (li + 1) * (C2LAYER / 4), li + 1);
+            V3 vc[3];
+            vc[0] = vsum3(h0.x, h0.y, h1.x, h1.y, h2.x, h2.y);
+            vc[1] = vsum3(h1.x, h1.y, h2.x, h2.y, h3.x, h3.y);
+            vc[2] = vsum3(h2.x, h2.y, h3.x, h3.y, h4.x, h4.y);
+            if (li >= 2 || !first) {
+                const unsigned dz = unsigned(zi - 1 - it.z0);  // output layer zi - 1 past z0 (wraps below it)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const uint32_t tmk = li < 2 ? mprev[k] : (RHO == 4 && li >= 6 ? m1[k] : m0[k]);
+                    const uint32_t o = life_v3(va[k], vb[k], vc[k], alive[k], tmk);
+                    if (dz < zn[k]) *optr[k] = o;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                optr[k] += zstride;
+                va[k] = vb[k];
+                vb[k] = vc[k];
+            }
+            alive[0] = an0;
+            alive[1] = an1;
+            alive[2] = an2;
+        };
+
+        const int t0 = wo * TPW;
+        for (int st = 0; st < nst; ++st) {
+            const uint32_t b = seq & 1;
+            if (lane == 0) {
+                fence_proxy_async();
+                if (st + 1 < nst) cols_issue12(tm, it, st + 1, wbase + (b ^ 1) * C2STAGE, mbar0 + 8 * (b ^ 1));
+                else if (nxt < nitems) cols_issue12(tm, itn, 0, wbase + (b ^ 1) * C2STAGE, mbar0 + 8 * (b ^ 1));
+            }
+            uint32_t m0[3], m1[3];
+            {
+                const uint32_t ma = tile_mask1<RHO>(bwa0, t0), mb = tile_mask1<RHO>(bwb0, t0);
+                m0[0] = ma & xm[0];
+                m0[1] = (sel1 ? mb : ma) & xm[1];
+                m0[2] = mb & xm[2];
+                if (RHO == 4) {
+                    const uint32_t na = tile_mask1<RHO>(bwa1, t0), nb = tile_mask1<RHO>(bwb1, t0);
+                    m1[0] = na & xm[0];
+                    m1[1] = (sel1 ? nb : na) & xm[1];
+                    m1[2] = nb & xm[2];
+                } else {
+                    m1[0] = m0[0], m1[1] = m0[1], m1[2] = m0[2];
+                }
+            }
+            if (st + 1 < nst) {
+                load_bw(it, it.z0 + CLZ * (st + 1));
+            } else {
+                nxt = __shfl_sync(0xffffffffu, nxt, 0);
+                itn.iy = __shfl_sync(0xffffffffu, itn.iy, 0);
+                itn.g = __shfl_sync(0xffffffffu, itn.g, 0);
+                itn.z0 = __shfl_sync(0xffffffffu, itn.z0, 0);
+                itn.z1 = __shfl_sync(0xffffffffu, itn.z1, 0);
+                if (nxt < nitems) load_bw(itn, itn.z0);
+            }
+            while (!mbar_try_wait(mbar0 + 8 * b, (seq >> 1) & 1u)) {
+            }
+            const uint32_t* buf = reinterpret_cast<const uint32_t*>(wbase + b * C2STAGE);
+            const int zbase = it.z0 - 1 + CLZ * st;
+            __syncwarp();
+            hsum(buf, 0);
+            const bool first = st == 0;
+            if (st < nfull) {
+                // the warm-up layers' branch on `first` stays inside layers
+                // 0 and 1 (not a second copy of the whole stage)
+                layer(buf, 0, CLZ, zbase, m0, m1, first);
+                layer(buf, 1, CLZ, zbase + 1, m0, m1, first);
+#pragma unroll
+                for (int li = 2; li < CLZ; ++li) layer(buf, li, CLZ, zbase + li, m0, m1, false);
+            } else if (tail == 2) {
+                layer(buf, 0, 2, zbase, m0, m1, first);
+                layer(buf, 1, 2, zbase + 1, m0, m1, first);
+            } else {
+#pragma unroll 1
+                for (int li = 0; li < tail; ++li) layer(buf, li, tail, zbase + li, m0, m1, first);
+            }
+#pragma unroll
+            for (int k = 0; k < 3; ++k) mprev[k] = RHO == 4 ? m1[k] : m0[k];
+            ++seq;
+        }
+        cur = nxt;
+        it = itn;
+    }
+}
+
 // The chunk engine's canonical plan: from the tile bitmap the map marked
 // (k_cols_mark), every tile row (ty, tz) of the domain is cut into chunks of
 // at most LMAX x-adjacent marked tiles — the same chunk list for every exact
@@ -1007,6 +1226,35 @@ __global__ void __launch_bounds__(CNW * 32) k_cols_run(const __grid_constant__ C
         const bool even = (st & 1) == 0;
         cols_step<RHO>(items, nitems, ctl + 1 + st, even ? &tmA : &tmB, even ? bitsB : bitsA, bm, D, TW, S, WP, wbase,
                        mbar0, seq);
+        if (st + 1 < steps) step_barrier(ctl);
+    }
+}
+
+template <int RHO>
+__global__ void __launch_bounds__(C2NW * 32) k_cols_run12(const __grid_constant__ CUtensorMap tmA,
+                                                          const __grid_constant__ CUtensorMap tmB, uint32_t* bitsA,
+                                                          uint32_t* bitsB, const ColItem* __restrict__ items,
+                                                          int nitems, unsigned* ctl, const uint32_t* __restrict__ bm,
+                                                          int D, int TW, int steps, int S, int WP) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t* wbase = smem + warp * C2WARP;
+    const uint32_t mbar0 = smem_u32(smem + C2NW * C2WARP + 16 * warp);
+    if (lane == 0) {
+        mbar_init(mbar0, 1);
+        mbar_init(mbar0 + 8, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    uint32_t seq = 0;
+    for (int st = 0; st < steps; ++st) {
+        const bool even = (st & 1) == 0;
+        cols_step12<RHO>(items, nitems, ctl + 1 + st, even ? &tmA : &tmB, even ? bitsB : bitsA, bm, D, TW, S, WP,
+                         wbase, mbar0, seq);
         if (st + 1 < steps) step_barrier(ctl);
     }
 }
@@ -1185,8 +1433,9 @@ void launch_chunkify(int rho, const uint32_t* bm, int D, int TW, unsigned* rowcn
 }
 
 // ---- the column engine's launchers ----
+// the item shapes: 8 or 12 output rows (the host picks per side)
 int cols_box_words() { return CBW; }
-int cols_box_rows() { return CBR; }
+int cols_box_rows(int rows) { return rows + 2; }
 int cols_box_layers() { return CLZ; }
 int cols_item_bytes() { return int(sizeof(ColItem)); }
 
@@ -1202,39 +1451,52 @@ void launch_cols_mark(const Geom& g, int kind, uint32_t* bm, int D, int TW, unsi
     else k_cols_mark<SMX_BB><<<unsigned(blocks), 256, 0, s>>>(g, bm, D, TW, stats, wz0, wz1);
 }
 
-int cols_grid() {
+// persistent grid of each shape (co-resident CTAs x SMs), attributes set once per device
+static int cols_grid(int rows) {
     static std::once_flag once[kMaxDevices];
-    static int grids[kMaxDevices];
+    static int grids[kMaxDevices][2];
     const int dev = current_device();
-    int local = 0;
+    int local[2] = {0, 0};
     once_per_device(once, dev, [&] {
-        const int smem = CNW * (CWARP + 16);
-        cudaFuncSetAttribute(k_cols_run<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_cols_run<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_cols_run<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        int per_sm = 0, nsm = 148;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cols_run<8>, CNW * 32, smem);
+        const int smem8 = CNW * (CWARP + 16), smem12 = C2NW * (C2WARP + 16);
+        cudaFuncSetAttribute(k_cols_run<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem8);
+        cudaFuncSetAttribute(k_cols_run<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem8);
+        cudaFuncSetAttribute(k_cols_run<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem8);
+        cudaFuncSetAttribute(k_cols_run12<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem12);
+        cudaFuncSetAttribute(k_cols_run12<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem12);
+        cudaFuncSetAttribute(k_cols_run12<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem12);
+        int per8 = 0, per12 = 0, nsm = 148;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per8, k_cols_run<8>, CNW * 32, smem8);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per12, k_cols_run12<8>, C2NW * 32, smem12);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        local = (per_sm > 0 ? per_sm : 1) * nsm;
-        if (dev >= 0 && dev < kMaxDevices) grids[dev] = local;
+        local[0] = (per8 > 0 ? per8 : 1) * nsm;
+        local[1] = (per12 > 0 ? per12 : 1) * nsm;
+        if (dev >= 0 && dev < kMaxDevices) grids[dev][0] = local[0], grids[dev][1] = local[1];
     });
-    return dev >= 0 && dev < kMaxDevices ? grids[dev] : local;
+    const int i = rows == C2R ? 1 : 0;
+    return dev >= 0 && dev < kMaxDevices ? grids[dev][i] : local[i];
 }
-int cols_warps() { return cols_grid() * CNW; }
+int cols_warps(int rows) { return cols_grid(rows) * (rows == C2R ? C2NW : CNW); }
 
-cudaError_t launch_cols_run(const Geom& g, const void* tmA, const void* tmB, uint32_t* A, uint32_t* B,
+cudaError_t launch_cols_run(const Geom& g, int rows, const void* tmA, const void* tmB, uint32_t* A, uint32_t* B,
                             const void* items, int nitems, unsigned* ctl, const uint32_t* bm, int D, int TW, int steps,
                             cudaStream_t s) {
-    const int grid = cols_grid();
-    const int smem = CNW * (CWARP + 16);
+    const int grid = cols_grid(rows);
+    const bool r12 = rows == C2R;
+    const int nthr = (r12 ? C2NW : CNW) * 32;
+    const int smem = r12 ? C2NW * (C2WARP + 16) : CNW * (CWARP + 16);
     int S = g.side, WP = bits_pitch_words(g.side);
     const ColItem* it = reinterpret_cast<const ColItem*>(items);
     void* args[] = {const_cast<void*>(tmA), const_cast<void*>(tmB), &A, &B, &it, &nitems, &ctl,
                     const_cast<uint32_t**>(&bm), &D, &TW, &steps, &S, &WP};
-    const void* fn = g.rho == 16 ? (const void*)k_cols_run<16>
-                     : g.rho == 8 ? (const void*)k_cols_run<8> : (const void*)k_cols_run<4>;
-    if (steps == 1) return cudaLaunchKernel(fn, dim3(grid), dim3(CNW * 32), args, smem, s);
-    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(CNW * 32), args, smem, s);
+    const void* fn = r12 ? (g.rho == 16  ? (const void*)k_cols_run12<16>
+                            : g.rho == 8 ? (const void*)k_cols_run12<8>
+                                         : (const void*)k_cols_run12<4>)
+                         : (g.rho == 16  ? (const void*)k_cols_run<16>
+                            : g.rho == 8 ? (const void*)k_cols_run<8>
+                                         : (const void*)k_cols_run<4>);
+    if (steps == 1) return cudaLaunchKernel(fn, dim3(grid), dim3(nthr), args, smem, s);
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(nthr), args, smem, s);
 }
 
 void launch_ca_bits(const Geom& g, int kind, int wz0, int wz1, const void* tmap_ptr, uint32_t* nbits, cudaStream_t s) {

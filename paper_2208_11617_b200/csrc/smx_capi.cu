@@ -84,6 +84,7 @@ struct DeviceRes {
     const void* shadow_ptr[2] = {nullptr, nullptr};
     int64_t shadow_side[2] = {-1, -1};
     int cols_nitems = 0;
+    int cols_rows = 8;  // output rows per item of the items in slot 8
     std::map<std::pair<const void*, std::pair<int64_t, int64_t>>, CUtensorMap> tmaps;
     smx::DevCounters* counters = nullptr;
     unsigned* sink = nullptr;
@@ -451,16 +452,17 @@ bool use_cols_side(int64_t side, int64_t rho) {
 bool use_cols(const smx::Geom& k) { return use_cols_side(k.side, k.rho); }
 
 // the column engine's work items (host): for layer segments of lz layers,
-// every 8-row band iy and 8-word group g with cells; item order keeps
+// every R-row band iy and 8-word group g with cells; item order keeps
 // concurrently running warps on neighbouring columns (shared halo in L2)
-std::vector<int32_t> col_items(int64_t S, int64_t lz) {
+std::vector<int32_t> col_items(int64_t S, int64_t lz, int64_t R) {
     std::vector<int32_t> v;
     for (int64_t zs = 0; zs < S; zs += lz)
-        for (int64_t iy = 0; 8 * iy <= S - 1; ++iy) {
-            const int64_t y0 = 8 * iy, zmax = S - y0;
+        for (int64_t iy = 0; R * iy <= S - 1; ++iy) {
+            const int64_t y0 = R * iy, zmax = S - y0;
             if (zs >= zmax) continue;
             const int64_t z1 = std::min(zs + lz, zmax);
-            for (int64_t g = 0; 256 * g <= y0 + 7; ++g) v.insert(v.end(), {int32_t(iy), int32_t(g), int32_t(zs), int32_t(z1)});
+            for (int64_t g = 0; 256 * g <= std::min(y0 + R - 1, S - 1); ++g)
+                v.insert(v.end(), {int32_t(iy), int32_t(g), int32_t(zs), int32_t(z1)});
         }
     return v;
 }
@@ -491,7 +493,23 @@ struct EnginePlan {
     int nitems = 0;
     uint32_t* bm = nullptr;
     int D = 0, TW = 0;
+    int rows = 8;  // column engine: output rows per item
 };
+
+// The column engine's item shape for a side: 12-row items (fewer h-sum lanes
+// idle, three rule chains per lane: C5 195 -> 184 us per step) while every
+// warp still gets >= 3 of them at 32 layers; 8-row items below (C4, 1.3
+// twelve-row items per warp: 42 vs 38 us per step). SMX_COLS_ROWS=8|12 forces.
+int cols_rows_for(int64_t side) {
+    static const int forced = [] {
+        const char* e = std::getenv("SMX_COLS_ROWS");
+        const int r = e ? std::atoi(e) : 0;
+        return r == 8 || r == 12 ? r : 0;
+    }();
+    if (forced) return forced;
+    const int64_t n12 = int64_t(col_items(side, 32, 12).size() / 4);
+    return n12 >= 3 * int64_t(smx::cols_warps(12)) ? 12 : 8;
+}
 
 // plan (map once -> chunk list, or -> tile bitmap + column items) + the
 // persistent multi-step run, A -> B -> A ...
@@ -543,17 +561,19 @@ int engine_plan(const smx_grid* g, const smx::Geom& k, int64_t steps, cudaStream
         // warm-up, short enough for ~6 items per warp where the side allows;
         // built and uploaded once per side (host work off the per-call path)
         if (r->cols_key.first != int64_t(k.side)) {
-            const int64_t target = 6 * int64_t(smx::cols_warps());
+            const int R = cols_rows_for(k.side);
+            const int64_t target = 6 * int64_t(smx::cols_warps(R));
             int64_t lz = 64;
-            std::vector<int32_t> v = col_items(k.side, lz);
+            std::vector<int32_t> v = col_items(k.side, lz, R);
             if (const char* e = std::getenv("SMX_COLS_LZ")) {  // experiments: a fixed item length
                 lz = std::max<int64_t>(8, std::atoll(e) / 8 * 8);
-                v = col_items(k.side, lz);
+                v = col_items(k.side, lz, R);
             } else {
                 // not below 32 layers: an item pays two warm-up layers and a
                 // partial tail stage (C4: lz 8 -> 32 is 43.4 -> 38.0 us per step)
-                while (lz > 32 && int64_t(v.size() / 4) < target) v = col_items(k.side, lz /= 2);
+                while (lz > 32 && int64_t(v.size() / 4) < target) v = col_items(k.side, lz /= 2, R);
             }
+            r->cols_rows = R;
             void* pit;
             if (int rc = pool_get(8, v.size() * 4, &pit)) return rc;
             TRY(cudaMemcpy(pit, v.data(), v.size() * 4, cudaMemcpyHostToDevice));
@@ -562,6 +582,7 @@ int engine_plan(const smx_grid* g, const smx::Geom& k, int64_t steps, cudaStream
         }
         P->items = r->pool[8];
         P->nitems = r->cols_nitems;
+        P->rows = r->cols_rows;
     }
     TRY(cudaGetLastError());
     TRY(cudaEventRecord(r->ev_plan, r->side));
@@ -586,9 +607,11 @@ int engine_run(const smx::Geom& k, uint32_t* A, uint32_t* B, int64_t steps, cuda
     if (dev < 0 || dev >= smx::kMaxDevices) return fail(SMX_EINVAL, "device ordinal beyond the library's table");
     const CUtensorMap *ta, *tb;
     if (P.cols) {
-        if (int rc = bits_tmap_box(A, k.side, smx::cols_box_words(), smx::cols_box_rows(), smx::cols_box_layers(), &ta))
+        if (int rc = bits_tmap_box(A, k.side, smx::cols_box_words(), smx::cols_box_rows(P.rows), smx::cols_box_layers(),
+                                    &ta))
             return rc;
-        if (int rc = bits_tmap_box(B, k.side, smx::cols_box_words(), smx::cols_box_rows(), smx::cols_box_layers(), &tb))
+        if (int rc = bits_tmap_box(B, k.side, smx::cols_box_words(), smx::cols_box_rows(P.rows), smx::cols_box_layers(),
+                                    &tb))
             return rc;
     } else {
         if (int rc = bits_tmap(A, k.side, k.rho, &ta)) return rc;
@@ -602,7 +625,7 @@ int engine_run(const smx::Geom& k, uint32_t* A, uint32_t* B, int64_t steps, cuda
         TRY(cudaStreamWaitEvent(s, done, 0));
     }
     if (P.cols)
-        TRY(smx::launch_cols_run(k, ta, tb, A, B, P.items, P.nitems, P.ctl, P.bm, P.D, P.TW, int(steps), s));
+        TRY(smx::launch_cols_run(k, P.rows, ta, tb, A, B, P.items, P.nitems, P.ctl, P.bm, P.D, P.TW, int(steps), s));
     else
         TRY(smx::launch_ca_bits_run(k, ta, tb, A, B, P.chunks, P.ctl, int(steps), s));
     TRY(cudaEventRecord(done, s));

@@ -60,10 +60,10 @@ cudaError_t launch_ca_bits_run(const Geom& g, const void* tmA, const void* tmB, 
 // persistent run over column items (int4 {iy, g, z0, z1}); ctl: [0] grid
 // barrier, [1 + s] step s's item counter, zeroed
 int cols_box_words();
-int cols_box_rows();
+int cols_box_rows(int rows);  // rows: output rows per column item (8 or 12)
 int cols_box_layers();
 int cols_item_bytes();
-int cols_warps();
+int cols_warps(int rows);
 // the map over blocks with wz in [wz0, wz1) (default: the whole grid) -> tile bitmap
 void launch_cols_mark(const Geom& g, int kind, uint32_t* bm, int D, int TW, unsigned* stats, cudaStream_t s,
                       int wz0 = 0, int wz1 = -1);
@@ -71,7 +71,7 @@ void launch_cols_mark(const Geom& g, int kind, uint32_t* bm, int D, int TW, unsi
 // rowcnt: D * D u32 scratch; *count receives the chunk total
 void launch_chunkify(int rho, const uint32_t* bm, int D, int TW, unsigned* rowcnt, void* chunks, unsigned* count,
                      cudaStream_t s);
-cudaError_t launch_cols_run(const Geom& g, const void* tmA, const void* tmB, uint32_t* A, uint32_t* B,
+cudaError_t launch_cols_run(const Geom& g, int rows, const void* tmA, const void* tmB, uint32_t* A, uint32_t* B,
                             const void* items, int nitems, unsigned* ctl, const uint32_t* bm, int D, int TW, int steps,
                             cudaStream_t s);
 // 2-simplex EDM (f64 points as x, y pairs) and periodic 2-D Life (smx_kernels2d.cu)
