@@ -74,9 +74,10 @@ struct DeviceRes {
     // first-defect result of smx_verify_cover (its own slot: a verify on one
     // stream never touches the words of an engine running on another)
     // 8 the column engine's items (host-built, key cols_key), 9 the tile
-    // bitmap (both engines), 10 the chunk plan's per-row counts
-    void* pool[11] = {};
-    size_t pool_bytes[11] = {};
+    // bitmap (both engines), 10 the chunk plan's per-row counts, 11 the
+    // periodic 2-D Life bit triangle
+    void* pool[12] = {};
+    size_t pool_bytes[12] = {};
     std::pair<int64_t, int64_t> cols_key{-1, -1};  // (side, layers per item) of the items in slot 8
     // the bit-shadow pools (slots 3, 4) keep every non-cell bit zero (the
     // column engine reads them unmasked): zeroed when (re)allocated or when
@@ -102,7 +103,7 @@ void free_res(int dev, DeviceRes& r) {
     if (cudaGetDevice(&cur) != cudaSuccess) return;
     if (cur != dev) cudaSetDevice(dev);
     for (auto& kv : r.prefix) cudaFree(kv.second);
-    for (int i = 0; i < 11; ++i)
+    for (int i = 0; i < 12; ++i)
         if (r.pool[i]) cudaFree(r.pool[i]);
     if (r.counters) cudaFree(r.counters);
     if (r.sink) cudaFree(r.sink);
@@ -1604,10 +1605,22 @@ static int ca_validate(const smx_grid* g, uint64_t ncells, int32_t* exec) {
     return SMX_OK;
 }
 
+// One periodic 2-D Life step. The x-run scheme first packs the state into a
+// bit triangle (bit i = packed cell i; 1/8 of the state, L2-resident at the
+// SURVEY sizes) and reads its neighbourhoods from it; every band of a
+// trapezoid grid reads the same triangle.
 static int ca2d_step(const smx_grid* g, const uint8_t* cur, uint8_t* next, int32_t exec, cudaStream_t s) {
     std::vector<smx::Geom> subs;
     if (int rc = sub_geoms(g, subs, false)) return rc;
-    for (const auto& k : subs) smx::launch_ca2d(k, cur, next, exec, s);  // bands: disjoint cells
+    const uint32_t* bits = nullptr;
+    if (exec == SMX_EXEC_RUNS) {
+        const uint64_t ncells = smx::tri_cells(cell_side_of(g));
+        void* p;
+        if (int rc = pool_get(11, size_t(smx::ca2d_bit_words(ncells)) * 4, &p)) return rc;
+        smx::launch_pack2d(cur, ncells, (uint32_t*)p, s);
+        bits = (const uint32_t*)p;
+    }
+    for (const auto& k : subs) smx::launch_ca2d(k, cur, bits, next, exec, s);  // bands: disjoint cells
     TRY(cudaGetLastError());
     return SMX_OK;
 }
@@ -2096,7 +2109,7 @@ uint64_t smx_scratch_bytes(void) {
     uint64_t b = 0;
     for (auto& kv : g_res) {
         if (kv.first.second != std::this_thread::get_id()) continue;
-        for (int i = 0; i < 11; ++i) b += kv.second.pool_bytes[i];
+        for (int i = 0; i < 12; ++i) b += kv.second.pool_bytes[i];
     }
     return b;
 }

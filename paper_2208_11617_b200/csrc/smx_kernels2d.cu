@@ -14,8 +14,10 @@
 // Each in two execution schemes: BLOCK (the paper's launch model: one CTA per
 // map block, rho^2 threads) and RUNS (a warp maps 32 blocks and merges
 // x-adjacent tiles into runs; EDM streams whole cell rows of the runs with
-// lane-consecutive 8-byte stores, Life cuts them into 32-cell bit-sliced items).
+// lane-consecutive 8-byte stores, Life cuts them into 32-cell bit-sliced items
+// whose neighbourhoods come from a bit triangle of the state, packed first).
 #include "smx_common.cuh"
+#include <algorithm>
 #include <cstdlib>
 
 #include "smx_launch.hpp"
@@ -150,51 +152,75 @@ __device__ __forceinline__ uint4 load_cells16(const uint8_t* __restrict__ cur, I
     return __ldg(reinterpret_cast<const uint4*>(cur + q));
 }
 
-// One row's contribution to the 3x3 sums of the 32 cells x0 .. x0+31: bits of
-// cells x0-1 .. x0+32 of the row starting at packed index Rr with len cells
-// (cells outside [0, len) are dead) -> the horizontal 3-sum as two bit-planes.
+// ---- the bit triangle: bit i of word i / 32 = packed cell i (0 / 1) ----
+// The x-run step reads its 3 x 34-cell neighbourhood windows from it: three
+// words per row instead of 64 bytes, no byte -> bit packing per chunk, and
+// the 1/8-size triangle stays in L2 while the u8 state streams once through
+// the pack and once as the step's stores.
+
+// words i and i + 1 of the triangle at a signed word index (0 before the
+// start; the buffer ends with zero words, so reads past the last cell are 0)
 template <bool GUARD, typename IDX>
-__device__ __forceinline__ void row_hsum(const uint8_t* __restrict__ cur, IDX ncells, IDX Rr, int len, int x0,
-                                         uint32_t& s0, uint32_t& s1, uint32_t* centre) {
+__device__ __forceinline__ uint32_t tri_word(const uint32_t* __restrict__ bits, IDX w) {
+    if (GUARD && w < 0) return 0u;
+    return __ldg(bits + w);
+}
+
+// row_hsum from the bit triangle: cells x0 - 1 .. x0 + 32 of the row starting
+// at packed index Rr with len cells
+// (MASK = false: the window lies inside the row, 1 <= x0 and x0 + 32 < len)
+template <bool GUARD, bool MASK, typename IDX>
+__device__ __forceinline__ void row_hsum_bits(const uint32_t* __restrict__ bits, IDX Rr, int len, int x0,
+                                              uint32_t& s0, uint32_t& s1, uint32_t* centre) {
     const IDX p = Rr + x0 - 1;
-    const IDX q = p & ~IDX(15);
-    const int d = int(p - q);
-    const uint8_t* b = cur + q;
-    uint32_t lo, hi;
-    if (GUARD) {
-        lo = ca::pack32(load_cells16<true>(cur, q, ncells), load_cells16<true>(cur, q + 16, ncells));
-        hi = ca::pack32(load_cells16<true>(cur, q + 32, ncells), load_cells16<true>(cur, q + 48, ncells));
-    } else {
-        const uint4* v = reinterpret_cast<const uint4*>(b);
-        lo = ca::pack32(__ldg(v), __ldg(v + 1));
-        hi = ca::pack32(__ldg(v + 2), __ldg(v + 3));
+    const IDX w = p >> 5;  // floor (arithmetic shift)
+    const int d = int(p & 31);
+    const uint32_t lo = tri_word<GUARD>(bits, w), hi = tri_word<GUARD>(bits, w + 1), hi2 = __ldg(bits + w + 2);
+    uint32_t M = __funnelshift_r(lo, hi, d);           // bit j = cell x0 - 1 + j
+    uint32_t T = __funnelshift_r(hi, hi2, d) & 3u;     // cells x0 + 31, x0 + 32
+    if (MASK) {
+        M &= ca::range_mask(1 - x0, len - x0);
+        T &= ((x0 + 31 >= 0 && x0 + 31 < len) ? 1u : 0u) | ((x0 + 32 >= 0 && x0 + 32 < len) ? 2u : 0u);
     }
-    uint32_t M = __funnelshift_r(lo, hi, d);  // bit j = cell x0 - 1 + j
-    uint32_t T = (hi >> d) & 3u;              // cells x0 + 31, x0 + 32
-    M &= ca::range_mask(1 - x0, len - x0);
-    T &= ((x0 + 31 >= 0 && x0 + 31 < len) ? 1u : 0u) | ((x0 + 32 >= 0 && x0 + 32 < len) ? 2u : 0u);
     const uint32_t l = M, c = (M >> 1) | (T << 31), r = (M >> 2) | (T << 30);
     s0 = l ^ c ^ r;
     s1 = (l & c) | (l & r) | (c & r);
     if (centre) *centre = c;
 }
 
-// next-state bits of cells x0 .. x0+31 of row cy (start R), 1 <= cy <= S-3
-// (bits past the row end are junk; callers mask them)
 template <typename IDX>
-__device__ __forceinline__ uint32_t life2d_bits(const uint8_t* __restrict__ cur, IDX ncells, IDX R, int cy, int x0) {
+__device__ __forceinline__ uint32_t life2d_bits_tri(const uint32_t* __restrict__ bits, IDX R, int cy, int x0) {
     uint32_t a0, a1, b0, b1, c0, c1, alive;
-    if (R - cy + x0 - 1 < 16 || R + cy + 1 + x0 + 63 >= ncells) {  // a window runs off the array
-        row_hsum<true>(cur, ncells, R - cy, cy, x0, a0, a1, nullptr);
-        row_hsum<true>(cur, ncells, R, cy + 1, x0, b0, b1, &alive);
-        row_hsum<true>(cur, ncells, R + cy + 1, cy + 2, x0, c0, c1, nullptr);
+    if (x0 >= 1 && x0 + 32 < cy) {  // all three windows inside their rows (the row above is the shortest)
+        row_hsum_bits<false, false>(bits, IDX(R - cy), cy, x0, a0, a1, nullptr);
+        row_hsum_bits<false, false>(bits, R, cy + 1, x0, b0, b1, &alive);
+        row_hsum_bits<false, false>(bits, IDX(R + cy + 1), cy + 2, x0, c0, c1, nullptr);
     } else {
-        row_hsum<false>(cur, ncells, R - cy, cy, x0, a0, a1, nullptr);
-        row_hsum<false>(cur, ncells, R, cy + 1, x0, b0, b1, &alive);
-        row_hsum<false>(cur, ncells, R + cy + 1, cy + 2, x0, c0, c1, nullptr);
+        // the upper window may start before the triangle (GUARD)
+        row_hsum_bits<true, true>(bits, IDX(R - cy), cy, x0, a0, a1, nullptr);
+        row_hsum_bits<false, true>(bits, R, cy + 1, x0, b0, b1, &alive);
+        row_hsum_bits<false, true>(bits, IDX(R + cy + 1), cy + 2, x0, c0, c1, nullptr);
     }
     const ca::Planes4 t = ca::add3x2(a0, a1, b0, b1, c0, c1);  // 9-sum incl. the cell
     return (~t.b3 & ~t.b2 & t.b1 & t.b0) | (~t.b3 & t.b2 & ~t.b1 & ~t.b0 & alive);
+}
+
+// u8 state (0/1) -> bit triangle, one word per thread (two 16-byte loads),
+// then the zero tail
+template <typename IDX>
+__global__ void __launch_bounds__(256) k_pack2d(const uint8_t* __restrict__ cur, IDX ncells, IDX nwords,
+                                                uint32_t* __restrict__ bits) {
+    for (IDX w = IDX(blockIdx.x) * blockDim.x + threadIdx.x; w < nwords; w += IDX(gridDim.x) * blockDim.x) {
+        const IDX q = 32 * w;
+        uint32_t v = 0u;
+        if (q + 32 <= ncells) {
+            const uint4* c = reinterpret_cast<const uint4*>(cur + q);
+            v = ca::pack32(__ldg(c), __ldg(c + 1));
+        } else if (q < ncells) {
+            v = ca::pack32(load_cells16<true>(cur, q, ncells), load_cells16<true>(cur, IDX(q + 16), ncells));
+        }
+        bits[w] = v;
+    }
 }
 
 // Strips per CTA for the 2-D x-run Life kernel: ~256+ chunks per CTA at rho >= 8,
@@ -213,6 +239,7 @@ __host__ __device__ constexpr int ca2d_strips(int rho) { return rho >= 16 ? 2 : 
 // more than two rows, near the apex) take the per-cell rule.
 template <int KIND, int NS, typename IDX>
 __global__ void __launch_bounds__(T2_THREADS) k_ca2d_runs(Geom g, const uint8_t* __restrict__ cur,
+                                                          const uint32_t* __restrict__ bits,
                                                           uint8_t* __restrict__ next) {
     constexpr int NR = NS * T2_KX;
     __shared__ int s_run[NR][3];
@@ -265,12 +292,12 @@ __global__ void __launch_bounds__(T2_THREADS) k_ca2d_runs(Geom g, const uint8_t*
         const int x0 = int(A - R);
         uint32_t res;
         if (cy >= 1 && cy <= S - 3 && x0 + 31 <= cy) {  // wholly inside row cy
-            res = life2d_bits(cur, ncells, R, cy, x0);
+            res = life2d_bits_tri(bits, R, cy, x0);
         } else if (cy >= 1 && cy + 1 <= S - 3 && A + 32 <= R + 2 * cy + 3) {  // rows cy, cy + 1
             const int n0 = cy - x0 + 1;  // cells of row cy in the chunk
             const uint32_t m0 = (1u << n0) - 1u;
-            res = (life2d_bits(cur, ncells, R, cy, x0) & m0) |
-                  (life2d_bits(cur, ncells, IDX(R + cy + 1), cy + 1, x0 - cy - 1) & ~m0);
+            res = (life2d_bits_tri(bits, R, cy, x0) & m0) |
+                  (life2d_bits_tri(bits, IDX(R + cy + 1), cy + 1, x0 - cy - 1) & ~m0);
         } else {  // per cell, rows found by walking down from cy
             res = 0;
             IDX Ry = R;
@@ -318,21 +345,21 @@ void launch_edm_k(const Geom& g, const double* pts, double* cells, int exec, cud
 }
 
 template <int KIND>
-void launch_ca2d_k(const Geom& g, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s) {
+void launch_ca2d_k(const Geom& g, const uint8_t* cur, const uint32_t* bits, uint8_t* next, int exec, cudaStream_t s) {
     if (exec == SMX_EXEC_BLOCK) k_ca2d_block<KIND><<<dim3(g.ex, g.ey, 1), block2(g), 0, s>>>(g, cur, next);
     else {
         const dim3 grid((g.ex + T2_KX - 1) / T2_KX, (g.ey + ca2d_strips(g.rho) - 1) / ca2d_strips(g.rho), 1);
         if ((unsigned long long)g.side * (g.side + 1) / 2 + 64 < (1ull << 31)) {
             switch (ca2d_strips(g.rho)) {
-                case 2: k_ca2d_runs<KIND, 2, int><<<grid, T2_THREADS, 0, s>>>(g, cur, next); break;
-                case 8: k_ca2d_runs<KIND, 8, int><<<grid, T2_THREADS, 0, s>>>(g, cur, next); break;
-                default: k_ca2d_runs<KIND, 32, int><<<grid, T2_THREADS, 0, s>>>(g, cur, next); break;
+                case 2: k_ca2d_runs<KIND, 2, int><<<grid, T2_THREADS, 0, s>>>(g, cur, bits, next); break;
+                case 8: k_ca2d_runs<KIND, 8, int><<<grid, T2_THREADS, 0, s>>>(g, cur, bits, next); break;
+                default: k_ca2d_runs<KIND, 32, int><<<grid, T2_THREADS, 0, s>>>(g, cur, bits, next); break;
             }
         } else {
             switch (ca2d_strips(g.rho)) {
-                case 2: k_ca2d_runs<KIND, 2, long long><<<grid, T2_THREADS, 0, s>>>(g, cur, next); break;
-                case 8: k_ca2d_runs<KIND, 8, long long><<<grid, T2_THREADS, 0, s>>>(g, cur, next); break;
-                default: k_ca2d_runs<KIND, 32, long long><<<grid, T2_THREADS, 0, s>>>(g, cur, next); break;
+                case 2: k_ca2d_runs<KIND, 2, long long><<<grid, T2_THREADS, 0, s>>>(g, cur, bits, next); break;
+                case 8: k_ca2d_runs<KIND, 8, long long><<<grid, T2_THREADS, 0, s>>>(g, cur, bits, next); break;
+                default: k_ca2d_runs<KIND, 32, long long><<<grid, T2_THREADS, 0, s>>>(g, cur, bits, next); break;
             }
         }
     }
@@ -344,8 +371,17 @@ void launch_edm(const Geom& g, const double* pts, double* cells, int exec, cudaS
     SMX_DISPATCH_2D(g.kind, launch_edm_k, g, pts, cells, exec, s);
 }
 
-void launch_ca2d(const Geom& g, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s) {
-    SMX_DISPATCH_2D(g.kind, launch_ca2d_k, g, cur, next, exec, s);
+void launch_ca2d(const Geom& g, const uint8_t* cur, const uint32_t* bits, uint8_t* next, int exec, cudaStream_t s) {
+    SMX_DISPATCH_2D(g.kind, launch_ca2d_k, g, cur, bits, next, exec, s);
+}
+
+uint64_t ca2d_bit_words(uint64_t ncells) { return (ncells + 31) / 32 + 3; }
+
+void launch_pack2d(const uint8_t* cur, uint64_t ncells, uint32_t* bits, cudaStream_t s) {
+    const uint64_t nw = ca2d_bit_words(ncells);
+    const unsigned blocks = unsigned(std::min<uint64_t>((nw + 255) / 256, 148ull * 64));
+    if (ncells + 64 < (1ull << 31)) k_pack2d<int><<<blocks, 256, 0, s>>>(cur, int(ncells), int(nw), bits);
+    else k_pack2d<long long><<<blocks, 256, 0, s>>>(cur, (long long)ncells, (long long)nw, bits);
 }
 
 }  // namespace smx

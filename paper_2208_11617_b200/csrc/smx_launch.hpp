@@ -76,7 +76,11 @@ cudaError_t launch_cols_run(const Geom& g, int rows, const void* tmA, const void
                             cudaStream_t s);
 // 2-simplex EDM (f64 points as x, y pairs) and periodic 2-D Life (smx_kernels2d.cu)
 void launch_edm(const Geom& g, const double* pts, double* cells, int exec, cudaStream_t s);
-void launch_ca2d(const Geom& g, const uint8_t* cur, uint8_t* next, int exec, cudaStream_t s);
+// periodic 2-D Life: `bits` = the packed state's bit triangle (launch_pack2d;
+// the x-run scheme reads neighbourhoods from it, the block scheme ignores it)
+void launch_ca2d(const Geom& g, const uint8_t* cur, const uint32_t* bits, uint8_t* next, int exec, cudaStream_t s);
+uint64_t ca2d_bit_words(uint64_t ncells);  // words of the bit triangle incl. the zero tail
+void launch_pack2d(const uint8_t* cur, uint64_t ncells, uint32_t* bits, cudaStream_t s);
 // first packed index with coverage != 1 (atomicMin into *first, preset to n)
 void launch_first_defect(const uint32_t* cov, unsigned long long n, unsigned long long* first, cudaStream_t s);
 // bit-shadow tiles for the sharded engine's halo (rho in {4, 8})
