@@ -170,6 +170,20 @@ __device__ __forceinline__ void accum_rows(uint32_t* __restrict__ cells, const u
     }
 }
 
+// one cell row [e0, e1) by one lane: 16-byte vectors between scalar ends
+__device__ __forceinline__ void accum_row_lane(uint32_t* __restrict__ cells, unsigned long long e0,
+                                               unsigned long long e1) {
+    unsigned long long a0 = (e0 + 3) & ~3ull, a1 = e1 & ~3ull;
+    if (a0 > a1) a0 = a1 = e1;
+    for (unsigned long long i = e0; i < a0; ++i) cells[i] += 1u;
+    for (unsigned long long p = a0; p < a1; p += 4) {
+        uint4 t = *reinterpret_cast<const uint4*>(cells + p);
+        t.x += 1u; t.y += 1u; t.z += 1u; t.w += 1u;
+        *reinterpret_cast<uint4*>(cells + p) = t;
+    }
+    for (unsigned long long i = a1; i < e1; ++i) cells[i] += 1u;
+}
+
 template <int KIND, int KX, int RR, int NV, int KS = 1>
 __global__ void __launch_bounds__(ACC_THREADS, 4) k_accum_runs(Geom g, uint32_t* __restrict__ cells) {
     // KS strips of KX blocks per CTA, mapped concurrently by warps 0 .. KS-1
@@ -186,6 +200,24 @@ __global__ void __launch_bounds__(ACC_THREADS, 4) k_accum_runs(Geom g, uint32_t*
     const int rho = g.rho, S = g.side;
     const int rows = nruns * rho;
     constexpr int NW = ACC_THREADS / 32;
+    // strips cut into short runs (H2D's first grid rows, level b < KX: runs of
+    // b tiles, each in another data row): one cell row per LANE, every thread
+    // with rows in flight, instead of a warp per row of a few vectors (at C1
+    // those CTAs held SM slots ~100 us: H 0.207 vs BB 0.173 ms per pass)
+    int wmax = 0;
+    for (int r = 0; r < nruns; ++r) wmax = max(wmax, s_run[r][2]);
+    if (wmax * rho < 128) {
+        for (int rr = threadIdx.x; rr < rows; rr += ACC_THREADS) {
+            const int r = rr / rho, ly = rr - r * rho;
+            const int cy = s_run[r][1] * rho + ly;
+            const int xlo = s_run[r][0] * rho;
+            const int xhi = min((s_run[r][0] + s_run[r][2]) * rho, cy + 1);  // tri_contains: x <= y
+            if (cy > S - 1 || xlo >= xhi) continue;
+            const unsigned long long base = tri_idx(0, cy);
+            accum_row_lane(cells, base + xlo, base + xhi);
+        }
+        return;
+    }
     for (int row = warp; row < rows; row += RR * NW) {
         unsigned long long e[RR][2];
 #pragma unroll
