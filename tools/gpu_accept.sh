@@ -17,3 +17,8 @@ run SMX_CA_ENGINE=auto "multi h3d 32 8 bits 2"
 run SMX_CA_ENGINE=auto "accum h2d 64 16 runs 2"
 run SMX_CA_ENGINE=auto "kaccum h2d 64 16 runs 2"
 run SMX_CA_ENGINE=auto "ca bb 15 4 block 2"
+run "SMX_CA_ENGINE=cols SMX_COLS_ROWS=12" "engine h3d 32 8 bits 2"
+run "SMX_CA_ENGINE=cols SMX_COLS_ROWS=12" "engine bb 31 4 bits 2"
+run "SMX_CA_ENGINE=cols SMX_COLS_ROWS=12" "engine h3d 16 16 bits 2"
+run SMX_CA_ENGINE=auto "ca2d h2d 64 16 runs 2"
+run SMX_CA_ENGINE=auto "ca2d h2d 64 4 runs 2"
