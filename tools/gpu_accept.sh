@@ -1,12 +1,14 @@
 # The reference's ten-criterion acceptance gate through the GPU path
+# (the pool closed compute-sanitizer late in round 2: the sanitizer lines of the
+# 12-row column engine and 2-D Life bit-triangle cases stay empty there)
 # (tests/acceptance_gpu.py) + compute-sanitizer memcheck / racecheck on small
 # cases of every kernel family. Outputs: gpurun_out/acceptance.txt, sanitizer.txt.
 python tests/acceptance_gpu.py > gpurun_out/acceptance.txt 2>&1; echo "rc=$?" >> gpurun_out/acceptance.txt
 run() {  # env, case
   echo "== memcheck $2 ($1)" >> gpurun_out/sanitizer.txt
-  env $1 timeout 300 compute-sanitizer --tool memcheck --leak-check no python tools/prof_case.py $2 2>&1 | grep -E "ERROR SUMMARY|Invalid|Error" | head -5 >> gpurun_out/sanitizer.txt
+  env $1 timeout 300 compute-sanitizer --tool memcheck --leak-check no python tools/prof_case.py $2 2>&1 | grep -E "ERROR SUMMARY|Invalid|Error|failed|No such" | head -5 >> gpurun_out/sanitizer.txt
   echo "== racecheck $2 ($1)" >> gpurun_out/sanitizer.txt
-  env $1 timeout 300 compute-sanitizer --tool racecheck python tools/prof_case.py $2 2>&1 | grep -E "RACECHECK SUMMARY|ERROR SUMMARY|hazard" | head -5 >> gpurun_out/sanitizer.txt
+  env $1 timeout 300 compute-sanitizer --tool racecheck python tools/prof_case.py $2 2>&1 | grep -E "RACECHECK SUMMARY|ERROR SUMMARY|hazard|failed|No such" | head -5 >> gpurun_out/sanitizer.txt
 }
 run SMX_CA_ENGINE=chunks "ca h3d 16 4 runs 2"
 run SMX_CA_ENGINE=chunks "ca h3d 16 8 bits 2"
