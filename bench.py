@@ -610,6 +610,24 @@ def extra_configs(api, sampler, peak, args, energy):
 
     out["C1_accum_n1024"] = accum_pair(1024, 16)
     out["C1_map_kernel_2d"] = map_pair(2, 1024)
+    # the C3 cell domain (side ~65.5 K, 8.6 GB) at smaller tiles: the map's
+    # per-block share grows as rho falls, and H's half-size grid shows
+    sweep = {}
+    for n, rho in ((32768, 2), (16384, 4), (8192, 8), (4096, 16)):
+        h = accum_case(api, "h2d", n, rho, K, W, api.EXEC_RUNS)
+        hms = statistics.mean(h["ms"])
+        del h["tensor"]
+        torch.cuda.empty_cache()
+        b = accum_case(api, "bb", n - 1, rho, K, W, api.EXEC_RUNS)
+        bms = statistics.mean(b["ms"])
+        del b["tensor"]
+        torch.cuda.empty_cache()
+        gbs = 8.0 * h["cells"] / (hms * 1e-3) / 1e9
+        sweep[f"rho{rho}"] = {"grid": f"h2d({n}) vs bb({n - 1}), rho={rho}, side {h['side']}",
+                              "h_gcells_s": round(gcells(h["cells"], hms), 2),
+                              "bb_gcells_s": round(gcells(b["cells"], bms), 2), "h_vs_bb": round(bms / hms, 3),
+                              "h_roofline_frac": round(gbs / peak, 4), "parity_ok": h["ok"] and b["ok"]}
+    out["C3_accum_rho_sweep"] = sweep
     for label, (desc, n, rho, ca_steps, key) in CA_CONFIGS.items():
         out[label] = ca_pair(label, n, rho, ca_steps, key, label != "C2_ca_n256")
         out[label]["workload"] = desc
@@ -646,10 +664,14 @@ def h_vs_bb_summary(configs):
     """The paper's headline comparison in one place: where the work is per
     launched block (the MAP kernel, the one-CTA-per-block launch model) H's
     fewer blocks show as the block ratio; the x-run schemes make BB's Void
-    blocks nearly free, so the streaming kernels run at the same roof."""
+    blocks nearly free, so the streaming kernels run at the same roof at
+    rho = 16 — at smaller tiles (the C3 rho sweep) the per-block share grows
+    and H's half-size grid keeps a lead."""
     out = {}
     pick = {"map_kernel_2d": ("C1_map_kernel_2d", None), "map_kernel_3d": ("map_kernel_3d", None),
             "accum_xrun_c1": ("C1_accum_n1024", "runs"), "accum_block_model_c1": ("C1_accum_n1024", "block"),
+            "accum_xrun_c3_rho8": ("C3_accum_rho_sweep", "rho8"), "accum_xrun_c3_rho4": ("C3_accum_rho_sweep", "rho4"),
+            "accum_xrun_c3_rho2": ("C3_accum_rho_sweep", "rho2"),
             "ca_engine_c2": ("C2_ca_n256", "engine"), "ca_engine_c4": ("C4_ca_n1024_1gpu", "engine"),
             "ca_engine_c5": ("C5_ca_n2048_1gpu", "engine"),
             "ca_single_step_c5": ("C5_ca_n2048_1gpu", "single_auto"),

@@ -481,7 +481,14 @@ static void launch_accum_k(const Geom& g, uint32_t* cells, int exec, cudaStream_
     // profiles/r2/accum_shapes.txt; GB/s H / BB): 1 strip, 2 rows x 4 vectors
     // 5645 / 5686; 2 strips, 2 x 4: 6102 / 6261; 2 strips, 1 x 8: 6267 / 6503;
     // 2 strips, 1 x 4: 6338 / 6596; 4 strips, 1 x 4: 6254 / 6444.
-    launch_runs_t<KIND, 32, 1, 4, 2>(g, cells, s);
+    // small tiles: eight strips per CTA, so a CTA still streams ~16 K cells
+    // (rho = 8: 256 blocks x 64 cells) instead of a few thousand per map pass,
+    // and several short rows in flight per warp. Side ~65.5 K, Gcells/s H / BB
+    // (profiles/r2/accum_rho_sweep.txt): rho 8: 563 / 524 -> 770 / 752 (0.94
+    // of HBM); rho 4: 247 / 200 -> 484 / 411; rho 2: 45 / 40 -> 220 / 157
+    if (g.rho >= 16) launch_runs_t<KIND, 32, 1, 4, 2>(g, cells, s);
+    else if (g.rho >= 8) launch_runs_t<KIND, 32, 2, 2, 8>(g, cells, s);  // 256-cell rows: 2 rows x 2 vectors
+    else launch_runs_t<KIND, 32, 4, 1, 8>(g, cells, s);  // 128-cell rows: 4 rows x 1 vector (rho <= 2: a row per lane)
 }
 void launch_accum(const Geom& g, uint32_t* cells, int exec, cudaStream_t s) {
     SMX_DISPATCH_KIND(g.kind, launch_accum_k, g, cells, exec, s);
