@@ -741,13 +741,11 @@ __device__ __forceinline__ void cols_issue(const CUtensorMap* tm, const ColItem&
 //   vertical 3-sums: lane (ly = lane >> 2, words jp = 2 (lane & 3), +1), three
 //     16-byte loads, kept in registers for three layers
 //   rule + masked 8-byte store for the output layer one behind.
-// x << 1 | prev >> 31 and x >> 1 | next << 31 on the FMA pipe (IMAD / IMAD.HI):
-// the rule's carry-save logic saturates the ALU pipe (LOP3, rt 2 cycles per
-// SMSP), so the word shifts of the horizontal sums run beside it
-__device__ __forceinline__ uint32_t shl1_fma(uint32_t prev, uint32_t x) { return x * 2u + __umulhi(prev, 2u); }
-__device__ __forceinline__ uint32_t shr1_fma(uint32_t x, uint32_t next) {
-    return __umulhi(x, 0x80000000u) + next * 0x80000000u;
-}
+// x << 1 | prev >> 31 and x >> 1 | next << 31: one funnel shift each (the
+// FMA-pipe pair IMAD.HI + IMAD used earlier measured 0.5 % slower at C4 and
+// C5 once the ALU pipe stopped being the limit: 53 % busy, latency bound)
+__device__ __forceinline__ uint32_t shl1(uint32_t prev, uint32_t x) { return __funnelshift_l(prev, x, 1); }
+__device__ __forceinline__ uint32_t shr1(uint32_t x, uint32_t next) { return __funnelshift_r(x, next, 1); }
 
 template <int RHO>
 __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int nitems, unsigned* ctr,
@@ -830,10 +828,10 @@ __device__ __forceinline__ void cols_step(const ColItem* __restrict__ items, int
             const uint32_t e = L[eoff];
             const uint32_t got = __shfl_xor_sync(0xffffffffu, hc ? m.x : m.w, 1);  // partner's word
             const uint32_t W0 = hc ? got : e, W5 = hc ? e : got;
-            const uint32_t l0 = shl1_fma(W0, m.x), r0 = shr1_fma(m.x, m.y);
-            const uint32_t l1 = shl1_fma(m.x, m.y), r1 = shr1_fma(m.y, m.z);
-            const uint32_t l2 = shl1_fma(m.y, m.z), r2 = shr1_fma(m.z, m.w);
-            const uint32_t l3 = shl1_fma(m.z, m.w), r3 = shr1_fma(m.w, W5);
+            const uint32_t l0 = shl1(W0, m.x), r0 = shr1(m.x, m.y);
+            const uint32_t l1 = shl1(m.x, m.y), r1 = shr1(m.y, m.z);
+            const uint32_t l2 = shl1(m.y, m.z), r2 = shr1(m.z, m.w);
+            const uint32_t l3 = shl1(m.z, m.w), r3 = shr1(m.w, W5);
             uint4* dst = reinterpret_cast<uint4*>(hsw + (li & 1) * (CBR * CW));
             dst[0] = make_uint4(lop3<0x96>(l0, m.x, r0), lop3<0xe8>(l0, m.x, r0), lop3<0x96>(l1, m.y, r1),
                                 lop3<0xe8>(l1, m.y, r1));
@@ -1047,10 +1045,10 @@ __device__ __forceinline__ void cols_step12(const ColItem* __restrict__ items, i
             const uint32_t e = L[eoff];
             const uint32_t got = __shfl_xor_sync(0xffffffffu, hc ? m.x : m.w, 1);  // partner's word
             const uint32_t W0 = hc ? got : e, W5 = hc ? e : got;
-            const uint32_t l0 = shl1_fma(W0, m.x), r0 = shr1_fma(m.x, m.y);
-            const uint32_t l1 = shl1_fma(m.x, m.y), r1 = shr1_fma(m.y, m.z);
-            const uint32_t l2 = shl1_fma(m.y, m.z), r2 = shr1_fma(m.z, m.w);
-            const uint32_t l3 = shl1_fma(m.z, m.w), r3 = shr1_fma(m.w, W5);
+            const uint32_t l0 = shl1(W0, m.x), r0 = shr1(m.x, m.y);
+            const uint32_t l1 = shl1(m.x, m.y), r1 = shr1(m.y, m.z);
+            const uint32_t l2 = shl1(m.y, m.z), r2 = shr1(m.z, m.w);
+            const uint32_t l3 = shl1(m.z, m.w), r3 = shr1(m.w, W5);
             uint4* dst = reinterpret_cast<uint4*>(hsw + (li & 1) * (C2BR * CW));
             dst[0] = make_uint4(lop3<0x96>(l0, m.x, r0), lop3<0xe8>(l0, m.x, r0), lop3<0x96>(l1, m.y, r1),
                                 lop3<0xe8>(l1, m.y, r1));
