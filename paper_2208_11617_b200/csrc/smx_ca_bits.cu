@@ -185,13 +185,28 @@ __global__ void __launch_bounds__(256) k_pack_bits(const uint8_t* __restrict__ c
         const int d = int(c.rowbase - A0);
         uint32_t* out = bits + ((long long)c.z * S + c.y) * WP;
         // lane gl packs chunk k; word k needs chunks k and k+1, so a pass emits
-        // 7 words (lanes 0..6) and the next pass starts 7 chunks on (loads of
-        // four passes issued ahead measured slower: 370 vs 358 us at C5)
-#pragma unroll 2
+        // 7 words (lanes 0..6) and the next pass starts 7 chunks on. Software
+        // pipelined: the next pass's 32 bytes are loaded before this pass is
+        // packed and stored
+        const long long rowend = c.rowbase + n;
+        auto fetch = [&](int base, uint4& x0, uint4& x1) {
+            const long long ck = A0 + 32ll * (base + gl);
+            x0 = x1 = make_uint4(0u, 0u, 0u, 0u);
+            if (ck < rowend && (unsigned long long)(ck + 32) <= ncells) {
+                const uint4* q = reinterpret_cast<const uint4*>(cur + ck);
+                x0 = __ldg(q);
+                x1 = __ldg(q + 1);
+            }
+        };
+        uint4 n0, n1;
+        fetch(0, n0, n1);
         for (int base = 0; base < nw; base += 7) {
+            const uint4 x0 = n0, x1 = n1;
+            if (base + 7 < nw) fetch(base + 7, n0, n1);
             const int k = base + gl;
             const long long ck = A0 + 32ll * k;
-            const uint32_t B = (ck < c.rowbase + n) ? load_chunk_bits(cur, ck, ncells) : 0u;
+            uint32_t B = pack32(x0, x1);
+            if (ck < rowend && (unsigned long long)(ck + 32) > ncells) B = load_chunk_bits(cur, ck, ncells);  // array end
             const uint32_t Bn = __shfl_down_sync(gmask, B, 1, 8);
             if (gl < 7 && k < nw) {
                 uint32_t wv = d ? __funnelshift_r(B, Bn, d) : B;
