@@ -170,20 +170,6 @@ __device__ __forceinline__ void accum_rows(uint32_t* __restrict__ cells, const u
     }
 }
 
-// one cell row [e0, e1) by one lane: 16-byte vectors between scalar ends
-__device__ __forceinline__ void accum_row_lane(uint32_t* __restrict__ cells, unsigned long long e0,
-                                               unsigned long long e1) {
-    unsigned long long a0 = (e0 + 3) & ~3ull, a1 = e1 & ~3ull;
-    if (a0 > a1) a0 = a1 = e1;
-    for (unsigned long long i = e0; i < a0; ++i) cells[i] += 1u;
-    for (unsigned long long p = a0; p < a1; p += 4) {
-        uint4 t = *reinterpret_cast<const uint4*>(cells + p);
-        t.x += 1u; t.y += 1u; t.z += 1u; t.w += 1u;
-        *reinterpret_cast<uint4*>(cells + p) = t;
-    }
-    for (unsigned long long i = a1; i < e1; ++i) cells[i] += 1u;
-}
-
 template <int KIND, int KX, int RR, int NV, int KS = 1>
 __global__ void __launch_bounds__(ACC_THREADS, 4) k_accum_runs(Geom g, uint32_t* __restrict__ cells) {
     // KS strips of KX blocks per CTA, mapped concurrently by warps 0 .. KS-1
@@ -200,21 +186,41 @@ __global__ void __launch_bounds__(ACC_THREADS, 4) k_accum_runs(Geom g, uint32_t*
     const int rho = g.rho, S = g.side;
     const int rows = nruns * rho;
     constexpr int NW = ACC_THREADS / 32;
-    // strips cut into short runs (H2D's first grid rows, level b < KX: runs of
-    // b tiles, each in another data row): one cell row per LANE, every thread
-    // with rows in flight, instead of a warp per row of a few vectors (at C1
-    // those CTAs held SM slots ~100 us: H 0.207 vs BB 0.173 ms per pass)
+    // short run rows (< 128 cells: H2D's first grid rows, level b < KX, runs
+    // of b tiles each in another data row; every row at rho <= 2): the CTA's
+    // threads tile the rows as W-lane slots (W = the power of two >= the
+    // widest row), one cell per thread and row, four rows in flight per
+    // thread — instead of a warp per row of a few vectors (at C1 those CTAs
+    // held SM slots ~100 us) or a lane per row (rho 2: 16 of 256 threads busy)
     int wmax = 0;
     for (int r = 0; r < nruns; ++r) wmax = max(wmax, s_run[r][2]);
     if (wmax * rho < 128) {
-        for (int rr = threadIdx.x; rr < rows; rr += ACC_THREADS) {
-            const int r = rr / rho, ly = rr - r * rho;
-            const int cy = s_run[r][1] * rho + ly;
-            const int xlo = s_run[r][0] * rho;
-            const int xhi = min((s_run[r][0] + s_run[r][2]) * rho, cy + 1);  // tri_contains: x <= y
-            if (cy > S - 1 || xlo >= xhi) continue;
-            const unsigned long long base = tri_idx(0, cy);
-            accum_row_lane(cells, base + xlo, base + xhi);
+        int lgW = 4;
+        while ((1 << lgW) < wmax * rho) ++lgW;
+        const int P = ACC_THREADS >> lgW, sub = threadIdx.x >> lgW, col = threadIdx.x & ((1 << lgW) - 1);
+        const bool p2 = (rho & (rho - 1)) == 0;
+        const int lr = __ffs(rho) - 1;
+        for (int rr0 = 0; rr0 < rows; rr0 += 4 * P) {
+            uint32_t* ptr[4];
+            uint32_t v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                ptr[u] = nullptr;
+                const int rr = rr0 + u * P + sub;
+                if (rr < rows) {
+                    const int r = p2 ? rr >> lr : rr / rho, ly = rr - r * rho;
+                    const int cy = s_run[r][1] * rho + ly;
+                    const int x = s_run[r][0] * rho + col;
+                    const int xhi = min((s_run[r][0] + s_run[r][2]) * rho, cy + 1);  // tri_contains: x <= y
+                    if (cy <= S - 1 && x < xhi) ptr[u] = cells + tri_idx(x, cy);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (ptr[u]) v[u] = *ptr[u];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (ptr[u]) *ptr[u] = v[u] + 1u;
         }
         return;
     }
@@ -485,7 +491,7 @@ static void launch_accum_k(const Geom& g, uint32_t* cells, int exec, cudaStream_
     // (rho = 8: 256 blocks x 64 cells) instead of a few thousand per map pass,
     // and several short rows in flight per warp. Side ~65.5 K, Gcells/s H / BB
     // (profiles/r2/accum_rho_sweep.txt): rho 8: 563 / 524 -> 770 / 752 (0.94
-    // of HBM); rho 4: 247 / 200 -> 484 / 411; rho 2: 45 / 40 -> 220 / 157
+    // of HBM); rho 4: 247 / 200 -> 484 / 411; rho 2: 45 / 40 -> 236 / 175
     if (g.rho >= 16) launch_runs_t<KIND, 32, 1, 4, 2>(g, cells, s);
     else if (g.rho >= 8) launch_runs_t<KIND, 32, 2, 2, 8>(g, cells, s);  // 256-cell rows: 2 rows x 2 vectors
     else launch_runs_t<KIND, 32, 4, 1, 8>(g, cells, s);  // 128-cell rows: 4 rows x 1 vector (rho <= 2: a row per lane)
