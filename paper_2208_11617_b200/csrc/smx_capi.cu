@@ -86,6 +86,8 @@ struct DeviceRes {
     int64_t shadow_side[2] = {-1, -1};
     int cols_nitems = 0;
     int cols_rows = 8;  // output rows per item of the items in slot 8
+    // ACCUM x-run launch orders (H2D grids), keyed by (n, rho): device table + CTA count
+    std::map<std::pair<int64_t, int64_t>, std::pair<void*, int>> accum_orders;
     std::map<std::pair<const void*, std::pair<int64_t, int64_t>>, CUtensorMap> tmaps;
     smx::DevCounters* counters = nullptr;
     unsigned* sink = nullptr;
@@ -103,6 +105,7 @@ void free_res(int dev, DeviceRes& r) {
     if (cudaGetDevice(&cur) != cudaSuccess) return;
     if (cur != dev) cudaSetDevice(dev);
     for (auto& kv : r.prefix) cudaFree(kv.second);
+    for (auto& kv : r.accum_orders) cudaFree(kv.second.first);
     for (int i = 0; i < 12; ++i)
         if (r.pool[i]) cudaFree(r.pool[i]);
     if (r.counters) cudaFree(r.counters);
@@ -1465,6 +1468,50 @@ int smx_map_kernel(const smx_grid* g, void* stream) {
     return SMX_OK;
 }
 
+// The ACCUM x-run kernel's CTAs in data order (H2D grids, rho >= 16, >= 2^18 blocks):
+// H2D's grid row wy of level b covers data tile rows wy + 1 + 2 q b, so in
+// blockIdx order a data row is written at ~log2(n) far-apart times; sorted by
+// the data tile row (then column) of each CTA's first block, the CTAs running
+// together stream consecutive data rows, as BB's grid rows do. Built on the
+// host once per (n, rho), cached on the device.
+int accum_order(const smx_grid* g, const smx::Geom& k, const int2** out, int* count) {
+    *out = nullptr;
+    *count = 0;
+    static const int mode = [] {
+        const char* e = std::getenv("SMX_ACCUM_ORDER");  // A/B: 0 = blockIdx order
+        return e ? std::atoi(e) : 1;
+    }();
+    // rho >= 16 only: at rho 8 / 4 the sorted order measured slower (C3 domain:
+    // 745 -> 730 / 481 -> 456 Gcells/s), at rho 16 it lifts H 791 -> 818 (= BB)
+    if (!mode || g->kind != SMX_H2D || g->rho < 16 || uint64_t(k.ex) * uint64_t(k.ey) < (uint64_t(1) << 18))
+        return SMX_OK;
+    DeviceRes* r;
+    if (int rc = device_res(&r)) return rc;
+    const auto key = std::make_pair(int64_t(g->n), int64_t(g->rho));
+    auto it = r->accum_orders.find(key);
+    if (it == r->accum_orders.end()) {
+        const int sb = smx::accum_strip_blocks(int(g->rho));
+        const int gx = (k.ex + sb - 1) / sb;
+        std::vector<std::pair<std::pair<int64_t, int64_t>, int2>> v;
+        v.reserve(size_t(gx) * size_t(k.ey));
+        for (int wy = 0; wy < k.ey; ++wy)
+            for (int xs = 0; xs < gx; ++xs) {
+                const auto o = smx::map_h2d<int64_t>(int64_t(xs) * sb, wy);
+                v.push_back({{o.y, o.x}, make_int2(xs, wy)});
+            }
+        std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        std::vector<int2> h(v.size());
+        for (size_t i = 0; i < v.size(); ++i) h[i] = v[i].second;
+        void* d;
+        TRY(cudaMalloc(&d, h.size() * sizeof(int2)));
+        TRY(cudaMemcpy(d, h.data(), h.size() * sizeof(int2), cudaMemcpyHostToDevice));
+        it = r->accum_orders.emplace(key, std::make_pair(d, int(h.size()))).first;
+    }
+    *out = (const int2*)it->second.first;
+    *count = it->second.second;
+    return SMX_OK;
+}
+
 int smx_accum(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passes, int32_t exec,
               int device_ptr, uint32_t* coverage, smx_counters* counters, void* stream) {
     std::vector<smx::Geom> subs;
@@ -1496,6 +1543,8 @@ int smx_accum(const smx_grid* g, uint32_t* cells, uint64_t ncells, int64_t passe
     }
     if (coverage || counters)
         if (int rc = fill_counters(g, counters, s, dcov)) return rc;
+    if (exec == SMX_EXEC_RUNS && subs.size() == 1)
+        if (int rc = accum_order(g, subs[0], &subs[0].order, &subs[0].norder)) return rc;
     for (int64_t p = 0; p < passes; ++p)
         for (const auto& k : subs) smx::launch_accum(k, d, exec, s);  // bands: disjoint cells
     TRY(cudaGetLastError());

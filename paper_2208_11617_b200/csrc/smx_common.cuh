@@ -23,6 +23,8 @@ struct Geom {
     int wy0;              // first grid row of this launch (row-range shards: wy = wy0 + blockIdx.y)
     int ty0, ty1;         // x-run 2-D kernels: only tiles whose data tile row is in [ty0, ty1)
                           // (ty1 == 0: no filter) — one chunk of a pipelined host-buffer call
+    const int2* order;    // ACCUM x-run: CTA i takes strip group order[i] = (x group, grid row)
+    int norder;           // (a launch order sorted by data tile row; nullptr: blockIdx order)
 };
 
 // strict_view (maps.hpp:35-38): outputs in { x < y }, shifted y - 1 by the sweep

@@ -181,7 +181,12 @@ __global__ void __launch_bounds__(ACC_THREADS, 4) k_accum_runs(Geom g, uint32_t*
     // consecutive segments of the same data rows (a launch order with
     // consecutive grid rows per strip column measured slower for both maps:
     // C3 H 5800 vs 6335 GB/s, profiles/r2/accum_order.txt)
-    strips_runs<KIND, KX, KS>(g, blockIdx.x, g.wy0 + blockIdx.y, s_run, s_nrun, &s_total);
+    int xs = blockIdx.x, wy = g.wy0 + blockIdx.y;
+    if (g.order) {
+        const int2 o = g.order[blockIdx.x];
+        xs = o.x, wy = o.y;
+    }
+    strips_runs<KIND, KX, KS>(g, xs, wy, s_run, s_nrun, &s_total);
     const int nruns = s_total;
     const int rho = g.rho, S = g.side;
     const int rows = nruns * rho;
@@ -466,7 +471,8 @@ void launch_map_block(const Geom& g, uint32_t* cov, DevCounters* cnt, unsigned* 
 
 template <int KIND, int KX, int RR, int NV, int KS = 1>
 static void launch_runs_t(const Geom& g, uint32_t* cells, cudaStream_t s) {
-    k_accum_runs<KIND, KX, RR, NV, KS><<<dim3((g.ex + KX * KS - 1) / (KX * KS), g.ey, 1), ACC_THREADS, 0, s>>>(g, cells);
+    const dim3 grid = g.order ? dim3(unsigned(g.norder), 1, 1) : dim3((g.ex + KX * KS - 1) / (KX * KS), g.ey, 1);
+    k_accum_runs<KIND, KX, RR, NV, KS><<<grid, ACC_THREADS, 0, s>>>(g, cells);
 }
 
 template <int KIND>
@@ -496,6 +502,7 @@ static void launch_accum_k(const Geom& g, uint32_t* cells, int exec, cudaStream_
     else if (g.rho >= 8) launch_runs_t<KIND, 32, 2, 2, 8>(g, cells, s);  // 256-cell rows: 2 rows x 2 vectors
     else launch_runs_t<KIND, 32, 4, 1, 8>(g, cells, s);  // 128-cell rows: 4 rows x 1 vector (rho <= 2: a row per lane)
 }
+int accum_strip_blocks(int rho) { return 32 * (rho >= 16 ? 2 : 8); }  // map blocks per x-run CTA
 void launch_accum(const Geom& g, uint32_t* cells, int exec, cudaStream_t s) {
     SMX_DISPATCH_KIND(g.kind, launch_accum_k, g, cells, exec, s);
 }

@@ -28,6 +28,7 @@ inline void once_per_device(std::once_flag (&flags)[kMaxDevices], int dev, Fn&& 
 void launch_outcomes(const Geom& g, smx_outcome* out, unsigned long long count, cudaStream_t s);
 void launch_map_block(const Geom& g, uint32_t* cov, DevCounters* cnt, unsigned* sink, cudaStream_t s);
 void launch_accum(const Geom& g, uint32_t* cells, int exec, cudaStream_t s);
+int accum_strip_blocks(int rho);  // map blocks per CTA of the ACCUM x-run kernel
 void launch_life_init(unsigned long long seed, uint8_t* cells, unsigned long long n, cudaStream_t s);
 // kernel_accum: every cell += 1 (no map)
 void launch_increment(uint32_t* cells, unsigned long long n, cudaStream_t s);
